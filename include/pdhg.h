@@ -1,0 +1,243 @@
+/*
+ * pdhg.h — C-ABI of the B200 restarted-PDHG LP solver (libpdhg_b200.so).
+ *
+ * This is the drop-in boundary for the reference's solve path
+ * `rpdlp::Solve(const LpProblem&, const SolverParams&, const EvalObserver&)`
+ * (reference proj/core/include/rpdlp/solver.hpp:145-146). Everything is plain
+ * C: borrowed pointers + sizes in, caller-allocated buffers out, an integer
+ * return code plus a message buffer instead of exceptions. The C++ shim in
+ * include/rpdlp/ maps the codes back onto the reference's exception types
+ * (std::invalid_argument, rpdlp::NumericalFailure).
+ *
+ * Layout contract: matrices are passed exactly as the reference stores them
+ * (CSR with int64 row_ptr / col_idx and double values,
+ * sparse_matrix.hpp:94-98), A (equality rows) and G (>= rows) separately
+ * (lp_problem.hpp:33-45). The library narrows indices to int32 on the device
+ * and builds K = [A; G] in CSR and CSC there. No host pointer is retained
+ * after a call returns (SURVEY §8b ownership rule).
+ */
+#ifndef PDHG_H_
+#define PDHG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDHG_ABI_VERSION 1
+
+/* Return codes (SURVEY §8b "Errors"). */
+enum {
+  PDHG_OK = 0,
+  PDHG_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  PDHG_NUMERICAL_FAILURE = 2, /* rpdlp::NumericalFailure (solver.cpp:391-394) */
+  PDHG_CUDA_ERROR = 3,
+  PDHG_NCCL_ERROR = 4,
+  PDHG_ABORTED = 5 /* the eval callback asked to stop */
+};
+
+/* rpdlp::SolveStatus (solver.hpp:57). */
+enum { PDHG_OPTIMAL = 0, PDHG_ITER_LIMIT = 1, PDHG_TIME_LIMIT = 2 };
+
+/* One CSR block, reference layout (sparse_matrix.hpp:83-101). */
+typedef struct {
+  int64_t rows;
+  int64_t cols;
+  const int64_t* row_ptr; /* rows + 1 */
+  const int64_t* col_idx; /* nnz, strictly increasing per row */
+  const double* values;   /* nnz, no explicit zeros */
+} pdhg_csr;
+
+/* rpdlp::LpProblem (lp_problem.hpp:33-45):
+ *   min c'x  s.t.  A x = b,  G x >= h,  l <= x <= u. */
+typedef struct {
+  pdhg_csr a; /* m1 x n */
+  pdhg_csr g; /* m2 x n */
+  int64_t n;  /* length of c, l, u */
+  const double* c;
+  const double* b; /* m1 */
+  const double* h; /* m2 */
+  const double* l; /* -inf allowed */
+  const double* u; /* +inf allowed */
+  double objective_offset;
+  int32_t negated_objective;
+} pdhg_lp;
+
+/* rpdlp::SolverParams (solver.hpp:32-55) with ScalingConfig
+ * (scaling.hpp:40-44) flattened, field for field, same defaults. */
+typedef struct {
+  double eps;
+  double time_limit;
+  int64_t iter_limit;
+  double sufficient_decay;
+  double necessary_decay;
+  double long_loop_frac;
+  int32_t restart_enabled;
+  int64_t check_every;
+  int32_t scaling_enabled;
+  int32_t ruiz_iters;
+  double pc_alpha;
+  uint64_t seed;
+  int32_t adaptive_step;
+  int64_t log_every;
+} pdhg_params;
+
+/* rpdlp::ResidualReport (kkt.hpp:32-41). */
+typedef struct {
+  double primal_res;
+  double dual_res;
+  double gap_abs;
+  double primal_obj;
+  double dual_obj;
+  double rel_primal;
+  double rel_dual;
+  double rel_gap;
+} pdhg_report;
+
+/* rpdlp::EvalInfo (solver.hpp:127-140). */
+typedef struct {
+  int64_t iteration;
+  int64_t inner_iteration;
+  int64_t restarts;
+  double omega;
+  double eta;
+  double kkt_candidate;
+  double kkt_loop_start;
+  int32_t candidate_is_current;
+  int32_t restarted;
+  pdhg_report original_report;
+  double seconds;
+} pdhg_eval_info;
+
+/* rpdlp::EvalObserver (solver.hpp:142). Called synchronously on the calling
+ * thread at every non-terminal check. A nonzero return aborts the solve with
+ * PDHG_ABORTED (used by the C++ shim to rethrow observer exceptions). */
+typedef int (*pdhg_eval_cb)(const pdhg_eval_info* info, void* user);
+
+/* rpdlp::SolveResult (solver.hpp:59-70). x (n), y (m1+m2) and lambda (n)
+ * are caller-allocated; any of them may be NULL to skip the copy-out. */
+typedef struct {
+  int32_t status;
+  double* x;
+  double* y;
+  double* lambda;
+  pdhg_report report;
+  int64_t iterations;
+  int64_t restarts;
+  double solve_seconds;
+  double scaling_seconds;
+} pdhg_result;
+
+/* Statistics of a resident session (sizes, partitions, timings). */
+typedef struct {
+  int64_t m1, m2, n, nnz;
+  int64_t csr_tiles, csc_tiles;
+  int64_t device_bytes;
+  double upload_seconds;  /* H2D + int32 narrowing + stacking + CSC build */
+  double scaling_seconds; /* Ruiz + Pock-Chambolle + ApplyScaling on device */
+  int32_t device;
+  int32_t l2_resident; /* 1 if the per-iteration working set fits in L2 */
+} pdhg_session_stats;
+
+typedef struct pdhg_session pdhg_session;
+
+/* Defaults of rpdlp::SolverParams{} (solver.hpp:33-54). */
+void pdhg_params_default(pdhg_params* p);
+
+/* Library / ABI identification. */
+int pdhg_abi_version(void);
+const char* pdhg_build_info(void);
+int pdhg_device_count(void);
+
+/* ---- the drop-in entry point: rpdlp::Solve (solver.cpp:521-543) ----------
+ * Validates problem and params (lp_problem.cpp:22-58, solver.cpp:59-70),
+ * uploads, scales on device, runs the restarted PDHG loop on `device`,
+ * copies the best iterate out. */
+int pdhg_solve(const pdhg_lp* lp, const pdhg_params* params, pdhg_eval_cb cb,
+               void* user, pdhg_result* out, char* err, size_t errlen);
+int pdhg_solve_on(const pdhg_lp* lp, const pdhg_params* params, int device,
+                  pdhg_eval_cb cb, void* user, pdhg_result* out, char* err,
+                  size_t errlen);
+
+/* ---- resident sessions (problem kept in HBM between solves) --------------
+ * create = validate + upload + StackK + CSC build + ComputeScaling +
+ * ApplyScaling (solver.cpp:523-537) on `device`. `params` supplies only the
+ * scaling configuration. */
+int pdhg_session_create(const pdhg_lp* lp, const pdhg_params* params,
+                        int device, pdhg_session** out, char* err,
+                        size_t errlen);
+void pdhg_session_destroy(pdhg_session* s);
+int pdhg_session_stats_get(pdhg_session* s, pdhg_session_stats* out);
+/* SolveLoop(...).Run() (solver.cpp:232-267) on the resident scaled problem.
+ * out->scaling_seconds reports the session's device scaling time. */
+int pdhg_session_solve(pdhg_session* s, const pdhg_params* params,
+                       pdhg_eval_cb cb, void* user, pdhg_result* out,
+                       char* err, size_t errlen);
+
+/* ---- kernel-level entry points (parity tests, benchmarks) ----------------
+ * All vectors are host buffers. */
+/* Composed Ruiz x PC scales (scaling.cpp:86-91): row_scale m, col_scale n. */
+int pdhg_session_scaling(pdhg_session* s, double* row_scale,
+                         double* col_scale, char* err, size_t errlen);
+/* The scaled problem as the loop sees it: K_s values in CSR order (nnz),
+ * c_s, l_s, u_s (n), q_s (m). Any pointer may be NULL. */
+int pdhg_session_scaled(pdhg_session* s, double* k_values, double* c,
+                        double* l, double* u, double* q, char* err,
+                        size_t errlen);
+/* SpMV with the scaled stacked K: transpose=0 -> out(m) = K_s in(n)
+ * (sparse_matrix.cpp:114-125); transpose=1 -> out(n) = K_s^T in(m)
+ * (sparse_matrix.cpp:127-138). */
+int pdhg_session_spmv(pdhg_session* s, int transpose, const double* in,
+                      double* out, char* err, size_t errlen);
+/* EstimateOpNorm(K_s, iters, seed) (solver.cpp:84-110). */
+int pdhg_session_opnorm(pdhg_session* s, int iters, uint64_t seed,
+                        double* out, char* err, size_t errlen);
+/* Times the two fused step kernels of one PDHG iteration (K-CSC primal and
+ * K-CSR dual) launched `iters` times each on the session stream, bracketed
+ * by CUDA events on that stream; returns mean milliseconds per launch and
+ * the whole-iteration mean from a graph-launched block. */
+int pdhg_session_time_kernels(pdhg_session* s, int iters, double* ms_primal,
+                              double* ms_dual, double* ms_iteration,
+                              char* err, size_t errlen);
+
+/* ---- unit-level exports (solver.hpp:81-125), device-backed ---------------
+ * PrimalStep (solver.cpp:112-129): out(n) = proj_[l,u](x - eta/omega (c - K'y))
+ * DualStep (solver.cpp:131-154): out(m) = proj_Y(y + eta*omega (q - K(2x_new - x_old)))
+ * These run on the unscaled problem's K. */
+int pdhg_primal_step(const pdhg_lp* lp, const double* x, const double* y,
+                     double eta, double omega, double* out, char* err,
+                     size_t errlen);
+int pdhg_dual_step(const pdhg_lp* lp, const double* x_new,
+                   const double* x_old, const double* y, double eta,
+                   double omega, double* out, char* err, size_t errlen);
+
+/* ---- instance generators (instance_gen.hpp:39-59 + SURVEY §8d shapes) ----
+ * Host-side input builders; they own their arrays until freed. */
+typedef struct pdhg_instance pdhg_instance;
+/* GenRandomLp (instance_gen.cpp:143-188), bit-identical per seed. */
+int pdhg_gen_random_lp(int64_t m, int64_t n, double density, uint64_t seed,
+                       pdhg_instance** out, char* err, size_t errlen);
+/* GenPagerank (instance_gen.cpp:27-64, 90-141), bit-identical per seed. */
+int pdhg_gen_pagerank(int64_t n_nodes, double damping, int64_t attachment,
+                      uint64_t seed, pdhg_instance** out, char* err,
+                      size_t errlen);
+/* Transportation LP, `sources` x `sinks`: demand rows
+ * sum_i x_ij = d_j in A, supply rows -sum_j x_ij >= -s_i in G, x >= 0. */
+int pdhg_gen_transport(int64_t sources, int64_t sinks, uint64_t seed,
+                       pdhg_instance** out, char* err, size_t errlen);
+/* Moves the first `m1` rows of G into A with b = G_rows * witness
+ * (SURVEY §8d config 1 post-pass). Requires a witness (GenRandomLp). */
+int pdhg_instance_make_equalities(pdhg_instance* inst, int64_t m1, char* err,
+                                  size_t errlen);
+int pdhg_instance_view(const pdhg_instance* inst, pdhg_lp* out);
+/* Witness x_hat of GenRandomLp (length n) or NULL. */
+const double* pdhg_instance_witness(const pdhg_instance* inst);
+void pdhg_instance_free(pdhg_instance* inst);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PDHG_H_ */

@@ -1,0 +1,215 @@
+// C-ABI entry points (include/pdhg.h). Exceptions never cross this boundary:
+// every entry maps pdhg::Error / std::invalid_argument onto a return code and
+// a message, which the C++ shim (include/rpdlp/) rethrows as the reference's
+// exception types.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "session.cuh"
+
+struct pdhg_session {
+  std::unique_ptr<pdhg::Session> impl;
+};
+
+namespace {
+
+using pdhg::Error;
+
+void put(char* err, size_t len, const std::string& m) {
+  if (err && len) std::snprintf(err, len, "%s", m.c_str());
+}
+
+template <class F>
+int Guard(char* err, size_t len, F&& f) {
+  try {
+    f();
+    return PDHG_OK;
+  } catch (const Error& e) {
+    put(err, len, e.what());
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    put(err, len, e.what());
+    return PDHG_INVALID_ARGUMENT;
+  } catch (const std::bad_alloc&) {
+    put(err, len, "host allocation failed");
+    return PDHG_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    put(err, len, e.what());
+    return PDHG_CUDA_ERROR;
+  }
+}
+
+void Invalid(const std::string& m) { throw Error(PDHG_INVALID_ARGUMENT, m); }
+
+// LpProblem::Validate (lp_problem.cpp:22-58), same checks and messages.
+void ValidateLp(const pdhg_lp& lp) {
+  const int64_t n = lp.n;
+  if (n < 0 || lp.a.rows < 0 || lp.g.rows < 0) Invalid("negative matrix dimension");
+  if (lp.a.cols != n || lp.g.cols != n) Invalid("matrix column count does not match c");
+  if ((lp.a.rows && !lp.a.row_ptr) || (lp.g.rows && !lp.g.row_ptr)) Invalid("missing row_ptr");
+  if ((n && (!lp.c || !lp.l || !lp.u)) || (lp.a.rows && !lp.b) || (lp.g.rows && !lp.h)) Invalid("missing vector");
+  for (int64_t i = 0; i < n; ++i)
+    if (std::isnan(lp.c[i])) Invalid("NaN in c");
+  for (int64_t i = 0; i < lp.a.rows; ++i)
+    if (std::isnan(lp.b[i])) Invalid("NaN in b");
+  for (int64_t i = 0; i < lp.g.rows; ++i)
+    if (std::isnan(lp.h[i])) Invalid("NaN in h");
+  for (int64_t i = 0; i < n; ++i)
+    if (std::isinf(lp.c[i])) Invalid("infinite entry in c");
+  for (int64_t i = 0; i < n; ++i) {
+    if (std::isnan(lp.l[i]) || std::isnan(lp.u[i])) Invalid("NaN bound");
+    if (lp.l[i] > lp.u[i]) Invalid("crossed bounds: l > u at index " + std::to_string(i));
+  }
+}
+
+// SolverParams::Validate (solver.cpp:59-70).
+void ValidateParams(const pdhg_params& p) {
+  if (p.eps <= 0.0) Invalid("eps must be positive");
+  if (!(0.0 < p.sufficient_decay && p.sufficient_decay < p.necessary_decay && p.necessary_decay < 1.0))
+    Invalid("restart decay constants out of order");
+  if (!(0.0 < p.long_loop_frac && p.long_loop_frac < 1.0)) Invalid("long_loop_frac must lie in (0, 1)");
+  if (p.check_every < 1) Invalid("check_every must be >= 1");
+  if (p.iter_limit < 0) Invalid("negative iter_limit");
+}
+
+pdhg::Session& S(pdhg_session* s) {
+  if (!s || !s->impl) Invalid("null session");
+  return *s->impl;
+}
+
+}  // namespace
+
+extern "C" {
+
+void pdhg_params_default(pdhg_params* p) {
+  p->eps = 1e-4;
+  p->time_limit = 3600.0;
+  p->iter_limit = INT64_MAX;
+  p->sufficient_decay = 0.2;
+  p->necessary_decay = 0.8;
+  p->long_loop_frac = 0.36;
+  p->restart_enabled = 1;
+  p->check_every = 64;
+  p->scaling_enabled = 1;
+  p->ruiz_iters = 10;
+  p->pc_alpha = 1.0;
+  p->seed = 0;
+  p->adaptive_step = 0;
+  p->log_every = 0;
+}
+
+int pdhg_abi_version(void) { return PDHG_ABI_VERSION; }
+
+const char* pdhg_build_info(void) {
+  return "libpdhg_b200: sm_100a FP64 restarted PDHG (tile-segmented SpMV, fused step/check epilogues, CUDA graphs)";
+}
+
+int pdhg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int pdhg_session_create(const pdhg_lp* lp, const pdhg_params* prm, int device, pdhg_session** out, char* err,
+                        size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!lp || !prm || !out) Invalid("null argument");
+    ValidateLp(*lp);
+    auto* s = new pdhg_session;
+    try {
+      s->impl = std::make_unique<pdhg::Session>(*lp, *prm, device);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+void pdhg_session_destroy(pdhg_session* s) { delete s; }
+
+int pdhg_session_stats_get(pdhg_session* s, pdhg_session_stats* out) {
+  return Guard(nullptr, 0, [&] { S(s).Stats(out); });
+}
+
+int pdhg_session_solve(pdhg_session* s, const pdhg_params* prm, pdhg_eval_cb cb, void* user, pdhg_result* out,
+                       char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    ValidateParams(*prm);
+    S(s).Solve(*prm, cb, user, out);
+  });
+}
+
+int pdhg_solve_on(const pdhg_lp* lp, const pdhg_params* prm, int device, pdhg_eval_cb cb, void* user,
+                  pdhg_result* out, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!lp || !prm || !out) Invalid("null argument");
+    ValidateLp(*lp);
+    ValidateParams(*prm);
+    pdhg::Session sess(*lp, *prm, device);
+    sess.Solve(*prm, cb, user, out);
+  });
+}
+
+int pdhg_solve(const pdhg_lp* lp, const pdhg_params* prm, pdhg_eval_cb cb, void* user, pdhg_result* out, char* err,
+               size_t errlen) {
+  return pdhg_solve_on(lp, prm, 0, cb, user, out, err, errlen);
+}
+
+int pdhg_session_scaling(pdhg_session* s, double* rs, double* cs, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] { S(s).Scaling(rs, cs); });
+}
+
+int pdhg_session_scaled(pdhg_session* s, double* kv, double* c, double* l, double* u, double* q, char* err,
+                        size_t errlen) {
+  return Guard(err, errlen, [&] { S(s).ScaledProblem(kv, c, l, u, q); });
+}
+
+int pdhg_session_spmv(pdhg_session* s, int transpose, const double* in, double* out, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] { S(s).Spmv(transpose, in, out); });
+}
+
+int pdhg_session_opnorm(pdhg_session* s, int iters, uint64_t seed, double* out, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (iters < 1) Invalid("iters must be >= 1");
+    *out = S(s).OpNorm(iters, seed);
+  });
+}
+
+int pdhg_session_time_kernels(pdhg_session* s, int iters, double* ms_primal, double* ms_dual, double* ms_iter,
+                              char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (iters < 1) Invalid("iters must be >= 1");
+    S(s).TimeKernels(iters, ms_primal, ms_dual, ms_iter);
+  });
+}
+
+int pdhg_primal_step(const pdhg_lp* lp, const double* x, const double* y, double eta, double omega, double* out,
+                     char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    ValidateLp(*lp);
+    pdhg_params p;
+    pdhg_params_default(&p);
+    p.scaling_enabled = 0;
+    pdhg::Session sess(*lp, p, 0);
+    sess.UnitPrimal(x, y, eta, omega, out);
+  });
+}
+
+int pdhg_dual_step(const pdhg_lp* lp, const double* xn, const double* xo, const double* y, double eta, double omega,
+                   double* out, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    ValidateLp(*lp);
+    pdhg_params p;
+    pdhg_params_default(&p);
+    p.scaling_enabled = 0;
+    pdhg::Session sess(*lp, p, 0);
+    sess.UnitDual(xn, xo, y, eta, omega, out);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// Shared definitions for the B200 restarted-PDHG library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace pdhg {
+
+// Error carrying a C-ABI code (include/pdhg.h).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PDHG_CUDA(call)                                                     \
+  do {                                                                      \
+    cudaError_t e_ = (call);                                                \
+    if (e_ != cudaSuccess)                                                  \
+      throw ::pdhg::Error(3, std::string(#call) + ": " +                   \
+                                 cudaGetErrorString(e_) + " (" __FILE__ ")"); \
+  } while (0)
+
+// Tile geometry of the segmented SpMV engine (see tile_spmv.cuh).
+constexpr int kBlock = 256;        // threads per CTA
+constexpr int kTile = 2048;        // nominal nonzeros per tile
+constexpr int kSnap = 64;          // segments this short never straddle tiles
+constexpr int kSeqMax = 32;        // segments up to this length: one thread, in order
+constexpr int kTileCap = kTile + kSnap;
+constexpr int kWarps = kBlock / 32;
+
+// A compressed sparse matrix in either role: CSR (segments = rows, gathered
+// vector indexed by columns) or CSC (segments = columns). Int32 indices,
+// FP64 values; nnz < 2^31 is enforced at upload.
+struct CMat {
+  int32_t nseg = 0;  // rows (CSR) or columns (CSC)
+  int32_t nvec = 0;  // length of the gathered vector
+  int64_t nnz = 0;
+  int32_t* ptr = nullptr;  // nseg + 1
+  int32_t* idx = nullptr;  // nnz
+  double* val = nullptr;   // nnz
+  // Tile partition (computed once per matrix, tile_partition in kernels.cu).
+  int32_t ntiles = 0;
+  int32_t* tile_begin = nullptr;  // ntiles + 1 nonzero offsets
+  int32_t* tile_seg = nullptr;    // ntiles + 1 first owned segment
+  int32_t* head_first = nullptr;  // ntiles: first tile of the spanning head segment or -1
+  int32_t* tail_owner = nullptr;  // ntiles: owner tile of the spanning tail segment or -1
+  // Cross-tile scratch for segments longer than a tile.
+  double* head_part = nullptr;  // ntiles * 2
+  double* tail_part = nullptr;  // ntiles * 2
+  unsigned* counter = nullptr;  // ntiles, zero between launches
+};
+
+// Device-resident solver scalars: the iteration kernels read these instead
+// of taking per-iteration host arguments, so a 64-iteration block can be
+// replayed as one CUDA graph.
+struct Scalars {
+  double eta;
+  double omega;
+  double inner_base;  // RunningAverage weight at the start of the block
+  double pw_norm;     // power iteration: norm of the current vector
+  int32_t pw_zero;    // power iteration hit a zero vector
+  int32_t pad;
+  double adapt_iter;  // iterations_ at the start of the block (adaptive step)
+};
+
+// Clamp with the reference's NaN behaviour: std::min(std::max(v, lo), hi)
+// (solver.cpp:33-35) returns NaN for NaN input; fmin/fmax would mask it.
+__device__ __forceinline__ double clamp_ref(double v, double lo, double hi) {
+  v = (v < lo) ? lo : v;        // std::max(v, lo) == (v < lo ? lo : v)
+  return (hi < v) ? hi : v;     // std::min(v, hi) == (hi < v ? hi : v)
+}
+__device__ __forceinline__ double max0_ref(double v) { return (v < 0.0) ? 0.0 : v; }
+__device__ __forceinline__ double min0_ref(double v) { return (0.0 < v) ? 0.0 : v; }
+
+// ProjectReducedCost (kkt.cpp:29-41). cls: 0 free, 1 upper-only,
+// 2 lower-only, 3 boxed (lp_problem.cpp:60-67).
+__device__ __forceinline__ int bound_class(double lo, double hi) {
+  const bool a = isfinite(lo), b = isfinite(hi);
+  return (!a && !b) ? 0 : (!a ? 1 : (!b ? 2 : 3));
+}
+__device__ __forceinline__ double project_reduced(double v, int cls) {
+  // std::min(v, 0.0) == (0.0 < v ? 0.0 : v); std::max(v, 0.0) == (v < 0.0 ? 0.0 : v)
+  return cls == 0 ? 0.0 : (cls == 1 ? min0_ref(v) : (cls == 2 ? max0_ref(v) : v));
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+}  // namespace pdhg

@@ -1,0 +1,292 @@
+// Host-side instance builders (input construction, off the solve path).
+//
+// GenRandomLp and GenPagerank restate the reference generators
+// (proj/core/src/instance_gen.cpp:27-64, 90-141, 143-188) draw for draw with
+// the same libstdc++ engines, so instances are bit-identical per seed
+// (pinned by tests/test_generators.py against the reference build and the
+// committed golden checksums). Matrices go through a FromTriplets
+// equivalent (sparse_matrix.cpp:25-69: sort by (row, col), sum duplicates,
+// drop zeros). The transportation generator is new.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <limits>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/pdhg.h"
+
+struct pdhg_instance {
+  int64_t n = 0;
+  int64_t a_rows = 0, g_rows = 0;
+  std::vector<int64_t> a_ptr{0}, a_idx, g_ptr{0}, g_idx;
+  std::vector<double> a_val, g_val, c, b, h, l, u, witness;
+  double offset = 0.0;
+};
+
+namespace {
+
+using I = int64_t;
+
+struct Trip {
+  I row, col;
+  double v;
+};
+
+// FromTriplets (sparse_matrix.cpp:25-69) into CSR arrays.
+void FromTriplets(I rows, std::vector<Trip> t, std::vector<I>* ptr, std::vector<I>* idx, std::vector<double>* val) {
+  std::sort(t.begin(), t.end(),
+            [](const Trip& a, const Trip& b) { return std::tie(a.row, a.col) < std::tie(b.row, b.col); });
+  ptr->assign(rows + 1, 0);
+  idx->clear();
+  val->clear();
+  idx->reserve(t.size());
+  val->reserve(t.size());
+  size_t i = 0;
+  while (i < t.size()) {
+    const I r = t[i].row, c = t[i].col;
+    double v = 0.0;
+    while (i < t.size() && t[i].row == r && t[i].col == c) v += t[i++].v;
+    if (v != 0.0) {
+      idx->push_back(c);
+      val->push_back(v);
+      ++(*ptr)[r + 1];
+    }
+  }
+  for (I r = 0; r < rows; ++r) (*ptr)[r + 1] += (*ptr)[r];
+}
+
+// Row-sequential host product, only for building right-hand sides.
+void CsrMul(const std::vector<I>& p, const std::vector<I>& j, const std::vector<double>& v, const double* x, I rows,
+            double* y) {
+  for (I r = 0; r < rows; ++r) {
+    double acc = 0.0;
+    for (I k = p[r]; k < p[r + 1]; ++k) acc += v[k] * x[j[k]];
+    y[r] = acc;
+  }
+}
+
+pdhg_instance* RandomLp(I m, I n, double density, uint64_t seed) {
+  if (m < 1 || n < 1) throw std::invalid_argument("m and n must be >= 1");
+  if (!(density > 0.0 && density <= 1.0)) throw std::invalid_argument("density must lie in (0, 1]");
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  std::uniform_real_distribution<double> sym(-1.0, 1.0);
+  auto* p = new pdhg_instance;
+  p->n = n;
+  p->witness.resize(n);
+  for (double& v : p->witness) v = unit(rng);
+  std::vector<Trip> t;
+  for (I i = 0; i < m; ++i) {
+    I row_nnz = 0;
+    for (I j = 0; j < n; ++j) {
+      if (unit(rng) < density) {
+        t.push_back({i, j, sym(rng)});
+        ++row_nnz;
+      }
+    }
+    if (row_nnz == 0) {
+      const I j = static_cast<I>(rng() % static_cast<uint64_t>(n));
+      t.push_back({i, j, sym(rng)});
+    }
+  }
+  p->g_rows = m;
+  FromTriplets(m, std::move(t), &p->g_ptr, &p->g_idx, &p->g_val);
+  std::vector<double> gx(m);
+  CsrMul(p->g_ptr, p->g_idx, p->g_val, p->witness.data(), m, gx.data());
+  p->h.resize(m);
+  for (I i = 0; i < m; ++i) p->h[i] = gx[i] - std::abs(0.3 * sym(rng));
+  p->c.resize(n);
+  for (double& v : p->c) v = sym(rng);
+  p->l.assign(n, 0.0);
+  p->u.assign(n, 1.0);
+  return p;
+}
+
+pdhg_instance* Pagerank(I n_nodes, double damping, I attachment, uint64_t seed) {
+  if (n_nodes < attachment + 1) throw std::invalid_argument("n_nodes must be at least attachment + 1");
+  if (!(damping > 0.0 && damping < 1.0)) throw std::invalid_argument("damping must lie in (0, 1)");
+  // GenPagerankGraph (instance_gen.cpp:27-64).
+  std::mt19937_64 rng(seed);
+  std::vector<std::pair<I, I>> edges;
+  edges.reserve(static_cast<size_t>(n_nodes * attachment));
+  const I core = attachment + 1;
+  for (I i = 0; i < core; ++i) edges.push_back({i, (i + 1) % core});
+  std::vector<I> pool;
+  pool.reserve(2 * static_cast<size_t>(n_nodes * attachment));
+  for (I i = 0; i < core; ++i) pool.push_back(i);
+  for (auto& e : edges) pool.push_back(e.second);
+  std::vector<I> targets;
+  for (I i = core; i < n_nodes; ++i) {
+    targets.clear();
+    while (static_cast<I>(targets.size()) < attachment) {
+      std::uniform_int_distribution<size_t> dist(0, pool.size() - 1);
+      const I pick = pool[dist(rng)];
+      if (std::find(targets.begin(), targets.end(), pick) == targets.end()) targets.push_back(pick);
+    }
+    for (I t : targets) {
+      edges.push_back({i, t});
+      pool.push_back(t);
+    }
+    pool.push_back(i);
+  }
+  pool = std::vector<I>();
+  // BuildPagerankLp (instance_gen.cpp:90-137).
+  std::vector<I> outdeg(n_nodes, 0);
+  for (auto& e : edges) ++outdeg[e.first];
+  std::vector<I> dangling;
+  for (I j = 0; j < n_nodes; ++j)
+    if (outdeg[j] == 0) {
+      dangling.push_back(j);
+      outdeg[j] = 1;
+    }
+  std::vector<Trip> t;
+  t.reserve(edges.size() + 2 * static_cast<size_t>(n_nodes));
+  for (I i = 0; i < n_nodes; ++i) t.push_back({i, i, 1.0});
+  for (auto& e : edges) t.push_back({e.second, e.first, -damping / outdeg[e.first]});
+  for (I j : dangling) t.push_back({j, j, -damping});
+  edges = std::vector<std::pair<I, I>>();
+  auto* p = new pdhg_instance;
+  p->n = n_nodes;
+  p->g_rows = n_nodes;
+  FromTriplets(n_nodes, std::move(t), &p->g_ptr, &p->g_idx, &p->g_val);
+  p->h.assign(n_nodes, (1.0 - damping) / static_cast<double>(n_nodes));
+  p->a_rows = 1;
+  p->a_ptr = {0, n_nodes};
+  p->a_idx.resize(n_nodes);
+  for (I j = 0; j < n_nodes; ++j) p->a_idx[j] = j;
+  p->a_val.assign(n_nodes, 1.0);
+  p->b = {1.0};
+  p->c.assign(n_nodes, 0.0);
+  p->l.assign(n_nodes, 0.0);
+  p->u.assign(n_nodes, std::numeric_limits<double>::infinity());
+  return p;
+}
+
+// Transportation LP. Variables x_ij, index i*T + j.
+// Draw order: demands d_j, supplies s_i, then costs c_ij row-major.
+pdhg_instance* Transport(I S, I T, uint64_t seed) {
+  if (S < 1 || T < 1) throw std::invalid_argument("sources and sinks must be >= 1");
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  std::vector<double> d(T), s(S);
+  double sd = 0.0, ss = 0.0;
+  for (double& v : d) {
+    v = 1.0 + unit(rng);
+    sd += v;
+  }
+  for (double& v : s) {
+    v = 1.0 + unit(rng);
+    ss += v;
+  }
+  const double f = 1.2 * sd / ss;
+  for (double& v : s) v *= f;
+  auto* p = new pdhg_instance;
+  const I n = S * T;
+  p->n = n;
+  p->c.resize(n);
+  for (double& v : p->c) v = unit(rng);
+  // A: demand rows (= d_j), row j holds x_ij for every source i.
+  p->a_rows = T;
+  p->a_ptr.resize(T + 1);
+  p->a_idx.resize(n);
+  p->a_val.assign(n, 1.0);
+  for (I j = 0; j <= T; ++j) p->a_ptr[j] = j * S;
+  for (I j = 0; j < T; ++j)
+    for (I i = 0; i < S; ++i) p->a_idx[j * S + i] = i * T + j;
+  p->b = d;
+  // G: supply rows -sum_j x_ij >= -s_i.
+  p->g_rows = S;
+  p->g_ptr.resize(S + 1);
+  p->g_idx.resize(n);
+  p->g_val.assign(n, -1.0);
+  for (I i = 0; i <= S; ++i) p->g_ptr[i] = i * T;
+  for (I k = 0; k < n; ++k) p->g_idx[k] = k;
+  p->h.resize(S);
+  for (I i = 0; i < S; ++i) p->h[i] = -s[i];
+  p->l.assign(n, 0.0);
+  p->u.assign(n, std::numeric_limits<double>::infinity());
+  return p;
+}
+
+template <class F>
+int Guard(char* err, size_t len, F&& f) {
+  try {
+    f();
+    return PDHG_OK;
+  } catch (const std::invalid_argument& e) {
+    if (err && len) std::snprintf(err, len, "%s", e.what());
+    return PDHG_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    if (err && len) std::snprintf(err, len, "%s", e.what());
+    return PDHG_INVALID_ARGUMENT;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int pdhg_gen_random_lp(int64_t m, int64_t n, double density, uint64_t seed, pdhg_instance** out, char* err,
+                       size_t errlen) {
+  return Guard(err, errlen, [&] { *out = RandomLp(m, n, density, seed); });
+}
+
+int pdhg_gen_pagerank(int64_t n_nodes, double damping, int64_t attachment, uint64_t seed, pdhg_instance** out,
+                      char* err, size_t errlen) {
+  return Guard(err, errlen, [&] { *out = Pagerank(n_nodes, damping, attachment, seed); });
+}
+
+int pdhg_gen_transport(int64_t sources, int64_t sinks, uint64_t seed, pdhg_instance** out, char* err,
+                       size_t errlen) {
+  return Guard(err, errlen, [&] { *out = Transport(sources, sinks, seed); });
+}
+
+int pdhg_instance_make_equalities(pdhg_instance* p, int64_t m1, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (p->witness.empty()) throw std::invalid_argument("instance has no witness");
+    if (m1 < 0 || m1 > p->g_rows) throw std::invalid_argument("m1 out of range");
+    if (p->a_rows != 0) throw std::invalid_argument("instance already has equality rows");
+    const I cut = p->g_ptr[m1];
+    p->a_rows = m1;
+    p->a_ptr.assign(p->g_ptr.begin(), p->g_ptr.begin() + m1 + 1);
+    p->a_idx.assign(p->g_idx.begin(), p->g_idx.begin() + cut);
+    p->a_val.assign(p->g_val.begin(), p->g_val.begin() + cut);
+    p->b.resize(m1);
+    CsrMul(p->a_ptr, p->a_idx, p->a_val, p->witness.data(), m1, p->b.data());
+    std::vector<I> gp(p->g_rows - m1 + 1);
+    for (I r = 0; r <= p->g_rows - m1; ++r) gp[r] = p->g_ptr[m1 + r] - cut;
+    p->g_ptr = std::move(gp);
+    p->g_idx.erase(p->g_idx.begin(), p->g_idx.begin() + cut);
+    p->g_val.erase(p->g_val.begin(), p->g_val.begin() + cut);
+    p->h.erase(p->h.begin(), p->h.begin() + m1);
+    p->g_rows -= m1;
+  });
+}
+
+int pdhg_instance_view(const pdhg_instance* p, pdhg_lp* v) {
+  if (!p || !v) return PDHG_INVALID_ARGUMENT;
+  v->a = {p->a_rows, p->n, p->a_ptr.data(), p->a_idx.data(), p->a_val.data()};
+  v->g = {p->g_rows, p->n, p->g_ptr.data(), p->g_idx.data(), p->g_val.data()};
+  v->n = p->n;
+  v->c = p->c.data();
+  v->b = p->b.data();
+  v->h = p->h.data();
+  v->l = p->l.data();
+  v->u = p->u.data();
+  v->objective_offset = p->offset;
+  v->negated_objective = 0;
+  return PDHG_OK;
+}
+
+const double* pdhg_instance_witness(const pdhg_instance* p) {
+  return (p && !p->witness.empty()) ? p->witness.data() : nullptr;
+}
+
+void pdhg_instance_free(pdhg_instance* p) { delete p; }
+
+}  // extern "C"

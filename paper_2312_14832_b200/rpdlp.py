@@ -1,0 +1,460 @@
+"""Python mirror of the reference's solve-path interface (rpdlp, C++).
+
+Names, fields, defaults and error behaviour follow
+/root/reference/proj/core/include/rpdlp/{lp_problem,solver,kkt,scaling}.hpp:
+
+    LpProblem        lp_problem.hpp:33-57   (A eq rows, G >= rows, c, b, h, l, u)
+    SolverParams     solver.hpp:32-55       (+ ScalingConfig, scaling.hpp:40-44)
+    SolveResult      solver.hpp:59-70
+    EvalInfo         solver.hpp:127-140     (observer snapshot)
+    ResidualReport   kkt.hpp:32-41
+    Solve            solver.hpp:145-146     -> pdhg_solve (C-ABI) on a B200
+    NumericalFailure solver.hpp:73-75       (ValueError plays std::invalid_argument)
+
+Everything computes in libpdhg_b200.so; this module only marshals arrays.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import abi
+
+INT64_MAX = (1 << 63) - 1
+kInf = float("inf")
+
+
+class NumericalFailure(RuntimeError):
+    """Non-finite iterate (solver.cpp:391-394)."""
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class SolveStatus(enum.IntEnum):
+    kOptimal = abi.PDHG_OPTIMAL
+    kIterLimit = abi.PDHG_ITER_LIMIT
+    kTimeLimit = abi.PDHG_TIME_LIMIT
+
+
+def ToString(status: SolveStatus) -> str:  # solver.cpp:72-82
+    return {0: "Optimal", 1: "IterLimit", 2: "TimeLimit"}.get(int(status), "Unknown")
+
+
+@dataclass
+class ScalingConfig:
+    enabled: bool = True
+    ruiz_iters: int = 10
+    pc_alpha: float = 1.0
+
+
+@dataclass
+class SolverParams:
+    eps: float = 1e-4
+    time_limit: float = 3600.0
+    iter_limit: int = INT64_MAX
+    sufficient_decay: float = 0.2
+    necessary_decay: float = 0.8
+    long_loop_frac: float = 0.36
+    restart_enabled: bool = True
+    check_every: int = 64
+    scaling: ScalingConfig = field(default_factory=ScalingConfig)
+    seed: int = 0
+    adaptive_step: bool = False
+    log_every: int = 0
+
+    def to_c(self) -> abi.Params:
+        return abi.Params(self.eps, self.time_limit, int(self.iter_limit), self.sufficient_decay,
+                          self.necessary_decay, self.long_loop_frac, int(bool(self.restart_enabled)),
+                          int(self.check_every), int(bool(self.scaling.enabled)), int(self.scaling.ruiz_iters),
+                          self.scaling.pc_alpha, int(self.seed) & ((1 << 64) - 1), int(bool(self.adaptive_step)),
+                          int(self.log_every))
+
+
+@dataclass
+class CsrMatrix:
+    """CSR block with the reference's int64 index layout (sparse_matrix.hpp:94-98)."""
+    rows: int
+    cols: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+
+    @staticmethod
+    def empty(rows: int, cols: int) -> "CsrMatrix":
+        return CsrMatrix(rows, cols, np.zeros(rows + 1, np.int64), np.zeros(0, np.int64), np.zeros(0))
+
+    @staticmethod
+    def from_triplets(rows: int, cols: int, trips) -> "CsrMatrix":
+        """SparseMatrix::FromTriplets (sparse_matrix.cpp:25-69): duplicates are
+        summed in sorted order, exact zeros dropped. Host-side input building."""
+        trips = sorted(((int(r), int(c), float(v)) for r, c, v in trips), key=lambda t: (t[0], t[1]))
+        for r, c, _ in trips:
+            if not (0 <= r < rows and 0 <= c < cols):
+                raise IndexError("triplet index out of range")
+        ptr = np.zeros(rows + 1, np.int64)
+        idx, val = [], []
+        i = 0
+        while i < len(trips):
+            r, c, v = trips[i][0], trips[i][1], 0.0
+            while i < len(trips) and trips[i][0] == r and trips[i][1] == c:
+                v += trips[i][2]
+                i += 1
+            if v != 0.0:
+                idx.append(c)
+                val.append(v)
+                ptr[r + 1] += 1
+        return CsrMatrix(rows, cols, np.cumsum(ptr).astype(np.int64), np.asarray(idx, np.int64),
+                         np.asarray(val, np.float64))
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1]) if self.rows else 0
+
+    def to_c(self) -> abi.Csr:
+        return abi.Csr(self.rows, self.cols, _i64p(self.row_ptr), _i64p(self.col_idx), _dp(self.values))
+
+    def to_dense(self) -> np.ndarray:
+        d = np.zeros((self.rows, self.cols))
+        for r in range(self.rows):
+            for k in range(self.row_ptr[r], self.row_ptr[r + 1]):
+                d[r, self.col_idx[k]] += self.values[k]
+        return d
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(abi.dptr)
+
+
+def _i64p(a: np.ndarray):
+    return a.ctypes.data_as(abi.i64ptr)
+
+
+@dataclass
+class LpProblem:
+    """min c'x  s.t.  A x = b,  G x >= h,  l <= x <= u (lp_problem.hpp:33-45)."""
+    a: CsrMatrix
+    g: CsrMatrix
+    c: np.ndarray
+    b: np.ndarray
+    h: np.ndarray
+    l: np.ndarray
+    u: np.ndarray
+    objective_offset: float = 0.0
+    negated_objective: bool = False
+    name: str = ""
+
+    def __post_init__(self):
+        for m in (self.a, self.g):
+            m.row_ptr, m.col_idx, m.values = _i64(m.row_ptr), _i64(m.col_idx), _f64(m.values)
+        self.c, self.b, self.h, self.l, self.u = map(_f64, (self.c, self.b, self.h, self.l, self.u))
+
+    def num_vars(self) -> int:
+        return len(self.c)
+
+    def num_eq_rows(self) -> int:
+        return self.a.rows
+
+    def num_ineq_rows(self) -> int:
+        return self.g.rows
+
+    def num_rows(self) -> int:
+        return self.a.rows + self.g.rows
+
+    def to_c(self) -> abi.Lp:
+        return abi.Lp(self.a.to_c(), self.g.to_c(), len(self.c), _dp(self.c), _dp(self.b), _dp(self.h),
+                      _dp(self.l), _dp(self.u), float(self.objective_offset), int(bool(self.negated_objective)))
+
+    def nnz(self) -> int:
+        return self.a.nnz + self.g.nnz
+
+
+@dataclass
+class ResidualReport:
+    primal_res: float = 0.0
+    dual_res: float = 0.0
+    gap_abs: float = 0.0
+    primal_obj: float = 0.0
+    dual_obj: float = 0.0
+    rel_primal: float = 0.0
+    rel_dual: float = 0.0
+    rel_gap: float = 0.0
+
+    @staticmethod
+    def from_c(r: abi.Report) -> "ResidualReport":
+        return ResidualReport(*(getattr(r, k) for k, _ in abi.Report._fields_))
+
+
+@dataclass
+class EvalInfo:
+    iteration: int
+    inner_iteration: int
+    restarts: int
+    omega: float
+    eta: float
+    kkt_candidate: float
+    kkt_loop_start: float
+    candidate_is_current: bool
+    restarted: bool
+    original_report: ResidualReport
+    seconds: float
+
+    @staticmethod
+    def from_c(e: abi.EvalInfo) -> "EvalInfo":
+        return EvalInfo(e.iteration, e.inner_iteration, e.restarts, e.omega, e.eta, e.kkt_candidate,
+                        e.kkt_loop_start, bool(e.candidate_is_current), bool(e.restarted),
+                        ResidualReport.from_c(e.original_report), e.seconds)
+
+
+@dataclass
+class SolveResult:
+    status: SolveStatus
+    x: np.ndarray
+    y: np.ndarray
+    lambda_: np.ndarray
+    report: ResidualReport
+    iterations: int
+    restarts: int
+    solve_seconds: float
+    scaling_seconds: float
+
+
+EvalObserver = Callable[[EvalInfo], None]
+
+
+def raise_for(code: int, err: bytes, pending: Optional[BaseException] = None) -> None:
+    if code == abi.PDHG_OK:
+        return
+    if pending is not None:
+        raise pending
+    msg = err.value.decode(errors="replace") if hasattr(err, "value") else str(err)
+    if code == abi.PDHG_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if code == abi.PDHG_NUMERICAL_FAILURE:
+        raise NumericalFailure(msg)
+    raise CudaError(f"code {code}: {msg}")
+
+
+class _Observer:
+    """Trampoline: Python observer -> C callback; exceptions abort the solve
+    and are re-raised after the device state is released."""
+
+    def __init__(self, fn: Optional[EvalObserver], factory=EvalInfo.from_c):
+        self.fn, self.error, self.factory = fn, None, factory
+
+        def cb(info_p, _user):
+            try:
+                self.fn(self.factory(info_p.contents))
+                return 0
+            except BaseException as e:  # noqa: BLE001 - rethrown by raise_for
+                self.error = e
+                return 1
+
+        self.c = abi.EVAL_CB(cb) if fn is not None else abi.EVAL_CB()
+
+
+def _result(problem: LpProblem):
+    n, m = problem.num_vars(), problem.num_rows()
+    x, y, lam = np.empty(n), np.empty(m), np.empty(n)
+    res = abi.Result()
+    res.x, res.y, res.lambda_ = _dp(x), _dp(y), _dp(lam)
+    return res, x, y, lam
+
+
+def _pack(res, x, y, lam) -> SolveResult:
+    return SolveResult(SolveStatus(res.status), x, y, lam, ResidualReport.from_c(res.report), res.iterations,
+                       res.restarts, res.solve_seconds, res.scaling_seconds)
+
+
+def Solve(problem: LpProblem, params: Optional[SolverParams] = None, observer: Optional[EvalObserver] = None,
+          device: int = 0) -> SolveResult:
+    """rpdlp::Solve (solver.cpp:521-543) on a B200 through pdhg_solve."""
+    lib = abi.load()
+    params = params or SolverParams()
+    lp, prm = problem.to_c(), params.to_c()
+    res, x, y, lam = _result(problem)
+    obs = _Observer(observer)
+    err = C.create_string_buffer(abi.ERRLEN)
+    code = lib.pdhg_solve_on(C.byref(lp), C.byref(prm), device, obs.c, None, C.byref(res), err, abi.ERRLEN)
+    raise_for(code, err, obs.error)
+    return _pack(res, x, y, lam)
+
+
+class Session:
+    """Problem resident in HBM (upload + CSC build + device scaling once)."""
+
+    def __init__(self, problem: LpProblem, params: Optional[SolverParams] = None, device: int = 0):
+        self.lib = abi.load()
+        self.problem = problem
+        self.params = params or SolverParams()
+        lp, prm = problem.to_c(), self.params.to_c()
+        self.h = C.c_void_p()
+        err = C.create_string_buffer(abi.ERRLEN)
+        raise_for(self.lib.pdhg_session_create(C.byref(lp), C.byref(prm), device, C.byref(self.h), err,
+                                               abi.ERRLEN), err)
+
+    def close(self):
+        if self.h:
+            self.lib.pdhg_session_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _err(self):
+        return C.create_string_buffer(abi.ERRLEN)
+
+    def solve(self, params: Optional[SolverParams] = None, observer: Optional[EvalObserver] = None) -> SolveResult:
+        prm = (params or self.params).to_c()
+        res, x, y, lam = _result(self.problem)
+        obs = _Observer(observer)
+        err = self._err()
+        code = self.lib.pdhg_session_solve(self.h, C.byref(prm), obs.c, None, C.byref(res), err, abi.ERRLEN)
+        raise_for(code, err, obs.error)
+        return _pack(res, x, y, lam)
+
+    def stats(self) -> abi.SessionStats:
+        s = abi.SessionStats()
+        self.lib.pdhg_session_stats_get(self.h, C.byref(s))
+        return s
+
+    def scaling(self):
+        rs, cs = np.empty(self.problem.num_rows()), np.empty(self.problem.num_vars())
+        err = self._err()
+        raise_for(self.lib.pdhg_session_scaling(self.h, _dp(rs), _dp(cs), err, abi.ERRLEN), err)
+        return rs, cs
+
+    def scaled(self):
+        p = self.problem
+        kv, c, l, u, q = (np.empty(p.nnz()), np.empty(p.num_vars()), np.empty(p.num_vars()),
+                          np.empty(p.num_vars()), np.empty(p.num_rows()))
+        err = self._err()
+        raise_for(self.lib.pdhg_session_scaled(self.h, _dp(kv), _dp(c), _dp(l), _dp(u), _dp(q), err, abi.ERRLEN),
+                  err)
+        return kv, c, l, u, q
+
+    def spmv(self, vec, transpose: bool = False) -> np.ndarray:
+        v = _f64(vec)
+        out = np.empty(self.problem.num_vars() if transpose else self.problem.num_rows())
+        err = self._err()
+        raise_for(self.lib.pdhg_session_spmv(self.h, int(transpose), _dp(v), _dp(out), err, abi.ERRLEN), err)
+        return out
+
+    def opnorm(self, iters: int = 100, seed: int = 0) -> float:
+        o = C.c_double()
+        err = self._err()
+        raise_for(self.lib.pdhg_session_opnorm(self.h, iters, seed, C.byref(o), err, abi.ERRLEN), err)
+        return o.value
+
+    def time_kernels(self, iters: int = 200):
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        err = self._err()
+        raise_for(self.lib.pdhg_session_time_kernels(self.h, iters, C.byref(a), C.byref(b), C.byref(c), err,
+                                                     abi.ERRLEN), err)
+        return a.value, b.value, c.value
+
+
+def PrimalStep(problem: LpProblem, x, y, eta: float, omega: float) -> np.ndarray:
+    """solver.cpp:112-129 on the unscaled problem (device)."""
+    lib = abi.load()
+    lp = problem.to_c()
+    xa, ya, out = _f64(x), _f64(y), np.empty(problem.num_vars())
+    err = C.create_string_buffer(abi.ERRLEN)
+    raise_for(lib.pdhg_primal_step(C.byref(lp), _dp(xa), _dp(ya), eta, omega, _dp(out), err, abi.ERRLEN), err)
+    return out
+
+
+def DualStep(problem: LpProblem, x_new, x_old, y, eta: float, omega: float) -> np.ndarray:
+    """solver.cpp:131-154 on the unscaled problem (device)."""
+    lib = abi.load()
+    lp = problem.to_c()
+    a, b, ya, out = _f64(x_new), _f64(x_old), _f64(y), np.empty(problem.num_rows())
+    err = C.create_string_buffer(abi.ERRLEN)
+    raise_for(lib.pdhg_dual_step(C.byref(lp), _dp(a), _dp(b), _dp(ya), eta, omega, _dp(out), err, abi.ERRLEN), err)
+    return out
+
+
+# ------------------------------------------------------------ generators
+def _from_instance(h: C.c_void_p, name: str) -> LpProblem:
+    lib = abi.load()
+    v = abi.Lp()
+    lib.pdhg_instance_view(h, C.byref(v))
+
+    def arr(p, n, dt):
+        return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True) if n else np.zeros(0, dt)
+
+    def csr(m: abi.Csr) -> CsrMatrix:
+        ptr = arr(m.row_ptr, m.rows + 1, np.int64)
+        nz = int(ptr[-1])
+        return CsrMatrix(m.rows, m.cols, ptr, arr(m.col_idx, nz, np.int64), arr(m.values, nz, np.float64))
+
+    a, g = csr(v.a), csr(v.g)
+    p = LpProblem(a, g, arr(v.c, v.n, np.float64), arr(v.b, a.rows, np.float64), arr(v.h, g.rows, np.float64),
+                  arr(v.l, v.n, np.float64), arr(v.u, v.n, np.float64), v.objective_offset, False, name)
+    w = lib.pdhg_instance_witness(h)
+    p.witness = arr(w, v.n, np.float64) if w else None
+    return p
+
+
+def _gen(fn, *args, name=""):
+    lib = abi.load()
+    h = C.c_void_p()
+    err = C.create_string_buffer(abi.ERRLEN)
+    raise_for(getattr(lib, fn)(*args, C.byref(h), err, abi.ERRLEN), err)
+    return h
+
+
+def GenRandomLp(m: int, n: int, density: float, seed: int, equality_rows: int = 0) -> LpProblem:
+    """instance_gen.cpp:143-188; `equality_rows` moves the first rows of G into
+    A with b = A x_hat."""
+    lib = abi.load()
+    h = _gen("pdhg_gen_random_lp", m, n, density, seed)
+    try:
+        if equality_rows:
+            err = C.create_string_buffer(abi.ERRLEN)
+            raise_for(lib.pdhg_instance_make_equalities(h, equality_rows, err, abi.ERRLEN), err)
+        return _from_instance(h, f"rand_{m}x{n}_s{seed}")
+    finally:
+        lib.pdhg_instance_free(h)
+
+
+def GenPagerank(n_nodes: int, damping: float = 0.85, attachment: int = 3, seed: int = 0) -> LpProblem:
+    """instance_gen.cpp:27-64, 90-141."""
+    lib = abi.load()
+    h = _gen("pdhg_gen_pagerank", n_nodes, damping, attachment, seed)
+    try:
+        return _from_instance(h, "pagerank")
+    finally:
+        lib.pdhg_instance_free(h)
+
+
+def GenTransport(sources: int, sinks: int, seed: int = 1) -> LpProblem:
+    """Transportation LP of SURVEY §8d config 2."""
+    lib = abi.load()
+    h = _gen("pdhg_gen_transport", sources, sinks, seed)
+    try:
+        return _from_instance(h, f"transport_{sources}x{sinks}_s{seed}")
+    finally:
+        lib.pdhg_instance_free(h)

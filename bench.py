@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py -- restarted-PDHG LP solve on B200 (BASELINE.json metric:
+"PDHG iterations/sec and time-to-1e-4 ...; SpMV GB/s vs HBM peak").
+
+A step is one full restarted-PDHG solve to eps=1e-4 of the workload (default
+BASELINE configs[1]: transportation LP, 1000 sources x 1000 sinks, 1M
+variables, 2M nonzeros), problem resident in HBM (upload, CSC build and device
+scaling happen once, outside the timed region -- the reference's
+solve_seconds also excludes scaling). value = PDHG iterations / device
+seconds over K solves (CUDA events on the solver's stream, L2 flushed between
+steps). e2e = the same metric through the public C-ABI entry pdhg_solve with
+pinned host buffers: H2D of the LP, int32 narrowing, CSC build, scaling, the
+solve and D2H of x, y, lambda all inside the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config transport|pagerank|random] [--eps 1e-4]
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+the UNMODIFIED rpdlp sources compiled by oracle/Makefile; else the oracle
+restatement) on rank 0 with a bounded iteration sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "PDHG iterations/sec (restarted PDHG solve to eps)"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------ workloads
+def make_problem(cfg: str, args):
+    from paper_2312_14832_b200 import rpdlp
+    if cfg == "transport":
+        s = args.transport
+        p = rpdlp.GenTransport(s, s, 1)
+        wl = f"transportation LP {s} sources x {s} sinks ({s * s} vars, {2 * s * s} nnz), eps={args.eps:g}"
+    elif cfg == "pagerank":
+        p = rpdlp.GenPagerank(args.pagerank_n, 0.85, 6, 1)
+        wl = f"PageRank LP n={args.pagerank_n} attachment=6 (GenPagerank seed 1), eps={args.eps:g}"
+    elif cfg == "random":
+        p = rpdlp.GenRandomLp(1000, 2000, 0.005, 1, equality_rows=300)
+        wl = f"random LP 1000x2000 0.5% (300 eq rows, boxed), eps={args.eps:g}"
+    else:
+        raise SystemExit(f"unknown config {cfg}")
+    return p, wl
+
+
+def algorithmic_bytes(m: int, n: int, nnz: int):
+    """per-kernel algorithmic bytes (int32 idx, f64 values).
+    K-CSC primal: 12 nnz (idx+val) + 4(n+1) ptr + 8 m (y gathered once)
+                  + 56 n (x, c, l, u, xbar read; x+, xbar written).
+    K-CSR dual:   12 nnz + 4(m+1) + 8 n (x+ gathered once)
+                  + 56 m (y, kx, q, ybar read; y+, kx+, ybar written)."""
+    primal = 12 * nnz + 4 * (n + 1) + 8 * m + 56 * n
+    dual = 12 * nnz + 4 * (m + 1) + 8 * n + 56 * m
+    return primal, dual, 24 * nnz + 68 * (m + n) + 8
+
+
+# ------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.proc, self.path = device, None, None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- distributed
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = td
+    return world, rank, local, dist
+
+
+def max_over_ranks(dist, local, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(dist, local, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(dist, local):
+    if dist is not None:
+        import torch
+        dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(local)
+
+
+# -------------------------------------------------------------- CPU baseline
+def cpu_iter_rate(problem, eps: float, budget_s: float):
+    """Reference CPU it/s on a bounded sample: iterations / (solve_seconds of
+    an iter_limit=S run minus that of an iter_limit=0 run, which isolates the
+    power iteration and the start-point evaluation)."""
+    from oracle import oracle
+    from paper_2312_14832_b200.rpdlp import SolverParams
+    chk = oracle.cpu_baseline()
+    kind = "reference" if chk is oracle.reference() else "port"
+    r0 = chk.solve(problem, SolverParams(eps=eps, iter_limit=0))
+    probe = 64
+    r1 = chk.solve(problem, SolverParams(eps=eps, iter_limit=probe))
+    per_it = max((r1.solve_seconds - r0.solve_seconds) / max(r1.iterations, 1), 1e-7)
+    sample = int(max(64, min(200000, budget_s / per_it)))
+    sample = (sample // 64) * 64 or 64
+    r2 = chk.solve(problem, SolverParams(eps=eps, iter_limit=sample))
+    dt = max(r2.solve_seconds - r0.solve_seconds, 1e-9)
+    return {"value": r2.iterations / dt, "unit": "it/s", "cores": 1, "kind": kind,
+            "sample": f"{r2.iterations} PDHG iterations (iter_limit={sample}, status={int(r2.status)}) of the same "
+                      f"instance; it/s = iterations / (solve_seconds - solve_seconds at iter_limit=0); "
+                      f"scaling {r2.scaling_seconds:.2f}s excluded; serial reference, 1 thread",
+            "host": platform.processor() or platform.machine(), "nproc": os.cpu_count(),
+            "setup_seconds": r0.solve_seconds}
+
+
+# --------------------------------------------------------------------- arms
+def run_reference(args, world, rank, local, dist):
+    if rank != 0:
+        return 0
+    problem, workload = make_problem(args.config, args)
+    from oracle import oracle
+    from paper_2312_14832_b200.rpdlp import SolverParams
+    chk = oracle.cpu_baseline()
+    kind = "reference" if chk is oracle.reference() else "port"
+    r0 = chk.solve(problem, SolverParams(eps=args.eps, iter_limit=0))
+    per = args.ref_iters
+    for _ in range(args.warmup):
+        chk.solve(problem, SolverParams(eps=args.eps, iter_limit=64))
+    times, iters = [], 0
+    for _ in range(args.steps):
+        r = chk.solve(problem, SolverParams(eps=args.eps, iter_limit=per))
+        times.append(max(r.solve_seconds - r0.solve_seconds, 1e-9))
+        iters += r.iterations
+    tot = sum(times)
+    value = iters / tot
+    line = {"metric": METRIC, "value": value, "unit": "it/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload, "m": problem.num_rows(), "n": problem.num_vars(),
+                                            "nnz": problem.nnz(), "eps": args.eps,
+                                            "sample_iterations_per_step": per},
+            "cpu_baseline": {"value": value, "unit": "it/s", "cores": 1, "kind": kind,
+                             "sample": f"{per} PDHG iterations per step of the same instance (serial reference, "
+                                       f"1 thread); power iteration/start evaluation subtracted"},
+            "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def pinned_copy(problem):
+    """The LP's arrays in page-locked host memory (H2D from pinned buffers)."""
+    import torch
+    from paper_2312_14832_b200.rpdlp import CsrMatrix, LpProblem
+
+    def pin(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        return t.numpy(), t
+
+    keep = []
+
+    def P(a):
+        arr, t = pin(a)
+        keep.append(t)
+        return arr
+
+    def csr(m):
+        return CsrMatrix(m.rows, m.cols, P(m.row_ptr), P(m.col_idx), P(m.values))
+
+    q = LpProblem(csr(problem.a), csr(problem.g), P(problem.c), P(problem.b), P(problem.h), P(problem.l),
+                  P(problem.u), problem.objective_offset)
+    q._pinned = keep
+    return q
+
+
+def load_traffic(config: str, kernel: str):
+    f = ROOT / "profiles" / "ncu_summary.json"
+    if not f.exists():
+        return None
+    try:
+        d = json.loads(f.read_text())
+        return d.get(config, {}).get(kernel, {}).get("dram_bytes_per_launch")
+    except (ValueError, AttributeError):
+        return None
+
+
+def run_ours(args, world, rank, local, dist):
+    from paper_2312_14832_b200 import rpdlp
+    from paper_2312_14832_b200.rpdlp import Session, SolverParams
+
+    peaks = {}
+    pf = ROOT / "MEASURED_PEAKS.json"
+    if pf.exists():
+        peaks = json.loads(pf.read_text())
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    t0 = time.time()
+    problem, workload = make_problem(args.config, args)
+    log(f"[rank {rank}] built {workload} in {time.time() - t0:.1f}s: m={problem.num_rows()} n={problem.num_vars()} "
+        f"nnz={problem.nnz()}")
+    params = SolverParams(eps=args.eps)
+    m, n, nnz = problem.num_rows(), problem.num_vars(), problem.nnz()
+
+    sess = Session(problem, params, device=local)
+    st = sess.stats()
+    log(f"[rank {rank}] session: upload {st.upload_seconds:.3f}s scaling {st.scaling_seconds:.3f}s "
+        f"tiles csr={st.csr_tiles} csc={st.csc_tiles} device bytes={st.device_bytes / 1e9:.2f} GB")
+    for _ in range(args.warmup):
+        r = sess.solve(params)
+    log(f"[rank {rank}] warmup solve: status={int(r.status)} iterations={r.iterations} restarts={r.restarts} "
+        f"obj={r.report.primal_obj:.10g}")
+
+    clocks = ClockSampler(local)
+    barrier(dist, local)
+    clocks.start()
+    dev_ms, iters, launches = 0.0, 0, 0
+    statuses = []
+    for _ in range(args.steps):
+        sess.flush_l2()
+        r = sess.solve(params)
+        ms, nl = sess.last_solve()
+        dev_ms += ms
+        iters += r.iterations
+        launches += nl
+        statuses.append(int(r.status))
+    barrier(dist, local)
+    clk = clocks.stop()
+
+    t_max = max_over_ranks(dist, local, dev_ms / 1e3)
+    tot_iters = sum_over_ranks(dist, local, float(iters))
+    value = tot_iters / t_max
+
+    # Per-kernel roofline (K-CSC primal / K-CSR dual), events on the solver stream.
+    ms_p, ms_d, ms_it = sess.time_kernels(args.kernel_iters)
+    b_p, b_d, b_it = algorithmic_bytes(m, n, nnz)
+    dom = "pdhg_primal_csc" if ms_p >= ms_d else "pdhg_dual_csr"
+    b_dom, ms_dom = (b_p, ms_p) if ms_p >= ms_d else (b_d, ms_d)
+    achieved = b_dom / (ms_dom * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                "traffic": load_traffic(args.config, dom), "kernel": dom, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": b_dom, "ms_per_launch": ms_dom,
+                "primal_csc": {"ms": ms_p, "bytes": b_p, "gbs": b_p / (ms_p * 1e-3) / 1e9},
+                "dual_csr": {"ms": ms_d, "bytes": b_d, "gbs": b_d / (ms_d * 1e-3) / 1e9},
+                "iteration": {"ms": ms_it, "bytes": b_it, "gbs": b_it / (ms_it * 1e-3) / 1e9,
+                              "it_per_s": 1e3 / ms_it},
+                "l2_resident_working_set": bool(st.l2_resident)}
+    sess.close()
+
+    # End to end through the public C-ABI, pinned host buffers.
+    pinned = pinned_copy(problem)
+    e2e_t, e2e_it = 0.0, 0
+    for _ in range(max(1, args.e2e_steps)):
+        ts = time.perf_counter()
+        r = rpdlp.Solve(pinned, params, device=local)
+        e2e_t += time.perf_counter() - ts
+        e2e_it += r.iterations
+    e2e_t = max_over_ranks(dist, local, e2e_t)
+    e2e_it = sum_over_ranks(dist, local, float(e2e_it))
+    h2d = sum(a.nbytes for a in (problem.a.row_ptr, problem.a.col_idx, problem.a.values, problem.g.row_ptr,
+                                 problem.g.col_idx, problem.g.values, problem.c, problem.b, problem.h, problem.l,
+                                 problem.u))
+    d2h = 8 * (2 * n + m)
+
+    if rank != 0:
+        return 0
+    cpu = None
+    if not args.no_cpu:
+        log("[rank 0] timing the CPU reference sample ...")
+        cpu = cpu_iter_rate(problem, args.eps, args.cpu_budget)
+    line = {
+        "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "m": m, "n": n, "nnz": nnz, "eps": args.eps,
+                   "step": "one full solve to eps on the resident scaled problem (power iteration included)",
+                   "l2_flush": "2x L2 written between timed steps",
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "iterations_per_solve": iters // max(args.steps, 1),
+                   "statuses": sorted(set(statuses))},
+        "time_to_eps_s": t_max / args.steps,
+        "e2e": {"value": e2e_it / e2e_t, "unit": "it/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h,
+                "seconds_per_solve": e2e_t / max(1, args.e2e_steps), "entry": "pdhg_solve_on (C-ABI)"},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="transport", choices=["transport", "pagerank", "random"])
+    ap.add_argument("--eps", type=float, default=1e-4)
+    ap.add_argument("--transport", type=int, default=1000)
+    ap.add_argument("--pagerank-n", type=int, default=1_000_000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--kernel-iters", type=int, default=256)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-iters", type=int, default=192)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        log("note: warmup < 3 violates the timing rules; using 3")
+        args.warmup = 3
+    world, rank, local, dist = dist_setup()
+    try:
+        if args.impl == "reference":
+            return run_reference(args, world, rank, local, dist)
+        return run_ours(args, world, rank, local, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -213,6 +213,28 @@ int pdhg_dual_step(const pdhg_lp* lp, const double* x_new,
                    const double* x_old, const double* y, double eta,
                    double omega, double* out, char* err, size_t errlen);
 
+/* ---- bench instrumentation ------------------------------------------------
+ * flush_l2 writes a buffer of twice the L2 size on the session stream.
+ * last_solve reports the device time of the most recent pdhg_session_solve
+ * (CUDA events on the session stream bracketing the whole solve, power
+ * iteration included) and how many kernels it launched (graph nodes
+ * counted individually). */
+int pdhg_session_flush_l2(pdhg_session* s, char* err, size_t errlen);
+int pdhg_session_last_solve(pdhg_session* s, double* device_ms,
+                            int64_t* kernel_launches);
+
+/* ---- host decision logic (pure host code, no device) -----------------------
+ * ShouldRestart (solver.cpp:178-189), UpdatePrimalWeight (solver.cpp:191-196),
+ * KktError (kkt.cpp:153-157), CheckTermination (kkt.cpp:147-151): the exact
+ * functions the solve loop uses, exported for unit tests and API parity. */
+int pdhg_should_restart(const pdhg_params* p, int64_t t, int64_t k,
+                        double kkt_candidate, double kkt_loop_start,
+                        double kkt_prev_candidate);
+double pdhg_update_primal_weight(double omega, double dx_norm, double dy_norm);
+double pdhg_kkt_error(double primal_res, double dual_res, double gap,
+                      double omega);
+int pdhg_check_termination(const pdhg_report* r, double eps);
+
 /* ---- instance generators (instance_gen.hpp:39-59 + SURVEY §8d shapes) ----
  * Host-side input builders; they own their arrays until freed. */
 typedef struct pdhg_instance pdhg_instance;

@@ -31,10 +31,12 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # elementwise updates and row sums.
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "--expt-relaxed-constexpr",
                   "-Xcompiler", "-fPIC,-O3", "-I", str(ROOT / "include")]
-CXXFLAGS = ["-std=c++17", "-O3", "-fPIC", "-Wall", "-Wextra", "-I", str(ROOT / "include")]
+CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", "-I", str(ROOT / "include")]
 
 CU_SRCS = ["session.cu", "abi.cu"]
-CPP_SRCS = ["instance_gen.cpp"]
+CPP_SRCS = ["instance_gen.cpp", "rpdlp_api.cpp"]
+DROPIN_TEST = ROOT / "tests" / "cpp" / "drop_in_test.cpp"
+DROPIN_BIN = BUILD / "drop_in_test"
 HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh"]
 
 
@@ -66,7 +68,7 @@ def build_product(force: bool = False, ptxas_verbose: bool = False) -> Path:
     for s in CPP_SRCS:
         o = BUILD / (s + ".o")
         objs.append(o)
-        if force or not _newer(o, [CSRC / s, ROOT / "include" / "pdhg.h"]):
+        if force or not _newer(o, [CSRC / s, ROOT / "include" / "pdhg.h"] + sorted((ROOT / "include" / "rpdlp").glob("*.hpp"))):
             jobs.append([CXX] + CXXFLAGS + ["-c", str(CSRC / s), "-o", str(o)])
     logs = []
     with cf.ThreadPoolExecutor(max_workers=max(1, len(jobs))) as ex:
@@ -76,6 +78,10 @@ def build_product(force: bool = False, ptxas_verbose: bool = False) -> Path:
         print("\n".join(l for l in logs if l.strip()))
     if force or jobs or not _newer(LIB, objs):
         _run([NVCC] + ARCH + ["-shared", "-o", str(LIB)] + [str(o) for o in objs] + ["-lcuda"])
+    # Reference-style C++ caller linked against the drop-in headers + library.
+    if force or not _newer(DROPIN_BIN, [DROPIN_TEST, LIB]):
+        _run([CXX] + CXXFLAGS + [str(DROPIN_TEST), "-o", str(DROPIN_BIN), "-L", str(PKG), "-lpdhg_b200",
+                                 f"-Wl,-rpath,$ORIGIN/.."])
     return LIB
 
 

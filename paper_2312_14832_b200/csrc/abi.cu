@@ -9,6 +9,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "host_logic.h"
 #include "session.cuh"
 
 struct pdhg_session {
@@ -187,6 +188,29 @@ int pdhg_session_time_kernels(pdhg_session* s, int iters, double* ms_primal, dou
     S(s).TimeKernels(iters, ms_primal, ms_dual, ms_iter);
   });
 }
+
+int pdhg_session_flush_l2(pdhg_session* s, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] { S(s).FlushL2(); });
+}
+
+int pdhg_session_last_solve(pdhg_session* s, double* device_ms, int64_t* kernel_launches) {
+  return Guard(nullptr, 0, [&] {
+    *device_ms = S(s).last_device_ms();
+    *kernel_launches = S(s).last_launches();
+  });
+}
+
+int pdhg_should_restart(const pdhg_params* p, int64_t t, int64_t k, double cand, double start, double prev) {
+  return pdhg::ShouldRestart(*p, t, k, cand, start, prev) ? 1 : 0;
+}
+
+double pdhg_update_primal_weight(double omega, double dx, double dy) {
+  return pdhg::UpdatePrimalWeight(omega, dx, dy);
+}
+
+double pdhg_kkt_error(double p, double d, double g, double w) { return pdhg::KktError(p, d, g, w); }
+
+int pdhg_check_termination(const pdhg_report* r, double eps) { return pdhg::Terminated(*r, eps) ? 1 : 0; }
 
 int pdhg_primal_step(const pdhg_lp* lp, const double* x, const double* y, double eta, double omega, double* out,
                      char* err, size_t errlen) {

@@ -1,0 +1,53 @@
+// Host-side decision logic of the solve loop, shared by the session and the
+// C-ABI exports. Restated from the reference (file:line per function).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#include "../../include/pdhg.h"
+
+namespace pdhg {
+
+// KktError (kkt.cpp:153-157).
+inline double KktError(double p, double d, double g, double w) {
+  return std::sqrt(w * w * p * p + d * d / (w * w) + g * g);
+}
+inline double Kkt1(const pdhg_report& r) { return KktError(r.primal_res, r.dual_res, r.gap_abs, 1.0); }
+
+// CheckTermination (kkt.cpp:147-151).
+inline bool Terminated(const pdhg_report& r, double eps) {
+  return r.rel_primal <= eps && r.rel_dual <= eps && r.rel_gap <= eps;
+}
+
+// ShouldRestart (solver.cpp:178-189): sufficient decay; necessary decay with
+// no local progress; long inner loop.
+inline bool ShouldRestart(const pdhg_params& p, int64_t t, int64_t k, double cand, double start, double prev) {
+  if (cand <= p.sufficient_decay * start) return true;
+  if (cand <= p.necessary_decay * start && cand > prev) return true;
+  return static_cast<double>(t) >= p.long_loop_frac * static_cast<double>(k);
+}
+
+// UpdatePrimalWeight (solver.cpp:191-196).
+inline double UpdatePrimalWeight(double w, double dx, double dy) {
+  constexpr double kMin = 1e-10;
+  if (dx <= kMin || dy <= kMin) return w;
+  return std::exp(0.5 * std::log(dy / dx) + 0.5 * std::log(w));
+}
+
+// ResidualReport from reduced sums (kkt.cpp:80-118).
+inline pdhg_report MakeReport(double pr2, double du2, double bound, double cx, double qy, double off, double qn,
+                              double cn) {
+  pdhg_report r{};
+  r.primal_res = std::sqrt(pr2);
+  r.dual_res = std::sqrt(du2);
+  r.primal_obj = off + cx;
+  r.dual_obj = off + bound + qy;
+  r.gap_abs = std::abs(r.dual_obj - r.primal_obj);
+  r.rel_primal = r.primal_res / (1.0 + qn);
+  r.rel_dual = r.dual_res / (1.0 + cn);
+  r.rel_gap = r.gap_abs / (1.0 + std::abs(r.dual_obj) + std::abs(r.primal_obj));
+  return r;
+}
+
+}  // namespace pdhg

@@ -1,0 +1,419 @@
+// C++ drop-in layer (include/rpdlp/*.hpp) over the C-ABI (include/pdhg.h).
+//
+// Problem-building storage (FromTriplets, VStack, StackK, Validate) stays on
+// the host, with the reference's semantics (sparse_matrix.cpp:25-112,
+// lp_problem.cpp:22-83). Solve, EstimateOpNorm, PrimalStep and DualStep run
+// on the device through pdhg_*; C-ABI codes are rethrown as the reference's
+// exception types.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+
+#include "pdhg.h"
+#include "rpdlp/solver.hpp"
+
+namespace rpdlp {
+
+// ------------------------------------------------------------ SparseMatrix
+SparseMatrix SparseMatrix::FromTriplets(Index n_rows, Index n_cols, std::vector<Triplet> t) {
+  if (n_rows < 0 || n_cols < 0) throw std::invalid_argument("negative matrix dimension");
+  for (const Triplet& e : t)
+    if (e.row < 0 || e.row >= n_rows || e.col < 0 || e.col >= n_cols)
+      throw std::out_of_range("triplet index out of range");
+  std::sort(t.begin(), t.end(),
+            [](const Triplet& a, const Triplet& b) { return std::tie(a.row, a.col) < std::tie(b.row, b.col); });
+  SparseMatrix m;
+  m.rows_ = n_rows;
+  m.cols_ = n_cols;
+  m.rp_.assign(n_rows + 1, 0);
+  for (size_t i = 0; i < t.size();) {
+    const Index r = t[i].row, c = t[i].col;
+    double v = 0.0;
+    for (; i < t.size() && t[i].row == r && t[i].col == c; ++i) v += t[i].value;
+    if (v != 0.0) {
+      m.ci_.push_back(c);
+      m.val_.push_back(v);
+      ++m.rp_[r + 1];
+    }
+  }
+  for (Index r = 0; r < n_rows; ++r) m.rp_[r + 1] += m.rp_[r];
+  m.BuildColumns();
+  return m;
+}
+
+void SparseMatrix::BuildColumns() {
+  cp_.assign(cols_ + 1, 0);
+  ri_.assign(val_.size(), 0);
+  cval_.assign(val_.size(), 0.0);
+  for (Index j : ci_) ++cp_[j + 1];
+  for (Index j = 0; j < cols_; ++j) cp_[j + 1] += cp_[j];
+  std::vector<Index> fill(cp_.begin(), cp_.end() - 1);
+  for (Index r = 0; r < rows_; ++r)
+    for (Index k = rp_[r]; k < rp_[r + 1]; ++k) {
+      const Index slot = fill[ci_[k]]++;
+      ri_[slot] = r;
+      cval_[slot] = val_[k];
+    }
+}
+
+SparseMatrix SparseMatrix::VStack(const SparseMatrix& top, const SparseMatrix& bottom) {
+  if (top.cols() != bottom.cols()) throw std::invalid_argument("VStack: column count mismatch");
+  SparseMatrix m;
+  m.rows_ = top.rows_ + bottom.rows_;
+  m.cols_ = top.cols_;
+  m.rp_ = top.rp_;
+  for (size_t i = 1; i < bottom.rp_.size(); ++i) m.rp_.push_back(bottom.rp_[i] + top.nnz());
+  m.ci_ = top.ci_;
+  m.ci_.insert(m.ci_.end(), bottom.ci_.begin(), bottom.ci_.end());
+  m.val_ = top.val_;
+  m.val_.insert(m.val_.end(), bottom.val_.begin(), bottom.val_.end());
+  m.BuildColumns();
+  return m;
+}
+
+SparseMatrix SparseMatrix::RowSlice(Index begin, Index end) const {
+  if (!(0 <= begin && begin <= end && end <= rows_)) throw std::out_of_range("RowSlice range");
+  SparseMatrix m;
+  m.rows_ = end - begin;
+  m.cols_ = cols_;
+  const Index base = rp_[begin];
+  m.rp_.assign(1, 0);
+  for (Index r = begin; r < end; ++r) m.rp_.push_back(rp_[r + 1] - base);
+  m.ci_.assign(ci_.begin() + base, ci_.begin() + rp_[end]);
+  m.val_.assign(val_.begin() + base, val_.begin() + rp_[end]);
+  m.BuildColumns();
+  return m;
+}
+
+std::vector<Triplet> SparseMatrix::ToTriplets() const {
+  std::vector<Triplet> out;
+  out.reserve(val_.size());
+  for (Index r = 0; r < rows_; ++r)
+    for (Index k = rp_[r]; k < rp_[r + 1]; ++k) out.push_back({r, ci_[k], val_[k]});
+  return out;
+}
+
+// --------------------------------------------------------------- LpProblem
+void LpProblem::Validate() const {
+  const Index n = num_vars();
+  if (a.cols() != n || g.cols() != n) throw std::invalid_argument("matrix column count does not match c");
+  if (static_cast<Index>(b.size()) != a.rows()) throw std::invalid_argument("b length does not match A row count");
+  if (static_cast<Index>(h.size()) != g.rows()) throw std::invalid_argument("h length does not match G row count");
+  if (static_cast<Index>(l.size()) != n || static_cast<Index>(u.size()) != n)
+    throw std::invalid_argument("bound vector length does not match c");
+  auto nan_in = [](const std::vector<double>& v, const char* what) {
+    for (double x : v)
+      if (std::isnan(x)) throw std::invalid_argument(std::string("NaN in ") + what);
+  };
+  nan_in(c, "c");
+  nan_in(b, "b");
+  nan_in(h, "h");
+  for (double x : c)
+    if (std::isinf(x)) throw std::invalid_argument("infinite entry in c");
+  for (Index i = 0; i < n; ++i) {
+    if (std::isnan(l[i]) || std::isnan(u[i])) throw std::invalid_argument("NaN bound");
+    if (l[i] > u[i]) throw std::invalid_argument("crossed bounds: l > u at index " + std::to_string(i));
+  }
+}
+
+BoundClass ClassifyBound(double lower, double upper) {
+  const bool lo = std::isfinite(lower), hi = std::isfinite(upper);
+  if (lo && hi) return BoundClass::kBoxed;
+  if (lo) return BoundClass::kLowerOnly;
+  if (hi) return BoundClass::kUpperOnly;
+  return BoundClass::kFree;
+}
+
+std::vector<BoundClass> ClassifyBounds(const LpProblem& p) {
+  std::vector<BoundClass> out;
+  out.reserve(p.l.size());
+  for (size_t i = 0; i < p.l.size(); ++i) out.push_back(ClassifyBound(p.l[i], p.u[i]));
+  return out;
+}
+
+std::pair<SparseMatrix, std::vector<double>> StackK(const LpProblem& p) {
+  std::vector<double> q = p.b;
+  q.insert(q.end(), p.h.begin(), p.h.end());
+  return {SparseMatrix::VStack(p.a, p.g), std::move(q)};
+}
+
+// ------------------------------------------------------------- host helpers
+bool CheckTermination(const ResidualReport& r, double eps) {
+  return r.rel_primal <= eps && r.rel_dual <= eps && r.rel_gap <= eps;
+}
+
+double KktError(double p, double d, double g, double w) { return pdhg_kkt_error(p, d, g, w); }
+
+namespace {
+
+pdhg_params ToC(const SolverParams& s) {
+  pdhg_params p;
+  p.eps = s.eps;
+  p.time_limit = s.time_limit;
+  p.iter_limit = s.iter_limit;
+  p.sufficient_decay = s.sufficient_decay;
+  p.necessary_decay = s.necessary_decay;
+  p.long_loop_frac = s.long_loop_frac;
+  p.restart_enabled = s.restart_enabled;
+  p.check_every = s.check_every;
+  p.scaling_enabled = s.scaling.enabled;
+  p.ruiz_iters = s.scaling.ruiz_iters;
+  p.pc_alpha = s.scaling.pc_alpha;
+  p.seed = s.seed;
+  p.adaptive_step = s.adaptive_step;
+  p.log_every = s.log_every;
+  return p;
+}
+
+pdhg_csr View(const SparseMatrix& m) {
+  return {m.rows(), m.cols(), m.row_ptr().data(), m.col_idx().data(), m.csr_values().data()};
+}
+
+pdhg_lp View(const LpProblem& p) {
+  pdhg_lp v{};
+  v.a = View(p.a);
+  v.g = View(p.g);
+  v.n = p.num_vars();
+  v.c = p.c.data();
+  v.b = p.b.data();
+  v.h = p.h.data();
+  v.l = p.l.data();
+  v.u = p.u.data();
+  v.objective_offset = p.objective_offset;
+  v.negated_objective = p.negated_objective;
+  return v;
+}
+
+ResidualReport FromC(const pdhg_report& r) {
+  return {r.primal_res, r.dual_res, r.gap_abs, r.primal_obj, r.dual_obj, r.rel_primal, r.rel_dual, r.rel_gap};
+}
+
+[[noreturn]] void Rethrow(int code, const char* msg) {
+  switch (code) {
+    case PDHG_INVALID_ARGUMENT:
+      throw std::invalid_argument(msg);
+    case PDHG_NUMERICAL_FAILURE:
+      throw NumericalFailure(msg);
+    default:
+      throw DeviceError(std::string("libpdhg_b200: ") + msg);
+  }
+}
+
+int Device() {
+  const char* d = std::getenv("PDHG_DEVICE");
+  return d ? std::atoi(d) : 0;
+}
+
+struct ObserverCtx {
+  const EvalObserver* fn;
+  std::exception_ptr error;
+};
+
+int Trampoline(const pdhg_eval_info* c, void* user) {
+  auto* ctx = static_cast<ObserverCtx*>(user);
+  try {
+    EvalInfo e;
+    e.iteration = c->iteration;
+    e.inner_iteration = c->inner_iteration;
+    e.restarts = c->restarts;
+    e.omega = c->omega;
+    e.eta = c->eta;
+    e.kkt_candidate = c->kkt_candidate;
+    e.kkt_loop_start = c->kkt_loop_start;
+    e.candidate_is_current = c->candidate_is_current != 0;
+    e.restarted = c->restarted != 0;
+    e.original_report = FromC(c->original_report);
+    e.seconds = c->seconds;
+    (*ctx->fn)(e);
+    return 0;
+  } catch (...) {
+    ctx->error = std::current_exception();
+    return 1;
+  }
+}
+
+}  // namespace
+
+void SolverParams::Validate() const {
+  const pdhg_params p = ToC(*this);
+  if (p.eps <= 0.0) throw std::invalid_argument("eps must be positive");
+  if (!(0.0 < sufficient_decay && sufficient_decay < necessary_decay && necessary_decay < 1.0))
+    throw std::invalid_argument("restart decay constants out of order");
+  if (!(0.0 < long_loop_frac && long_loop_frac < 1.0)) throw std::invalid_argument("long_loop_frac must lie in (0, 1)");
+  if (check_every < 1) throw std::invalid_argument("check_every must be >= 1");
+  if (iter_limit < 0) throw std::invalid_argument("negative iter_limit");
+}
+
+std::string ToString(SolveStatus s) {
+  switch (s) {
+    case SolveStatus::kOptimal:
+      return "Optimal";
+    case SolveStatus::kIterLimit:
+      return "IterLimit";
+    case SolveStatus::kTimeLimit:
+      return "TimeLimit";
+  }
+  return "Unknown";
+}
+
+bool ShouldRestart(const SolverParams& params, Index t, Index k, double cand, double start, double prev) {
+  const pdhg_params p = ToC(params);
+  return pdhg_should_restart(&p, t, k, cand, start, prev) != 0;
+}
+
+double UpdatePrimalWeight(double omega, double dx, double dy) { return pdhg_update_primal_weight(omega, dx, dy); }
+
+void RunningAverage::Add(std::span<const double> x, std::span<const double> y) {
+  const double w = weight_;
+  for (size_t j = 0; j < x_.size(); ++j) x_[j] = (w * x_[j] + x[j]) / (w + 1.0);
+  for (size_t i = 0; i < y_.size(); ++i) y_[i] = (w * y_[i] + y[i]) / (w + 1.0);
+  weight_ = w + 1.0;
+}
+
+void RunningAverage::Reset() {
+  std::fill(x_.begin(), x_.end(), 0.0);
+  std::fill(y_.begin(), y_.end(), 0.0);
+  weight_ = 0.0;
+}
+
+SolveResult Solve(const LpProblem& problem, const SolverParams& params, const EvalObserver& observer) {
+  problem.Validate();
+  params.Validate();
+  const pdhg_lp lp = View(problem);
+  const pdhg_params prm = ToC(params);
+  SolveResult r;
+  r.x.resize(problem.num_vars());
+  r.y.resize(problem.num_rows());
+  r.lambda.resize(problem.num_vars());
+  pdhg_result out{};
+  out.x = r.x.data();
+  out.y = r.y.data();
+  out.lambda = r.lambda.data();
+  ObserverCtx ctx{&observer, nullptr};
+  char err[512] = {0};
+  const int code = pdhg_solve_on(&lp, &prm, Device(), observer ? Trampoline : nullptr, &ctx, &out, err, sizeof(err));
+  if (ctx.error) std::rethrow_exception(ctx.error);
+  if (code != PDHG_OK) Rethrow(code, err);
+  r.status = static_cast<SolveStatus>(out.status);
+  r.report = FromC(out.report);
+  r.iterations = out.iterations;
+  r.restarts = out.restarts;
+  r.solve_seconds = out.solve_seconds;
+  r.scaling_seconds = out.scaling_seconds;
+  return r;
+}
+
+double EstimateOpNorm(const SparseMatrix& k, int iters, std::uint64_t seed) {
+  if (iters < 1) throw std::invalid_argument("iters must be >= 1");
+  LpProblem p;
+  p.a = SparseMatrix::FromTriplets(0, k.cols(), {});
+  p.g = k;
+  p.c.assign(k.cols(), 0.0);
+  p.h.assign(k.rows(), 0.0);
+  p.l.assign(k.cols(), 0.0);
+  p.u.assign(k.cols(), 1.0);
+  const pdhg_lp lp = View(p);
+  pdhg_params prm;
+  pdhg_params_default(&prm);
+  prm.scaling_enabled = 0;
+  pdhg_session* s = nullptr;
+  char err[512] = {0};
+  int code = pdhg_session_create(&lp, &prm, Device(), &s, err, sizeof(err));
+  if (code != PDHG_OK) Rethrow(code, err);
+  double out = 0.0;
+  code = pdhg_session_opnorm(s, iters, seed, &out, err, sizeof(err));
+  pdhg_session_destroy(s);
+  if (code != PDHG_OK) Rethrow(code, err);
+  return out;
+}
+
+std::vector<double> PrimalStep(const LpProblem& problem, std::span<const double> x, std::span<const double> y,
+                               double eta, double omega) {
+  const pdhg_lp lp = View(problem);
+  std::vector<double> out(problem.num_vars());
+  char err[512] = {0};
+  const int code = pdhg_primal_step(&lp, x.data(), y.data(), eta, omega, out.data(), err, sizeof(err));
+  if (code != PDHG_OK) Rethrow(code, err);
+  return out;
+}
+
+std::vector<double> DualStep(const LpProblem& problem, std::span<const double> x_new, std::span<const double> x_old,
+                             std::span<const double> y, double eta, double omega) {
+  const pdhg_lp lp = View(problem);
+  std::vector<double> out(problem.num_rows());
+  char err[512] = {0};
+  const int code =
+      pdhg_dual_step(&lp, x_new.data(), x_old.data(), y.data(), eta, omega, out.data(), err, sizeof(err));
+  if (code != PDHG_OK) Rethrow(code, err);
+  return out;
+}
+
+}  // namespace rpdlp
+
+// ------------------------------------------------------------- generators
+#include "rpdlp/instance_gen.hpp"
+
+namespace rpdlp {
+namespace {
+
+SparseMatrix FromCsr(const pdhg_csr& c) {
+  std::vector<Triplet> t;
+  const Index nz = c.rows ? c.row_ptr[c.rows] : 0;
+  t.reserve(nz);
+  for (Index r = 0; r < c.rows; ++r)
+    for (Index k = c.row_ptr[r]; k < c.row_ptr[r + 1]; ++k) t.push_back({r, c.col_idx[k], c.values[k]});
+  return SparseMatrix::FromTriplets(c.rows, c.cols, std::move(t));
+}
+
+LpProblem Take(pdhg_instance* inst, std::vector<double>* witness) {
+  pdhg_lp v{};
+  pdhg_instance_view(inst, &v);
+  LpProblem p;
+  p.a = FromCsr(v.a);
+  p.g = FromCsr(v.g);
+  p.c.assign(v.c, v.c + v.n);
+  p.b.assign(v.b, v.b + v.a.rows);
+  p.h.assign(v.h, v.h + v.g.rows);
+  p.l.assign(v.l, v.l + v.n);
+  p.u.assign(v.u, v.u + v.n);
+  p.objective_offset = v.objective_offset;
+  if (witness) {
+    const double* w = pdhg_instance_witness(inst);
+    if (w) witness->assign(w, w + v.n);
+  }
+  pdhg_instance_free(inst);
+  return p;
+}
+
+}  // namespace
+
+LpProblem GenPagerank(const PagerankConfig& cfg) {
+  pdhg_instance* inst = nullptr;
+  char err[512] = {0};
+  if (pdhg_gen_pagerank(cfg.n_nodes, cfg.damping, cfg.attachment, cfg.seed, &inst, err, sizeof(err)) != PDHG_OK)
+    throw std::invalid_argument(err);
+  LpProblem p = Take(inst, nullptr);
+  p.name = "pagerank";
+  return p;
+}
+
+LpProblem GenRandomLp(Index m, Index n, double density, std::uint64_t seed, std::vector<double>* witness) {
+  pdhg_instance* inst = nullptr;
+  char err[512] = {0};
+  if (pdhg_gen_random_lp(m, n, density, seed, &inst, err, sizeof(err)) != PDHG_OK) throw std::invalid_argument(err);
+  LpProblem p = Take(inst, witness);
+  p.name = "rand_" + std::to_string(m) + "x" + std::to_string(n) + "_s" + std::to_string(seed);
+  return p;
+}
+
+LpProblem GenTransport(Index sources, Index sinks, std::uint64_t seed) {
+  pdhg_instance* inst = nullptr;
+  char err[512] = {0};
+  if (pdhg_gen_transport(sources, sinks, seed, &inst, err, sizeof(err)) != PDHG_OK) throw std::invalid_argument(err);
+  return Take(inst, nullptr);
+}
+
+}  // namespace rpdlp

@@ -20,6 +20,7 @@
 #include <limits>
 #include <random>
 
+#include "host_logic.h"
 #include "ops.cuh"
 
 namespace pdhg {
@@ -336,6 +337,8 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device) : device
 
 Session::~Session() {
   cudaSetDevice(device_);
+  for (cudaEvent_t e : ev_)
+    if (e) cudaEventDestroy(e);
   for (Graph& g : graphs_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (host_red_) cudaFreeHost(host_red_);
@@ -565,6 +568,7 @@ void Session::DeviceNorms() {
 // ================================================================== kernels
 void Session::LaunchStep(int parity, int j, bool adapt) {
   const int a = parity, b = 1 - parity;
+  launches_ += adapt ? 3 : 2;
   if (adapt) {
     launch_tiles(csc_, OpPrimal<true>{y_[a].p, x_[a].p, x_[b].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, j},
                  red_tile_[1].p, red_span_[1].p, st_);
@@ -601,6 +605,7 @@ void Session::RunSteps(int parity, int count, bool adapt) {
     g = &graphs_.back();
   }
   if (g) {
+    launches_ += static_cast<int64_t>(count) * (adapt ? 3 : 2);
     PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
   } else {
     for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
@@ -609,6 +614,7 @@ void Session::RunSteps(int parity, int count, bool adapt) {
 }
 
 void Session::LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx) {
+  launches_ += 4;
   OpCheckRow row{xb, kxavg_.p, kx, y, yb, ystart_.p, q_s_.p, q_o_.p, rs_.p, (int32_t)m1_};
   launch_tiles(csr_, row, red_tile_[0].p, red_span_[0].p, st_);
   OpCheckCol col{y, yb, x, xb, xstart_.p, c_s_.p, l_s_.p, u_s_.p, c_o_.p, l_o_.p, u_o_.p, cs_.p};
@@ -628,42 +634,16 @@ void Session::ReadCheck(CheckOut* out) {
 // ================================================================ solve loop
 namespace {
 
-// ResidualReport from the reduced sums (kkt.cpp:80-118).
-pdhg_report MakeReport(double pr2, double du2, double bound, double cx, double qy, double off, double qn, double cn) {
-  pdhg_report r{};
-  r.primal_res = std::sqrt(pr2);
-  r.dual_res = std::sqrt(du2);
-  r.primal_obj = off + cx;
-  r.dual_obj = off + bound + qy;
-  r.gap_abs = std::abs(r.dual_obj - r.primal_obj);
-  r.rel_primal = r.primal_res / (1.0 + qn);
-  r.rel_dual = r.dual_res / (1.0 + cn);
-  r.rel_gap = r.gap_abs / (1.0 + std::abs(r.dual_obj) + std::abs(r.primal_obj));
-  return r;
-}
-
-double KktError(double p, double d, double g, double w) {  // kkt.cpp:153-157
-  return std::sqrt(w * w * p * p + d * d / (w * w) + g * g);
-}
-double Kkt1(const pdhg_report& r) { return KktError(r.primal_res, r.dual_res, r.gap_abs, 1.0); }
-bool Terminated(const pdhg_report& r, double eps) {  // kkt.cpp:147-151
-  return r.rel_primal <= eps && r.rel_dual <= eps && r.rel_gap <= eps;
-}
-bool ShouldRestart(const pdhg_params& p, int64_t t, int64_t k, double cand, double start, double prev) {
-  if (cand <= p.sufficient_decay * start) return true;  // solver.cpp:178-189
-  if (cand <= p.necessary_decay * start && cand > prev) return true;
-  return static_cast<double>(t) >= p.long_loop_frac * static_cast<double>(k);
-}
-double UpdatePrimalWeight(double w, double dx, double dy) {  // solver.cpp:191-196
-  constexpr double kMin = 1e-10;
-  if (dx <= kMin || dy <= kMin) return w;
-  return std::exp(0.5 * std::log(dy / dx) + 0.5 * std::log(w));
-}
-
 }  // namespace
 
 void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_result* out) {
   PDHG_CUDA(cudaSetDevice(device_));
+  if (!ev_[0]) {
+    PDHG_CUDA(cudaEventCreate(&ev_[0]));
+    PDHG_CUDA(cudaEventCreate(&ev_[1]));
+  }
+  launches_ = 0;
+  PDHG_CUDA(cudaEventRecord(ev_[0], st_));
   const auto t0 = std::chrono::steady_clock::now();
   auto secs = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
 
@@ -865,7 +845,12 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     launch_tiles(csc_, OpLambda{ybest_.p, c_o_.p, l_o_.p, u_o_.p, cs_.p, nvec_.p}, nullptr, nullptr, st_);
     PDHG_CUDA(cudaMemcpyAsync(out->lambda, nvec_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
   }
+  PDHG_CUDA(cudaEventRecord(ev_[1], st_));
   Sync();
+  float ms = 0.f;
+  PDHG_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
+  last_ms_ = ms;
+  last_launches_ = launches_ + 4;  // + clamp0, kx0 SpMV, unscale/lambda kernels
   out->status = status;
   out->report = best_rep;
   out->iterations = iters;
@@ -897,6 +882,7 @@ double Session::OpNorm(int iters, uint64_t seed) {
   Scalars sc{};
   sc.pw_norm = vnorm;
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
+  launches_ += 4 * static_cast<int64_t>(iters) + 2;
   for (int it = 0; it < iters; ++it) {
     launch_tiles(csr_, OpPowerStep<false>{u.p, scal_.p, 1, kv.p}, nullptr, nullptr, st_);
     launch_tiles(csc_, OpPowerStep<true>{kv.p, scal_.p, 0, u.p}, red_tile_[1].p, red_span_[1].p, st_);
@@ -1032,6 +1018,17 @@ void Session::UnitDual(const double* xn, const double* xo, const double* y, doub
   launch_tiles(csr_, OpUnitDual{ext.p, dy.p, q_s_.p, (int32_t)m1_, eta * omega, dout.p}, nullptr, nullptr, st_);
   check_launch<int>("dual step");
   if (m_) PDHG_CUDA(cudaMemcpyAsync(out, dout.p, m_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  Sync();
+}
+
+// Evict the working set between benchmark steps: write 2x the L2 capacity.
+void Session::FlushL2() {
+  PDHG_CUDA(cudaSetDevice(device_));
+  int l2 = 0;
+  PDHG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device_));
+  const size_t bytes = std::max<size_t>(2 * static_cast<size_t>(l2), 64u << 20);
+  if (flush_.n < bytes) flush_.alloc(bytes);
+  PDHG_CUDA(cudaMemsetAsync(flush_.p, 0x5a, bytes, st_));
   Sync();
 }
 

@@ -28,6 +28,9 @@ class Session {
   void UnitPrimal(const double* x, const double* y, double eta, double omega, double* out);
   void UnitDual(const double* xn, const double* xo, const double* y, double eta, double omega, double* out);
   int device() const { return device_; }
+  void FlushL2();
+  double last_device_ms() const { return last_ms_; }
+  int64_t last_launches() const { return last_launches_; }
 
  private:
   struct Graph {
@@ -79,6 +82,10 @@ class Session {
   double* host_red_ = nullptr;  // pinned
 
   std::vector<Graph> graphs_;
+  DArray<char> flush_;
+  cudaEvent_t ev_[2] = {nullptr, nullptr};
+  double last_ms_ = 0.0;
+  int64_t launches_ = 0, last_launches_ = 0;
 };
 
 }  // namespace pdhg

@@ -335,6 +335,16 @@ class Session:
         raise_for(code, err, obs.error)
         return _pack(res, x, y, lam)
 
+    def flush_l2(self) -> None:
+        err = self._err()
+        raise_for(self.lib.pdhg_session_flush_l2(self.h, err, abi.ERRLEN), err)
+
+    def last_solve(self):
+        """(device milliseconds, kernel launches) of the latest solve."""
+        ms, n = C.c_double(), C.c_int64()
+        self.lib.pdhg_session_last_solve(self.h, C.byref(ms), C.byref(n))
+        return ms.value, n.value
+
     def stats(self) -> abi.SessionStats:
         s = abi.SessionStats()
         self.lib.pdhg_session_stats_get(self.h, C.byref(s))
@@ -394,6 +404,31 @@ def DualStep(problem: LpProblem, x_new, x_old, y, eta: float, omega: float) -> n
     err = C.create_string_buffer(abi.ERRLEN)
     raise_for(lib.pdhg_dual_step(C.byref(lp), _dp(a), _dp(b), _dp(ya), eta, omega, _dp(out), err, abi.ERRLEN), err)
     return out
+
+
+# ------------------------------------------- host decision logic (no device)
+def ShouldRestart(params: SolverParams, t: int, k: int, kkt_candidate: float, kkt_loop_start: float,
+                  kkt_prev_candidate: float) -> bool:
+    """solver.cpp:178-189."""
+    prm = params.to_c()
+    return bool(abi.load().pdhg_should_restart(C.byref(prm), t, k, kkt_candidate, kkt_loop_start,
+                                               kkt_prev_candidate))
+
+
+def UpdatePrimalWeight(omega: float, dx_norm: float, dy_norm: float) -> float:
+    """solver.cpp:191-196."""
+    return abi.load().pdhg_update_primal_weight(omega, dx_norm, dy_norm)
+
+
+def KktError(primal_res: float, dual_res: float, gap: float, omega: float) -> float:
+    """kkt.cpp:153-157."""
+    return abi.load().pdhg_kkt_error(primal_res, dual_res, gap, omega)
+
+
+def CheckTermination(report: ResidualReport, eps: float) -> bool:
+    """kkt.cpp:147-151."""
+    r = abi.Report(*(getattr(report, k) for k, _ in abi.Report._fields_))
+    return bool(abi.load().pdhg_check_termination(C.byref(r), eps))
 
 
 # ------------------------------------------------------------ generators

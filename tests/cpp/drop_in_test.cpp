@@ -1,0 +1,164 @@
+// Drop-in check: reference-style C++ caller code compiled against
+// include/rpdlp/*.hpp and linked to libpdhg_b200.so (no reference code).
+// Cases follow the reference's own unit tests (test_solver.cpp, test_kkt.cpp)
+// and acceptance criteria C1/C5 shapes. Exit code = number of failures.
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rpdlp/instance_gen.hpp"
+#include "rpdlp/solver.hpp"
+
+using namespace rpdlp;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                      \
+  do {                                                                   \
+    if (cond) {                                                          \
+      ++g_pass;                                                          \
+    } else {                                                             \
+      ++g_fail;                                                          \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+    }                                                                    \
+  } while (0)
+
+static bool Near(double a, double b, double rel) { return std::abs(a - b) <= rel * std::max(1.0, std::abs(b)); }
+
+static LpProblem TinyLp() {
+  LpProblem p;
+  p.a = SparseMatrix::FromTriplets(0, 1, {});
+  p.g = SparseMatrix::FromTriplets(1, 1, {{0, 0, 1.0}});
+  p.c = {1.0};
+  p.h = {1.0};
+  p.l = {0.0};
+  p.u = {kInf};
+  return p;
+}
+
+int main() {
+  {  // test_solver.cpp:198-208
+    SolverParams prm;
+    prm.eps = 1e-8;
+    SolveResult r = Solve(TinyLp(), prm);
+    CHECK(r.status == SolveStatus::kOptimal);
+    CHECK(Near(r.x[0], 1.0, 1e-6) && Near(r.y[0], 1.0, 1e-6));
+    CHECK(r.report.rel_primal <= 1e-8 && r.report.rel_dual <= 1e-8 && r.report.rel_gap <= 1e-8);
+  }
+  {  // operator norms (test_solver.cpp:41-57)
+    CHECK(Near(EstimateOpNorm(SparseMatrix::FromTriplets(1, 1, {{0, 0, 3.0}}), 50, 1), 3.0, 1e-12));
+    const double est = EstimateOpNorm(SparseMatrix::FromTriplets(3, 3, {{0, 0, 1.0}, {1, 1, 2.0}, {2, 2, 5.0}}), 200, 1);
+    CHECK(est > 4.95 && est <= 5.0 + 1e-12);
+    CHECK(EstimateOpNorm(SparseMatrix::FromTriplets(2, 3, {}), 20, 1) == 0.0);
+  }
+  {  // PrimalStep / DualStep hand examples (test_solver.cpp:65-112)
+    LpProblem p;
+    p.a = SparseMatrix::FromTriplets(0, 1, {});
+    p.g = SparseMatrix::FromTriplets(1, 1, {{0, 0, 1.0}});
+    p.c = {1.0};
+    p.h = {0.0};
+    p.l = {0.0};
+    p.u = {1.0};
+    CHECK(PrimalStep(p, std::vector<double>{0.2}, std::vector<double>{0.5}, 0.5, 1.0)[0] == 0.0);
+    CHECK(Near(PrimalStep(p, std::vector<double>{0.2}, std::vector<double>{0.5}, 0.5, 2.0)[0], 0.075, 1e-15));
+    CHECK(PrimalStep(p, std::vector<double>{0.9}, std::vector<double>{5.0}, 0.5, 1.0)[0] == 1.0);
+    LpProblem d;
+    d.a = SparseMatrix::FromTriplets(1, 1, {{0, 0, 1.0}});
+    d.g = SparseMatrix::FromTriplets(1, 1, {{0, 0, 1.0}});
+    d.c = {0.0};
+    d.b = {2.0};
+    d.h = {2.0};
+    d.l = {0.0};
+    d.u = {kInf};
+    auto y = DualStep(d, std::vector<double>{1.0}, std::vector<double>{0.5}, std::vector<double>{0.1, 0.1}, 0.5, 1.0);
+    CHECK(Near(y[0], 0.35, 1e-15) && Near(y[1], 0.35, 1e-15));
+    auto y2 = DualStep(d, std::vector<double>{3.0}, std::vector<double>{3.0}, std::vector<double>{0.1, 0.1}, 0.5, 1.0);
+    CHECK(Near(y2[0], -0.4, 1e-15) && y2[1] == 0.0);
+  }
+  {  // restart truth table (test_solver.cpp:155-183)
+    SolverParams prm;
+    const double inf = std::numeric_limits<double>::infinity();
+    CHECK(ShouldRestart(prm, 1, 100, 0.10, 1.0, 0.05));
+    CHECK(ShouldRestart(prm, 1, 100, 0.50, 1.0, 0.40));
+    CHECK(!ShouldRestart(prm, 1, 100, 0.50, 1.0, 0.60));
+    CHECK(ShouldRestart(prm, 36, 100, 0.90, 1.0, inf));
+    CHECK(!ShouldRestart(prm, 35, 100, 0.90, 1.0, inf));
+    CHECK(Near(UpdatePrimalWeight(1.0, 1.0, 4.0), 2.0, 1e-15));
+    CHECK(Near(KktError(3.0, 4.0, 0.0, 1.0), 5.0, 1e-15));
+  }
+  {  // limits (test_solver.cpp:251-263)
+    SolverParams prm;
+    prm.eps = 1e-16;
+    prm.iter_limit = 10;
+    SolveResult r = Solve(GenRandomLp(5, 5, 0.6, 7), prm);
+    CHECK(r.status == SolveStatus::kIterLimit && r.iterations <= 10);
+    prm.iter_limit = std::numeric_limits<Index>::max();
+    prm.time_limit = 0.0;
+    CHECK(Solve(GenRandomLp(5, 5, 0.6, 7), prm).status == SolveStatus::kTimeLimit);
+  }
+  {  // errors map back to the reference's exception types
+    LpProblem p = TinyLp();
+    p.l = {2.0};
+    p.u = {1.0};
+    bool threw = false;
+    try {
+      Solve(p, SolverParams{});
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    SolverParams bad;
+    bad.check_every = 0;
+    threw = false;
+    try {
+      Solve(TinyLp(), bad);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
+  {  // observer (test_solver.cpp:277-292) and its exceptions
+    SolverParams prm;
+    prm.eps = 1e-6;
+    Index last = -1, seen = 0;
+    bool order = true;
+    SolveResult r = Solve(GenPagerank({200, 0.85, 3, 4}), prm, [&](const EvalInfo& e) {
+      if (e.iteration < last) order = false;
+      last = e.iteration;
+      seen += e.restarted;
+    });
+    CHECK(r.status == SolveStatus::kOptimal && order && seen == r.restarts);
+    bool threw = false;
+    try {
+      Solve(GenPagerank({200, 0.85, 3, 4}), prm, [](const EvalInfo&) { throw std::runtime_error("stop"); });
+    } catch (const std::runtime_error& e) {
+      threw = std::string(e.what()) == "stop";
+    }
+    CHECK(threw);
+  }
+  {  // acceptance C5 shape: PageRank n in {100, 1000, 10000} at 1e-6
+    for (Index n : {100, 1000, 10000}) {
+      SolverParams prm;
+      prm.eps = 1e-6;
+      SolveResult r = Solve(GenPagerank({n, 0.85, 3, 2026}), prm);
+      const double s = std::accumulate(r.x.begin(), r.x.end(), 0.0);
+      CHECK(r.status == SolveStatus::kOptimal);
+      CHECK(std::abs(s - 1.0) <= 1e-4);
+      double mn = 0.0;
+      for (double v : r.x) mn = std::min(mn, v);
+      CHECK(mn >= 0.0);
+    }
+  }
+  {  // determinism (test_solver.cpp:265-275)
+    SolverParams prm;
+    prm.eps = 1e-8;
+    LpProblem p = GenRandomLp(6, 8, 0.5, 55);
+    SolveResult a = Solve(p, prm), b = Solve(p, prm);
+    CHECK(a.iterations == b.iterations && a.x == b.x && a.y == b.y);
+  }
+  std::printf("drop_in_test: %d passed, %d failed\n", g_pass, g_fail);
+  return g_fail;
+}

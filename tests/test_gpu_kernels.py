@@ -1,0 +1,156 @@
+"""Kernel-level parity: device scaling, SpMV, power iteration, unit steps
+against the oracle restatement (itself pinned to the reference), through the
+C-ABI of libpdhg_b200.so."""
+import numpy as np
+import pytest
+
+from paper_2312_14832_b200 import rpdlp
+from paper_2312_14832_b200.rpdlp import GenPagerank, GenRandomLp, GenTransport, Session, SolverParams
+
+from problems import config1, empty_rows_lp, hand_dual_lp, hand_primal_lp, long_row_lp, mixed_bounds_lp, small_cases
+
+pytestmark = pytest.mark.gpu
+
+
+def kernel_cases():
+    d = small_cases()
+    d["config1"] = config1(2)
+    d["long_row"] = long_row_lp()
+    d["pagerank_3k"] = GenPagerank(3000, 0.85, 6, 2)
+    d["transport_60x70"] = GenTransport(60, 70, 3)
+    return d
+
+
+CASES = kernel_cases()
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("scaled", [True, False])
+def test_scaled_problem_bit_exact(name, scaled, restatement):
+    """Ruiz x10 + Pock-Chambolle + ApplyScaling on device == reference, bit
+    for bit, whenever no row/col of K exceeds 32 nonzeros (storage-order sums);
+    otherwise within 4 ulp-scale (PC power sums of long rows differ in order)."""
+    p = CASES[name]
+    prm = SolverParams()
+    prm.scaling.enabled = scaled
+    with Session(p, prm) as s:
+        rs, cs = s.scaling()
+        kv, c, l, u, q = s.scaled()
+    rs0, cs0 = restatement.scaling(p, prm)
+    kv0, c0, l0, u0, q0 = restatement.scaled(p, prm)
+    if max_segment(p) <= 32:
+        for got, want in ((rs, rs0), (cs, cs0), (kv, kv0), (c, c0), (l, l0), (u, u0), (q, q0)):
+            assert np.array_equal(got, want)
+    else:
+        for got, want in ((rs, rs0), (cs, cs0), (kv, kv0), (c, c0), (q, q0)):
+            np.testing.assert_allclose(got, want, rtol=1e-15 * 8, atol=0)
+        np.testing.assert_array_equal(np.isinf(l), np.isinf(l0))
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("transpose", [False, True])
+def test_spmv_matches_reference_sums(name, transpose, restatement):
+    """K_s x and K_s^T y: segments of <= 32 nonzeros are summed in storage
+    order (bit-exact with sparse_matrix.cpp:114-138); longer ones with a fixed
+    tree (1e-13 relative to sum |terms|)."""
+    p = CASES[name]
+    rng = np.random.default_rng(11)
+    n, m = p.num_vars(), p.num_rows()
+    vec = rng.standard_normal(m if transpose else n)
+    # With segments > 32 the PC power sums (hence K_s) may differ in the last
+    # ulp; check SpMV summation order on the unscaled K there.
+    prm = SolverParams()
+    prm.scaling.enabled = max_segment(p) <= 32
+    with Session(p, prm) as s:
+        got = s.spmv(vec, transpose)
+        kv = s.scaled()[0]
+    want = restatement.spmv(p, vec, transpose, prm)
+    rows = np.concatenate([np.repeat(np.arange(p.a.rows), np.diff(p.a.row_ptr)),
+                           p.a.rows + np.repeat(np.arange(p.g.rows), np.diff(p.g.row_ptr))])
+    cols = np.concatenate([p.a.col_idx, p.g.col_idx])
+    if transpose:
+        mag = np.bincount(cols, weights=np.abs(kv * vec[rows]), minlength=n)
+        seglen = np.bincount(cols, minlength=n)
+    else:
+        mag = np.bincount(rows, weights=np.abs(kv * vec[cols]), minlength=m)
+        seglen = np.bincount(rows, minlength=m)
+    short = seglen <= 32
+    assert np.array_equal(got[short], want[short])
+    assert np.all(np.abs(got - want) <= 1e-13 * mag + 1e-300)
+
+
+def max_segment(p):
+    cols = np.concatenate([p.a.col_idx, p.g.col_idx])
+    lens = np.concatenate([np.diff(p.a.row_ptr), np.diff(p.g.row_ptr), np.bincount(cols, minlength=p.num_vars())])
+    return int(lens.max(initial=0))
+
+
+def test_spmv_deterministic_long_rows():
+    p = long_row_lp()
+    vec = np.random.default_rng(1).standard_normal(p.num_vars())
+    with Session(p) as s:
+        a = s.spmv(vec)
+        b = s.spmv(vec)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["config1", "pagerank_3k", "transport_60x70", "long_row", "mixed"])
+def test_opnorm(name, restatement):
+    """EstimateOpNorm (solver.cpp:84-110), same libstdc++ start vector."""
+    p = CASES[name]
+    with Session(p) as s:
+        got = s.opnorm(100, 0)
+        got7 = s.opnorm(40, 7)
+    want = restatement.opnorm(p, 100, 0)
+    want7 = restatement.opnorm(p, 40, 7)
+    assert got == pytest.approx(want, rel=1e-12)
+    assert got7 == pytest.approx(want7, rel=1e-12)
+
+
+def test_opnorm_known_matrices():
+    """test_solver.cpp:41-57 (through the unscaled session)."""
+    from paper_2312_14832_b200.rpdlp import CsrMatrix, LpProblem
+    prm = SolverParams()
+    prm.scaling.enabled = False
+
+    def of(rows, cols, trips, iters, seed=1):
+        g = CsrMatrix.from_triplets(rows, cols, trips)
+        p = LpProblem(CsrMatrix.empty(0, cols), g, np.zeros(cols), [], np.zeros(rows), np.zeros(cols),
+                      np.ones(cols))
+        with Session(p, prm) as s:
+            return s.opnorm(iters, seed)
+
+    assert of(1, 1, [(0, 0, 3.0)], 50) == pytest.approx(3.0, rel=1e-12)
+    est = of(3, 3, [(0, 0, 1.0), (1, 1, 2.0), (2, 2, 5.0)], 200)
+    assert 4.95 < est <= 5.0 + 1e-12
+    assert of(2, 2, [(0, 0, 1.0), (0, 1, 1.0), (1, 0, 1.0), (1, 1, 1.0)], 100) == pytest.approx(2.0, rel=1e-6)
+    assert of(2, 3, [], 20) == 0.0
+
+
+def test_primal_step_hand_example():
+    """test_solver.cpp:65-88."""
+    p = hand_primal_lp()
+    assert rpdlp.PrimalStep(p, [0.2], [0.5], 0.5, 1.0)[0] == 0.0
+    assert rpdlp.PrimalStep(p, [0.2], [0.5], 0.5, 2.0)[0] == pytest.approx(0.075, rel=1e-15)
+    assert rpdlp.PrimalStep(p, [0.9], [5.0], 0.5, 1.0)[0] == 1.0
+
+
+def test_dual_step_hand_example():
+    """test_solver.cpp:90-112."""
+    p = hand_dual_lp()
+    y = rpdlp.DualStep(p, [1.0], [0.5], [0.1, 0.1], 0.5, 1.0)
+    assert y[0] == pytest.approx(0.35, rel=1e-15) and y[1] == pytest.approx(0.35, rel=1e-15)
+    y2 = rpdlp.DualStep(p, [3.0], [3.0], [0.1, 0.1], 0.5, 1.0)
+    assert y2[0] == pytest.approx(-0.4, rel=1e-15) and y2[1] == 0.0
+
+
+@pytest.mark.parametrize("name", ["mixed", "rand_40x30", "empty_rows", "pagerank_200"])
+def test_unit_steps_vs_reference(name, restatement):
+    p = CASES[name]
+    rng = np.random.default_rng(5)
+    n, m = p.num_vars(), p.num_rows()
+    x, xo, y = rng.uniform(-1, 2, n), rng.uniform(-1, 2, n), rng.uniform(0, 1, m)
+    np.testing.assert_allclose(rpdlp.PrimalStep(p, x, y, 0.3, 1.7), restatement.primal_step(p, x, y, 0.3, 1.7),
+                               rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(rpdlp.DualStep(p, x, xo, y, 0.3, 1.7), restatement.dual_step(p, x, xo, y, 0.3, 1.7),
+                               rtol=1e-14, atol=1e-15)

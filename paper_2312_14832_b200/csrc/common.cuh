@@ -29,6 +29,8 @@ constexpr int kBlock = 256;        // threads per CTA
 constexpr int kTile = 2048;        // nominal nonzeros per tile
 constexpr int kSnap = 64;          // segments this short never straddle tiles
 constexpr int kSeqMax = 32;        // segments up to this length: one thread, in order
+constexpr int kWarpMax = 512;      // segments up to this length: one warp
+constexpr int kCtaMax = 16384;     // segments up to this length: one CTA
 constexpr int kTileCap = kTile + kSnap;
 constexpr int kWarps = kBlock / 32;
 

@@ -25,7 +25,9 @@ struct DArray {
     arena = a;
     n = count;
     if (count) {
-      PDHG_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+      // 32 bytes of tail slack: TMA bulk copies widen ranges to 16 bytes
+      // (the widened elements are staged but never consumed).
+      PDHG_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T) + 32));
       if (arena) arena->bytes += static_cast<int64_t>(count * sizeof(T));
     }
   }

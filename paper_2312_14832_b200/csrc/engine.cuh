@@ -1,0 +1,227 @@
+// Length-class dispatch of every matrix pass.
+//
+// At setup the rows of K (CSR) and the columns (CSC) are permuted into three
+// contiguous length classes, keeping the storage order inside each segment
+// (so every segment sum is formed exactly as before):
+//   S  (<= kSeqMax = 32 nonzeros): one thread per segment, direct loads, sum
+//      in storage order -- bit-identical to the reference's `acc += v * x[j]`
+//      loops;
+//   M  (33 .. kWarpMax = 512): one warp per segment, lane-strided loads,
+//      fixed butterfly;
+//   L  (513 .. kCtaMax = 16384): one CTA per segment, fixed tree;
+//   XL (> kCtaMax): the TMA tile engine (tile_spmv.cuh), several CTAs per
+//      segment with last-arriver combination.
+// Each class writes its own reduction partials; `k_reduce_parts` sums them in
+// a fixed order, so every pass stays bitwise reproducible.
+#pragma once
+
+#include "tile_spmv.cuh"
+
+namespace pdhg {
+
+constexpr int kUnroll = 4;
+
+// Equality rows after the class permutation: within each class the equality
+// rows come first. [0,e0) eq S, [s1,e1) eq M, [s2,e2) eq L, [s3,e3) eq XL.
+struct RowKind {
+  int32_t e0, s1, e1, s2, e2, s3, e3;
+  __device__ __forceinline__ bool eq(int32_t s) const {
+    return s < e0 || (s >= s1 && s < e1) || (s >= s2 && s < e2) || (s >= s3 && s < e3);
+  }
+};
+
+// One matrix layout split into classes.
+struct Layout {
+  int32_t nseg = 0, nvec = 0;
+  int64_t nnz = 0;
+  int32_t* ptr = nullptr;
+  int32_t* idx = nullptr;
+  double* val = nullptr;
+  int32_t s1 = 0, s2 = 0, s3 = 0;  // class bounds S | M | L | XL
+  CMat lng;                        // tile-engine view of [s3, nseg)
+  int nb_s() const { return ceil_div(s1, kBlock); }
+  int nb_m() const { return ceil_div(static_cast<int64_t>(s2 - s1) * 32, kBlock); }
+  int nb_l() const { return s3 - s2; }
+  int nt_x() const { return nseg > s3 ? lng.ntiles : 0; }
+  int parts() const { return nb_s() + nb_m() + nb_l() + 2 * nt_x(); }  // reduction slots
+};
+
+template <class Op>
+__device__ __forceinline__ void block_reduce_out(double (&red)[Op::kRed > 0 ? Op::kRed : 1], double* out) {
+  if constexpr (Op::kRed > 0) {
+    __shared__ double sh[kWarps][Op::kRed];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < Op::kRed; ++i) {
+      const double v = warp_combine<false>(red[i]);
+      if (lane == 0) sh[warp][i] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < Op::kRed) {
+      double v = sh[0][threadIdx.x];
+      for (int w = 1; w < kWarps; ++w) v += sh[w][threadIdx.x];
+      out[static_cast<int64_t>(blockIdx.x) * Op::kRed + threadIdx.x] = v;
+    }
+  }
+}
+
+// Class S: one thread per segment, direct loads (consecutive threads read
+// adjacent ranges, so L1 turns the per-thread streams into full-line use),
+// sum in storage order -- bit-identical to the reference's serial loops.
+template <class Op>
+__global__ void __launch_bounds__(kBlock) seg_thread_kernel(const int32_t* __restrict__ ptr,
+                                                            const int32_t* __restrict__ idx,
+                                                            const double* __restrict__ val, int32_t s_end,
+                                                            const Op op, double* __restrict__ red_out) {
+  constexpr int R = Op::kRhs;
+  constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
+  constexpr bool MX = Op::kMax;
+  double red[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) red[i] = 0.0;
+  const int s = blockIdx.x * kBlock + threadIdx.x;
+  if (s < s_end) {
+    const int b = ptr[s], e = ptr[s + 1];
+    const typename Op::Pre pre = op.prefetch(s);
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    int k = b;
+    for (; k + kUnroll <= e; k += kUnroll) {
+      int32_t j[kUnroll];
+      double v[kUnroll], p[kUnroll][R];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        j[u] = ld_stream(idx + k + u);
+        v[u] = ld_stream(val + k + u);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) op.map(j[u], v[u], p[u]);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[u][r]);  // storage order
+    }
+    for (; k < e; ++k) {
+      double p[R];
+      op.map(ld_stream(idx + k), ld_stream(val + k), p);
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[r]);
+    }
+    op.finish(s, acc, pre, red);
+  }
+  block_reduce_out<Op>(red, red_out);
+}
+
+// Lane-strided partial sum of [b, e) with kUnroll loads in flight per lane.
+template <class Op, int kStride>
+__device__ __forceinline__ void strided_sum(const Op& op, const int32_t* __restrict__ idx,
+                                            const double* __restrict__ val, int b, int e, int t,
+                                            double (&acc)[Op::kRhs]) {
+  constexpr int R = Op::kRhs;
+  constexpr bool MX = Op::kMax;
+  int k = b + t;
+  for (; k + kStride * (kUnroll - 1) < e; k += kStride * kUnroll) {
+    int32_t j[kUnroll];
+    double v[kUnroll], p[kUnroll][R];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      j[u] = ld_stream(idx + k + kStride * u);
+      v[u] = ld_stream(val + k + kStride * u);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) op.map(j[u], v[u], p[u]);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[u][r]);
+  }
+  for (; k < e; k += kStride) {
+    double p[R];
+    op.map(ld_stream(idx + k), ld_stream(val + k), p);
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[r]);
+  }
+}
+
+// Class M: one warp per segment.
+template <class Op>
+__global__ void __launch_bounds__(kBlock) seg_warp_kernel(const int32_t* __restrict__ ptr,
+                                                          const int32_t* __restrict__ idx,
+                                                          const double* __restrict__ val, int32_t s_begin,
+                                                          int32_t s_end, const Op op, double* __restrict__ red_out) {
+  constexpr int R = Op::kRhs;
+  constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
+  constexpr bool MX = Op::kMax;
+  double red[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) red[i] = 0.0;
+  const int lane = threadIdx.x & 31;
+  const int s = s_begin + blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (s < s_end) {  // warp-uniform
+    const int b = ptr[s], e = ptr[s + 1];
+    typename Op::Pre pre{};
+    if (lane == 0) pre = op.prefetch(s);
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    strided_sum<Op, 32>(op, idx, val, b, e, lane, acc);
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = warp_combine<MX>(acc[r]);
+    if (lane == 0) op.finish(s, acc, pre, red);
+  }
+  block_reduce_out<Op>(red, red_out);
+}
+
+// Class L: one CTA per segment (fixed tree over the block).
+template <class Op>
+__global__ void __launch_bounds__(kBlock) seg_cta_kernel(const int32_t* __restrict__ ptr,
+                                                         const int32_t* __restrict__ idx,
+                                                         const double* __restrict__ val, int32_t s_begin,
+                                                         const Op op, double* __restrict__ red_out) {
+  constexpr int R = Op::kRhs;
+  constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
+  constexpr bool MX = Op::kMax;
+  __shared__ double sh[kWarps][R];
+  double red[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) red[i] = 0.0;
+  const int s = s_begin + blockIdx.x;
+  const int b = ptr[s], e = ptr[s + 1];
+  typename Op::Pre pre{};
+  if (threadIdx.x == 0) pre = op.prefetch(s);
+  double acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.0;
+  strided_sum<Op, kBlock>(op, idx, val, b, e, threadIdx.x, acc);
+  block_combine<R, MX, R>(acc, sh);
+  if (threadIdx.x == 0) op.finish(s, acc, pre, red);
+  block_reduce_out<Op>(red, red_out);
+}
+
+// Reduction slots of one pass: [S blocks | M blocks | L CTAs | XL tiles | XL spans].
+struct RedSlots {
+  double* base = nullptr;
+  double* at(int64_t slot, int nr) const { return base ? base + slot * nr : nullptr; }
+};
+
+template <class Op>
+inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, cudaStream_t st) {
+  constexpr int nr = Op::kRed > 0 ? Op::kRed : 1;
+  int64_t slot = 0;
+  if (L.s1 > 0) seg_thread_kernel<Op><<<L.nb_s(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, op, red.at(slot, nr));
+  slot += L.nb_s();
+  if (L.s2 > L.s1)
+    seg_warp_kernel<Op><<<L.nb_m(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, L.s2, op, red.at(slot, nr));
+  slot += L.nb_m();
+  if (L.s3 > L.s2) seg_cta_kernel<Op><<<L.nb_l(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s2, op, red.at(slot, nr));
+  slot += L.nb_l();
+  if (L.nseg > L.s3) launch_tiles(L.lng, op, red.at(slot, nr), red.at(slot + L.nt_x(), nr), st);
+}
+
+// Number of kernels run_pass launches.
+inline int pass_launches(const Layout& L) {
+  return (L.s1 > 0) + (L.s2 > L.s1) + (L.s3 > L.s2) + (L.nseg > L.s3);
+}
+
+}  // namespace pdhg

@@ -2,9 +2,14 @@
 // the SpMV that feeds it. Reference loops cited per op. All arithmetic is
 // compiled with -fmad=false so every `a * b + c` rounds twice, as on the
 // reference's x86-64 baseline build (no FMA contraction).
+//
+// Per-segment epilogue operands come from `operand(k)` arrays that the engine
+// stages by TMA for the tile's whole segment range (`staged`); `prefetch`
+// reads the same operands from global memory for the rare segments finished
+// outside their own tile. The epilogue itself only stores.
 #pragma once
 
-#include "tile_spmv.cuh"
+#include "engine.cuh"
 
 namespace pdhg {
 
@@ -13,10 +18,16 @@ namespace pdhg {
 struct OpSpmv {
   static constexpr int kRhs = 1, kRed = 0;
   static constexpr bool kMax = false;
+  using Pre = Nil;
   const double* x;
   double* y;
   __device__ void map(int32_t j, double v, double (&p)[1]) const { p[0] = v * x[j]; }
-  __device__ void finish(int32_t s, const double (&a)[1], double*) const { y[s] = a[0]; }
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 0;
+  __device__ const double* operand(int) const { return nullptr; }
+  __device__ Pre staged(int32_t, const double*, int) const { return {}; }
+  __device__ Pre prefetch(int32_t) const { return {}; }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre&, double*) const { y[s] = a[0]; }
 };
 
 // ------------------------------------------------------------ power iteration
@@ -27,14 +38,20 @@ template <bool kSumSq>
 struct OpPowerStep {
   static constexpr int kRhs = 1, kRed = kSumSq ? 1 : 0;
   static constexpr bool kMax = false;
+  using Pre = Nil;
   const double* x;
-  const Scalars* sc;  // pw_norm divides the gathered operand (1.0 for none)
+  const Scalars* sc;  // pw_norm divides the gathered operand
   int divide;
   double* y;
   __device__ void map(int32_t j, double v, double (&p)[1]) const {
     p[0] = divide ? v * (x[j] / sc->pw_norm) : v * x[j];
   }
-  __device__ void finish(int32_t s, const double (&a)[1], double* red) const {
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 0;
+  __device__ const double* operand(int) const { return nullptr; }
+  __device__ Pre staged(int32_t, const double*, int) const { return {}; }
+  __device__ Pre prefetch(int32_t) const { return {}; }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre&, double* red) const {
     y[s] = a[0];
     if constexpr (kSumSq) red[0] += a[0] * a[0];
   }
@@ -46,10 +63,16 @@ struct OpPowerStep {
 struct OpInfNormScale {
   static constexpr int kRhs = 1, kRed = 0;
   static constexpr bool kMax = true;
+  using Pre = Nil;
   double* d;      // this sweep's factor
   double* scale;  // accumulated Ruiz scale
   __device__ void map(int32_t, double v, double (&p)[1]) const { p[0] = fabs(v); }
-  __device__ void finish(int32_t s, const double (&a)[1], double*) const {
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 0;
+  __device__ const double* operand(int) const { return nullptr; }
+  __device__ Pre staged(int32_t, const double*, int) const { return {}; }
+  __device__ Pre prefetch(int32_t) const { return {}; }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre&, double*) const {
     const double f = a[0] > 0.0 ? 1.0 / sqrt(a[0]) : 1.0;
     d[s] = f;
     scale[s] *= f;
@@ -62,6 +85,7 @@ struct OpInfNormScale {
 struct OpPowerSumScale {
   static constexpr int kRhs = 1, kRed = 0;
   static constexpr bool kMax = false;
+  using Pre = Nil;
   double pw;
   int mode;  // 0: |v|^0 = 1, 1: |v|, 2: v*v, 3: pow
   double* scale;
@@ -69,7 +93,12 @@ struct OpPowerSumScale {
     const double a = fabs(v);
     p[0] = mode == 1 ? a : (mode == 2 ? a * a : (mode == 0 ? 1.0 : pow(a, pw)));
   }
-  __device__ void finish(int32_t s, const double (&a)[1], double*) const {
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 0;
+  __device__ const double* operand(int) const { return nullptr; }
+  __device__ Pre staged(int32_t, const double*, int) const { return {}; }
+  __device__ Pre prefetch(int32_t) const { return {}; }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre&, double*) const {
     if (a[0] > 0.0) scale[s] *= 1.0 / sqrt(a[0]);
   }
 };
@@ -81,6 +110,9 @@ template <bool kAdapt>
 struct OpPrimal {
   static constexpr int kRhs = 1, kRed = kAdapt ? 1 : 0;
   static constexpr bool kMax = false;
+  struct Pre {
+    double x, c, l, u, xbar, w, step;
+  };
   const double* y;  // current dual
   const double* x;  // current primal
   double* xn;       // next primal
@@ -91,16 +123,40 @@ struct OpPrimal {
   const Scalars* sc;
   int j_in_block;
   __device__ void map(int32_t i, double v, double (&p)[1]) const { p[0] = v * y[i]; }
-  __device__ void finish(int32_t s, const double (&a)[1], double* red) const {
-    const double step = sc->eta / sc->omega;
-    const double xo = x[s];
-    const double xv = clamp_ref(xo - step * (c[s] - a[0]), l[s], u[s]);
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 5;
+  __device__ const double* operand(int k) const {
+    const double* a[5] = {x, c, l, u, xbar};
+    return a[k];
+  }
+  __device__ Pre staged(int32_t, const double* st, int ld) const {
+    Pre p;
+    p.w = sc->inner_base + static_cast<double>(j_in_block);
+    p.step = sc->eta / sc->omega;
+    p.x = st[0];
+    p.c = st[ld];
+    p.l = st[2 * ld];
+    p.u = st[3 * ld];
+    p.xbar = (p.w == 0.0) ? 0.0 : st[4 * ld];
+    return p;
+  }
+  __device__ Pre prefetch(int32_t s) const {
+    Pre p;
+    p.w = sc->inner_base + static_cast<double>(j_in_block);
+    p.step = sc->eta / sc->omega;
+    p.x = x[s];
+    p.c = c[s];
+    p.l = l[s];
+    p.u = u[s];
+    p.xbar = (p.w == 0.0) ? 0.0 : xbar[s];  // Reset() zeroes the average
+    return p;
+  }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double* red) const {
+    const double xv = clamp_ref(p.x - p.step * (p.c - a[0]), p.l, p.u);
     xn[s] = xv;
-    const double w = sc->inner_base + static_cast<double>(j_in_block);
-    const double xb = (w == 0.0) ? 0.0 : xbar[s];  // Reset() zeroes the average
-    xbar[s] = (w * xb + xv) / (w + 1.0);
+    xbar[s] = (p.w * p.xbar + xv) / (p.w + 1.0);
     if constexpr (kAdapt) {
-      const double d = xv - xo;  // AdaptStepSize (solver.cpp:312-315)
+      const double d = xv - p.x;  // AdaptStepSize (solver.cpp:312-315)
       red[0] += d * d;
     }
   }
@@ -113,6 +169,9 @@ template <bool kAdapt>
 struct OpDual {
   static constexpr int kRhs = 1, kRed = kAdapt ? 2 : 0;
   static constexpr bool kMax = false;
+  struct Pre {
+    double kx, y, q, ybar, w, step;
+  };
   const double* xn;  // next primal (gathered)
   const double* y;
   double* yn;
@@ -120,25 +179,46 @@ struct OpDual {
   const double* kx;  // K x (current)
   double* kxn;       // K x+ (next)
   const double* q;
-  int32_t m1;
+  RowKind rk;  // equality rows (permuted order)
   const Scalars* sc;
   int j_in_block;
   __device__ void map(int32_t j, double v, double (&p)[1]) const { p[0] = v * xn[j]; }
-  __device__ void finish(int32_t s, const double (&a)[1], double* red) const {
-    const double step = sc->eta * sc->omega;
-    const double k0 = kx[s];
-    const double yo = y[s];
-    const double v = yo + step * (q[s] - (2.0 * a[0] - k0));
-    const double yv = s < m1 ? v : max0_ref(v);
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 4;
+  __device__ const double* operand(int k) const {
+    const double* a[4] = {kx, y, q, ybar};
+    return a[k];
+  }
+  __device__ Pre staged(int32_t, const double* st, int ld) const {
+    Pre p;
+    p.w = sc->inner_base + static_cast<double>(j_in_block);
+    p.step = sc->eta * sc->omega;
+    p.kx = st[0];
+    p.y = st[ld];
+    p.q = st[2 * ld];
+    p.ybar = (p.w == 0.0) ? 0.0 : st[3 * ld];
+    return p;
+  }
+  __device__ Pre prefetch(int32_t s) const {
+    Pre p;
+    p.w = sc->inner_base + static_cast<double>(j_in_block);
+    p.step = sc->eta * sc->omega;
+    p.kx = kx[s];
+    p.y = y[s];
+    p.q = q[s];
+    p.ybar = (p.w == 0.0) ? 0.0 : ybar[s];
+    return p;
+  }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double* red) const {
+    const double v = p.y + p.step * (p.q - (2.0 * a[0] - p.kx));
+    const double yv = rk.eq(s) ? v : max0_ref(v);
     yn[s] = yv;
     kxn[s] = a[0];
-    const double w = sc->inner_base + static_cast<double>(j_in_block);
-    const double yb = (w == 0.0) ? 0.0 : ybar[s];
-    ybar[s] = (w * yb + yv) / (w + 1.0);
+    ybar[s] = (p.w * p.ybar + yv) / (p.w + 1.0);
     if constexpr (kAdapt) {
-      const double d = yv - yo;  // AdaptStepSize (solver.cpp:316-320)
+      const double d = yv - p.y;  // AdaptStepSize (solver.cpp:316-320)
       red[0] += d * d;
-      red[1] += d * (a[0] - k0);
+      red[1] += d * (a[0] - p.kx);
     }
   }
 };
@@ -159,6 +239,9 @@ constexpr int kColRed = 2 * kColPer + 1;
 struct OpCheckRow {
   static constexpr int kRhs = 1, kRed = kRowRed;
   static constexpr bool kMax = false;
+  struct Pre {
+    double kx, y, yb, y0, qs, qo, r;
+  };
   const double* xbar;  // gathered: K xbar
   double* kx_avg;      // out
   const double* kx_cur;
@@ -168,27 +251,38 @@ struct OpCheckRow {
   const double* q_s;
   const double* q_o;
   const double* rs;
-  int32_t m1;
+  RowKind rk;  // equality rows (permuted order)
   __device__ void map(int32_t j, double v, double (&p)[1]) const { p[0] = v * xbar[j]; }
-  __device__ void finish(int32_t s, const double (&a)[1], double* red) const {
+  static constexpr int kOcc = 2;
+  static constexpr int kOps = 7;
+  __device__ const double* operand(int k) const {
+    const double* a[7] = {kx_cur, y_cur, ybar, y_start, q_s, q_o, rs};
+    return a[k];
+  }
+  __device__ Pre staged(int32_t, const double* st, int ld) const {
+    return {st[0], st[ld], st[2 * ld], st[3 * ld], st[4 * ld], st[5 * ld], st[6 * ld]};
+  }
+  __device__ Pre prefetch(int32_t s) const {
+    return {kx_cur[s], y_cur[s], ybar[s], y_start[s], q_s[s], q_o[s], rs[s]};
+  }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double* red) const {
     kx_avg[s] = a[0];
-    const double qs = q_s[s], qo = q_o[s], r = rs[s], ys0 = y_start[s];
 #pragma unroll
     for (int P = 0; P < 2; ++P) {
-      const double kx = P == 0 ? kx_cur[s] : a[0];
-      const double yv = P == 0 ? y_cur[s] : ybar[s];
+      const double kx = P == 0 ? p.kx : a[0];
+      const double yv = P == 0 ? p.y : p.yb;
       double* o = red + P * kRowPer;
-      const double es = s < m1 ? kx - qs : max0_ref(qs - kx);
+      const double es = rk.eq(s) ? kx - p.qs : max0_ref(p.qs - kx);
       o[kPrS] += es * es;
-      const double kxo = kx / r;
-      const double eo = s < m1 ? kxo - qo : max0_ref(qo - kxo);
+      const double kxo = kx / p.r;
+      const double eo = rk.eq(s) ? kxo - p.qo : max0_ref(p.qo - kxo);
       o[kPrO] += eo * eo;
-      o[kQyS] += qs * yv;
-      o[kQyO] += qo * (yv * r);
-      const double dy = yv - ys0;
+      o[kQyS] += p.qs * yv;
+      o[kQyO] += p.qo * (yv * p.r);
+      const double dy = yv - p.y0;
       o[kDy2] += dy * dy;
     }
-    if (!isfinite(y_cur[s])) red[2 * kRowPer] += 1.0;
+    if (!isfinite(p.y)) red[2 * kRowPer] += 1.0;
   }
 };
 
@@ -199,6 +293,9 @@ struct OpCheckRow {
 struct OpCheckCol {
   static constexpr int kRhs = 2, kRed = kColRed;
   static constexpr bool kMax = false;
+  struct Pre {
+    double x, xb, x0, cS, lS, uS, cO, lO, uO, f;
+  };
   const double* y_cur;
   const double* ybar;
   const double* x_cur;
@@ -215,33 +312,44 @@ struct OpCheckCol {
     p[0] = v * y_cur[i];
     p[1] = v * ybar[i];
   }
-  __device__ void finish(int32_t s, const double (&a)[2], double* red) const {
-    const double cS = c_s[s], lS = l_s[s], uS = u_s[s];
-    const double cO = c_o[s], lO = l_o[s], uO = u_o[s], f = cs[s], x0 = x_start[s];
-    const int cls = bound_class(lO, uO);
+  static constexpr int kOcc = 2;
+  static constexpr int kOps = 10;
+  __device__ const double* operand(int k) const {
+    const double* a[10] = {x_cur, xbar, x_start, c_s, l_s, u_s, c_o, l_o, u_o, cs};
+    return a[k];
+  }
+  __device__ Pre staged(int32_t, const double* st, int ld) const {
+    return {st[0], st[ld], st[2 * ld], st[3 * ld], st[4 * ld], st[5 * ld], st[6 * ld], st[7 * ld], st[8 * ld],
+            st[9 * ld]};
+  }
+  __device__ Pre prefetch(int32_t s) const {
+    return {x_cur[s], xbar[s], x_start[s], c_s[s], l_s[s], u_s[s], c_o[s], l_o[s], u_o[s], cs[s]};
+  }
+  __device__ void finish(int32_t s, const double (&a)[2], const Pre& p, double* red) const {
+    const int cls = bound_class(p.lO, p.uO);
 #pragma unroll
     for (int P = 0; P < 2; ++P) {
       const double kty = a[P];
-      const double xv = P == 0 ? x_cur[s] : xbar[s];
+      const double xv = P == 0 ? p.x : p.xb;
       double* o = red + P * kColPer;
-      const double rS = cS - kty;
+      const double rS = p.cS - kty;
       const double lamS = project_reduced(rS, cls);
       const double dS = rS - lamS;
       o[kDuS] += dS * dS;
-      if (lamS > 0.0) o[kBdS] += lS * lamS;
-      else if (lamS < 0.0) o[kBdS] += uS * lamS;
-      const double rO = cO - kty / f;
+      if (lamS > 0.0) o[kBdS] += p.lS * lamS;
+      else if (lamS < 0.0) o[kBdS] += p.uS * lamS;
+      const double rO = p.cO - kty / p.f;
       const double lamO = project_reduced(rO, cls);
       const double dO = rO - lamO;
       o[kDuO] += dO * dO;
-      if (lamO > 0.0) o[kBdO] += lO * lamO;
-      else if (lamO < 0.0) o[kBdO] += uO * lamO;
-      o[kCxS] += cS * xv;
-      o[kCxO] += cO * (xv * f);
-      const double dx = xv - x0;
+      if (lamO > 0.0) o[kBdO] += p.lO * lamO;
+      else if (lamO < 0.0) o[kBdO] += p.uO * lamO;
+      o[kCxS] += p.cS * xv;
+      o[kCxO] += p.cO * (xv * p.f);
+      const double dx = xv - p.x0;
       o[kDx2] += dx * dx;
     }
-    if (!isfinite(x_cur[s])) red[2 * kColPer] += 1.0;
+    if (!isfinite(p.x)) red[2 * kColPer] += 1.0;
   }
 };
 
@@ -249,6 +357,9 @@ struct OpCheckCol {
 struct OpLambda {
   static constexpr int kRhs = 1, kRed = 0;
   static constexpr bool kMax = false;
+  struct Pre {
+    double c, l, u, f;
+  };
   const double* y_s;  // scaled dual
   const double* c_o;
   const double* l_o;
@@ -256,8 +367,18 @@ struct OpLambda {
   const double* cs;
   double* lam;
   __device__ void map(int32_t i, double v, double (&p)[1]) const { p[0] = v * y_s[i]; }
-  __device__ void finish(int32_t s, const double (&a)[1], double*) const {
-    lam[s] = project_reduced(c_o[s] - a[0] / cs[s], bound_class(l_o[s], u_o[s]));
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 4;
+  __device__ const double* operand(int k) const {
+    const double* a[4] = {c_o, l_o, u_o, cs};
+    return a[k];
+  }
+  __device__ Pre staged(int32_t, const double* st, int ld) const {
+    return {st[0], st[ld], st[2 * ld], st[3 * ld]};
+  }
+  __device__ Pre prefetch(int32_t s) const { return {c_o[s], l_o[s], u_o[s], cs[s]}; }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double*) const {
+    lam[s] = project_reduced(p.c - a[0] / p.f, bound_class(p.l, p.u));
   }
 };
 
@@ -265,6 +386,9 @@ struct OpLambda {
 struct OpUnitPrimal {
   static constexpr int kRhs = 1, kRed = 0;
   static constexpr bool kMax = false;
+  struct Pre {
+    double x, c, l, u;
+  };
   const double* y;
   const double* x;
   const double* c;
@@ -273,24 +397,45 @@ struct OpUnitPrimal {
   double step;  // eta / omega
   double* out;
   __device__ void map(int32_t i, double v, double (&p)[1]) const { p[0] = v * y[i]; }
-  __device__ void finish(int32_t s, const double (&a)[1], double*) const {
-    out[s] = clamp_ref(x[s] - step * (c[s] - a[0]), l[s], u[s]);
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 4;
+  __device__ const double* operand(int k) const {
+    const double* a[4] = {x, c, l, u};
+    return a[k];
+  }
+  __device__ Pre staged(int32_t, const double* st, int ld) const {
+    return {st[0], st[ld], st[2 * ld], st[3 * ld]};
+  }
+  __device__ Pre prefetch(int32_t s) const { return {x[s], c[s], l[s], u[s]}; }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double*) const {
+    out[s] = clamp_ref(p.x - step * (p.c - a[0]), p.l, p.u);
   }
 };
 
 struct OpUnitDual {
   static constexpr int kRhs = 1, kRed = 0;
   static constexpr bool kMax = false;
+  struct Pre {
+    double y, q;
+  };
   const double* ext;  // 2 x_new - x_old
   const double* y;
   const double* q;
-  int32_t m1;
+  RowKind rk;  // equality rows (permuted order)
   double step;  // eta * omega
   double* out;
   __device__ void map(int32_t j, double v, double (&p)[1]) const { p[0] = v * ext[j]; }
-  __device__ void finish(int32_t s, const double (&a)[1], double*) const {
-    const double v = y[s] + step * (q[s] - a[0]);
-    out[s] = s < m1 ? v : max0_ref(v);
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 2;
+  __device__ const double* operand(int k) const {
+    const double* a[2] = {y, q};
+    return a[k];
+  }
+  __device__ Pre staged(int32_t, const double* st, int ld) const { return {st[0], st[ld]}; }
+  __device__ Pre prefetch(int32_t s) const { return {y[s], q[s]}; }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double*) const {
+    const double v = p.y + step * (p.q - a[0]);
+    out[s] = rk.eq(s) ? v : max0_ref(v);
   }
 };
 

@@ -3,13 +3,16 @@
 // Reference map (all under /root/reference/proj/core/src):
 //   Solve               solver.cpp:521-543   -> pdhg_solve (abi.cu) = Session + Solve
 //   StackK / VStack     lp_problem.cpp:78-83, sparse_matrix.cpp:90-112 -> Session::Upload
-//   BuildCscFromCsr     sparse_matrix.cpp:71-88 -> Session::BuildCsc (stable radix sort)
+//   BuildCscFromCsr     sparse_matrix.cpp:71-88 -> Session::Permute (stable radix sort)
 //   ComputeScaling      scaling.cpp:49-91    -> Session::ComputeScaling (device)
 //   ApplyScaling        scaling.cpp:93-116   -> Session::ComputeScaling (device)
 //   EstimateOpNorm      solver.cpp:84-110    -> Session::OpNorm
 //   SolveLoop::Run      solver.cpp:232-267   -> Session::Solve
 //   Step                solver.cpp:284-306   -> OpPrimal + OpDual (ops.cuh), CUDA graph per block
 //   Check / Restart     solver.cpp:390-446   -> LaunchCheck + host decision logic
+//
+// Internally rows and columns live in length-class order (engine.cuh); the
+// permutation is applied once at upload and undone at the boundary.
 #include "session.cuh"
 
 #include <cub/cub.cuh>
@@ -22,251 +25,12 @@
 
 #include "host_logic.h"
 #include "ops.cuh"
+#include "setup_kernels.cuh"
 
 namespace pdhg {
 
 namespace {
 
-constexpr int kEw = 256;  // elementwise block size
-
-inline int ew_grid(int64_t n) {
-  int64_t g = (n + kEw - 1) / kEw;
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
-}
-
-#define GRID_STRIDE(i, n) for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
-
-// ---------------------------------------------------------------- setup
-__global__ void k_narrow(const int64_t* in, int32_t* out, int64_t count, int64_t limit, int* bad) {
-  GRID_STRIDE(i, count) {
-    const int64_t v = in[i];
-    if (v < 0 || v >= limit) atomicOr(bad, 1);
-    out[i] = static_cast<int32_t>(v);
-  }
-}
-
-// K row_ptr = [A.row_ptr ; nnz(A) + G.row_ptr[1:]] (VStack, sparse_matrix.cpp:98-103).
-__global__ void k_stack_ptr(const int64_t* ap, const int64_t* gp, int64_t m1, int64_t m2, int64_t nnz_a, int32_t* out) {
-  GRID_STRIDE(i, m1 + m2 + 1) {
-    out[i] = static_cast<int32_t>(i <= m1 ? ap[i] : nnz_a + gp[i - m1]);
-  }
-}
-
-__global__ void k_check_ptr(const int32_t* p, int64_t rows, int64_t nnz, int* bad) {
-  GRID_STRIDE(i, rows) {
-    if (p[i] > p[i + 1]) atomicOr(bad, 2);
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && (p[0] != 0 || p[rows] != nnz)) atomicOr(bad, 2);
-}
-
-// Row id of every CSR nonzero: count row starts, then inclusive scan.
-__global__ void k_row_marks(const int32_t* p, int64_t rows, int64_t nnz, int32_t* cnt) {
-  GRID_STRIDE(r, rows) {
-    if (r >= 1 && p[r] < nnz) atomicAdd(cnt + p[r], 1);
-  }
-}
-
-__global__ void k_iota(int32_t* v, int64_t n) {
-  GRID_STRIDE(i, n) v[i] = static_cast<int32_t>(i);
-}
-
-__global__ void k_csc_gather(const int32_t* perm, const int32_t* row_of, const double* v, int32_t* ri, double* cv,
-                             int64_t nnz) {
-  GRID_STRIDE(q, nnz) {
-    const int32_t k = perm[q];
-    ri[q] = row_of[k];
-    cv[q] = v[k];
-  }
-}
-
-// col_ptr[j] = first CSC slot with column >= j (sorted column keys).
-__global__ void k_colptr(const int32_t* keys, int64_t nnz, int64_t n, int32_t* cp) {
-  GRID_STRIDE(j, n + 1) {
-    int64_t lo = 0, hi = nnz;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (keys[mid] < j) lo = mid + 1;
-      else hi = mid;
-    }
-    cp[j] = static_cast<int32_t>(lo);
-  }
-}
-
-// Scaled (sparse_matrix.cpp:213, :218): (row_scale * v) * col_scale.
-__global__ void k_scale_vals(const int32_t* seg_of, const int32_t* idx, const double* vin, double* vout,
-                             const double* rs, const double* cs, int64_t nnz, int csr_role) {
-  GRID_STRIDE(k, nnz) {
-    const int32_t r = csr_role ? seg_of[k] : idx[k];
-    const int32_t c = csr_role ? idx[k] : seg_of[k];
-    vout[k] = rs[r] * vin[k] * cs[c];
-  }
-}
-
-__global__ void k_fill(double* v, double a, int64_t n) {
-  GRID_STRIDE(i, n) v[i] = a;
-}
-__global__ void k_mul(const double* a, const double* b, double* out, int64_t n) {
-  GRID_STRIDE(i, n) out[i] = a[i] * b[i];
-}
-__global__ void k_div(const double* a, const double* b, double* out, int64_t n) {
-  GRID_STRIDE(i, n) out[i] = a[i] / b[i];
-}
-// x0 = Clamp(0, l, u) (solver.cpp:240-243).
-__global__ void k_clamp0(const double* l, const double* u, double* x, int64_t n) {
-  GRID_STRIDE(i, n) x[i] = clamp_ref(0.0, l[i], u[i]);
-}
-
-// ------------------------------------------------------- tile partitioning
-__device__ int64_t upper_bound_i32(const int32_t* a, int64_t n, int64_t v) {
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (a[mid] <= v) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
-// Effective end position of a segment (its last nonzero; empty segments sit
-// at their start), clamped into the last tile.
-__device__ int64_t seg_end_pos(const int32_t* p, int64_t s, int64_t nnz) {
-  const int64_t b = p[s], e = p[s + 1];
-  const int64_t pos = e > b ? e - 1 : b;
-  return pos < nnz - 1 ? pos : nnz - 1;
-}
-
-__global__ void k_part_begin(const int32_t* p, int32_t nseg, int64_t nnz, int32_t ntiles, int32_t* tb) {
-  GRID_STRIDE(t, (int64_t)ntiles + 1) {
-    int64_t v;
-    if (t == ntiles) {
-      v = nnz;
-    } else if (t == 0) {
-      v = 0;
-    } else {
-      const int64_t pos = t * (int64_t)kTile;
-      const int64_t s = upper_bound_i32(p, nseg + 1, pos) - 1;
-      const int64_t st = p[s], len = p[s + 1] - st;
-      v = (st < pos && len <= kSnap) ? st : pos;
-    }
-    tb[t] = static_cast<int32_t>(v);
-  }
-}
-
-__global__ void k_part_seg(const int32_t* p, int32_t nseg, int64_t nnz, int32_t ntiles, const int32_t* tb,
-                           int32_t* ts) {
-  GRID_STRIDE(t, (int64_t)ntiles + 1) {
-    int64_t v;
-    if (t == 0 || nnz == 0) {
-      v = (t == 0) ? 0 : nseg;
-    } else if (t == ntiles) {
-      v = nseg;
-    } else {
-      const int64_t key = tb[t];
-      int64_t lo = 0, hi = nseg;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (seg_end_pos(p, mid, nnz) < key) lo = mid + 1;
-        else hi = mid;
-      }
-      v = lo;
-    }
-    ts[t] = static_cast<int32_t>(v);
-  }
-}
-
-__global__ void k_part_span(const int32_t* p, int32_t nseg, int64_t nnz, int32_t ntiles, const int32_t* tb,
-                            const int32_t* ts, int32_t* hf, int32_t* to) {
-  GRID_STRIDE(t, (int64_t)ntiles) {
-    const int64_t sb = ts[t], se = ts[t + 1], kb = tb[t], ke = tb[t + 1];
-    int32_t h = -1, o = -1;
-    if (nnz > 0) {
-      if (sb < se && p[sb] < kb) h = static_cast<int32_t>(upper_bound_i32(tb, ntiles + 1, p[sb]) - 1);
-      if (se < nseg && p[se] < ke)
-        o = static_cast<int32_t>(upper_bound_i32(tb, ntiles + 1, seg_end_pos(p, se, nnz)) - 1);
-    }
-    hf[t] = h;
-    to[t] = o;
-  }
-}
-
-// --------------------------------------------------------------- reductions
-// out[i] = sum_t (tile[t][i] + span[t][i]), fixed order; one CTA per output.
-__global__ void k_reduce_tiles(const double* tile, const double* span, int ntiles, int nred, double* out) {
-  __shared__ double sh[kBlock / 32];
-  const int i = blockIdx.x;
-  double acc = 0.0;
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
-    acc += tile[(int64_t)t * nred + i] + (span ? span[(int64_t)t * nred + i] : 0.0);
-  acc = warp_combine<false>(acc);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double v = sh[0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v += sh[w];
-    out[i] = v;
-  }
-}
-
-// Deterministic sum of squares, two stages.
-__global__ void k_sumsq_partial(const double* v, int64_t n, double* part) {
-  __shared__ double sh[kEw / 32];
-  double acc = 0.0;
-  GRID_STRIDE(i, n) acc += v[i] * v[i];
-  acc = warp_combine<false>(acc);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = sh[0];
-    for (int w = 1; w < kEw / 32; ++w) s += sh[w];
-    part[blockIdx.x] = s;
-  }
-}
-
-// Power-iteration normalisation (solver.cpp:103-105): norm = sqrt(sum);
-// norm == 0 ends the estimate with 0 (flagged, host returns 0).
-__global__ void k_power_norm(const double* sum, Scalars* sc) {
-  const double nr = sqrt(sum[0]);
-  if (nr == 0.0) {
-    sc->pw_zero = 1;
-    sc->pw_norm = 1.0;
-  } else {
-    sc->pw_norm = nr;
-  }
-}
-
-// AdaptStepSize (solver.cpp:310-328) from the per-iteration partials.
-__global__ void k_adapt(const double* ctile, const double* cspan, int cnt, const double* rtile, const double* rspan,
-                        int rnt, Scalars* sc, int j) {
-  __shared__ double sh[3][kBlock / 32];
-  double a[3] = {0.0, 0.0, 0.0};
-  for (int t = threadIdx.x; t < cnt; t += blockDim.x) a[0] += ctile[t] + cspan[t];
-  for (int t = threadIdx.x; t < rnt; t += blockDim.x) {
-    a[1] += rtile[2 * t] + rspan[2 * t];
-    a[2] += rtile[2 * t + 1] + rspan[2 * t + 1];
-  }
-  for (int k = 0; k < 3; ++k) {
-    a[k] = warp_combine<false>(a[k]);
-    if ((threadIdx.x & 31) == 0) sh[k][threadIdx.x >> 5] = a[k];
-  }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  double dx = 0, dy = 0, it = 0;
-  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-    dx += sh[0][w];
-    dy += sh[1][w];
-    it += sh[2][w];
-  }
-  it = fabs(it);
-  if (it <= 0.0) return;
-  const double om = sc->omega;
-  const double lim = (om * dx + dy / om) / (2.0 * it);
-  const double k = sc->adapt_iter + static_cast<double>(j) + 1.0;
-  const double a1 = lim * (1.0 - pow(k, -0.3));
-  const double a2 = sc->eta * (1.0 + pow(k, -0.6));
-  sc->eta = (a2 < a1) ? a2 : a1;  // std::min(a1, a2)
-}
-
-template <class T>
 void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw Error(PDHG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
@@ -274,6 +38,44 @@ void check_launch(const char* what) {
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <class T>
+void scan_exclusive(const T* in, T* out, int64_t n, cudaStream_t st) {
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, (int)n, st);
+  DArray<char> tmp;
+  tmp.alloc(tb);
+  PDHG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, (int)n, st));
+  PDHG_CUDA(cudaStreamSynchronize(st));
+}
+
+// seg_of[k] for every nonzero of a compressed layout.
+void segment_ids(const int32_t* ptr, int64_t nseg, int64_t nnz, DArray<int32_t>& out, cudaStream_t st) {
+  out.alloc(nnz);
+  if (!nnz) return;
+  PDHG_CUDA(cudaMemsetAsync(out.p, 0, nnz * sizeof(int32_t), st));
+  k_seg_marks<<<ew_grid(nseg), kEw, 0, st>>>(ptr, nseg, nnz, out.p);
+  size_t tb = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, out.p, out.p, (int)nnz, st);
+  DArray<char> tmp;
+  tmp.alloc(tb);
+  PDHG_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, out.p, out.p, (int)nnz, st));
+  PDHG_CUDA(cudaStreamSynchronize(st));
+}
+
+// Stable sort of segment keys -> permutation new -> old.
+void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, cudaStream_t st) {
+  DArray<int32_t> iota, kout;
+  iota.alloc(std::max<int64_t>(n, 1));
+  kout.alloc(std::max<int64_t>(n, 1));
+  k_iota<<<ew_grid(n), kEw, 0, st>>>(iota.p, n);
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, 3, st);
+  DArray<char> tmp;
+  tmp.alloc(tb);
+  PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, 3, st));
+  PDHG_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace
@@ -295,18 +97,20 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device) : device
   n_ = lp.n;
   offset_ = lp.objective_offset;
   const double t0 = now_s();
-  Upload(lp);
-  BuildCsc();
-  Sync();
-  Partition(csr_);
-  Partition(csc_);
+  {
+    DArray<int32_t> ptr0, idx0;
+    DArray<double> val0;
+    Upload(lp, ptr0, idx0, val0);
+    Permute(ptr0, idx0, val0);
+  }
+  PartitionLong(csr_, csr_st_);
+  PartitionLong(csc_, csc_st_);
   Sync();
   upload_s_ = now_s() - t0;
   const double t1 = now_s();
   ComputeScaling(prm);
   Sync();
   scaling_s_ = now_s() - t1;
-  // Iterate state.
   for (int p = 0; p < 2; ++p) {
     x_[p].alloc(n_, &arena_);
     y_[p].alloc(m_, &arena_);
@@ -321,15 +125,11 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device) : device
   ybest_.alloc(m_, &arena_);
   kxavg_.alloc(m_, &arena_);
   scal_.alloc(1, &arena_);
-  for (int r = 0; r < 2; ++r) {
-    const CMat& M = r == 0 ? csr_ : csc_;
-    const int nred = std::max(kRowRed, kColRed);
-    red_tile_[r].alloc((size_t)M.ntiles * nred, &arena_);
-    red_span_[r].alloc((size_t)M.ntiles * nred, &arena_);
-  }
+  const int nred = std::max(kRowRed, kColRed);
+  red_[0].alloc(static_cast<size_t>(std::max(csr_.parts(), 1)) * nred, &arena_);
+  red_[1].alloc(static_cast<size_t>(std::max(csc_.parts(), 1)) * nred, &arena_);
   red_out_.alloc(64, &arena_);
   DeviceNorms();
-  // Working set of one iteration vs L2 (126 MB on B200).
   const double iter_bytes = 24.0 * nnz_ + 68.0 * (m_ + n_);
   l2_resident_ = iter_bytes < 100e6;
   Sync();
@@ -352,41 +152,38 @@ void Session::Copy(double* dst, const double* src, size_t n) {
 }
 
 // H2D + int64 -> int32 narrowing + VStack of A and G straight into K's CSR.
-void Session::Upload(const pdhg_lp& lp) {
+void Session::Upload(const pdhg_lp& lp, DArray<int32_t>& ptr0, DArray<int32_t>& idx0, DArray<double>& val0) {
   const int64_t nnz_a = lp.a.rows ? lp.a.row_ptr[lp.a.rows] : 0;
   const int64_t nnz_g = lp.g.rows ? lp.g.row_ptr[lp.g.rows] : 0;
   nnz_ = nnz_a + nnz_g;
   if (nnz_ >= (int64_t(1) << 31) - kTile || m_ >= (int64_t(1) << 31) - 1 || n_ >= (int64_t(1) << 31) - 1)
     throw Error(PDHG_INVALID_ARGUMENT, "problem too large for int32 device indices (nnz, rows, cols < 2^31)");
-  csr_ptr_.alloc(m_ + 1, &arena_);
-  csr_idx_.alloc(nnz_, &arena_);
-  csr_val_.alloc(nnz_, &arena_);
+  ptr0.alloc(m_ + 1);
+  idx0.alloc(std::max<int64_t>(nnz_, 1));
+  val0.alloc(std::max<int64_t>(nnz_, 1));
   DArray<int64_t> stage;
   stage.alloc(std::max<int64_t>({nnz_a, nnz_g, m1_ + 1, m2_ + 1, 1}) * 2);
   DArray<int> bad;
   bad.alloc(1);
   PDHG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st_));
-  // Row pointers.
   int64_t* ap = stage.p;
   int64_t* gp = stage.p + std::max<int64_t>(m1_ + 1, 1);
   PDHG_CUDA(cudaMemcpyAsync(ap, lp.a.row_ptr, (m1_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
   PDHG_CUDA(cudaMemcpyAsync(gp, lp.g.row_ptr, (m2_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
-  k_stack_ptr<<<ew_grid(m_ + 1), kEw, 0, st_>>>(ap, gp, m1_, m2_, nnz_a, csr_ptr_.p);
+  k_stack_ptr<<<ew_grid(m_ + 1), kEw, 0, st_>>>(ap, gp, m1_, m2_, nnz_a, ptr0.p);
   Sync();
-  // Column indices and values.
   if (nnz_a) {
     PDHG_CUDA(cudaMemcpyAsync(stage.p, lp.a.col_idx, nnz_a * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
-    k_narrow<<<ew_grid(nnz_a), kEw, 0, st_>>>(stage.p, csr_idx_.p, nnz_a, n_, bad.p);
-    PDHG_CUDA(cudaMemcpyAsync(csr_val_.p, lp.a.values, nnz_a * sizeof(double), cudaMemcpyHostToDevice, st_));
+    k_narrow<<<ew_grid(nnz_a), kEw, 0, st_>>>(stage.p, idx0.p, nnz_a, n_, bad.p);
+    PDHG_CUDA(cudaMemcpyAsync(val0.p, lp.a.values, nnz_a * sizeof(double), cudaMemcpyHostToDevice, st_));
     Sync();
   }
   if (nnz_g) {
     PDHG_CUDA(cudaMemcpyAsync(stage.p, lp.g.col_idx, nnz_g * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
-    k_narrow<<<ew_grid(nnz_g), kEw, 0, st_>>>(stage.p, csr_idx_.p + nnz_a, nnz_g, n_, bad.p);
-    PDHG_CUDA(cudaMemcpyAsync(csr_val_.p + nnz_a, lp.g.values, nnz_g * sizeof(double), cudaMemcpyHostToDevice, st_));
+    k_narrow<<<ew_grid(nnz_g), kEw, 0, st_>>>(stage.p, idx0.p + nnz_a, nnz_g, n_, bad.p);
+    PDHG_CUDA(cudaMemcpyAsync(val0.p + nnz_a, lp.g.values, nnz_g * sizeof(double), cudaMemcpyHostToDevice, st_));
   }
-  k_check_ptr<<<ew_grid(m_), kEw, 0, st_>>>(csr_ptr_.p, m_, nnz_, bad.p);
-  // Vectors (original space).
+  k_check_ptr<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, nnz_, bad.p);
   c_o_.alloc(n_, &arena_);
   l_o_.alloc(n_, &arena_);
   u_o_.alloc(n_, &arena_);
@@ -404,76 +201,188 @@ void Session::Upload(const pdhg_lp& lp) {
   Sync();
   if (hbad & 1) throw Error(PDHG_INVALID_ARGUMENT, "column index out of range");
   if (hbad & 2) throw Error(PDHG_INVALID_ARGUMENT, "row_ptr is not a valid CSR offset array");
-  csr_.nseg = static_cast<int32_t>(m_);
-  csr_.nvec = static_cast<int32_t>(n_);
-  csr_.nnz = nnz_;
-  csr_.ptr = csr_ptr_.p;
-  csr_.idx = csr_idx_.p;
-  csr_.val = csr_val_.p;
+  check_launch("upload");
 }
 
-// CSC of K via a stable radix sort of (column, CSR position): rows stay in
-// ascending order inside each column, as BuildCscFromCsr guarantees.
-void Session::BuildCsc() {
-  csc_ptr_.alloc(n_ + 1, &arena_);
-  csc_idx_.alloc(nnz_, &arena_);
-  csc_val_.alloc(nnz_, &arena_);
-  csc_.nseg = static_cast<int32_t>(n_);
-  csc_.nvec = static_cast<int32_t>(m_);
-  csc_.nnz = nnz_;
-  csc_.ptr = csc_ptr_.p;
-  csc_.idx = csc_idx_.p;
-  csc_.val = csc_val_.p;
-  if (nnz_ == 0) {
-    PDHG_CUDA(cudaMemsetAsync(csc_ptr_.p, 0, (n_ + 1) * sizeof(int32_t), st_));
-    return;
+// Builds the CSC of K (stable radix sort of (column, CSR position): rows stay
+// ascending inside each column, as BuildCscFromCsr guarantees), then permutes
+// rows and columns into length classes (engine.cuh) for both layouts,
+// keeping every segment's internal order.
+void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, const DArray<double>& val0) {
+  // --- original-order CSC
+  DArray<int32_t> cptr0, ridx0, row_of;
+  DArray<double> cval0;
+  cptr0.alloc(n_ + 1);
+  ridx0.alloc(std::max<int64_t>(nnz_, 1));
+  cval0.alloc(std::max<int64_t>(nnz_, 1));
+  segment_ids(ptr0.p, m_, nnz_, row_of, st_);
+  if (nnz_ > 0) {
+    DArray<int32_t> perm_in, perm_out, keys_out;
+    perm_in.alloc(nnz_);
+    perm_out.alloc(nnz_);
+    keys_out.alloc(nnz_);
+    int end_bit = 1;
+    while ((int64_t(1) << end_bit) <= n_) ++end_bit;
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, idx0.p, keys_out.p, perm_in.p, perm_out.p, (int)nnz_, 0, end_bit,
+                                    st_);
+    DArray<char> tmp;
+    tmp.alloc(tb);
+    k_iota<<<ew_grid(nnz_), kEw, 0, st_>>>(perm_in.p, nnz_);
+    PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, idx0.p, keys_out.p, perm_in.p, perm_out.p, (int)nnz_, 0,
+                                              end_bit, st_));
+    k_csc_gather<<<ew_grid(nnz_), kEw, 0, st_>>>(perm_out.p, row_of.p, val0.p, ridx0.p, cval0.p, nnz_);
+    k_colptr<<<ew_grid(n_ + 1), kEw, 0, st_>>>(keys_out.p, nnz_, n_, cptr0.p);
+    Sync();
+  } else {
+    PDHG_CUDA(cudaMemsetAsync(cptr0.p, 0, (n_ + 1) * sizeof(int32_t), st_));
   }
-  DArray<int32_t> row_of, perm_in, perm_out, keys_out;
-  row_of.alloc(nnz_);
-  perm_in.alloc(nnz_);
-  perm_out.alloc(nnz_);
-  keys_out.alloc(nnz_);
-  PDHG_CUDA(cudaMemsetAsync(row_of.p, 0, nnz_ * sizeof(int32_t), st_));
-  k_row_marks<<<ew_grid(m_), kEw, 0, st_>>>(csr_ptr_.p, m_, nnz_, row_of.p);
-  size_t tmp_bytes = 0, tmp2 = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, row_of.p, row_of.p, (int)nnz_, st_);
-  int end_bit = 1;
-  while ((int64_t(1) << end_bit) <= n_) ++end_bit;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp2, csr_idx_.p, keys_out.p, perm_in.p, perm_out.p, (int)nnz_, 0,
-                                  end_bit, st_);
-  DArray<char> tmp;
-  tmp.alloc(std::max(tmp_bytes, tmp2));
-  PDHG_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tmp_bytes, row_of.p, row_of.p, (int)nnz_, st_));
-  k_iota<<<ew_grid(nnz_), kEw, 0, st_>>>(perm_in.p, nnz_);
-  PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp2, csr_idx_.p, keys_out.p, perm_in.p, perm_out.p, (int)nnz_, 0,
-                                            end_bit, st_));
-  k_csc_gather<<<ew_grid(nnz_), kEw, 0, st_>>>(perm_out.p, row_of.p, csr_val_.p, csc_idx_.p, csc_val_.p, nnz_);
-  k_colptr<<<ew_grid(n_ + 1), kEw, 0, st_>>>(keys_out.p, nnz_, n_, csc_ptr_.p);
+  // --- length classes: key = class * 2 + inequality row
+  perm_r_.alloc(std::max<int64_t>(m_, 1), &arena_);
+  inv_r_.alloc(std::max<int64_t>(m_, 1), &arena_);
+  perm_c_.alloc(std::max<int64_t>(n_, 1), &arena_);
+  inv_c_.alloc(std::max<int64_t>(n_, 1), &arena_);
+  int hr[8] = {0}, hc[8] = {0};
+  {
+    DArray<int32_t> kr, kc, hist;
+    kr.alloc(std::max<int64_t>(m_, 1));
+    kc.alloc(std::max<int64_t>(n_, 1));
+    hist.alloc(16);
+    PDHG_CUDA(cudaMemsetAsync(hist.p, 0, 16 * sizeof(int32_t), st_));
+    k_class_keys<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, m1_, kr.p);
+    k_class_keys<<<ew_grid(n_), kEw, 0, st_>>>(cptr0.p, n_, n_, kc.p);
+    k_key_hist<<<ew_grid(m_), kEw, 0, st_>>>(kr.p, m_, hist.p);
+    k_key_hist<<<ew_grid(n_), kEw, 0, st_>>>(kc.p, n_, hist.p + 8);
+    if (m_) stable_order(kr.p, m_, perm_r_, st_);
+    if (n_) stable_order(kc.p, n_, perm_c_, st_);
+    int h[16];
+    PDHG_CUDA(cudaMemcpyAsync(h, hist.p, sizeof(h), cudaMemcpyDeviceToHost, st_));
+    Sync();
+    std::copy(h, h + 8, hr);
+    std::copy(h + 8, h + 16, hc);
+  }
+  k_invert<<<ew_grid(m_), kEw, 0, st_>>>(perm_r_.p, inv_r_.p, m_);
+  k_invert<<<ew_grid(n_), kEw, 0, st_>>>(perm_c_.p, inv_c_.p, n_);
+  rk_.e0 = hr[0];
+  rk_.s1 = hr[0] + hr[1];
+  rk_.e1 = rk_.s1 + hr[2];
+  rk_.s2 = rk_.s1 + hr[2] + hr[3];
+  rk_.e2 = rk_.s2 + hr[4];
+  rk_.s3 = rk_.s2 + hr[4] + hr[5];
+  rk_.e3 = rk_.s3 + hr[6];
+  // --- permuted layouts
+  auto build = [&](Layout& L, Store& S, const DArray<int32_t>& p0, const DArray<int32_t>& i0,
+                   const DArray<double>& v0, const DArray<int32_t>& seg_of, int64_t nseg, int64_t nvec,
+                   const DArray<int32_t>& perm, const DArray<int32_t>& inv_seg, const DArray<int32_t>& inv_other) {
+    S.ptr.alloc(nseg + 1, &arena_);
+    S.idx.alloc(std::max<int64_t>(nnz_, 1), &arena_);
+    S.val.alloc(std::max<int64_t>(nnz_, 1), &arena_);
+    DArray<int32_t> len;
+    len.alloc(nseg + 1);
+    PDHG_CUDA(cudaMemsetAsync(len.p, 0, (nseg + 1) * sizeof(int32_t), st_));
+    k_perm_len<<<ew_grid(nseg), kEw, 0, st_>>>(p0.p, perm.p, nseg, len.p);
+    scan_exclusive(len.p, S.ptr.p, nseg + 1, st_);
+    if (nnz_)
+      k_perm_nnz<<<ew_grid(nnz_), kEw, 0, st_>>>(p0.p, seg_of.p, i0.p, v0.p, inv_seg.p, inv_other.p, S.ptr.p,
+                                                  S.idx.p, S.val.p, nnz_);
+    L.nseg = static_cast<int32_t>(nseg);
+    L.nvec = static_cast<int32_t>(nvec);
+    L.nnz = nnz_;
+    L.ptr = S.ptr.p;
+    L.idx = S.idx.p;
+    L.val = S.val.p;
+  };
+  build(csr_, csr_st_, ptr0, idx0, val0, row_of, m_, n_, perm_r_, inv_r_, inv_c_);
+  csr_.s1 = rk_.s1;
+  csr_.s2 = rk_.s2;
+  csr_.s3 = rk_.s3;
+  {
+    DArray<int32_t> col_of;
+    segment_ids(cptr0.p, n_, nnz_, col_of, st_);
+    build(csc_, csc_st_, cptr0, ridx0, cval0, col_of, n_, m_, perm_c_, inv_c_, inv_r_);
+    Sync();
+  }
+  csc_.s1 = hc[0] + hc[1];
+  csc_.s2 = csc_.s1 + hc[2] + hc[3];
+  csc_.s3 = csc_.s2 + hc[4] + hc[5];
+  ptr0_.alloc(m_ + 1, &arena_);
+  PDHG_CUDA(cudaMemcpyAsync(ptr0_.p, ptr0.p, (m_ + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st_));
+  // --- vectors into internal order
+  DArray<double> tmp;
+  tmp.alloc(std::max<int64_t>(std::max(m_, n_), 1));
+  auto perm_vec = [&](DArray<double>& v, const DArray<int32_t>& perm, int64_t k) {
+    if (!k) return;
+    Copy(tmp.p, v.p, k);
+    k_gather<<<ew_grid(k), kEw, 0, st_>>>(tmp.p, perm.p, v.p, k);
+  };
+  perm_vec(c_o_, perm_c_, n_);
+  perm_vec(l_o_, perm_c_, n_);
+  perm_vec(u_o_, perm_c_, n_);
+  perm_vec(q_o_, perm_r_, m_);
   Sync();
+  check_launch("permute");
 }
 
-// Tile partition of one layout (see tile_spmv.cuh).
-void Session::Partition(CMat& M) {
-  const int r = (&M == &csr_) ? 0 : 1;
-  M.ntiles = std::max(1, ceil_div(M.nnz, kTile));
-  for (int k = 0; k < 4; ++k) part_[r][k].alloc(M.ntiles + 1, &arena_);
-  head_[r].alloc(2 * (size_t)M.ntiles, &arena_);
-  tail_[r].alloc(2 * (size_t)M.ntiles, &arena_);
-  cnt_[r].alloc(M.ntiles, &arena_);
-  PDHG_CUDA(cudaMemsetAsync(cnt_[r].p, 0, M.ntiles * sizeof(unsigned), st_));
-  M.tile_begin = part_[r][0].p;
-  M.tile_seg = part_[r][1].p;
-  M.head_first = part_[r][2].p;
-  M.tail_owner = part_[r][3].p;
-  M.head_part = head_[r].p;
-  M.tail_part = tail_[r].p;
-  M.counter = cnt_[r].p;
-  const int g = ew_grid(M.ntiles + 1);
-  k_part_begin<<<g, kEw, 0, st_>>>(M.ptr, M.nseg, M.nnz, M.ntiles, M.tile_begin);
-  k_part_seg<<<g, kEw, 0, st_>>>(M.ptr, M.nseg, M.nnz, M.ntiles, M.tile_begin, M.tile_seg);
-  k_part_span<<<g, kEw, 0, st_>>>(M.ptr, M.nseg, M.nnz, M.ntiles, M.tile_begin, M.tile_seg, M.head_first,
-                                  M.tail_owner);
-  check_launch<int>("partition");
+// Tile partition of the extra-long class [s3, nseg) of one layout (tile_spmv.cuh):
+// sorted unique boundary candidates, owned-segment ranges, cross-tile links.
+void Session::PartitionLong(Layout& L, Store& S) {
+  CMat& M = L.lng;
+  M.nseg = L.nseg;
+  M.nvec = L.nvec;
+  M.nnz = L.nnz;
+  M.ptr = L.ptr;
+  M.idx = L.idx;
+  M.val = L.val;
+  M.ntiles = 0;
+  if (L.nseg <= L.s3) return;
+  const int32_t lo = L.s3, hi = L.nseg;
+  int32_t nz0 = 0;
+  PDHG_CUDA(cudaMemcpyAsync(&nz0, L.ptr + lo, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+  Sync();
+  const int64_t nz1 = L.nnz;
+  const int ngroups = ceil_div(hi - lo, kBlock);
+  const int ncuts = std::max(0, ceil_div(nz1 - nz0, kTile) - 1);
+  const int nc = ngroups + ncuts;
+  DArray<int32_t> cand, sorted, uniq, nsel;
+  cand.alloc(nc);
+  sorted.alloc(nc);
+  uniq.alloc(nc + 1);
+  nsel.alloc(1);
+  k_part_cand<<<ew_grid(nc), kEw, 0, st_>>>(L.ptr, lo, hi, nz0, nz1, ngroups, ncuts, cand.p);
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, t1, cand.p, sorted.p, nc, 0, 32, st_);
+  cub::DeviceSelect::Unique(nullptr, t2, sorted.p, uniq.p, nsel.p, nc, st_);
+  DArray<char> tmp;
+  tmp.alloc(std::max(t1, t2));
+  PDHG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, t1, cand.p, sorted.p, nc, 0, 32, st_));
+  PDHG_CUDA(cub::DeviceSelect::Unique(tmp.p, t2, sorted.p, uniq.p, nsel.p, nc, st_));
+  int nu = 0, last = 0;
+  PDHG_CUDA(cudaMemcpyAsync(&nu, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  Sync();
+  PDHG_CUDA(cudaMemcpyAsync(&last, uniq.p + nu - 1, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  Sync();
+  const int ntiles = (last == INT32_MAX) ? nu - 1 : nu;
+  M.ntiles = ntiles;
+  for (int k = 0; k < 4; ++k) S.part[k].alloc(ntiles + 1, &arena_);
+  S.head.alloc(2 * (size_t)ntiles, &arena_);
+  S.tail.alloc(2 * (size_t)ntiles, &arena_);
+  S.cnt.alloc(ntiles, &arena_);
+  PDHG_CUDA(cudaMemsetAsync(S.cnt.p, 0, ntiles * sizeof(unsigned), st_));
+  M.tile_begin = S.part[0].p;
+  M.tile_seg = S.part[1].p;
+  M.head_first = S.part[2].p;
+  M.tail_owner = S.part[3].p;
+  M.head_part = S.head.p;
+  M.tail_part = S.tail.p;
+  M.counter = S.cnt.p;
+  const int32_t end = static_cast<int32_t>(nz1);
+  PDHG_CUDA(cudaMemcpyAsync(M.tile_begin, uniq.p, ntiles * sizeof(int32_t), cudaMemcpyDeviceToDevice, st_));
+  PDHG_CUDA(cudaMemcpyAsync(M.tile_begin + ntiles, &end, sizeof(int32_t), cudaMemcpyHostToDevice, st_));
+  const int g = ew_grid(ntiles + 1);
+  k_part_seg<<<g, kEw, 0, st_>>>(L.ptr, lo, hi, nz1, ntiles, M.tile_begin, M.tile_seg);
+  k_part_span<<<g, kEw, 0, st_>>>(L.ptr, hi, nz1, ntiles, M.tile_begin, M.tile_seg, M.head_first, M.tail_owner);
+  Sync();
+  check_launch("partition");
 }
 
 // Ruiz x10 + Pock-Chambolle on device (scaling.cpp:49-91), then
@@ -496,52 +405,40 @@ void Session::ComputeScaling(const pdhg_params& prm) {
     throw Error(PDHG_INVALID_ARGUMENT, "pock-chambolle alpha must lie in [0, 2]");
   if (scaled_ && nnz_ > 0) {
     DArray<int32_t> row_of, col_of;
-    row_of.alloc(nnz_);
-    col_of.alloc(nnz_);
-    PDHG_CUDA(cudaMemsetAsync(row_of.p, 0, nnz_ * sizeof(int32_t), st_));
-    k_row_marks<<<ew_grid(m_), kEw, 0, st_>>>(csr_ptr_.p, m_, nnz_, row_of.p);
-    PDHG_CUDA(cudaMemsetAsync(col_of.p, 0, nnz_ * sizeof(int32_t), st_));
-    k_row_marks<<<ew_grid(n_), kEw, 0, st_>>>(csc_ptr_.p, n_, nnz_, col_of.p);
-    {
-      size_t tb = 0;
-      cub::DeviceScan::InclusiveSum(nullptr, tb, row_of.p, row_of.p, (int)nnz_, st_);
-      DArray<char> tmp;
-      tmp.alloc(tb);
-      PDHG_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, row_of.p, row_of.p, (int)nnz_, st_));
-      PDHG_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, col_of.p, col_of.p, (int)nnz_, st_));
-    }
+    segment_ids(csr_.ptr, m_, nnz_, row_of, st_);
+    segment_ids(csc_.ptr, n_, nnz_, col_of, st_);
     DArray<double> orig_r, orig_c, dr, dc;
     orig_r.alloc(nnz_);
     orig_c.alloc(nnz_);
     dr.alloc(m_);
     dc.alloc(n_);
-    Copy(orig_r.p, csr_val_.p, nnz_);
-    Copy(orig_c.p, csc_val_.p, nnz_);
+    Copy(orig_r.p, csr_.val, nnz_);
+    Copy(orig_c.p, csc_.val, nnz_);
+    const RedSlots none{};
     for (int s = 0; s < prm.ruiz_iters; ++s) {
-      launch_tiles(csr_, OpInfNormScale{dr.p, rs_.p}, nullptr, nullptr, st_);
-      launch_tiles(csc_, OpInfNormScale{dc.p, cs_.p}, nullptr, nullptr, st_);
-      k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(row_of.p, csr_idx_.p, csr_val_.p, csr_val_.p, dr.p, dc.p, nnz_, 1);
-      k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(col_of.p, csc_idx_.p, csc_val_.p, csc_val_.p, dr.p, dc.p, nnz_, 0);
+      run_pass(csr_, OpInfNormScale{dr.p, rs_.p}, none, st_);
+      run_pass(csc_, OpInfNormScale{dc.p, cs_.p}, none, st_);
+      k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(row_of.p, csr_.idx, csr_.val, csr_.val, dr.p, dc.p, nnz_, 1);
+      k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(col_of.p, csc_.idx, csc_.val, csc_.val, dr.p, dc.p, nnz_, 0);
     }
     // PC on K.Scaled(ruiz) recomputed from the original values (scaling.cpp:89).
-    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(row_of.p, csr_idx_.p, orig_r.p, csr_val_.p, rs_.p, cs_.p, nnz_, 1);
-    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(col_of.p, csc_idx_.p, orig_c.p, csc_val_.p, rs_.p, cs_.p, nnz_, 0);
+    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(row_of.p, csr_.idx, orig_r.p, csr_.val, rs_.p, cs_.p, nnz_, 1);
+    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(col_of.p, csc_.idx, orig_c.p, csc_.val, rs_.p, cs_.p, nnz_, 0);
     auto mode_of = [](double p) { return p == 0.0 ? 0 : (p == 1.0 ? 1 : (p == 2.0 ? 2 : 3)); };
     const double pr = 2.0 - prm.pc_alpha, pc = prm.pc_alpha;
-    launch_tiles(csr_, OpPowerSumScale{pr, mode_of(pr), rs_.p}, nullptr, nullptr, st_);
-    launch_tiles(csc_, OpPowerSumScale{pc, mode_of(pc), cs_.p}, nullptr, nullptr, st_);
+    run_pass(csr_, OpPowerSumScale{pr, mode_of(pr), rs_.p}, none, st_);
+    run_pass(csc_, OpPowerSumScale{pc, mode_of(pc), cs_.p}, none, st_);
     // Final K_s from the original values (ApplyScaling, scaling.cpp:105-106).
-    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(row_of.p, csr_idx_.p, orig_r.p, csr_val_.p, rs_.p, cs_.p, nnz_, 1);
-    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(col_of.p, csc_idx_.p, orig_c.p, csc_val_.p, rs_.p, cs_.p, nnz_, 0);
-    check_launch<int>("scaling");
+    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(row_of.p, csr_.idx, orig_r.p, csr_.val, rs_.p, cs_.p, nnz_, 1);
+    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(col_of.p, csc_.idx, orig_c.p, csc_.val, rs_.p, cs_.p, nnz_, 0);
+    check_launch("scaling");
     Sync();
   }
-  // Vectors (scaling.cpp:107-115). With identity scales these are exact copies.
   k_mul<<<ew_grid(n_), kEw, 0, st_>>>(c_o_.p, cs_.p, c_s_.p, n_);
   k_div<<<ew_grid(n_), kEw, 0, st_>>>(l_o_.p, cs_.p, l_s_.p, n_);
   k_div<<<ew_grid(n_), kEw, 0, st_>>>(u_o_.p, cs_.p, u_s_.p, n_);
   k_mul<<<ew_grid(m_), kEw, 0, st_>>>(q_o_.p, rs_.p, q_s_.p, m_);
-  check_launch<int>("apply scaling");
+  check_launch("apply scaling");
 }
 
 // ||c||, ||q|| in both spaces (kkt.cpp:45-56), deterministic device sums.
@@ -565,36 +462,55 @@ void Session::DeviceNorms() {
   q_norm_o_ = std::sqrt(h[3]);
 }
 
+void Session::ToInternal(const double* host, const DArray<int32_t>& perm, double* dev, int64_t n) {
+  if (!n) return;
+  DArray<double> tmp;
+  tmp.alloc(n);
+  PDHG_CUDA(cudaMemcpyAsync(tmp.p, host, n * sizeof(double), cudaMemcpyHostToDevice, st_));
+  k_gather<<<ew_grid(n), kEw, 0, st_>>>(tmp.p, perm.p, dev, n);
+  Sync();
+}
+
+void Session::ToHost(const double* dev, const double* scale, const DArray<int32_t>& inv, double* host, int64_t n) {
+  if (!n || !host) return;
+  DArray<double> tmp;
+  tmp.alloc(n);
+  k_unpermute<<<ew_grid(n), kEw, 0, st_>>>(dev, scale, inv.p, tmp.p, n);
+  PDHG_CUDA(cudaMemcpyAsync(host, tmp.p, n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  Sync();
+}
+
 // ================================================================== kernels
 void Session::LaunchStep(int parity, int j, bool adapt) {
   const int a = parity, b = 1 - parity;
-  launches_ += adapt ? 3 : 2;
+  launches_ += pass_launches(csc_) + pass_launches(csr_) + (adapt ? 1 : 0);
   if (adapt) {
-    launch_tiles(csc_, OpPrimal<true>{y_[a].p, x_[a].p, x_[b].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, j},
-                 red_tile_[1].p, red_span_[1].p, st_);
-    launch_tiles(csr_, OpDual<true>{x_[b].p, y_[a].p, y_[b].p, ybar_.p, kx_[a].p, kx_[b].p, q_s_.p, (int32_t)m1_, scal_.p, j},
-                 red_tile_[0].p, red_span_[0].p, st_);
-    k_adapt<<<1, kBlock, 0, st_>>>(red_tile_[1].p, red_span_[1].p, csc_.ntiles, red_tile_[0].p, red_span_[0].p,
-                                   csr_.ntiles, scal_.p, j);
+    run_pass(csc_, OpPrimal<true>{y_[a].p, x_[a].p, x_[b].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, j},
+             RedSlots{red_[1].p}, st_);
+    run_pass(csr_, OpDual<true>{x_[b].p, y_[a].p, y_[b].p, ybar_.p, kx_[a].p, kx_[b].p, q_s_.p, rk_, scal_.p, j},
+             RedSlots{red_[0].p}, st_);
+    k_adapt<<<1, kBlock, 0, st_>>>(red_[1].p, csc_.parts(), red_[0].p, csr_.parts(), scal_.p, j);
   } else {
-    launch_tiles(csc_, OpPrimal<false>{y_[a].p, x_[a].p, x_[b].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, j},
-                 nullptr, nullptr, st_);
-    launch_tiles(csr_, OpDual<false>{x_[b].p, y_[a].p, y_[b].p, ybar_.p, kx_[a].p, kx_[b].p, q_s_.p, (int32_t)m1_, scal_.p, j},
-                 nullptr, nullptr, st_);
+    run_pass(csc_, OpPrimal<false>{y_[a].p, x_[a].p, x_[b].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, j},
+             RedSlots{}, st_);
+    run_pass(csr_, OpDual<false>{x_[b].p, y_[a].p, y_[b].p, ybar_.p, kx_[a].p, kx_[b].p, q_s_.p, rk_, scal_.p, j},
+             RedSlots{}, st_);
   }
 }
 
-// `count` PDHG iterations starting from buffer `parity`. Full check blocks are
-// replayed from a captured CUDA graph (one per parity/length/adapt combo).
+// `count` PDHG iterations starting from buffer `parity`. Blocks are replayed
+// from captured CUDA graphs (one per parity/length/adapt combination).
 void Session::RunSteps(int parity, int count, bool adapt) {
   Graph* g = nullptr;
   for (Graph& gg : graphs_)
     if (gg.steps == count && gg.parity == parity && gg.adapt == adapt) g = &gg;
   if (!g && count >= 4) {
     cudaGraph_t graph;
+    const int64_t before = launches_;
     PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
     for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
     PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
+    launches_ = before;
     Graph ng;
     ng.steps = count;
     ng.parity = parity;
@@ -605,24 +521,23 @@ void Session::RunSteps(int parity, int count, bool adapt) {
     g = &graphs_.back();
   }
   if (g) {
-    launches_ += static_cast<int64_t>(count) * (adapt ? 3 : 2);
+    launches_ += static_cast<int64_t>(count) * (pass_launches(csc_) + pass_launches(csr_) + (adapt ? 1 : 0));
     PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
   } else {
     for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
   }
-  check_launch<int>("pdhg steps");
+  check_launch("pdhg steps");
 }
 
 void Session::LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx) {
-  launches_ += 4;
-  OpCheckRow row{xb, kxavg_.p, kx, y, yb, ystart_.p, q_s_.p, q_o_.p, rs_.p, (int32_t)m1_};
-  launch_tiles(csr_, row, red_tile_[0].p, red_span_[0].p, st_);
+  launches_ += pass_launches(csr_) + pass_launches(csc_) + 2;
+  OpCheckRow row{xb, kxavg_.p, kx, y, yb, ystart_.p, q_s_.p, q_o_.p, rs_.p, rk_};
+  run_pass(csr_, row, RedSlots{red_[0].p}, st_);
   OpCheckCol col{y, yb, x, xb, xstart_.p, c_s_.p, l_s_.p, u_s_.p, c_o_.p, l_o_.p, u_o_.p, cs_.p};
-  launch_tiles(csc_, col, red_tile_[1].p, red_span_[1].p, st_);
-  k_reduce_tiles<<<kRowRed, kBlock, 0, st_>>>(red_tile_[0].p, red_span_[0].p, csr_.ntiles, kRowRed, red_out_.p);
-  k_reduce_tiles<<<kColRed, kBlock, 0, st_>>>(red_tile_[1].p, red_span_[1].p, csc_.ntiles, kColRed,
-                                              red_out_.p + kRowRed);
-  check_launch<int>("check");
+  run_pass(csc_, col, RedSlots{red_[1].p}, st_);
+  k_reduce_tiles<<<kRowRed, kBlock, 0, st_>>>(red_[0].p, nullptr, csr_.parts(), kRowRed, red_out_.p);
+  k_reduce_tiles<<<kColRed, kBlock, 0, st_>>>(red_[1].p, nullptr, csc_.parts(), kColRed, red_out_.p + kRowRed);
+  check_launch("check");
 }
 
 void Session::ReadCheck(CheckOut* out) {
@@ -632,10 +547,6 @@ void Session::ReadCheck(CheckOut* out) {
 }
 
 // ================================================================ solve loop
-namespace {
-
-}  // namespace
-
 void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_result* out) {
   PDHG_CUDA(cudaSetDevice(device_));
   if (!ev_[0]) {
@@ -661,7 +572,8 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   int par = 0;
   k_clamp0<<<ew_grid(n_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, n_);
   if (m_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, m_ * sizeof(double), st_));
-  launch_tiles(csr_, OpSpmv{x_[0].p, kx_[0].p}, nullptr, nullptr, st_);
+  run_pass(csr_, OpSpmv{x_[0].p, kx_[0].p}, RedSlots{}, st_);
+  launches_ += 1 + pass_launches(csr_);
 
   int64_t iters = 0, inner = 0, restarts = 0;
   double kkt_start = 0.0, kkt_prev = std::numeric_limits<double>::infinity();
@@ -706,8 +618,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   };
 
   // Start point: scaled KKT for the loop start and the first termination test
-  // (solver.cpp:246-249). The running average is not formed yet: evaluate
-  // the current point as both operands.
+  // (solver.cpp:246-249); the current point stands in for the average.
   LaunchCheck(x_[0].p, y_[0].p, x_[0].p, y_[0].p, kx_[0].p);
   ReadCheck(&ck);
   pdhg_report s_cur, o_cur, s_avg, o_avg;
@@ -831,26 +742,18 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   }
 
   // Finish (solver.cpp:473-481): unscale best, lambda on the original problem.
-  if (out->x) {
-    k_mul<<<ew_grid(n_), kEw, 0, st_>>>(xbest_.p, cs_.p, nvec_.p, n_);
-    PDHG_CUDA(cudaMemcpyAsync(out->x, nvec_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
-    Sync();
-  }
-  if (out->y) {
-    k_mul<<<ew_grid(m_), kEw, 0, st_>>>(ybest_.p, rs_.p, kxavg_.p, m_);
-    PDHG_CUDA(cudaMemcpyAsync(out->y, kxavg_.p, m_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
-    Sync();
-  }
+  ToHost(xbest_.p, cs_.p, inv_c_, out->x, n_);
+  ToHost(ybest_.p, rs_.p, inv_r_, out->y, m_);
   if (out->lambda) {
-    launch_tiles(csc_, OpLambda{ybest_.p, c_o_.p, l_o_.p, u_o_.p, cs_.p, nvec_.p}, nullptr, nullptr, st_);
-    PDHG_CUDA(cudaMemcpyAsync(out->lambda, nvec_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    run_pass(csc_, OpLambda{ybest_.p, c_o_.p, l_o_.p, u_o_.p, cs_.p, nvec_.p}, RedSlots{}, st_);
+    ToHost(nvec_.p, nullptr, inv_c_, out->lambda, n_);
   }
   PDHG_CUDA(cudaEventRecord(ev_[1], st_));
   Sync();
   float ms = 0.f;
   PDHG_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
   last_ms_ = ms;
-  last_launches_ = launches_ + 4;  // + clamp0, kx0 SpMV, unscale/lambda kernels
+  last_launches_ = launches_ + 3 + pass_launches(csc_);
   out->status = status;
   out->report = best_rep;
   out->iterations = iters;
@@ -860,7 +763,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 }
 
 // EstimateOpNorm (solver.cpp:84-110) with the host start vector drawn from the
-// same libstdc++ engines as the reference.
+// same libstdc++ engines as the reference (original column order).
 double Session::OpNorm(int iters, uint64_t seed) {
   PDHG_CUDA(cudaSetDevice(device_));
   if (nnz_ == 0) return 0.0;
@@ -878,20 +781,20 @@ double Session::OpNorm(int iters, uint64_t seed) {
   DArray<double> u, kv;
   u.alloc(n_);
   kv.alloc(m_);
-  PDHG_CUDA(cudaMemcpyAsync(u.p, v.data(), n_ * sizeof(double), cudaMemcpyHostToDevice, st_));
+  ToInternal(v.data(), perm_c_, u.p, n_);
   Scalars sc{};
   sc.pw_norm = vnorm;
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
-  launches_ += 4 * static_cast<int64_t>(iters) + 2;
+  launches_ += static_cast<int64_t>(iters) * (pass_launches(csr_) + pass_launches(csc_) + 2) + pass_launches(csr_) + 1;
   for (int it = 0; it < iters; ++it) {
-    launch_tiles(csr_, OpPowerStep<false>{u.p, scal_.p, 1, kv.p}, nullptr, nullptr, st_);
-    launch_tiles(csc_, OpPowerStep<true>{kv.p, scal_.p, 0, u.p}, red_tile_[1].p, red_span_[1].p, st_);
-    k_reduce_tiles<<<1, kBlock, 0, st_>>>(red_tile_[1].p, red_span_[1].p, csc_.ntiles, 1, red_out_.p);
+    run_pass(csr_, OpPowerStep<false>{u.p, scal_.p, 1, kv.p}, RedSlots{}, st_);
+    run_pass(csc_, OpPowerStep<true>{kv.p, scal_.p, 0, u.p}, RedSlots{red_[1].p}, st_);
+    k_reduce_tiles<<<1, kBlock, 0, st_>>>(red_[1].p, nullptr, csc_.parts(), 1, red_out_.p);
     k_power_norm<<<1, 1, 0, st_>>>(red_out_.p, scal_.p);
   }
-  launch_tiles(csr_, OpPowerStep<true>{u.p, scal_.p, 1, kv.p}, red_tile_[0].p, red_span_[0].p, st_);
-  k_reduce_tiles<<<1, kBlock, 0, st_>>>(red_tile_[0].p, red_span_[0].p, csr_.ntiles, 1, red_out_.p);
-  check_launch<int>("power iteration");
+  run_pass(csr_, OpPowerStep<true>{u.p, scal_.p, 1, kv.p}, RedSlots{red_[0].p}, st_);
+  k_reduce_tiles<<<1, kBlock, 0, st_>>>(red_[0].p, nullptr, csr_.parts(), 1, red_out_.p);
+  check_launch("power iteration");
   double sum = 0.0;
   Scalars hs{};
   PDHG_CUDA(cudaMemcpyAsync(&sum, red_out_.p, sizeof(double), cudaMemcpyDeviceToHost, st_));
@@ -904,22 +807,23 @@ double Session::OpNorm(int iters, uint64_t seed) {
 // ============================================================ kernel probes
 void Session::Scaling(double* rs, double* cs) {
   PDHG_CUDA(cudaSetDevice(device_));
-  if (m_) PDHG_CUDA(cudaMemcpyAsync(rs, rs_.p, m_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  if (n_) PDHG_CUDA(cudaMemcpyAsync(cs, cs_.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  Sync();
+  ToHost(rs_.p, nullptr, inv_r_, rs, m_);
+  ToHost(cs_.p, nullptr, inv_c_, cs, n_);
 }
 
 void Session::ScaledProblem(double* kv, double* c, double* l, double* u, double* q) {
   PDHG_CUDA(cudaSetDevice(device_));
-  auto d2h = [&](double* h, const double* d, int64_t k) {
-    if (h && k) PDHG_CUDA(cudaMemcpyAsync(h, d, k * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  };
-  d2h(kv, csr_val_.p, nnz_);
-  d2h(c, c_s_.p, n_);
-  d2h(l, l_s_.p, n_);
-  d2h(u, u_s_.p, n_);
-  d2h(q, q_s_.p, m_);
-  Sync();
+  if (kv && nnz_) {
+    DArray<double> tmp;
+    tmp.alloc(nnz_);
+    k_values_orig<<<ew_grid(nnz_), kEw, 0, st_>>>(ptr0_.p, m_, inv_r_.p, csr_.ptr, csr_.val, tmp.p, nnz_);
+    PDHG_CUDA(cudaMemcpyAsync(kv, tmp.p, nnz_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    Sync();
+  }
+  ToHost(c_s_.p, nullptr, inv_c_, c, n_);
+  ToHost(l_s_.p, nullptr, inv_c_, l, n_);
+  ToHost(u_s_.p, nullptr, inv_c_, u, n_);
+  ToHost(q_s_.p, nullptr, inv_r_, q, m_);
 }
 
 void Session::Spmv(int transpose, const double* in, double* out) {
@@ -928,11 +832,10 @@ void Session::Spmv(int transpose, const double* in, double* out) {
   DArray<double> a, b;
   a.alloc(std::max<int64_t>(nin, 1));
   b.alloc(std::max<int64_t>(nout, 1));
-  if (nin) PDHG_CUDA(cudaMemcpyAsync(a.p, in, nin * sizeof(double), cudaMemcpyHostToDevice, st_));
-  launch_tiles(transpose ? csc_ : csr_, OpSpmv{a.p, b.p}, nullptr, nullptr, st_);
-  check_launch<int>("spmv");
-  if (nout) PDHG_CUDA(cudaMemcpyAsync(out, b.p, nout * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  Sync();
+  ToInternal(in, transpose ? perm_r_ : perm_c_, a.p, nin);
+  run_pass(transpose ? csc_ : csr_, OpSpmv{a.p, b.p}, RedSlots{}, st_);
+  check_launch("spmv");
+  ToHost(b.p, nullptr, transpose ? inv_c_ : inv_r_, out, nout);
 }
 
 void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double* ms_iter) {
@@ -940,32 +843,31 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   Scalars sc{};
   sc.eta = 1e-3;
   sc.omega = 1.0;
+  sc.inner_base = 1.0;
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   k_clamp0<<<ew_grid(n_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, n_);
   if (m_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, m_ * sizeof(double), st_));
-  launch_tiles(csr_, OpSpmv{x_[0].p, kx_[0].p}, nullptr, nullptr, st_);
+  run_pass(csr_, OpSpmv{x_[0].p, kx_[0].p}, RedSlots{}, st_);
   cudaEvent_t e0, e1, e2;
   PDHG_CUDA(cudaEventCreate(&e0));
   PDHG_CUDA(cudaEventCreate(&e1));
   PDHG_CUDA(cudaEventCreate(&e2));
   for (int w = 0; w < 3; ++w) LaunchStep(w & 1, w, false);
   Sync();
-  // Each kernel alone, iters launches back to back, on the session stream.
   float t_p = 0, t_d = 0, t_i = 0;
   PDHG_CUDA(cudaEventRecord(e0, st_));
   for (int i = 0; i < iters; ++i)
-    launch_tiles(csc_, OpPrimal<false>{y_[0].p, x_[0].p, x_[1].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, i + 1},
-                 nullptr, nullptr, st_);
+    run_pass(csc_, OpPrimal<false>{y_[0].p, x_[0].p, x_[1].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, i + 1},
+             RedSlots{}, st_);
   PDHG_CUDA(cudaEventRecord(e1, st_));
   for (int i = 0; i < iters; ++i)
-    launch_tiles(csr_, OpDual<false>{x_[1].p, y_[0].p, y_[1].p, ybar_.p, kx_[0].p, kx_[1].p, q_s_.p, (int32_t)m1_,
-                                     scal_.p, i + 1},
-                 nullptr, nullptr, st_);
+    run_pass(csr_,
+             OpDual<false>{x_[1].p, y_[0].p, y_[1].p, ybar_.p, kx_[0].p, kx_[1].p, q_s_.p, rk_, scal_.p, i + 1},
+             RedSlots{}, st_);
   PDHG_CUDA(cudaEventRecord(e2, st_));
   PDHG_CUDA(cudaEventSynchronize(e2));
   PDHG_CUDA(cudaEventElapsedTime(&t_p, e0, e1));
   PDHG_CUDA(cudaEventElapsedTime(&t_d, e1, e2));
-  // Whole iterations through the block graph.
   const int blk = 64;
   const int reps = std::max(1, iters / blk);
   RunSteps(0, blk, false);
@@ -983,22 +885,17 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   cudaEventDestroy(e2);
 }
 
-__global__ void k_reflect(const double* xn, const double* xo, double* ext, int64_t n) {
-  GRID_STRIDE(i, n) ext[i] = 2.0 * xn[i] - xo[i];  // solver.cpp:141
-}
-
 void Session::UnitPrimal(const double* x, const double* y, double eta, double omega, double* out) {
   PDHG_CUDA(cudaSetDevice(device_));
   DArray<double> dx, dy, dout;
   dx.alloc(std::max<int64_t>(n_, 1));
   dy.alloc(std::max<int64_t>(m_, 1));
   dout.alloc(std::max<int64_t>(n_, 1));
-  if (n_) PDHG_CUDA(cudaMemcpyAsync(dx.p, x, n_ * sizeof(double), cudaMemcpyHostToDevice, st_));
-  if (m_) PDHG_CUDA(cudaMemcpyAsync(dy.p, y, m_ * sizeof(double), cudaMemcpyHostToDevice, st_));
-  launch_tiles(csc_, OpUnitPrimal{dy.p, dx.p, c_s_.p, l_s_.p, u_s_.p, eta / omega, dout.p}, nullptr, nullptr, st_);
-  check_launch<int>("primal step");
-  if (n_) PDHG_CUDA(cudaMemcpyAsync(out, dout.p, n_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  Sync();
+  ToInternal(x, perm_c_, dx.p, n_);
+  ToInternal(y, perm_r_, dy.p, m_);
+  run_pass(csc_, OpUnitPrimal{dy.p, dx.p, c_s_.p, l_s_.p, u_s_.p, eta / omega, dout.p}, RedSlots{}, st_);
+  check_launch("primal step");
+  ToHost(dout.p, nullptr, inv_c_, out, n_);
 }
 
 void Session::UnitDual(const double* xn, const double* xo, const double* y, double eta, double omega, double* out) {
@@ -1009,16 +906,13 @@ void Session::UnitDual(const double* xn, const double* xo, const double* y, doub
   ext.alloc(std::max<int64_t>(n_, 1));
   dy.alloc(std::max<int64_t>(m_, 1));
   dout.alloc(std::max<int64_t>(m_, 1));
-  if (n_) {
-    PDHG_CUDA(cudaMemcpyAsync(a.p, xn, n_ * sizeof(double), cudaMemcpyHostToDevice, st_));
-    PDHG_CUDA(cudaMemcpyAsync(b.p, xo, n_ * sizeof(double), cudaMemcpyHostToDevice, st_));
-  }
-  if (m_) PDHG_CUDA(cudaMemcpyAsync(dy.p, y, m_ * sizeof(double), cudaMemcpyHostToDevice, st_));
+  ToInternal(xn, perm_c_, a.p, n_);
+  ToInternal(xo, perm_c_, b.p, n_);
+  ToInternal(y, perm_r_, dy.p, m_);
   k_reflect<<<ew_grid(n_), kEw, 0, st_>>>(a.p, b.p, ext.p, n_);
-  launch_tiles(csr_, OpUnitDual{ext.p, dy.p, q_s_.p, (int32_t)m1_, eta * omega, dout.p}, nullptr, nullptr, st_);
-  check_launch<int>("dual step");
-  if (m_) PDHG_CUDA(cudaMemcpyAsync(out, dout.p, m_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
-  Sync();
+  run_pass(csr_, OpUnitDual{ext.p, dy.p, q_s_.p, rk_, eta * omega, dout.p}, RedSlots{}, st_);
+  check_launch("dual step");
+  ToHost(dout.p, nullptr, inv_r_, out, m_);
 }
 
 // Evict the working set between benchmark steps: write 2x the L2 capacity.
@@ -1037,8 +931,8 @@ void Session::Stats(pdhg_session_stats* s) const {
   s->m2 = m2_;
   s->n = n_;
   s->nnz = nnz_;
-  s->csr_tiles = csr_.ntiles;
-  s->csc_tiles = csc_.ntiles;
+  s->csr_tiles = csr_.parts();
+  s->csc_tiles = csc_.parts();
   s->device_bytes = arena_.bytes;
   s->upload_seconds = upload_s_;
   s->scaling_seconds = scaling_s_;

@@ -8,6 +8,7 @@
 
 #include "../../include/pdhg.h"
 #include "darray.cuh"
+#include "engine.cuh"
 
 namespace pdhg {
 
@@ -39,11 +40,19 @@ class Session {
     int parity = 0;
     bool adapt = false;
   };
+  // Storage of one permuted layout (CSR of K or CSC of K).
+  struct Store {
+    DArray<int32_t> ptr, idx;
+    DArray<double> val;
+    DArray<int32_t> part[4];  // tile_begin, tile_seg, head_first, tail_owner (long class)
+    DArray<double> head, tail;
+    DArray<unsigned> cnt;
+  };
 
-  void Upload(const pdhg_lp& lp);
-  void BuildCsc();
+  void Upload(const pdhg_lp& lp, DArray<int32_t>& ptr0, DArray<int32_t>& idx0, DArray<double>& val0);
+  void Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, const DArray<double>& val0);
   void ComputeScaling(const pdhg_params& prm);
-  void Partition(CMat& M);
+  void PartitionLong(Layout& L, Store& S);
   void DeviceNorms();
   void Sync();
   void LaunchStep(int parity, int j, bool adapt);
@@ -51,6 +60,8 @@ class Session {
   void LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx);
   void ReadCheck(CheckOut* out);
   void Copy(double* dst, const double* src, size_t n);
+  void ToInternal(const double* host, const DArray<int32_t>& perm, double* dev, int64_t n);
+  void ToHost(const double* dev, const double* scale, const DArray<int32_t>& inv, double* host, int64_t n);
 
   int device_ = 0;
   cudaStream_t st_ = nullptr;
@@ -61,24 +72,23 @@ class Session {
   bool scaled_ = false;
   bool l2_resident_ = false;
 
-  // K_s in both layouts and the tile partitions.
-  CMat csr_, csc_;
-  DArray<int32_t> csr_ptr_, csr_idx_, csc_ptr_, csc_idx_;
-  DArray<double> csr_val_, csc_val_;
-  DArray<int32_t> part_[2][4];  // [csr/csc][begin, seg, head_first, tail_owner]
-  DArray<double> head_[2], tail_[2];
-  DArray<unsigned> cnt_[2];
+  // K_s in both layouts, rows / columns permuted into length classes.
+  Layout csr_, csc_;
+  Store csr_st_, csc_st_;
+  RowKind rk_{};
+  DArray<int32_t> perm_r_, inv_r_, perm_c_, inv_c_;  // new->old, old->new
+  DArray<int32_t> ptr0_;                             // original CSR row_ptr (probe only)
 
-  // Problem vectors: scaled (loop) and original (termination) spaces.
+  // Problem vectors (permuted order): scaled (loop) and original (termination).
   DArray<double> c_s_, l_s_, u_s_, c_o_, l_o_, u_o_, cs_;  // n
   DArray<double> q_s_, q_o_, rs_;                          // m
   double c_norm_s_ = 0, q_norm_s_ = 0, c_norm_o_ = 0, q_norm_o_ = 0;
 
   // Iterates (ping-pong x/y/kx), averages, loop start, best, scratch.
-  DArray<double> x_[2], xbar_, xstart_, xbest_, nvec_;  // n
+  DArray<double> x_[2], xbar_, xstart_, xbest_, nvec_;            // n
   DArray<double> y_[2], ybar_, ystart_, ybest_, kx_[2], kxavg_;  // m
   DArray<Scalars> scal_;
-  DArray<double> red_tile_[2], red_span_[2], red_out_;
+  DArray<double> red_[2], red_out_;
   double* host_red_ = nullptr;  // pinned
 
   std::vector<Graph> graphs_;

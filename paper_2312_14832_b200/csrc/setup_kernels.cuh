@@ -1,0 +1,312 @@
+// Setup-time device kernels: upload narrowing, VStack, CSC build support,
+// length-class permutation, scaling helpers, tile partitioning, reductions.
+#pragma once
+
+#include "common.cuh"
+#include "tile_spmv.cuh"
+
+namespace pdhg {
+
+constexpr int kEw = 256;  // elementwise block size
+
+inline int ew_grid(int64_t n) {
+  int64_t g = (n + kEw - 1) / kEw;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
+}
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// ------------------------------------------------------------------ upload
+__global__ void k_narrow(const int64_t* in, int32_t* out, int64_t count, int64_t limit, int* bad) {
+  GRID_STRIDE(i, count) {
+    const int64_t v = in[i];
+    if (v < 0 || v >= limit) atomicOr(bad, 1);
+    out[i] = static_cast<int32_t>(v);
+  }
+}
+
+// K row_ptr = [A.row_ptr ; nnz(A) + G.row_ptr[1:]] (VStack, sparse_matrix.cpp:98-103).
+__global__ void k_stack_ptr(const int64_t* ap, const int64_t* gp, int64_t m1, int64_t m2, int64_t nnz_a,
+                            int32_t* out) {
+  GRID_STRIDE(i, m1 + m2 + 1) { out[i] = static_cast<int32_t>(i <= m1 ? ap[i] : nnz_a + gp[i - m1]); }
+}
+
+__global__ void k_check_ptr(const int32_t* p, int64_t rows, int64_t nnz, int* bad) {
+  GRID_STRIDE(i, rows) {
+    if (p[i] > p[i + 1]) atomicOr(bad, 2);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (p[0] != 0 || p[rows] != nnz)) atomicOr(bad, 2);
+}
+
+// Segment id of every nonzero: count segment starts, then inclusive scan.
+__global__ void k_seg_marks(const int32_t* p, int64_t nseg, int64_t nnz, int32_t* cnt) {
+  GRID_STRIDE(r, nseg) {
+    if (r >= 1 && p[r] < nnz) atomicAdd(cnt + p[r], 1);
+  }
+}
+
+__global__ void k_iota(int32_t* v, int64_t n) {
+  GRID_STRIDE(i, n) v[i] = static_cast<int32_t>(i);
+}
+
+// col_ptr[j] = first CSC slot with column >= j (sorted column keys).
+__global__ void k_colptr(const int32_t* keys, int64_t nnz, int64_t n, int32_t* cp) {
+  GRID_STRIDE(j, n + 1) {
+    int64_t lo = 0, hi = nnz;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < j) lo = mid + 1;
+      else hi = mid;
+    }
+    cp[j] = static_cast<int32_t>(lo);
+  }
+}
+
+__global__ void k_csc_gather(const int32_t* perm, const int32_t* row_of, const double* v, int32_t* ri, double* cv,
+                             int64_t nnz) {
+  GRID_STRIDE(q, nnz) {
+    const int32_t k = perm[q];
+    ri[q] = row_of[k];
+    cv[q] = v[k];
+  }
+}
+
+// ------------------------------------------------------- class permutation
+// key = class(len) * 2 + (row is an inequality row); columns use eq_end = n.
+__global__ void k_class_keys(const int32_t* p, int64_t nseg, int64_t eq_end, int32_t* key) {
+  GRID_STRIDE(s, nseg) {
+    const int len = p[s + 1] - p[s];
+    const int cls = len <= kSeqMax ? 0 : (len <= kWarpMax ? 1 : (len <= kCtaMax ? 2 : 3));
+    key[s] = cls * 2 + (s >= eq_end ? 1 : 0);
+  }
+}
+
+__global__ void k_key_hist(const int32_t* key, int64_t n, int32_t* hist) {
+  GRID_STRIDE(i, n) atomicAdd(hist + key[i], 1);
+}
+
+__global__ void k_invert(const int32_t* perm, int32_t* inv, int64_t n) {
+  GRID_STRIDE(i, n) inv[perm[i]] = static_cast<int32_t>(i);
+}
+
+__global__ void k_perm_len(const int32_t* p, const int32_t* perm, int64_t n, int32_t* len) {
+  GRID_STRIDE(i, n) len[i] = p[perm[i] + 1] - p[perm[i]];
+}
+
+// Move every nonzero of segment s to the permuted layout, keeping its
+// position inside the segment; remap the other dimension's index.
+__global__ void k_perm_nnz(const int32_t* p0, const int32_t* seg_of, const int32_t* idx0, const double* val0,
+                           const int32_t* inv_seg, const int32_t* inv_other, const int32_t* p1, int32_t* idx1,
+                           double* val1, int64_t nnz) {
+  GRID_STRIDE(k, nnz) {
+    const int32_t s = seg_of[k];
+    const int64_t dst = p1[inv_seg[s]] + (k - p0[s]);
+    idx1[dst] = inv_other[idx0[k]];
+    val1[dst] = val0[k];
+  }
+}
+
+// out[i'] = in[perm[i']] (original -> permuted order).
+__global__ void k_gather(const double* in, const int32_t* perm, double* out, int64_t n) {
+  GRID_STRIDE(i, n) out[i] = in[perm[i]];
+}
+
+// out[i] = in[inv[i]] * (scale ? scale[inv[i]] : 1)  (permuted -> original).
+__global__ void k_unpermute(const double* in, const double* scale, const int32_t* inv, double* out, int64_t n) {
+  GRID_STRIDE(i, n) {
+    const int32_t j = inv[i];
+    out[i] = scale ? in[j] * scale[j] : in[j];
+  }
+}
+
+// ------------------------------------------------------------- vectors
+// Scaled (sparse_matrix.cpp:213, :218): (row_scale * v) * col_scale.
+__global__ void k_scale_vals(const int32_t* seg_of, const int32_t* idx, const double* vin, double* vout,
+                             const double* rs, const double* cs, int64_t nnz, int csr_role) {
+  GRID_STRIDE(k, nnz) {
+    const int32_t r = csr_role ? seg_of[k] : idx[k];
+    const int32_t c = csr_role ? idx[k] : seg_of[k];
+    vout[k] = rs[r] * vin[k] * cs[c];
+  }
+}
+
+__global__ void k_fill(double* v, double a, int64_t n) {
+  GRID_STRIDE(i, n) v[i] = a;
+}
+__global__ void k_mul(const double* a, const double* b, double* out, int64_t n) {
+  GRID_STRIDE(i, n) out[i] = a[i] * b[i];
+}
+__global__ void k_div(const double* a, const double* b, double* out, int64_t n) {
+  GRID_STRIDE(i, n) out[i] = a[i] / b[i];
+}
+// x0 = Clamp(0, l, u) (solver.cpp:240-243).
+__global__ void k_clamp0(const double* l, const double* u, double* x, int64_t n) {
+  GRID_STRIDE(i, n) x[i] = clamp_ref(0.0, l[i], u[i]);
+}
+__global__ void k_reflect(const double* xn, const double* xo, double* ext, int64_t n) {
+  GRID_STRIDE(i, n) ext[i] = 2.0 * xn[i] - xo[i];  // solver.cpp:141
+}
+
+// ------------------------------------------------------- tile partitioning
+// For the long-segment class [lo, hi) of one layout; positions are absolute.
+__device__ int64_t upper_bound_i32(const int32_t* a, int64_t n, int64_t v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ int64_t seg_end_pos(const int32_t* p, int64_t s, int64_t nz1) {
+  const int64_t b = p[s], e = p[s + 1];
+  const int64_t pos = e > b ? e - 1 : b;
+  return pos < nz1 - 1 ? pos : nz1 - 1;
+}
+
+// K_s values in the ORIGINAL CSR order (for the parity probe).
+__global__ void k_values_orig(const int32_t* p0, int64_t m, const int32_t* inv_r, const int32_t* p1,
+                              const double* v1, double* out, int64_t nnz) {
+  GRID_STRIDE(k, nnz) {
+    const int64_t r = upper_bound_i32(p0, m + 1, k) - 1;
+    out[k] = v1[p1[inv_r[r]] + (k - p0[r])];
+  }
+}
+
+// Tile-boundary candidates: every kBlock-th segment start and every kTile-th
+// nonzero inside segment groups of more than kTile nonzeros (snapped back to
+// the start of a segment of <= kSnap nonzeros). Dropped: INT32_MAX.
+__global__ void k_part_cand(const int32_t* p, int32_t lo, int32_t hi, int64_t nz0, int64_t nz1, int32_t ngroups,
+                            int32_t ncuts, int32_t* cand) {
+  GRID_STRIDE(i, (int64_t)ngroups + ncuts) {
+    int64_t v = INT32_MAX;
+    if (i < ngroups) {
+      const int64_t pos = p[lo + i * (int64_t)kBlock];
+      if (pos < nz1) v = pos;
+    } else {
+      const int64_t pos = nz0 + (i - ngroups + 1) * (int64_t)kTile;
+      if (pos < nz1) {
+        const int64_t s = lo + upper_bound_i32(p + lo, hi - lo + 1, pos) - 1;
+        const int64_t g0 = lo + ((s - lo) / kBlock) * kBlock;
+        const int64_t g1 = g0 + kBlock < hi ? g0 + kBlock : hi;
+        if (p[g1] - p[g0] > kTile) {
+          const int64_t st = p[s], len = p[s + 1] - st;
+          v = (st < pos && len <= kSnap) ? st : pos;
+        }
+      }
+    }
+    cand[i] = static_cast<int32_t>(v);
+  }
+}
+
+__global__ void k_part_seg(const int32_t* p, int32_t lo, int32_t hi, int64_t nz1, int32_t ntiles, const int32_t* tb,
+                           int32_t* ts) {
+  GRID_STRIDE(t, (int64_t)ntiles + 1) {
+    int64_t v;
+    if (t == 0) {
+      v = lo;
+    } else if (t == ntiles) {
+      v = hi;
+    } else {
+      const int64_t key = tb[t];
+      int64_t a = lo, b = hi;
+      while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (seg_end_pos(p, mid, nz1) < key) a = mid + 1;
+        else b = mid;
+      }
+      v = a;
+    }
+    ts[t] = static_cast<int32_t>(v);
+  }
+}
+
+__global__ void k_part_span(const int32_t* p, int32_t hi, int64_t nz1, int32_t ntiles, const int32_t* tb,
+                            const int32_t* ts, int32_t* hf, int32_t* to) {
+  GRID_STRIDE(t, (int64_t)ntiles) {
+    const int64_t sb = ts[t], se = ts[t + 1], kb = tb[t], ke = tb[t + 1];
+    int32_t h = -1, o = -1;
+    if (sb < se && p[sb] < kb) h = static_cast<int32_t>(upper_bound_i32(tb, ntiles + 1, p[sb]) - 1);
+    if (se < hi && p[se] < ke) o = static_cast<int32_t>(upper_bound_i32(tb, ntiles + 1, seg_end_pos(p, se, nz1)) - 1);
+    hf[t] = h;
+    to[t] = o;
+  }
+}
+
+// --------------------------------------------------------------- reductions
+// out[i] = sum over slots (fixed order); one CTA per output.
+__global__ void k_reduce_tiles(const double* tile, const double* span, int ntiles, int nred, double* out) {
+  __shared__ double sh[kBlock / 32];
+  const int i = blockIdx.x;
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
+    acc += tile[(int64_t)t * nred + i] + (span ? span[(int64_t)t * nred + i] : 0.0);
+  acc = warp_combine<false>(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = sh[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v += sh[w];
+    out[i] = v;
+  }
+}
+
+__global__ void k_sumsq_partial(const double* v, int64_t n, double* part) {
+  __shared__ double sh[kEw / 32];
+  double acc = 0.0;
+  GRID_STRIDE(i, n) acc += v[i] * v[i];
+  acc = warp_combine<false>(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = sh[0];
+    for (int w = 1; w < kEw / 32; ++w) s += sh[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+// Power-iteration normalisation (solver.cpp:103-105).
+__global__ void k_power_norm(const double* sum, Scalars* sc) {
+  const double nr = sqrt(sum[0]);
+  if (nr == 0.0) {
+    sc->pw_zero = 1;
+    sc->pw_norm = 1.0;
+  } else {
+    sc->pw_norm = nr;
+  }
+}
+
+// AdaptStepSize (solver.cpp:310-328) from the per-iteration partials.
+__global__ void k_adapt(const double* cred, int cn, const double* rred, int rn, Scalars* sc, int j) {
+  __shared__ double sh[3][kBlock / 32];
+  double a[3] = {0.0, 0.0, 0.0};
+  for (int t = threadIdx.x; t < cn; t += blockDim.x) a[0] += cred[t];
+  for (int t = threadIdx.x; t < rn; t += blockDim.x) {
+    a[1] += rred[2 * t];
+    a[2] += rred[2 * t + 1];
+  }
+  for (int k = 0; k < 3; ++k) {
+    a[k] = warp_combine<false>(a[k]);
+    if ((threadIdx.x & 31) == 0) sh[k][threadIdx.x >> 5] = a[k];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double dx = 0, dy = 0, it = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+    dx += sh[0][w];
+    dy += sh[1][w];
+    it += sh[2][w];
+  }
+  it = fabs(it);
+  if (it <= 0.0) return;
+  const double om = sc->omega;
+  const double lim = (om * dx + dy / om) / (2.0 * it);
+  const double k = sc->adapt_iter + static_cast<double>(j) + 1.0;
+  const double a1 = lim * (1.0 - pow(k, -0.3));
+  const double a2 = sc->eta * (1.0 + pow(k, -0.6));
+  sc->eta = (a2 < a1) ? a2 : a1;  // std::min(a1, a2)
+}
+
+}  // namespace pdhg

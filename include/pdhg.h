@@ -139,7 +139,31 @@ typedef struct {
   double scaling_seconds; /* Ruiz + Pock-Chambolle + ApplyScaling on device */
   int32_t device;
   int32_t l2_resident; /* 1 if the per-iteration working set fits in L2 */
+  int32_t world;        /* shards K is split into */
+  int32_t local_shards; /* shards held by this session (1 or world) */
+  int32_t rank;         /* this session's shard when local_shards == 1 */
+  int32_t pad;
 } pdhg_session_stats;
+
+/* Distribution of K over shards: `world` balanced row blocks
+ * (K x, CSR) and column blocks (K^T y, CSC).
+ *   world = 1                      one GPU, no exchange (the default path);
+ *   local_shards = world           every shard in this session on one device,
+ *                                  exchanges are in-place no-ops (exercises
+ *                                  the sharded path on a single GPU);
+ *   local_shards = 1, nccl_id set  one process per GPU: this session holds
+ *                                  shard `rank`; x+ / y+ slices are
+ *                                  all-gathered with NCCL every half-step,
+ *                                  the check sums all-reduced every
+ *                                  check_every iterations. Every rank passes
+ *                                  the same problem and params and receives
+ *                                  the same result. */
+typedef struct {
+  int32_t world;
+  int32_t rank;
+  int32_t local_shards;
+  const void* nccl_id; /* 128-byte ncclUniqueId from pdhg_nccl_unique_id */
+} pdhg_shard_spec;
 
 typedef struct pdhg_session pdhg_session;
 
@@ -168,6 +192,24 @@ int pdhg_solve_on(const pdhg_lp* lp, const pdhg_params* params, int device,
 int pdhg_session_create(const pdhg_lp* lp, const pdhg_params* params,
                         int device, pdhg_session** out, char* err,
                         size_t errlen);
+/* Same as pdhg_session_create with K distributed by `spec`. */
+int pdhg_session_create_sharded(const pdhg_lp* lp, const pdhg_params* params,
+                                int device, const pdhg_shard_spec* spec,
+                                pdhg_session** out, char* err, size_t errlen);
+/* One-shot sharded solve (rpdlp::Solve semantics on every rank). */
+int pdhg_solve_sharded(const pdhg_lp* lp, const pdhg_params* params,
+                       int device, const pdhg_shard_spec* spec,
+                       pdhg_eval_cb cb, void* user, pdhg_result* out,
+                       char* err, size_t errlen);
+/* ncclGetUniqueId (rank 0 creates it and broadcasts the 128 bytes). */
+int pdhg_nccl_unique_id(void* out128, char* err, size_t errlen);
+/* Block boundaries in original row / column order (world + 1 each). */
+int pdhg_session_blocks(pdhg_session* s, int64_t* row_begin,
+                        int64_t* col_begin);
+/* The balanced split every rank computes: `parts` contiguous blocks of the
+ * `nseg` segments of a CSR/CSC offset array (`begin`: parts + 1 entries). */
+int pdhg_partition_blocks(const int64_t* ptr, int64_t nseg, int parts,
+                          int64_t seg_weight, int64_t* begin);
 void pdhg_session_destroy(pdhg_session* s);
 int pdhg_session_stats_get(pdhg_session* s, pdhg_session_stats* out);
 /* SolveLoop(...).Run() (solver.cpp:232-267) on the resident scaled problem.
@@ -249,12 +291,28 @@ int pdhg_gen_pagerank(int64_t n_nodes, double damping, int64_t attachment,
  * sum_i x_ij = d_j in A, supply rows -sum_j x_ij >= -s_i in G, x >= 0. */
 int pdhg_gen_transport(int64_t sources, int64_t sinks, uint64_t seed,
                        pdhg_instance** out, char* err, size_t errlen);
+/* Multicommodity network flow: power-law digraph of
+ * `nodes` nodes and `arcs` arcs, `commodities` commodities; conservation rows
+ * (=, heavy-tailed lengths) in A, arc capacity rows (>= after negation) in G,
+ * x >= 0. Feasible by construction (witness flow available). */
+int pdhg_gen_mcf(int64_t nodes, int64_t arcs, int64_t commodities,
+                 uint64_t seed, pdhg_instance** out, char* err, size_t errlen);
+/* Block-angular staircase: `stages` stages of
+ * `rows_per_stage` x `cols_per_stage`, `nnz_per_row` nonzeros per row of which
+ * `linking_per_row` reach into the previous stage; the first
+ * `eq_rows_per_stage` rows of each stage are equalities. Generated by
+ * `threads` host threads (0 = all), bit-identical for any thread count. */
+int pdhg_gen_staircase(int64_t stages, int64_t rows_per_stage,
+                       int64_t cols_per_stage, int64_t nnz_per_row,
+                       int64_t linking_per_row, int64_t eq_rows_per_stage,
+                       uint64_t seed, int threads, pdhg_instance** out,
+                       char* err, size_t errlen);
 /* Moves the first `m1` rows of G into A with b = G_rows * witness
  * (SURVEY §8d config 1 post-pass). Requires a witness (GenRandomLp). */
 int pdhg_instance_make_equalities(pdhg_instance* inst, int64_t m1, char* err,
                                   size_t errlen);
 int pdhg_instance_view(const pdhg_instance* inst, pdhg_lp* out);
-/* Witness x_hat of GenRandomLp (length n) or NULL. */
+/* Witness x_hat (GenRandomLp, MCF, staircase; length n) or NULL. */
 const double* pdhg_instance_witness(const pdhg_instance* inst);
 void pdhg_instance_free(pdhg_instance* inst);
 

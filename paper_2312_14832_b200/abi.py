@@ -67,7 +67,12 @@ class SessionStats(C.Structure):
     _fields_ = [("m1", C.c_int64), ("m2", C.c_int64), ("n", C.c_int64), ("nnz", C.c_int64),
                 ("csr_tiles", C.c_int64), ("csc_tiles", C.c_int64), ("device_bytes", C.c_int64),
                 ("upload_seconds", C.c_double), ("scaling_seconds", C.c_double), ("device", C.c_int32),
-                ("l2_resident", C.c_int32)]
+                ("l2_resident", C.c_int32), ("world", C.c_int32), ("local_shards", C.c_int32),
+                ("rank", C.c_int32), ("pad", C.c_int32)]
+
+
+class ShardSpec(C.Structure):
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("local_shards", C.c_int32), ("nccl_id", C.c_void_p)]
 
 
 EVAL_CB = C.CFUNCTYPE(C.c_int, C.POINTER(EvalInfo), C.c_void_p)
@@ -85,6 +90,13 @@ SIGNATURES = {
                                 C.c_char_p, C.c_size_t]),
     "pdhg_session_create": (C.c_int, [C.POINTER(Lp), C.POINTER(Params), C.c_int, C.POINTER(C.c_void_p), C.c_char_p,
                                       C.c_size_t]),
+    "pdhg_session_create_sharded": (C.c_int, [C.POINTER(Lp), C.POINTER(Params), C.c_int, C.POINTER(ShardSpec),
+                                              C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]),
+    "pdhg_solve_sharded": (C.c_int, [C.POINTER(Lp), C.POINTER(Params), C.c_int, C.POINTER(ShardSpec), EVAL_CB,
+                                     C.c_void_p, C.POINTER(Result), C.c_char_p, C.c_size_t]),
+    "pdhg_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
+    "pdhg_session_blocks": (C.c_int, [C.c_void_p, i64ptr, i64ptr]),
+    "pdhg_partition_blocks": (C.c_int, [i64ptr, C.c_int64, C.c_int, C.c_int64, i64ptr]),
     "pdhg_session_destroy": (None, [C.c_void_p]),
     "pdhg_session_stats_get": (C.c_int, [C.c_void_p, C.POINTER(SessionStats)]),
     "pdhg_session_solve": (C.c_int, [C.c_void_p, C.POINTER(Params), EVAL_CB, C.c_void_p, C.POINTER(Result),
@@ -111,6 +123,10 @@ SIGNATURES = {
                                     C.c_char_p, C.c_size_t]),
     "pdhg_gen_transport": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, C.POINTER(C.c_void_p), C.c_char_p,
                                      C.c_size_t]),
+    "pdhg_gen_mcf": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.POINTER(C.c_void_p), C.c_char_p,
+                               C.c_size_t]),
+    "pdhg_gen_staircase": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
+                                     C.c_int, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]),
     "pdhg_instance_make_equalities": (C.c_int, [C.c_void_p, C.c_int64, C.c_char_p, C.c_size_t]),
     "pdhg_instance_view": (C.c_int, [C.c_void_p, C.POINTER(Lp)]),
     "pdhg_instance_witness": (dptr, [C.c_void_p]),

@@ -31,13 +31,13 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # elementwise updates and row sums.
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "--expt-relaxed-constexpr",
                   "-Xcompiler", "-fPIC,-O3", "-I", str(ROOT / "include")]
-CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-Wall", "-Wextra", "-I", str(ROOT / "include")]
+CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-pthread", "-Wall", "-Wextra", "-I", str(ROOT / "include")]
 
 CU_SRCS = ["session.cu", "abi.cu"]
 CPP_SRCS = ["instance_gen.cpp", "rpdlp_api.cpp"]
 DROPIN_TEST = ROOT / "tests" / "cpp" / "drop_in_test.cpp"
 DROPIN_BIN = BUILD / "drop_in_test"
-HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh", "tma.cuh", "host_logic.h", "engine.cuh", "setup_kernels.cuh"]
+HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh", "tma.cuh", "host_logic.h", "engine.cuh", "setup_kernels.cuh", "comm.cuh"]
 
 
 def _newer(target: Path, deps) -> bool:
@@ -77,7 +77,7 @@ def build_product(force: bool = False, ptxas_verbose: bool = False) -> Path:
     if ptxas_verbose:
         print("\n".join(l for l in logs if l.strip()))
     if force or jobs or not _newer(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", str(LIB)] + [str(o) for o in objs] + ["-lcuda"])
+        _run([NVCC] + ARCH + ["-shared", "-o", str(LIB)] + [str(o) for o in objs] + ["-lcuda", "-lpthread"])
     # Reference-style C++ caller linked against the drop-in headers + library.
     if force or not _newer(DROPIN_BIN, [DROPIN_TEST, LIB]):
         _run([CXX] + CXXFLAGS + [str(DROPIN_TEST), "-o", str(DROPIN_BIN), "-L", str(PKG), "-lpdhg_b200",

@@ -77,6 +77,15 @@ void ValidateParams(const pdhg_params& p) {
   if (p.iter_limit < 0) Invalid("negative iter_limit");
 }
 
+pdhg::ShardSpec Spec(const pdhg_shard_spec& s) {
+  pdhg::ShardSpec r;
+  r.world = s.world;
+  r.rank = s.rank;
+  r.local = s.local_shards;
+  r.nccl_id = s.nccl_id;
+  return r;
+}
+
 pdhg::Session& S(pdhg_session* s) {
   if (!s || !s->impl) Invalid("null session");
   return *s->impl;
@@ -129,6 +138,50 @@ int pdhg_session_create(const pdhg_lp* lp, const pdhg_params* prm, int device, p
     }
     *out = s;
   });
+}
+
+int pdhg_session_create_sharded(const pdhg_lp* lp, const pdhg_params* prm, int device, const pdhg_shard_spec* spec,
+                                pdhg_session** out, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!lp || !prm || !out || !spec) Invalid("null argument");
+    ValidateLp(*lp);
+    auto* s = new pdhg_session;
+    try {
+      s->impl = std::make_unique<pdhg::Session>(*lp, *prm, device, Spec(*spec));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int pdhg_solve_sharded(const pdhg_lp* lp, const pdhg_params* prm, int device, const pdhg_shard_spec* spec,
+                       pdhg_eval_cb cb, void* user, pdhg_result* out, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!lp || !prm || !out || !spec) Invalid("null argument");
+    ValidateLp(*lp);
+    ValidateParams(*prm);
+    pdhg::Session sess(*lp, *prm, device, Spec(*spec));
+    sess.Solve(*prm, cb, user, out);
+  });
+}
+
+int pdhg_nccl_unique_id(void* out128, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!out128) Invalid("null argument");
+    pdhg::nccl_unique_id(out128);
+  });
+}
+
+int pdhg_session_blocks(pdhg_session* s, int64_t* row_begin, int64_t* col_begin) {
+  return Guard(nullptr, 0, [&] { S(s).Blocks(row_begin, col_begin); });
+}
+
+int pdhg_partition_blocks(const int64_t* ptr, int64_t nseg, int parts, int64_t seg_weight, int64_t* begin) {
+  if (!ptr || !begin || nseg < 0 || parts < 1 || seg_weight < 0) return PDHG_INVALID_ARGUMENT;
+  pdhg::BalancedBlocks(ptr, nseg, parts, seg_weight, begin);
+  return PDHG_OK;
 }
 
 void pdhg_session_destroy(pdhg_session* s) { delete s; }

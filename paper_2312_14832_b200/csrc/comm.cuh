@@ -1,0 +1,126 @@
+// Exchange layer of the sharded solver.
+//
+// K is split into P row blocks (K x, CSR) and P column blocks (K^T y, CSC).
+// Every vector lives in a PADDED index space: block b's entries occupy
+// [b * slice, b * slice + size_b), so one in-place all-gather of `slice`
+// doubles per rank rebuilds the full vector on every rank, and a column
+// index of K (already remapped into that space at setup) addresses the
+// gathered buffer directly -- no unpacking, no extra copy.
+//
+// Implementations:
+//   LocalComm  every shard lives in this process and writes straight into the
+//              shared full buffers: exchanges are no-ops (P = 1, and the
+//              in-process multi-shard mode the parity tests drive on one GPU);
+//   NcclComm   one shard per process/GPU; ncclAllGather in place over
+//              NVLink/NVSwitch, ncclAllReduce for the check pack. NCCL is
+//              dlopen'ed on first use (whichever libnccl.so.2 the process
+//              already holds -- torch's -- or the system one), so the library
+//              has no link-time NCCL dependency. Calls are stream-ordered and
+//              graph-capturable, so they sit inside the captured PDHG block.
+#pragma once
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "common.cuh"
+
+namespace pdhg {
+
+class Comm {
+ public:
+  virtual ~Comm() = default;
+  virtual bool local() const = 0;
+  // In place: this rank's slice is buf[rank * slice, (rank + 1) * slice).
+  virtual void AllGather(double* buf, int64_t slice, cudaStream_t st) = 0;
+  virtual void AllReduceSum(double* buf, int64_t n, cudaStream_t st) = 0;
+  virtual void AllReduceMax(double* buf, int64_t n, cudaStream_t st) = 0;
+};
+
+class LocalComm final : public Comm {
+ public:
+  bool local() const override { return true; }
+  void AllGather(double*, int64_t, cudaStream_t) override {}
+  void AllReduceSum(double*, int64_t, cudaStream_t) override {}
+  void AllReduceMax(double*, int64_t, cudaStream_t) override {}
+};
+
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  static const NcclApi& Get() {
+    static NcclApi api = Load();
+    if (!api.AllGather) throw Error(4, "NCCL unavailable: libnccl.so.2 could not be loaded");
+    return api;
+  }
+
+ private:
+  static NcclApi Load() {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!a.GetUniqueId || !a.CommInitRank || !a.CommDestroy || !a.AllReduce || !a.GetErrorString)
+      a.AllGather = nullptr;
+    return a;
+  }
+};
+
+inline void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw Error(4, std::string(what) + ": " + NcclApi::Get().GetErrorString(r));
+}
+
+class NcclComm final : public Comm {
+ public:
+  NcclComm(const void* id, int world, int rank) : rank_(rank) {
+    const NcclApi& api = NcclApi::Get();
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    nccl_check(api.CommInitRank(&comm_, world, uid, rank), "ncclCommInitRank");
+  }
+  ~NcclComm() override {
+    if (comm_) NcclApi::Get().CommDestroy(comm_);
+  }
+  bool local() const override { return false; }
+  void AllGather(double* buf, int64_t slice, cudaStream_t st) override {
+    if (slice <= 0) return;
+    nccl_check(NcclApi::Get().AllGather(buf + rank_ * slice, buf, static_cast<size_t>(slice), ncclFloat64, comm_, st),
+               "ncclAllGather");
+  }
+  void AllReduceSum(double* buf, int64_t n, cudaStream_t st) override {
+    nccl_check(NcclApi::Get().AllReduce(buf, buf, static_cast<size_t>(n), ncclFloat64, ncclSum, comm_, st),
+               "ncclAllReduce");
+  }
+  void AllReduceMax(double* buf, int64_t n, cudaStream_t st) override {
+    nccl_check(NcclApi::Get().AllReduce(buf, buf, static_cast<size_t>(n), ncclFloat64, ncclMax, comm_, st),
+               "ncclAllReduce");
+  }
+
+ private:
+  ncclComm_t comm_ = nullptr;
+  int rank_ = 0;
+};
+
+inline void nccl_unique_id(void* out) {
+  ncclUniqueId uid;
+  nccl_check(NcclApi::Get().GetUniqueId(&uid), "ncclGetUniqueId");
+  std::memcpy(out, &uid, sizeof(uid));
+}
+
+}  // namespace pdhg

@@ -39,6 +39,17 @@ struct DArray {
     p = nullptr;
     n = 0;
   }
+  // Ownership transfer (e.g. a setup temporary becoming session storage).
+  void take(DArray& o, Arena* a) {
+    release();
+    p = o.p;
+    n = o.n;
+    arena = a;
+    if (o.arena) o.arena->bytes -= static_cast<int64_t>(o.n * sizeof(T));
+    if (arena) arena->bytes += static_cast<int64_t>(n * sizeof(T));
+    o.p = nullptr;
+    o.n = 0;
+  }
   T* get() const { return p; }
   size_t size() const { return n; }
 };

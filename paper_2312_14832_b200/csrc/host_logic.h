@@ -50,4 +50,27 @@ inline pdhg_report MakeReport(double pr2, double du2, double bound, double cx, d
   return r;
 }
 
+// Contiguous block partition of `nseg` segments (rows or columns, original
+// order) into `parts` blocks balanced by W(s) = ptr[s] + seg_weight * s (the
+// nonzeros plus a per-segment charge for the vector traffic): block b ends at
+// the smallest s with W(s) * parts >= (b + 1) * W(nseg). Every rank computes
+// it from the same ptr array, so the split needs no communication.
+template <class P>
+inline void BalancedBlocks(const P* ptr, int64_t nseg, int parts, int64_t seg_weight, int64_t* begin) {
+  const auto W = [&](int64_t s) { return static_cast<long double>(ptr[s]) + static_cast<long double>(seg_weight) * s; };
+  const long double total = W(nseg);
+  begin[0] = 0;
+  for (int b = 1; b < parts; ++b) {
+    const long double target = total * b;
+    int64_t lo = begin[b - 1], hi = nseg;
+    while (lo < hi) {
+      const int64_t mid = lo + (hi - lo) / 2;
+      if (W(mid) * parts >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    begin[b] = lo;
+  }
+  begin[parts] = nseg;
+}
+
 }  // namespace pdhg

@@ -15,6 +15,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -213,6 +214,199 @@ pdhg_instance* Transport(I S, I T, uint64_t seed) {
   return p;
 }
 
+// Multicommodity network flow LP. A power-law digraph
+// of V nodes and E arcs (tail and head drawn from Zipf-like node weights
+// w_v = (v + 1)^-0.8, self-loops redrawn), K commodities, variables
+// x_{a,k} at column a*K + k, x >= 0, costs U(0,1).
+//   A: conservation row k*V + v:  sum_{a out of v} x_{a,k} - sum_{a into v} x_{a,k} = b
+//   G: capacity row a:            -sum_k x_{a,k} >= -cap_a
+// Feasible by construction: a random witness flow (each x_{a,k} nonzero with
+// probability 0.2, value U(0,1)) gives b = A x_hat and
+// cap_a = 1.1 * sum_k x_hat_{a,k} + 0.1 U(0,1). Conservation row lengths are
+// node degrees (heavy-tailed), capacity rows hold K, every column exactly 3.
+// Draw order: arcs (tail, head), witness row-major over (a, k), capacity
+// slack per arc, costs row-major over (a, k).
+pdhg_instance* Mcf(I V, I E, I K, uint64_t seed) {
+  if (V < 2 || E < 1 || K < 1) throw std::invalid_argument("need V >= 2, E >= 1, K >= 1");
+  if (E * K >= (I(1) << 31) || 3 * E * K >= (I(1) << 31) - 4096)
+    throw std::invalid_argument("instance too large for int32 device indices");
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  std::vector<double> cdf(V);
+  double acc = 0.0;
+  for (I v = 0; v < V; ++v) {
+    acc += std::pow(static_cast<double>(v + 1), -0.8);
+    cdf[v] = acc;
+  }
+  auto draw = [&]() -> I {
+    const double r = unit(rng) * acc;
+    const I v = static_cast<I>(std::upper_bound(cdf.begin(), cdf.end(), r) - cdf.begin());
+    return std::min(v, V - 1);
+  };
+  std::vector<I> tail(E), head(E);
+  for (I a = 0; a < E; ++a) {
+    tail[a] = draw();
+    do head[a] = draw();
+    while (head[a] == tail[a]);
+  }
+  const I n = E * K;
+  auto* p = new pdhg_instance;
+  p->n = n;
+  p->witness.assign(n, 0.0);
+  for (I k = 0; k < n; ++k)
+    if (unit(rng) < 0.2) p->witness[k] = unit(rng);
+  // Incidence lists per node, arcs ascending (so columns ascend in each row).
+  std::vector<I> deg(V + 1, 0);
+  for (I a = 0; a < E; ++a) {
+    ++deg[tail[a] + 1];
+    ++deg[head[a] + 1];
+  }
+  for (I v = 0; v < V; ++v) deg[v + 1] += deg[v];
+  std::vector<I> inc(2 * E), fill(deg.begin(), deg.end() - 1);
+  for (I a = 0; a < E; ++a) {  // ascending a -> each list sorted
+    inc[fill[tail[a]]++] = a;
+    inc[fill[head[a]]++] = a;
+  }
+  p->a_rows = V * K;
+  p->a_ptr.resize(V * K + 1);
+  p->a_idx.resize(2 * n);
+  p->a_val.resize(2 * n);
+  p->b.assign(V * K, 0.0);
+  I w = 0;
+  for (I k = 0; k < K; ++k) {
+    for (I v = 0; v < V; ++v) {
+      p->a_ptr[k * V + v] = w;
+      double bv = 0.0;
+      for (I e = deg[v]; e < deg[v + 1]; ++e) {
+        const I a = inc[e];
+        const double s = tail[a] == v ? 1.0 : -1.0;
+        p->a_idx[w] = a * K + k;
+        p->a_val[w] = s;
+        bv += s * p->witness[a * K + k];
+        ++w;
+      }
+      p->b[k * V + v] = bv;
+    }
+  }
+  p->a_ptr[V * K] = w;
+  p->g_rows = E;
+  p->g_ptr.resize(E + 1);
+  p->g_idx.resize(n);
+  p->g_val.assign(n, -1.0);
+  p->h.resize(E);
+  for (I a = 0; a < E; ++a) {
+    double flow = 0.0;
+    for (I k = 0; k < K; ++k) {
+      p->g_idx[a * K + k] = a * K + k;
+      flow += p->witness[a * K + k];
+    }
+    p->g_ptr[a] = a * K;
+    p->h[a] = -(1.1 * flow + 0.1 * unit(rng));
+  }
+  p->g_ptr[E] = n;
+  p->c.resize(n);
+  for (double& v : p->c) v = unit(rng);
+  p->l.assign(n, 0.0);
+  p->u.assign(n, std::numeric_limits<double>::infinity());
+  return p;
+}
+
+// Block-angular staircase LP. T stages of R rows and C
+// columns; every row holds exactly D nonzeros U(-1,1): D - Dl in its own
+// stage's columns and Dl linking ones in stage t-1's (stage 0: all D own).
+// The first Req rows of each stage are equalities (A, b = row . x_hat), the
+// rest inequalities (G, h = row . x_hat - |0.3 U(-1,1)|); x_hat ~ U(0,1),
+// 0 <= x <= 2, c ~ U(-1,1). Stages are generated in parallel, each from its
+// own engine mt19937_64(seed ^ (0x9E3779B97F4A7C15 * (t + 1))) (witness and
+// costs of stage t first, then its rows), so the instance is bit-identical
+// per seed for any thread count. Row layouts are fixed-length, so every
+// thread writes its slice of the final CSR arrays in place.
+pdhg_instance* Staircase(I T, I R, I C, I D, I Dl, I Req, uint64_t seed, int threads) {
+  if (T < 1 || R < 1 || C < 1 || D < 1) throw std::invalid_argument("T, R, C, D must be >= 1");
+  if (Dl < 0 || Dl >= D || D - Dl > C || Dl > C) throw std::invalid_argument("need 0 <= Dl < D, D - Dl <= C, Dl <= C");
+  if (Req < 0 || Req > R) throw std::invalid_argument("need 0 <= Req <= R");
+  const I n = T * C, rows = T * R;
+  if (rows * D >= (I(1) << 31) - 4096 || n >= (I(1) << 31) - 1)
+    throw std::invalid_argument("instance too large for int32 device indices");
+  auto* p = new pdhg_instance;
+  p->n = n;
+  p->a_rows = T * Req;
+  p->g_rows = T * (R - Req);
+  p->a_ptr.resize(p->a_rows + 1);
+  p->g_ptr.resize(p->g_rows + 1);
+  for (I r = 0; r <= p->a_rows; ++r) p->a_ptr[r] = r * D;
+  for (I r = 0; r <= p->g_rows; ++r) p->g_ptr[r] = r * D;
+  p->a_idx.resize(p->a_rows * D);
+  p->a_val.resize(p->a_rows * D);
+  p->g_idx.resize(p->g_rows * D);
+  p->g_val.resize(p->g_rows * D);
+  p->b.resize(p->a_rows);
+  p->h.resize(p->g_rows);
+  p->witness.resize(n);
+  p->c.resize(n);
+  p->l.assign(n, 0.0);
+  p->u.assign(n, 2.0);
+  auto engine = [&](I t) { return std::mt19937_64(seed ^ (0x9E3779B97F4A7C15ull * static_cast<uint64_t>(t + 1))); };
+  // Pass 1: witness + costs per stage (rows of stage t read stage t-1's x_hat).
+  std::vector<std::mt19937_64> eng;
+  eng.reserve(T);
+  for (I t = 0; t < T; ++t) eng.push_back(engine(t));
+  auto stage_vec = [&](I t) {
+    std::uniform_real_distribution<double> unit(0.0, 1.0), sym(-1.0, 1.0);
+    for (I j = t * C; j < (t + 1) * C; ++j) p->witness[j] = unit(eng[t]);
+    for (I j = t * C; j < (t + 1) * C; ++j) p->c[j] = sym(eng[t]);
+  };
+  auto stage_rows = [&](I t) {
+    std::mt19937_64& g = eng[t];
+    std::uniform_real_distribution<double> sym(-1.0, 1.0);
+    std::vector<I> cols;
+    for (I i = 0; i < R; ++i) {
+      const I dl = t > 0 ? Dl : 0, dn = D - dl;
+      cols.clear();
+      auto pick = [&](I lo, I cnt, I span) {
+        std::uniform_int_distribution<I> dist(lo, lo + span - 1);
+        const size_t base = cols.size();
+        while (static_cast<I>(cols.size() - base) < cnt) {
+          const I j = dist(g);
+          if (std::find(cols.begin() + base, cols.end(), j) == cols.end()) cols.push_back(j);
+        }
+      };
+      pick((t - 1) * C, dl, C);  // linking columns (stage t-1) come first: ascending
+      pick(t * C, dn, C);
+      std::sort(cols.begin(), cols.begin() + dl);
+      std::sort(cols.begin() + dl, cols.end());
+      const bool eq = i < Req;
+      const I row = eq ? t * Req + i : t * (R - Req) + (i - Req);
+      int64_t* idx = (eq ? p->a_idx.data() : p->g_idx.data()) + row * D;
+      double* val = (eq ? p->a_val.data() : p->g_val.data()) + row * D;
+      double acc = 0.0;
+      for (I k = 0; k < D; ++k) {
+        double v;
+        do v = sym(g);
+        while (v == 0.0);
+        idx[k] = cols[k];
+        val[k] = v;
+        acc += v * p->witness[cols[k]];
+      }
+      if (eq) p->b[row] = acc;
+      else p->h[row] = acc - std::abs(0.3 * sym(g));
+    }
+  };
+  const int nt = std::max(1, std::min<int>(threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency()),
+                                           static_cast<int>(T)));
+  auto parallel = [&](auto&& fn) {
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nt; ++w)
+      pool.emplace_back([&, w] {
+        for (I t = w; t < T; t += nt) fn(t);
+      });
+    for (auto& th : pool) th.join();
+  };
+  parallel(stage_vec);
+  parallel(stage_rows);
+  return p;
+}
+
 template <class F>
 int Guard(char* err, size_t len, F&& f) {
   try {
@@ -244,6 +438,20 @@ int pdhg_gen_pagerank(int64_t n_nodes, double damping, int64_t attachment, uint6
 int pdhg_gen_transport(int64_t sources, int64_t sinks, uint64_t seed, pdhg_instance** out, char* err,
                        size_t errlen) {
   return Guard(err, errlen, [&] { *out = Transport(sources, sinks, seed); });
+}
+
+int pdhg_gen_mcf(int64_t nodes, int64_t arcs, int64_t commodities, uint64_t seed, pdhg_instance** out, char* err,
+                 size_t errlen) {
+  return Guard(err, errlen, [&] { *out = Mcf(nodes, arcs, commodities, seed); });
+}
+
+int pdhg_gen_staircase(int64_t stages, int64_t rows_per_stage, int64_t cols_per_stage, int64_t nnz_per_row,
+                       int64_t linking_per_row, int64_t eq_rows_per_stage, uint64_t seed, int threads,
+                       pdhg_instance** out, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    *out = Staircase(stages, rows_per_stage, cols_per_stage, nnz_per_row, linking_per_row, eq_rows_per_stage, seed,
+                     threads);
+  });
 }
 
 int pdhg_instance_make_equalities(pdhg_instance* p, int64_t m1, char* err, size_t errlen) {

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -64,19 +65,23 @@ void segment_ids(const int32_t* ptr, int64_t nseg, int64_t nnz, DArray<int32_t>&
   PDHG_CUDA(cudaStreamSynchronize(st));
 }
 
-// Stable sort of segment keys -> permutation new -> old.
-void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, cudaStream_t st) {
+// Stable sort of segment keys (values < 2^bits) -> permutation new -> old.
+void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, int bits, cudaStream_t st) {
   DArray<int32_t> iota, kout;
   iota.alloc(std::max<int64_t>(n, 1));
   kout.alloc(std::max<int64_t>(n, 1));
   k_iota<<<ew_grid(n), kEw, 0, st>>>(iota.p, n);
   size_t tb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, 3, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, bits, st);
   DArray<char> tmp;
   tmp.alloc(tb);
-  PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, 3, st));
+  PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, bits, st));
   PDHG_CUDA(cudaStreamSynchronize(st));
 }
+
+// Per-segment charge of the block balance (in nonzeros): the ~68 bytes of
+// vector traffic per row / column against 12 bytes per nonzero.
+constexpr int64_t kSegWeight = 6;
 
 }  // namespace
 
@@ -87,10 +92,24 @@ struct CheckOut {
 };
 
 // ============================================================== construction
-Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device) : device_(device) {
+Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const ShardSpec& spec) : device_(device) {
+  if (spec.world < 1 || spec.world > 64) throw Error(PDHG_INVALID_ARGUMENT, "shard world must lie in [1, 64]");
+  if (spec.local != 1 && spec.local != spec.world)
+    throw Error(PDHG_INVALID_ARGUMENT, "a session holds either one shard or all of them");
+  if (spec.rank < 0 || spec.rank >= spec.world) throw Error(PDHG_INVALID_ARGUMENT, "shard rank out of range");
+  world_ = spec.world;
+  rank_ = spec.local == spec.world ? 0 : spec.rank;
   PDHG_CUDA(cudaSetDevice(device_));
   PDHG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
-  PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&host_red_), sizeof(CheckOut) + 64));
+  PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&host_red_), kPack * sizeof(double) + 64));
+  if (world_ > 1 && spec.local == 1) {
+    if (!spec.nccl_id) throw Error(PDHG_INVALID_ARGUMENT, "a one-shard-per-process session needs an NCCL id");
+    comm_ = std::make_unique<NcclComm>(spec.nccl_id, world_, rank_);
+  } else {
+    comm_ = std::make_unique<LocalComm>();
+  }
+  shards_ = std::vector<Shard>(spec.local);
+  for (int k = 0; k < spec.local; ++k) shards_[k].block = spec.local == 1 ? rank_ : k;
   m1_ = lp.a.rows;
   m2_ = lp.g.rows;
   m_ = m1_ + m2_;
@@ -103,34 +122,57 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device) : device
     Upload(lp, ptr0, idx0, val0);
     Permute(ptr0, idx0, val0);
   }
-  PartitionLong(csr_, csr_st_);
-  PartitionLong(csc_, csc_st_);
+  for (Shard& h : shards_) {
+    PartitionLong(h.csr, h.csr_st);
+    PartitionLong(h.csc, h.csc_st);
+  }
+  // Original-space problem vectors into padded order.
+  c_o_.alloc(np_, &arena_);
+  l_o_.alloc(np_, &arena_);
+  u_o_.alloc(np_, &arena_);
+  q_o_.alloc(mp_, &arena_);
+  ToInternal(lp.c, pad_c_, c_o_.p, n_, np_);
+  ToInternal(lp.l, pad_c_, l_o_.p, n_, np_);
+  ToInternal(lp.u, pad_c_, u_o_.p, n_, np_);
+  {
+    std::vector<double> q(static_cast<size_t>(m_));
+    if (m1_) std::memcpy(q.data(), lp.b, m1_ * sizeof(double));
+    if (m2_) std::memcpy(q.data() + m1_, lp.h, m2_ * sizeof(double));
+    ToInternal(q.data(), pad_r_, q_o_.p, m_, mp_);
+  }
   Sync();
   upload_s_ = now_s() - t0;
+  for (int p = 0; p < 2; ++p) {
+    x_[p].alloc(np_, &arena_);
+    y_[p].alloc(mp_, &arena_);
+    kx_[p].alloc(mp_, &arena_);
+  }
+  xbar_.alloc(np_, &arena_);
+  xstart_.alloc(np_, &arena_);
+  xbest_.alloc(np_, &arena_);
+  nvec_.alloc(np_, &arena_);
+  ybar_.alloc(mp_, &arena_);
+  ystart_.alloc(mp_, &arena_);
+  ybest_.alloc(mp_, &arena_);
+  kxavg_.alloc(mp_, &arena_);
+  // Padding entries are never addressed by an index but travel with the
+  // all-gathers: keep them zero.
+  for (DArray<double>* v : {&x_[0], &x_[1], &xbar_, &xstart_, &xbest_, &nvec_, &y_[0], &y_[1], &ybar_, &ystart_,
+                            &ybest_, &kx_[0], &kx_[1], &kxavg_})
+    if (v->n) PDHG_CUDA(cudaMemsetAsync(v->p, 0, v->n * sizeof(double), st_));
+  scal_.alloc(1, &arena_);
+  const int nred = std::max(kRowRed, kColRed);
+  for (Shard& h : shards_) {
+    h.red[0].alloc(static_cast<size_t>(std::max(h.csr.parts(), 1)) * nred, &arena_);
+    h.red[1].alloc(static_cast<size_t>(std::max(h.csc.parts(), 1)) * nred, &arena_);
+  }
+  red_out_.alloc(static_cast<size_t>(kPack) * shards_.size(), &arena_);
   const double t1 = now_s();
   ComputeScaling(prm);
   Sync();
   scaling_s_ = now_s() - t1;
-  for (int p = 0; p < 2; ++p) {
-    x_[p].alloc(n_, &arena_);
-    y_[p].alloc(m_, &arena_);
-    kx_[p].alloc(m_, &arena_);
-  }
-  xbar_.alloc(n_, &arena_);
-  xstart_.alloc(n_, &arena_);
-  xbest_.alloc(n_, &arena_);
-  nvec_.alloc(n_, &arena_);
-  ybar_.alloc(m_, &arena_);
-  ystart_.alloc(m_, &arena_);
-  ybest_.alloc(m_, &arena_);
-  kxavg_.alloc(m_, &arena_);
-  scal_.alloc(1, &arena_);
-  const int nred = std::max(kRowRed, kColRed);
-  red_[0].alloc(static_cast<size_t>(std::max(csr_.parts(), 1)) * nred, &arena_);
-  red_[1].alloc(static_cast<size_t>(std::max(csc_.parts(), 1)) * nred, &arena_);
-  red_out_.alloc(64, &arena_);
   DeviceNorms();
-  const double iter_bytes = 24.0 * nnz_ + 68.0 * (m_ + n_);
+  const double iter_bytes = (24.0 * nnz_ + 68.0 * (m_ + n_)) / world_;
   l2_resident_ = iter_bytes < 100e6;
   Sync();
 }
@@ -142,6 +184,7 @@ Session::~Session() {
   for (Graph& g : graphs_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (host_red_) cudaFreeHost(host_red_);
+  comm_.reset();
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -149,6 +192,27 @@ void Session::Sync() { PDHG_CUDA(cudaStreamSynchronize(st_)); }
 
 void Session::Copy(double* dst, const double* src, size_t n) {
   if (n) PDHG_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+}
+
+int Session::parts_csr() const {
+  int k = 0;
+  for (const Shard& h : shards_) k += h.csr.parts();
+  return k;
+}
+int Session::parts_csc() const {
+  int k = 0;
+  for (const Shard& h : shards_) k += h.csc.parts();
+  return k;
+}
+int Session::launches_csr() const {
+  int k = 0;
+  for (const Shard& h : shards_) k += pass_launches(h.csr);
+  return k;
+}
+int Session::launches_csc() const {
+  int k = 0;
+  for (const Shard& h : shards_) k += pass_launches(h.csc);
+  return k;
 }
 
 // H2D + int64 -> int32 narrowing + VStack of A and G straight into K's CSR.
@@ -184,18 +248,6 @@ void Session::Upload(const pdhg_lp& lp, DArray<int32_t>& ptr0, DArray<int32_t>& 
     PDHG_CUDA(cudaMemcpyAsync(val0.p + nnz_a, lp.g.values, nnz_g * sizeof(double), cudaMemcpyHostToDevice, st_));
   }
   k_check_ptr<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, nnz_, bad.p);
-  c_o_.alloc(n_, &arena_);
-  l_o_.alloc(n_, &arena_);
-  u_o_.alloc(n_, &arena_);
-  q_o_.alloc(m_, &arena_);
-  auto h2d = [&](double* d, const double* h, int64_t k) {
-    if (k) PDHG_CUDA(cudaMemcpyAsync(d, h, k * sizeof(double), cudaMemcpyHostToDevice, st_));
-  };
-  h2d(c_o_.p, lp.c, n_);
-  h2d(l_o_.p, lp.l, n_);
-  h2d(u_o_.p, lp.u, n_);
-  h2d(q_o_.p, lp.b, m1_);
-  h2d(q_o_.p + m1_, lp.h, m2_);
   int hbad = 0;
   PDHG_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
   Sync();
@@ -205,9 +257,11 @@ void Session::Upload(const pdhg_lp& lp, DArray<int32_t>& ptr0, DArray<int32_t>& 
 }
 
 // Builds the CSC of K (stable radix sort of (column, CSR position): rows stay
-// ascending inside each column, as BuildCscFromCsr guarantees), then permutes
-// rows and columns into length classes (engine.cuh) for both layouts,
-// keeping every segment's internal order.
+// ascending inside each column, as BuildCscFromCsr guarantees), splits rows
+// and columns into balanced blocks, and permutes each block into length
+// classes (engine.cuh) for both layouts, keeping every segment's internal
+// order. Indices are remapped into the padded vector spaces; each local shard
+// receives its row block's CSR and its column block's CSC.
 void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, const DArray<double>& val0) {
   // --- original-order CSC
   DArray<int32_t> cptr0, ridx0, row_of;
@@ -237,88 +291,165 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
   } else {
     PDHG_CUDA(cudaMemsetAsync(cptr0.p, 0, (n_ + 1) * sizeof(int32_t), st_));
   }
-  // --- length classes: key = class * 2 + inequality row
-  perm_r_.alloc(std::max<int64_t>(m_, 1), &arena_);
-  inv_r_.alloc(std::max<int64_t>(m_, 1), &arena_);
-  perm_c_.alloc(std::max<int64_t>(n_, 1), &arena_);
-  inv_c_.alloc(std::max<int64_t>(n_, 1), &arena_);
-  int hr[8] = {0}, hc[8] = {0};
+  // --- balanced blocks (identical on every rank: same ptr arrays)
+  row_begin_.assign(world_ + 1, 0);
+  col_begin_.assign(world_ + 1, 0);
+  if (world_ == 1) {
+    row_begin_[1] = m_;
+    col_begin_[1] = n_;
+  } else {
+    std::vector<int32_t> hp(std::max(m_, n_) + 1);
+    PDHG_CUDA(cudaMemcpyAsync(hp.data(), ptr0.p, (m_ + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+    Sync();
+    BalancedBlocks(hp.data(), m_, world_, kSegWeight, row_begin_.data());
+    PDHG_CUDA(cudaMemcpyAsync(hp.data(), cptr0.p, (n_ + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+    Sync();
+    BalancedBlocks(hp.data(), n_, world_, kSegWeight, col_begin_.data());
+  }
+  pm_ = pn_ = 0;
+  for (int b = 0; b < world_; ++b) {
+    pm_ = std::max(pm_, row_begin_[b + 1] - row_begin_[b]);
+    pn_ = std::max(pn_, col_begin_[b + 1] - col_begin_[b]);
+  }
+  mp_ = pm_ * world_;
+  np_ = pn_ * world_;
+  if (mp_ >= (int64_t(1) << 31) - 1 || np_ >= (int64_t(1) << 31) - 1)
+    throw Error(PDHG_INVALID_ARGUMENT, "padded vectors too large for int32 device indices");
+  DArray<int64_t> rbeg, cbeg;
+  rbeg.alloc(world_ + 1);
+  cbeg.alloc(world_ + 1);
+  PDHG_CUDA(cudaMemcpyAsync(rbeg.p, row_begin_.data(), (world_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+  PDHG_CUDA(cudaMemcpyAsync(cbeg.p, col_begin_.data(), (world_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+
+  // --- length classes per block: key = block * 8 + class * 2 + inequality row
+  DArray<int32_t> perm_r, perm_c, inv_r, inv_c;  // compact order <-> original
+  perm_r.alloc(std::max<int64_t>(m_, 1));
+  perm_c.alloc(std::max<int64_t>(n_, 1));
+  inv_r.alloc(std::max<int64_t>(m_, 1));
+  inv_c.alloc(std::max<int64_t>(n_, 1));
+  const int nkeys = 8 * world_;
+  std::vector<int> hr(nkeys, 0), hc(nkeys, 0);
   {
     DArray<int32_t> kr, kc, hist;
     kr.alloc(std::max<int64_t>(m_, 1));
     kc.alloc(std::max<int64_t>(n_, 1));
-    hist.alloc(16);
-    PDHG_CUDA(cudaMemsetAsync(hist.p, 0, 16 * sizeof(int32_t), st_));
-    k_class_keys<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, m1_, kr.p);
-    k_class_keys<<<ew_grid(n_), kEw, 0, st_>>>(cptr0.p, n_, n_, kc.p);
+    hist.alloc(2 * nkeys);
+    PDHG_CUDA(cudaMemsetAsync(hist.p, 0, 2 * nkeys * sizeof(int32_t), st_));
+    // Class bounds: kWarpMax / kCtaMax unless overridden (PDHG_WARP_MAX,
+    // PDHG_CTA_MAX; tuning experiments only -- the one-thread class is fixed
+    // at kSeqMax so short segments keep the reference's summation order).
+    auto env_int = [](const char* k, int d) {
+      const char* v = std::getenv(k);
+      return v ? std::max(kSeqMax, std::atoi(v)) : d;
+    };
+    const int warp_max = env_int("PDHG_WARP_MAX", kWarpMax);
+    const int cta_max = std::max(warp_max, env_int("PDHG_CTA_MAX", kCtaMax));
+    k_class_keys<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, m1_, rbeg.p, world_, warp_max, cta_max, kr.p);
+    k_class_keys<<<ew_grid(n_), kEw, 0, st_>>>(cptr0.p, n_, n_, cbeg.p, world_, warp_max, cta_max, kc.p);
     k_key_hist<<<ew_grid(m_), kEw, 0, st_>>>(kr.p, m_, hist.p);
-    k_key_hist<<<ew_grid(n_), kEw, 0, st_>>>(kc.p, n_, hist.p + 8);
-    if (m_) stable_order(kr.p, m_, perm_r_, st_);
-    if (n_) stable_order(kc.p, n_, perm_c_, st_);
-    int h[16];
-    PDHG_CUDA(cudaMemcpyAsync(h, hist.p, sizeof(h), cudaMemcpyDeviceToHost, st_));
+    k_key_hist<<<ew_grid(n_), kEw, 0, st_>>>(kc.p, n_, hist.p + nkeys);
+    int bits = 3;
+    while ((1 << bits) < nkeys) ++bits;
+    if (m_) stable_order(kr.p, m_, perm_r, bits, st_);
+    if (n_) stable_order(kc.p, n_, perm_c, bits, st_);
+    std::vector<int> h(2 * nkeys);
+    PDHG_CUDA(cudaMemcpyAsync(h.data(), hist.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st_));
     Sync();
-    std::copy(h, h + 8, hr);
-    std::copy(h + 8, h + 16, hc);
+    std::copy(h.begin(), h.begin() + nkeys, hr.begin());
+    std::copy(h.begin() + nkeys, h.end(), hc.begin());
   }
-  k_invert<<<ew_grid(m_), kEw, 0, st_>>>(perm_r_.p, inv_r_.p, m_);
-  k_invert<<<ew_grid(n_), kEw, 0, st_>>>(perm_c_.p, inv_c_.p, n_);
-  rk_.e0 = hr[0];
-  rk_.s1 = hr[0] + hr[1];
-  rk_.e1 = rk_.s1 + hr[2];
-  rk_.s2 = rk_.s1 + hr[2] + hr[3];
-  rk_.e2 = rk_.s2 + hr[4];
-  rk_.s3 = rk_.s2 + hr[4] + hr[5];
-  rk_.e3 = rk_.s3 + hr[6];
-  // --- permuted layouts
-  auto build = [&](Layout& L, Store& S, const DArray<int32_t>& p0, const DArray<int32_t>& i0,
-                   const DArray<double>& v0, const DArray<int32_t>& seg_of, int64_t nseg, int64_t nvec,
-                   const DArray<int32_t>& perm, const DArray<int32_t>& inv_seg, const DArray<int32_t>& inv_other) {
-    S.ptr.alloc(nseg + 1, &arena_);
-    S.idx.alloc(std::max<int64_t>(nnz_, 1), &arena_);
-    S.val.alloc(std::max<int64_t>(nnz_, 1), &arena_);
+  k_invert<<<ew_grid(m_), kEw, 0, st_>>>(perm_r.p, inv_r.p, m_);
+  k_invert<<<ew_grid(n_), kEw, 0, st_>>>(perm_c.p, inv_c.p, n_);
+  pad_r_.alloc(std::max<int64_t>(m_, 1), &arena_);
+  pad_c_.alloc(std::max<int64_t>(n_, 1), &arena_);
+  k_pad_index<<<ew_grid(m_), kEw, 0, st_>>>(inv_r.p, rbeg.p, world_, pm_, pad_r_.p, m_);
+  k_pad_index<<<ew_grid(n_), kEw, 0, st_>>>(inv_c.p, cbeg.p, world_, pn_, pad_c_.p, n_);
+
+  // --- full compact layouts (every block, class order), indices padded
+  auto build = [&](DArray<int32_t>& ptr, DArray<int32_t>& idx, DArray<double>& val, const DArray<int32_t>& p0,
+                   const DArray<int32_t>& i0, const DArray<double>& v0, const DArray<int32_t>& seg_of, int64_t nseg,
+                   const DArray<int32_t>& perm, const DArray<int32_t>& inv_seg, const DArray<int32_t>& pad_other) {
+    ptr.alloc(nseg + 1);
+    idx.alloc(std::max<int64_t>(nnz_, 1));
+    val.alloc(std::max<int64_t>(nnz_, 1));
     DArray<int32_t> len;
     len.alloc(nseg + 1);
     PDHG_CUDA(cudaMemsetAsync(len.p, 0, (nseg + 1) * sizeof(int32_t), st_));
     k_perm_len<<<ew_grid(nseg), kEw, 0, st_>>>(p0.p, perm.p, nseg, len.p);
-    scan_exclusive(len.p, S.ptr.p, nseg + 1, st_);
+    scan_exclusive(len.p, ptr.p, nseg + 1, st_);
     if (nnz_)
-      k_perm_nnz<<<ew_grid(nnz_), kEw, 0, st_>>>(p0.p, seg_of.p, i0.p, v0.p, inv_seg.p, inv_other.p, S.ptr.p,
-                                                  S.idx.p, S.val.p, nnz_);
+      k_perm_nnz<<<ew_grid(nnz_), kEw, 0, st_>>>(p0.p, seg_of.p, i0.p, v0.p, inv_seg.p, pad_other.p, ptr.p, idx.p,
+                                                  val.p, nnz_);
+  };
+  // One layout's block slice -> shard storage (ownership moves when the
+  // session holds the whole matrix in one shard).
+  auto slice = [&](Layout& L, Store& S, DArray<int32_t>& ptr, DArray<int32_t>& idx, DArray<double>& val, int64_t b0,
+                   int64_t b1, const int* hist) {
+    const int64_t nseg = b1 - b0;
+    int32_t k0 = 0, k1 = 0;
+    PDHG_CUDA(cudaMemcpyAsync(&k0, ptr.p + b0, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+    PDHG_CUDA(cudaMemcpyAsync(&k1, ptr.p + b1, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+    Sync();
+    if (world_ == 1) {
+      S.ptr.take(ptr, &arena_);
+      S.idx.take(idx, &arena_);
+      S.val.take(val, &arena_);
+    } else {
+      S.ptr.alloc(nseg + 1, &arena_);
+      S.idx.alloc(std::max<int32_t>(k1 - k0, 1), &arena_);
+      S.val.alloc(std::max<int32_t>(k1 - k0, 1), &arena_);
+      k_rebase<<<ew_grid(nseg + 1), kEw, 0, st_>>>(ptr.p + b0, nseg, S.ptr.p);
+      if (k1 > k0) {
+        PDHG_CUDA(cudaMemcpyAsync(S.idx.p, idx.p + k0, (k1 - k0) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st_));
+        PDHG_CUDA(cudaMemcpyAsync(S.val.p, val.p + k0, (k1 - k0) * sizeof(double), cudaMemcpyDeviceToDevice, st_));
+      }
+    }
     L.nseg = static_cast<int32_t>(nseg);
-    L.nvec = static_cast<int32_t>(nvec);
-    L.nnz = nnz_;
+    L.nnz = k1 - k0;
     L.ptr = S.ptr.p;
     L.idx = S.idx.p;
     L.val = S.val.p;
+    L.s1 = hist[0] + hist[1];
+    L.s2 = L.s1 + hist[2] + hist[3];
+    L.s3 = L.s2 + hist[4] + hist[5];
   };
-  build(csr_, csr_st_, ptr0, idx0, val0, row_of, m_, n_, perm_r_, inv_r_, inv_c_);
-  csr_.s1 = rk_.s1;
-  csr_.s2 = rk_.s2;
-  csr_.s3 = rk_.s3;
   {
-    DArray<int32_t> col_of;
-    segment_ids(cptr0.p, n_, nnz_, col_of, st_);
-    build(csc_, csc_st_, cptr0, ridx0, cval0, col_of, n_, m_, perm_c_, inv_c_, inv_r_);
+    DArray<int32_t> fptr, fidx;
+    DArray<double> fval;
+    build(fptr, fidx, fval, ptr0, idx0, val0, row_of, m_, perm_r, inv_r, pad_c_);
+    for (Shard& h : shards_) {
+      const int b = h.block;
+      const int* hb = hr.data() + 8 * b;
+      h.roff = b * pm_;
+      h.rows = row_begin_[b + 1] - row_begin_[b];
+      slice(h.csr, h.csr_st, fptr, fidx, fval, row_begin_[b], row_begin_[b + 1], hb);
+      h.csr.nvec = static_cast<int32_t>(np_);
+      h.rk.e0 = hb[0];
+      h.rk.s1 = hb[0] + hb[1];
+      h.rk.e1 = h.rk.s1 + hb[2];
+      h.rk.s2 = h.rk.s1 + hb[2] + hb[3];
+      h.rk.e2 = h.rk.s2 + hb[4];
+      h.rk.s3 = h.rk.s2 + hb[4] + hb[5];
+      h.rk.e3 = h.rk.s3 + hb[6];
+    }
     Sync();
   }
-  csc_.s1 = hc[0] + hc[1];
-  csc_.s2 = csc_.s1 + hc[2] + hc[3];
-  csc_.s3 = csc_.s2 + hc[4] + hc[5];
+  {
+    DArray<int32_t> col_of, fptr, fidx;
+    DArray<double> fval;
+    segment_ids(cptr0.p, n_, nnz_, col_of, st_);
+    build(fptr, fidx, fval, cptr0, ridx0, cval0, col_of, n_, perm_c, inv_c, pad_r_);
+    for (Shard& h : shards_) {
+      const int b = h.block;
+      h.coff = b * pn_;
+      h.cols = col_begin_[b + 1] - col_begin_[b];
+      slice(h.csc, h.csc_st, fptr, fidx, fval, col_begin_[b], col_begin_[b + 1], hc.data() + 8 * b);
+      h.csc.nvec = static_cast<int32_t>(mp_);
+    }
+    Sync();
+  }
   ptr0_.alloc(m_ + 1, &arena_);
   PDHG_CUDA(cudaMemcpyAsync(ptr0_.p, ptr0.p, (m_ + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st_));
-  // --- vectors into internal order
-  DArray<double> tmp;
-  tmp.alloc(std::max<int64_t>(std::max(m_, n_), 1));
-  auto perm_vec = [&](DArray<double>& v, const DArray<int32_t>& perm, int64_t k) {
-    if (!k) return;
-    Copy(tmp.p, v.p, k);
-    k_gather<<<ew_grid(k), kEw, 0, st_>>>(tmp.p, perm.p, v.p, k);
-  };
-  perm_vec(c_o_, perm_c_, n_);
-  perm_vec(l_o_, perm_c_, n_);
-  perm_vec(u_o_, perm_c_, n_);
-  perm_vec(q_o_, perm_r_, m_);
   Sync();
   check_launch("permute");
 }
@@ -390,65 +521,96 @@ void Session::PartitionLong(Layout& L, Store& S) {
 // values with the composed scales, c_s = c cs, l_s = l / cs, u_s = u / cs,
 // q_s = q rs. Max is exact and 1/sqrt is IEEE on both sides, so the scales
 // are bit-identical to the reference (power sums too for rows/cols of <= 32
-// nonzeros, which are summed in storage order).
+// nonzeros, which are summed in storage order) -- for any shard count: each
+// shard owns whole rows (CSR) and whole columns (CSC), and the per-sweep
+// factors are all-gathered before the values are rescaled.
 void Session::ComputeScaling(const pdhg_params& prm) {
-  rs_.alloc(m_, &arena_);
-  cs_.alloc(n_, &arena_);
-  c_s_.alloc(n_, &arena_);
-  l_s_.alloc(n_, &arena_);
-  u_s_.alloc(n_, &arena_);
-  q_s_.alloc(m_, &arena_);
-  k_fill<<<ew_grid(m_), kEw, 0, st_>>>(rs_.p, 1.0, m_);
-  k_fill<<<ew_grid(n_), kEw, 0, st_>>>(cs_.p, 1.0, n_);
+  rs_.alloc(mp_, &arena_);
+  cs_.alloc(np_, &arena_);
+  c_s_.alloc(np_, &arena_);
+  l_s_.alloc(np_, &arena_);
+  u_s_.alloc(np_, &arena_);
+  q_s_.alloc(mp_, &arena_);
+  k_fill<<<ew_grid(mp_), kEw, 0, st_>>>(rs_.p, 1.0, mp_);
+  k_fill<<<ew_grid(np_), kEw, 0, st_>>>(cs_.p, 1.0, np_);
   scaled_ = prm.scaling_enabled != 0;
   if (scaled_ && (prm.pc_alpha < 0.0 || prm.pc_alpha > 2.0))
     throw Error(PDHG_INVALID_ARGUMENT, "pock-chambolle alpha must lie in [0, 2]");
   if (scaled_ && nnz_ > 0) {
-    DArray<int32_t> row_of, col_of;
-    segment_ids(csr_.ptr, m_, nnz_, row_of, st_);
-    segment_ids(csc_.ptr, n_, nnz_, col_of, st_);
-    DArray<double> orig_r, orig_c, dr, dc;
-    orig_r.alloc(nnz_);
-    orig_c.alloc(nnz_);
-    dr.alloc(m_);
-    dc.alloc(n_);
-    Copy(orig_r.p, csr_.val, nnz_);
-    Copy(orig_c.p, csc_.val, nnz_);
+    const size_t ns = shards_.size();
+    std::vector<DArray<int32_t>> row_of(ns), col_of(ns);
+    std::vector<DArray<double>> orig_r(ns), orig_c(ns);
+    DArray<double> dr, dc;
+    dr.alloc(mp_);
+    dc.alloc(np_);
+    PDHG_CUDA(cudaMemsetAsync(dr.p, 0, mp_ * sizeof(double), st_));
+    PDHG_CUDA(cudaMemsetAsync(dc.p, 0, np_ * sizeof(double), st_));
+    for (size_t k = 0; k < ns; ++k) {
+      const Shard& h = shards_[k];
+      segment_ids(h.csr.ptr, h.csr.nseg, h.csr.nnz, row_of[k], st_);
+      segment_ids(h.csc.ptr, h.csc.nseg, h.csc.nnz, col_of[k], st_);
+      orig_r[k].alloc(std::max<int64_t>(h.csr.nnz, 1));
+      orig_c[k].alloc(std::max<int64_t>(h.csc.nnz, 1));
+      Copy(orig_r[k].p, h.csr.val, h.csr.nnz);
+      Copy(orig_c[k].p, h.csc.val, h.csc.nnz);
+    }
+    // Rescale every local layout: src values -> dst = (r * v) * c.
+    auto rescale = [&](bool from_orig, const double* r, const double* c) {
+      for (size_t k = 0; k < ns; ++k) {
+        Shard& h = shards_[k];
+        if (h.csr.nnz)
+          k_scale_vals<<<ew_grid(h.csr.nnz), kEw, 0, st_>>>(row_of[k].p, h.csr.idx,
+                                                           from_orig ? orig_r[k].p : h.csr.val, h.csr.val, r, c,
+                                                           h.csr.nnz, 1, h.roff);
+        if (h.csc.nnz)
+          k_scale_vals<<<ew_grid(h.csc.nnz), kEw, 0, st_>>>(col_of[k].p, h.csc.idx,
+                                                           from_orig ? orig_c[k].p : h.csc.val, h.csc.val, r, c,
+                                                           h.csc.nnz, 0, h.coff);
+      }
+    };
     const RedSlots none{};
     for (int s = 0; s < prm.ruiz_iters; ++s) {
-      run_pass(csr_, OpInfNormScale{dr.p, rs_.p}, none, st_);
-      run_pass(csc_, OpInfNormScale{dc.p, cs_.p}, none, st_);
-      k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(row_of.p, csr_.idx, csr_.val, csr_.val, dr.p, dc.p, nnz_, 1);
-      k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(col_of.p, csc_.idx, csc_.val, csc_.val, dr.p, dc.p, nnz_, 0);
+      for (Shard& h : shards_) {
+        run_pass(h.csr, OpInfNormScale{dr.p + h.roff, rs_.p + h.roff}, none, st_);
+        run_pass(h.csc, OpInfNormScale{dc.p + h.coff, cs_.p + h.coff}, none, st_);
+      }
+      GatherY(dr.p);
+      GatherX(dc.p);
+      rescale(false, dr.p, dc.p);
     }
+    GatherY(rs_.p);
+    GatherX(cs_.p);
     // PC on K.Scaled(ruiz) recomputed from the original values (scaling.cpp:89).
-    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(row_of.p, csr_.idx, orig_r.p, csr_.val, rs_.p, cs_.p, nnz_, 1);
-    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(col_of.p, csc_.idx, orig_c.p, csc_.val, rs_.p, cs_.p, nnz_, 0);
+    rescale(true, rs_.p, cs_.p);
     auto mode_of = [](double p) { return p == 0.0 ? 0 : (p == 1.0 ? 1 : (p == 2.0 ? 2 : 3)); };
     const double pr = 2.0 - prm.pc_alpha, pc = prm.pc_alpha;
-    run_pass(csr_, OpPowerSumScale{pr, mode_of(pr), rs_.p}, none, st_);
-    run_pass(csc_, OpPowerSumScale{pc, mode_of(pc), cs_.p}, none, st_);
+    for (Shard& h : shards_) {
+      run_pass(h.csr, OpPowerSumScale{pr, mode_of(pr), rs_.p + h.roff}, none, st_);
+      run_pass(h.csc, OpPowerSumScale{pc, mode_of(pc), cs_.p + h.coff}, none, st_);
+    }
+    GatherY(rs_.p);
+    GatherX(cs_.p);
     // Final K_s from the original values (ApplyScaling, scaling.cpp:105-106).
-    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(row_of.p, csr_.idx, orig_r.p, csr_.val, rs_.p, cs_.p, nnz_, 1);
-    k_scale_vals<<<ew_grid(nnz_), kEw, 0, st_>>>(col_of.p, csc_.idx, orig_c.p, csc_.val, rs_.p, cs_.p, nnz_, 0);
+    rescale(true, rs_.p, cs_.p);
     check_launch("scaling");
     Sync();
   }
-  k_mul<<<ew_grid(n_), kEw, 0, st_>>>(c_o_.p, cs_.p, c_s_.p, n_);
-  k_div<<<ew_grid(n_), kEw, 0, st_>>>(l_o_.p, cs_.p, l_s_.p, n_);
-  k_div<<<ew_grid(n_), kEw, 0, st_>>>(u_o_.p, cs_.p, u_s_.p, n_);
-  k_mul<<<ew_grid(m_), kEw, 0, st_>>>(q_o_.p, rs_.p, q_s_.p, m_);
+  k_mul<<<ew_grid(np_), kEw, 0, st_>>>(c_o_.p, cs_.p, c_s_.p, np_);
+  k_div<<<ew_grid(np_), kEw, 0, st_>>>(l_o_.p, cs_.p, l_s_.p, np_);
+  k_div<<<ew_grid(np_), kEw, 0, st_>>>(u_o_.p, cs_.p, u_s_.p, np_);
+  k_mul<<<ew_grid(mp_), kEw, 0, st_>>>(q_o_.p, rs_.p, q_s_.p, mp_);
   check_launch("apply scaling");
 }
 
-// ||c||, ||q|| in both spaces (kkt.cpp:45-56), deterministic device sums.
+// ||c||, ||q|| in both spaces (kkt.cpp:45-56), deterministic device sums over
+// the full (padded, zero-filled) vectors every rank holds.
 void Session::DeviceNorms() {
   const int g = 148;
   DArray<double> part, out;
   part.alloc(g * 4);
   out.alloc(4);
   const double* vecs[4] = {c_s_.p, q_s_.p, c_o_.p, q_o_.p};
-  const int64_t lens[4] = {n_, m_, n_, m_};
+  const int64_t lens[4] = {np_, mp_, np_, mp_};
   for (int k = 0; k < 4; ++k) {
     k_sumsq_partial<<<g, kEw, 0, st_>>>(vecs[k], lens[k], part.p + k * g);
     k_reduce_tiles<<<1, kBlock, 0, st_>>>(part.p + k * g, nullptr, g, 1, out.p + k);
@@ -462,40 +624,76 @@ void Session::DeviceNorms() {
   q_norm_o_ = std::sqrt(h[3]);
 }
 
-void Session::ToInternal(const double* host, const DArray<int32_t>& perm, double* dev, int64_t n) {
+// Host vector (original order) -> device (padded order); padding zeroed.
+void Session::ToInternal(const double* host, const DArray<int32_t>& pad, double* dev, int64_t n, int64_t padded) {
+  if (padded) PDHG_CUDA(cudaMemsetAsync(dev, 0, padded * sizeof(double), st_));
   if (!n) return;
   DArray<double> tmp;
   tmp.alloc(n);
   PDHG_CUDA(cudaMemcpyAsync(tmp.p, host, n * sizeof(double), cudaMemcpyHostToDevice, st_));
-  k_gather<<<ew_grid(n), kEw, 0, st_>>>(tmp.p, perm.p, dev, n);
+  k_scatter<<<ew_grid(n), kEw, 0, st_>>>(tmp.p, pad.p, dev, n);
   Sync();
 }
 
-void Session::ToHost(const double* dev, const double* scale, const DArray<int32_t>& inv, double* host, int64_t n) {
+void Session::ToHost(const double* dev, const double* scale, const DArray<int32_t>& pad, double* host, int64_t n) {
   if (!n || !host) return;
   DArray<double> tmp;
   tmp.alloc(n);
-  k_unpermute<<<ew_grid(n), kEw, 0, st_>>>(dev, scale, inv.p, tmp.p, n);
+  k_unpermute<<<ew_grid(n), kEw, 0, st_>>>(dev, scale, pad.p, tmp.p, n);
   PDHG_CUDA(cudaMemcpyAsync(host, tmp.p, n * sizeof(double), cudaMemcpyDeviceToHost, st_));
   Sync();
 }
 
 // ================================================================== kernels
+// One PDHG iteration (solver.cpp:284-306): every local shard's K-CSC primal
+// pass writes its slice of x+, one all-gather rebuilds x+ everywhere, then the
+// K-CSR dual passes and the all-gather of y+.
 void Session::LaunchStep(int parity, int j, bool adapt) {
   const int a = parity, b = 1 - parity;
-  launches_ += pass_launches(csc_) + pass_launches(csr_) + (adapt ? 1 : 0);
-  if (adapt) {
-    run_pass(csc_, OpPrimal<true>{y_[a].p, x_[a].p, x_[b].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, j},
-             RedSlots{red_[1].p}, st_);
-    run_pass(csr_, OpDual<true>{x_[b].p, y_[a].p, y_[b].p, ybar_.p, kx_[a].p, kx_[b].p, q_s_.p, rk_, scal_.p, j},
-             RedSlots{red_[0].p}, st_);
-    k_adapt<<<1, kBlock, 0, st_>>>(red_[1].p, csc_.parts(), red_[0].p, csr_.parts(), scal_.p, j);
-  } else {
-    run_pass(csc_, OpPrimal<false>{y_[a].p, x_[a].p, x_[b].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, j},
-             RedSlots{}, st_);
-    run_pass(csr_, OpDual<false>{x_[b].p, y_[a].p, y_[b].p, ybar_.p, kx_[a].p, kx_[b].p, q_s_.p, rk_, scal_.p, j},
-             RedSlots{}, st_);
+  launches_ += launches_csc() + launches_csr();
+  for (Shard& h : shards_) {
+    const int64_t o = h.coff;
+    if (adapt)
+      run_pass(h.csc,
+               OpPrimal<true>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
+                              scal_.p, j},
+               RedSlots{h.red[1].p}, st_);
+    else
+      run_pass(h.csc,
+               OpPrimal<false>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
+                               scal_.p, j},
+               RedSlots{}, st_);
   }
+  GatherX(x_[b].p);
+  for (Shard& h : shards_) {
+    const int64_t o = h.roff;
+    if (adapt)
+      run_pass(h.csr,
+               OpDual<true>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
+                            h.rk, scal_.p, j},
+               RedSlots{h.red[0].p}, st_);
+    else
+      run_pass(h.csr,
+               OpDual<false>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
+                             h.rk, scal_.p, j},
+               RedSlots{}, st_);
+  }
+  GatherY(y_[b].p);
+  if (adapt) {
+    for (size_t k = 0; k < shards_.size(); ++k) {
+      Shard& h = shards_[k];
+      k_adapt_sum<<<1, kBlock, 0, st_>>>(h.red[1].p, h.csc.parts(), h.red[0].p, h.csr.parts(), red_out_.p + k * kPack);
+    }
+    SumPacks(3);
+    k_adapt_apply<<<1, 1, 0, st_>>>(red_out_.p, scal_.p, j);
+    launches_ += static_cast<int64_t>(shards_.size()) + 1 + (shards_.size() > 1);
+  }
+}
+
+// Shard packs -> pack 0 (fixed shard order), then the sum over ranks.
+void Session::SumPacks(int n) {
+  if (shards_.size() > 1) k_sum_packs<<<1, kPack, 0, st_>>>(red_out_.p, static_cast<int>(shards_.size()), kPack, n);
+  comm_->AllReduceSum(red_out_.p, n, st_);
 }
 
 // `count` PDHG iterations starting from buffer `parity`. Blocks are replayed
@@ -521,7 +719,9 @@ void Session::RunSteps(int parity, int count, bool adapt) {
     g = &graphs_.back();
   }
   if (g) {
-    launches_ += static_cast<int64_t>(count) * (pass_launches(csc_) + pass_launches(csr_) + (adapt ? 1 : 0));
+    const int64_t per = launches_csc() + launches_csr() +
+                        (adapt ? static_cast<int64_t>(shards_.size()) + 1 + (shards_.size() > 1) : 0);
+    launches_ += static_cast<int64_t>(count) * per;
     PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
   } else {
     for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
@@ -529,14 +729,27 @@ void Session::RunSteps(int parity, int count, bool adapt) {
   check_launch("pdhg steps");
 }
 
+// The check (solver.cpp:390-428) as two matrix passes per shard: the row
+// side gathers x_bar (K x_bar), the column side gathers [y, y_bar]. Both
+// gathered operands are all-gathered first; the 26 sums are reduced per
+// shard, over local shards and over ranks.
 void Session::LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx) {
-  launches_ += pass_launches(csr_) + pass_launches(csc_) + 2;
-  OpCheckRow row{xb, kxavg_.p, kx, y, yb, ystart_.p, q_s_.p, q_o_.p, rs_.p, rk_};
-  run_pass(csr_, row, RedSlots{red_[0].p}, st_);
-  OpCheckCol col{y, yb, x, xb, xstart_.p, c_s_.p, l_s_.p, u_s_.p, c_o_.p, l_o_.p, u_o_.p, cs_.p};
-  run_pass(csc_, col, RedSlots{red_[1].p}, st_);
-  k_reduce_tiles<<<kRowRed, kBlock, 0, st_>>>(red_[0].p, nullptr, csr_.parts(), kRowRed, red_out_.p);
-  k_reduce_tiles<<<kColRed, kBlock, 0, st_>>>(red_[1].p, nullptr, csc_.parts(), kColRed, red_out_.p + kRowRed);
+  if (xb != x) GatherX(const_cast<double*>(xb));
+  if (yb != y) GatherY(const_cast<double*>(yb));
+  launches_ += launches_csr() + launches_csc() + 2 * static_cast<int64_t>(shards_.size()) + (shards_.size() > 1);
+  for (size_t k = 0; k < shards_.size(); ++k) {
+    Shard& h = shards_[k];
+    const int64_t r = h.roff, c = h.coff;
+    OpCheckRow row{xb, kxavg_.p + r, kx + r, y + r, yb + r, ystart_.p + r, q_s_.p + r, q_o_.p + r, rs_.p + r, h.rk};
+    run_pass(h.csr, row, RedSlots{h.red[0].p}, st_);
+    OpCheckCol col{y, yb, x + c, xb + c, xstart_.p + c, c_s_.p + c, l_s_.p + c, u_s_.p + c, c_o_.p + c,
+                   l_o_.p + c, u_o_.p + c, cs_.p + c};
+    run_pass(h.csc, col, RedSlots{h.red[1].p}, st_);
+    double* pk = red_out_.p + k * kPack;
+    k_reduce_tiles<<<kRowRed, kBlock, 0, st_>>>(h.red[0].p, nullptr, h.csr.parts(), kRowRed, pk);
+    k_reduce_tiles<<<kColRed, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), kColRed, pk + kRowRed);
+  }
+  SumPacks(kRowRed + kColRed);
   check_launch("check");
 }
 
@@ -570,10 +783,10 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 
   // x0 = proj(0), y0 = 0, kx = K x0 (solver.cpp:240-245).
   int par = 0;
-  k_clamp0<<<ew_grid(n_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, n_);
-  if (m_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, m_ * sizeof(double), st_));
-  run_pass(csr_, OpSpmv{x_[0].p, kx_[0].p}, RedSlots{}, st_);
-  launches_ += 1 + pass_launches(csr_);
+  k_clamp0<<<ew_grid(np_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, np_);
+  if (mp_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, mp_ * sizeof(double), st_));
+  for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, st_);
+  launches_ += 1 + launches_csr();
 
   int64_t iters = 0, inner = 0, restarts = 0;
   double kkt_start = 0.0, kkt_prev = std::numeric_limits<double>::infinity();
@@ -591,8 +804,8 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     *orig = MakeReport(r[kPrO], c[kDuO], c[kBdO], c[kCxO], r[kQyO], offset_, q_norm_o_, c_norm_o_);
   };
   auto copy_best = [&](int P) {
-    Copy(xbest_.p, P == 0 ? x_[par].p : xbar_.p, n_);
-    Copy(ybest_.p, P == 0 ? y_[par].p : ybar_.p, m_);
+    Copy(xbest_.p, P == 0 ? x_[par].p : xbar_.p, np_);
+    Copy(ybest_.p, P == 0 ? y_[par].p : ybar_.p, mp_);
   };
   // RecordBest (solver.cpp:341-351).
   auto record_best = [&](int P, const pdhg_report& r) {
@@ -606,8 +819,8 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   };
   // StartLoopAt (solver.cpp:275-281) with the candidate's scaled residuals.
   auto start_loop = [&](const pdhg_report& s) {
-    Copy(xstart_.p, x_[par].p, n_);
-    Copy(ystart_.p, y_[par].p, m_);
+    Copy(xstart_.p, x_[par].p, np_);
+    Copy(ystart_.p, y_[par].p, mp_);
     kkt_start = KktError(s.primal_res, s.dual_res, s.gap_abs, sc.omega);
     kkt_prev = std::numeric_limits<double>::infinity();
     sc.inner_base = 0.0;
@@ -637,12 +850,16 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     last_rep = o_cur;
   }
 
+  // Time limit: one clock decides for every rank (rank 0's, shipped in the
+  // check pack), so all ranks leave the loop after the same block.
+  bool time_up = !(prm.time_limit > 0.0);
   while (!finished) {
     if (iters >= prm.iter_limit) {
       status = PDHG_ITER_LIMIT;
       break;
     }
-    if (secs() >= prm.time_limit) {
+    if (!nccl()) time_up = secs() >= prm.time_limit;
+    if (time_up) {
       status = PDHG_TIME_LIMIT;
       break;
     }
@@ -662,8 +879,17 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 
     // ---- Check (solver.cpp:390-428).
     LaunchCheck(x_[par].p, y_[par].p, xbar_.p, ybar_.p, kx_[par].p);
+    if (nccl()) {  // rank 0's clock, summed into slot kPack - 1 of every rank
+      host_red_[kPack - 1] = (rank_ == 0 && secs() >= prm.time_limit) ? 1.0 : 0.0;
+      PDHG_CUDA(cudaMemcpyAsync(red_out_.p + kPack - 1, host_red_ + kPack - 1, sizeof(double), cudaMemcpyHostToDevice,
+                                st_));
+      comm_->AllReduceMax(red_out_.p + kPack - 1, 1, st_);
+      PDHG_CUDA(cudaMemcpyAsync(host_red_ + kPack - 1, red_out_.p + kPack - 1, sizeof(double), cudaMemcpyDeviceToHost,
+                                st_));
+    }
     if (adapt) PDHG_CUDA(cudaMemcpyAsync(&sc.eta, &scal_.p->eta, sizeof(double), cudaMemcpyDeviceToHost, st_));
     ReadCheck(&ck);
+    if (nccl()) time_up = host_red_[kPack - 1] > 0.0;
     if (ck.row[2 * kRowPer] > 0.0 || ck.col[2 * kColPer] > 0.0)
       throw Error(PDHG_NUMERICAL_FAILURE, "non-finite iterate at iteration " + std::to_string(iters));
     reports(0, &s_cur, &o_cur);
@@ -713,9 +939,9 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
       const double dy = std::sqrt(ck.row[P * kRowPer + kDy2]);
       sc.omega = UpdatePrimalWeight(sc.omega, dx, dy);
       if (!take_cur) {
-        Copy(x_[par].p, xbar_.p, n_);
-        Copy(y_[par].p, ybar_.p, m_);
-        Copy(kx_[par].p, kxavg_.p, m_);  // ComputeKx(candidate): same pass, same sums
+        Copy(x_[par].p, xbar_.p, np_);
+        Copy(y_[par].p, ybar_.p, mp_);
+        Copy(kx_[par].p, kxavg_.p, mp_);  // ComputeKx(candidate): same pass, same sums
       }
       start_loop(take_cur ? s_cur : s_avg);
       ++restarts;
@@ -731,7 +957,18 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
                   info.original_report.rel_dual, info.original_report.rel_gap, info.omega,
                   (long long)info.restarts);
     }
-    if (cb && cb(&info, user) != 0) throw Error(PDHG_ABORTED, "aborted by observer");
+    int stop = (cb && cb(&info, user) != 0) ? 1 : 0;
+    if (nccl() && cb) {  // an abort on any rank stops every rank
+      host_red_[kPack - 1] = stop;
+      PDHG_CUDA(cudaMemcpyAsync(red_out_.p + kPack - 1, host_red_ + kPack - 1, sizeof(double), cudaMemcpyHostToDevice,
+                                st_));
+      comm_->AllReduceMax(red_out_.p + kPack - 1, 1, st_);
+      PDHG_CUDA(cudaMemcpyAsync(host_red_ + kPack - 1, red_out_.p + kPack - 1, sizeof(double), cudaMemcpyDeviceToHost,
+                                st_));
+      Sync();
+      stop = host_red_[kPack - 1] > 0.0;
+    }
+    if (stop) throw Error(PDHG_ABORTED, "aborted by observer");
   }
 
   if (!have_best) {  // UseBestSeen (solver.cpp:464-471)
@@ -742,18 +979,22 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   }
 
   // Finish (solver.cpp:473-481): unscale best, lambda on the original problem.
-  ToHost(xbest_.p, cs_.p, inv_c_, out->x, n_);
-  ToHost(ybest_.p, rs_.p, inv_r_, out->y, m_);
+  ToHost(xbest_.p, cs_.p, pad_c_, out->x, n_);
+  ToHost(ybest_.p, rs_.p, pad_r_, out->y, m_);
   if (out->lambda) {
-    run_pass(csc_, OpLambda{ybest_.p, c_o_.p, l_o_.p, u_o_.p, cs_.p, nvec_.p}, RedSlots{}, st_);
-    ToHost(nvec_.p, nullptr, inv_c_, out->lambda, n_);
+    for (Shard& h : shards_) {
+      const int64_t c = h.coff;
+      run_pass(h.csc, OpLambda{ybest_.p, c_o_.p + c, l_o_.p + c, u_o_.p + c, cs_.p + c, nvec_.p + c}, RedSlots{}, st_);
+    }
+    GatherX(nvec_.p);
+    ToHost(nvec_.p, nullptr, pad_c_, out->lambda, n_);
   }
   PDHG_CUDA(cudaEventRecord(ev_[1], st_));
   Sync();
   float ms = 0.f;
   PDHG_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
   last_ms_ = ms;
-  last_launches_ = launches_ + 3 + pass_launches(csc_);
+  last_launches_ = launches_ + 3 + launches_csc();
   out->status = status;
   out->report = best_rep;
   out->iterations = iters;
@@ -763,7 +1004,9 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 }
 
 // EstimateOpNorm (solver.cpp:84-110) with the host start vector drawn from the
-// same libstdc++ engines as the reference (original column order).
+// same libstdc++ engines as the reference (original column order). Per step:
+// K-CSR passes (gather u) -> all-gather kv -> K-CSC passes with sum(u^2)
+// partials -> normalisation from the shard/rank sum -> all-gather u.
 double Session::OpNorm(int iters, uint64_t seed) {
   PDHG_CUDA(cudaSetDevice(device_));
   if (nnz_ == 0) return 0.0;
@@ -779,21 +1022,34 @@ double Session::OpNorm(int iters, uint64_t seed) {
     vnorm = 1.0;
   }
   DArray<double> u, kv;
-  u.alloc(n_);
-  kv.alloc(m_);
-  ToInternal(v.data(), perm_c_, u.p, n_);
+  u.alloc(np_);
+  kv.alloc(mp_);
+  PDHG_CUDA(cudaMemsetAsync(kv.p, 0, mp_ * sizeof(double), st_));
+  ToInternal(v.data(), pad_c_, u.p, n_, np_);
   Scalars sc{};
   sc.pw_norm = vnorm;
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
-  launches_ += static_cast<int64_t>(iters) * (pass_launches(csr_) + pass_launches(csc_) + 2) + pass_launches(csr_) + 1;
+  const int64_t ns = static_cast<int64_t>(shards_.size());
+  launches_ += static_cast<int64_t>(iters) * (launches_csr() + launches_csc() + ns + (ns > 1) + 1) + launches_csr() +
+               ns + (ns > 1);
   for (int it = 0; it < iters; ++it) {
-    run_pass(csr_, OpPowerStep<false>{u.p, scal_.p, 1, kv.p}, RedSlots{}, st_);
-    run_pass(csc_, OpPowerStep<true>{kv.p, scal_.p, 0, u.p}, RedSlots{red_[1].p}, st_);
-    k_reduce_tiles<<<1, kBlock, 0, st_>>>(red_[1].p, nullptr, csc_.parts(), 1, red_out_.p);
+    for (Shard& h : shards_) run_pass(h.csr, OpPowerStep<false>{u.p, scal_.p, 1, kv.p + h.roff}, RedSlots{}, st_);
+    GatherY(kv.p);
+    for (size_t k = 0; k < shards_.size(); ++k) {
+      Shard& h = shards_[k];
+      run_pass(h.csc, OpPowerStep<true>{kv.p, scal_.p, 0, u.p + h.coff}, RedSlots{h.red[1].p}, st_);
+      k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), 1, red_out_.p + k * kPack);
+    }
+    SumPacks(1);
     k_power_norm<<<1, 1, 0, st_>>>(red_out_.p, scal_.p);
+    GatherX(u.p);
   }
-  run_pass(csr_, OpPowerStep<true>{u.p, scal_.p, 1, kv.p}, RedSlots{red_[0].p}, st_);
-  k_reduce_tiles<<<1, kBlock, 0, st_>>>(red_[0].p, nullptr, csr_.parts(), 1, red_out_.p);
+  for (size_t k = 0; k < shards_.size(); ++k) {
+    Shard& h = shards_[k];
+    run_pass(h.csr, OpPowerStep<true>{u.p, scal_.p, 1, kv.p + h.roff}, RedSlots{h.red[0].p}, st_);
+    k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[0].p, nullptr, h.csr.parts(), 1, red_out_.p + k * kPack);
+  }
+  SumPacks(1);
   check_launch("power iteration");
   double sum = 0.0;
   Scalars hs{};
@@ -807,37 +1063,53 @@ double Session::OpNorm(int iters, uint64_t seed) {
 // ============================================================ kernel probes
 void Session::Scaling(double* rs, double* cs) {
   PDHG_CUDA(cudaSetDevice(device_));
-  ToHost(rs_.p, nullptr, inv_r_, rs, m_);
-  ToHost(cs_.p, nullptr, inv_c_, cs, n_);
+  ToHost(rs_.p, nullptr, pad_r_, rs, m_);
+  ToHost(cs_.p, nullptr, pad_c_, cs, n_);
 }
 
 void Session::ScaledProblem(double* kv, double* c, double* l, double* u, double* q) {
   PDHG_CUDA(cudaSetDevice(device_));
   if (kv && nnz_) {
+    if (nccl()) throw Error(PDHG_INVALID_ARGUMENT, "scaled values are only available when all shards are local");
+    std::vector<int32_t> hp(static_cast<size_t>(m_) + 1);
+    PDHG_CUDA(cudaMemcpyAsync(hp.data(), ptr0_.p, (m_ + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+    Sync();
     DArray<double> tmp;
     tmp.alloc(nnz_);
-    k_values_orig<<<ew_grid(nnz_), kEw, 0, st_>>>(ptr0_.p, m_, inv_r_.p, csr_.ptr, csr_.val, tmp.p, nnz_);
+    for (Shard& h : shards_) {
+      const int64_t k0 = hp[row_begin_[h.block]], k1 = hp[row_begin_[h.block + 1]];
+      if (k1 > k0)
+        k_values_orig<<<ew_grid(k1 - k0), kEw, 0, st_>>>(ptr0_.p, m_, k0, k1, pad_r_.p, h.roff, h.csr.ptr,
+                                                          h.csr.val, tmp.p);
+    }
     PDHG_CUDA(cudaMemcpyAsync(kv, tmp.p, nnz_ * sizeof(double), cudaMemcpyDeviceToHost, st_));
     Sync();
   }
-  ToHost(c_s_.p, nullptr, inv_c_, c, n_);
-  ToHost(l_s_.p, nullptr, inv_c_, l, n_);
-  ToHost(u_s_.p, nullptr, inv_c_, u, n_);
-  ToHost(q_s_.p, nullptr, inv_r_, q, m_);
+  ToHost(c_s_.p, nullptr, pad_c_, c, n_);
+  ToHost(l_s_.p, nullptr, pad_c_, l, n_);
+  ToHost(u_s_.p, nullptr, pad_c_, u, n_);
+  ToHost(q_s_.p, nullptr, pad_r_, q, m_);
 }
 
 void Session::Spmv(int transpose, const double* in, double* out) {
   PDHG_CUDA(cudaSetDevice(device_));
   const int64_t nin = transpose ? m_ : n_, nout = transpose ? n_ : m_;
+  const int64_t pin = transpose ? mp_ : np_, pout = transpose ? np_ : mp_;
   DArray<double> a, b;
-  a.alloc(std::max<int64_t>(nin, 1));
-  b.alloc(std::max<int64_t>(nout, 1));
-  ToInternal(in, transpose ? perm_r_ : perm_c_, a.p, nin);
-  run_pass(transpose ? csc_ : csr_, OpSpmv{a.p, b.p}, RedSlots{}, st_);
+  a.alloc(std::max<int64_t>(pin, 1));
+  b.alloc(std::max<int64_t>(pout, 1));
+  PDHG_CUDA(cudaMemsetAsync(b.p, 0, std::max<int64_t>(pout, 1) * sizeof(double), st_));
+  ToInternal(in, transpose ? pad_r_ : pad_c_, a.p, nin, pin);
+  for (Shard& h : shards_) run_pass(transpose ? h.csc : h.csr, OpSpmv{a.p, b.p + (transpose ? h.coff : h.roff)},
+                                    RedSlots{}, st_);
+  if (transpose) GatherX(b.p);
+  else GatherY(b.p);
   check_launch("spmv");
-  ToHost(b.p, nullptr, transpose ? inv_c_ : inv_r_, out, nout);
+  ToHost(b.p, nullptr, transpose ? pad_c_ : pad_r_, out, nout);
 }
 
+// Mean device time of the two fused step kernels (all local shards, gathers
+// included) and of a graph-launched 64-iteration block, on the solver stream.
 void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double* ms_iter) {
   PDHG_CUDA(cudaSetDevice(device_));
   Scalars sc{};
@@ -845,9 +1117,9 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   sc.omega = 1.0;
   sc.inner_base = 1.0;
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
-  k_clamp0<<<ew_grid(n_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, n_);
-  if (m_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, m_ * sizeof(double), st_));
-  run_pass(csr_, OpSpmv{x_[0].p, kx_[0].p}, RedSlots{}, st_);
+  k_clamp0<<<ew_grid(np_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, np_);
+  if (mp_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, mp_ * sizeof(double), st_));
+  for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, st_);
   cudaEvent_t e0, e1, e2;
   PDHG_CUDA(cudaEventCreate(&e0));
   PDHG_CUDA(cudaEventCreate(&e1));
@@ -856,14 +1128,27 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   Sync();
   float t_p = 0, t_d = 0, t_i = 0;
   PDHG_CUDA(cudaEventRecord(e0, st_));
-  for (int i = 0; i < iters; ++i)
-    run_pass(csc_, OpPrimal<false>{y_[0].p, x_[0].p, x_[1].p, xbar_.p, c_s_.p, l_s_.p, u_s_.p, scal_.p, i + 1},
-             RedSlots{}, st_);
+  for (int i = 0; i < iters; ++i) {
+    for (Shard& h : shards_) {
+      const int64_t o = h.coff;
+      run_pass(h.csc,
+               OpPrimal<false>{y_[0].p, x_[0].p + o, x_[1].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
+                               scal_.p, i + 1},
+               RedSlots{}, st_);
+    }
+    GatherX(x_[1].p);
+  }
   PDHG_CUDA(cudaEventRecord(e1, st_));
-  for (int i = 0; i < iters; ++i)
-    run_pass(csr_,
-             OpDual<false>{x_[1].p, y_[0].p, y_[1].p, ybar_.p, kx_[0].p, kx_[1].p, q_s_.p, rk_, scal_.p, i + 1},
-             RedSlots{}, st_);
+  for (int i = 0; i < iters; ++i) {
+    for (Shard& h : shards_) {
+      const int64_t o = h.roff;
+      run_pass(h.csr,
+               OpDual<false>{x_[1].p, y_[0].p + o, y_[1].p + o, ybar_.p + o, kx_[0].p + o, kx_[1].p + o, q_s_.p + o,
+                             h.rk, scal_.p, i + 1},
+               RedSlots{}, st_);
+    }
+    GatherY(y_[1].p);
+  }
   PDHG_CUDA(cudaEventRecord(e2, st_));
   PDHG_CUDA(cudaEventSynchronize(e2));
   PDHG_CUDA(cudaEventElapsedTime(&t_p, e0, e1));
@@ -888,31 +1173,40 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
 void Session::UnitPrimal(const double* x, const double* y, double eta, double omega, double* out) {
   PDHG_CUDA(cudaSetDevice(device_));
   DArray<double> dx, dy, dout;
-  dx.alloc(std::max<int64_t>(n_, 1));
-  dy.alloc(std::max<int64_t>(m_, 1));
-  dout.alloc(std::max<int64_t>(n_, 1));
-  ToInternal(x, perm_c_, dx.p, n_);
-  ToInternal(y, perm_r_, dy.p, m_);
-  run_pass(csc_, OpUnitPrimal{dy.p, dx.p, c_s_.p, l_s_.p, u_s_.p, eta / omega, dout.p}, RedSlots{}, st_);
+  dx.alloc(std::max<int64_t>(np_, 1));
+  dy.alloc(std::max<int64_t>(mp_, 1));
+  dout.alloc(std::max<int64_t>(np_, 1));
+  ToInternal(x, pad_c_, dx.p, n_, np_);
+  ToInternal(y, pad_r_, dy.p, m_, mp_);
+  for (Shard& h : shards_) {
+    const int64_t o = h.coff;
+    run_pass(h.csc, OpUnitPrimal{dy.p, dx.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o, eta / omega, dout.p + o},
+             RedSlots{}, st_);
+  }
+  GatherX(dout.p);
   check_launch("primal step");
-  ToHost(dout.p, nullptr, inv_c_, out, n_);
+  ToHost(dout.p, nullptr, pad_c_, out, n_);
 }
 
 void Session::UnitDual(const double* xn, const double* xo, const double* y, double eta, double omega, double* out) {
   PDHG_CUDA(cudaSetDevice(device_));
   DArray<double> a, b, ext, dy, dout;
-  a.alloc(std::max<int64_t>(n_, 1));
-  b.alloc(std::max<int64_t>(n_, 1));
-  ext.alloc(std::max<int64_t>(n_, 1));
-  dy.alloc(std::max<int64_t>(m_, 1));
-  dout.alloc(std::max<int64_t>(m_, 1));
-  ToInternal(xn, perm_c_, a.p, n_);
-  ToInternal(xo, perm_c_, b.p, n_);
-  ToInternal(y, perm_r_, dy.p, m_);
-  k_reflect<<<ew_grid(n_), kEw, 0, st_>>>(a.p, b.p, ext.p, n_);
-  run_pass(csr_, OpUnitDual{ext.p, dy.p, q_s_.p, rk_, eta * omega, dout.p}, RedSlots{}, st_);
+  a.alloc(std::max<int64_t>(np_, 1));
+  b.alloc(std::max<int64_t>(np_, 1));
+  ext.alloc(std::max<int64_t>(np_, 1));
+  dy.alloc(std::max<int64_t>(mp_, 1));
+  dout.alloc(std::max<int64_t>(mp_, 1));
+  ToInternal(xn, pad_c_, a.p, n_, np_);
+  ToInternal(xo, pad_c_, b.p, n_, np_);
+  ToInternal(y, pad_r_, dy.p, m_, mp_);
+  k_reflect<<<ew_grid(np_), kEw, 0, st_>>>(a.p, b.p, ext.p, np_);
+  for (Shard& h : shards_) {
+    const int64_t o = h.roff;
+    run_pass(h.csr, OpUnitDual{ext.p, dy.p + o, q_s_.p + o, h.rk, eta * omega, dout.p + o}, RedSlots{}, st_);
+  }
+  GatherY(dout.p);
   check_launch("dual step");
-  ToHost(dout.p, nullptr, inv_r_, out, m_);
+  ToHost(dout.p, nullptr, pad_r_, out, m_);
 }
 
 // Evict the working set between benchmark steps: write 2x the L2 capacity.
@@ -931,13 +1225,21 @@ void Session::Stats(pdhg_session_stats* s) const {
   s->m2 = m2_;
   s->n = n_;
   s->nnz = nnz_;
-  s->csr_tiles = csr_.parts();
-  s->csc_tiles = csc_.parts();
+  s->csr_tiles = parts_csr();
+  s->csc_tiles = parts_csc();
   s->device_bytes = arena_.bytes;
   s->upload_seconds = upload_s_;
   s->scaling_seconds = scaling_s_;
   s->device = device_;
   s->l2_resident = l2_resident_ ? 1 : 0;
+  s->world = world_;
+  s->local_shards = static_cast<int32_t>(shards_.size());
+  s->rank = rank_;
+}
+
+void Session::Blocks(int64_t* row_begin, int64_t* col_begin) const {
+  std::copy(row_begin_.begin(), row_begin_.end(), row_begin);
+  std::copy(col_begin_.begin(), col_begin_.end(), col_begin);
 }
 
 }  // namespace pdhg

@@ -1,12 +1,22 @@
 // Resident solve session: the scaled stacked problem in HBM plus all PDHG
 // state. Host orchestration mirrors SolveLoop (reference solver.cpp:203-517).
+//
+// Sharding: K is split into `world` contiguous row blocks (the
+// CSR side, K x) and column blocks (the CSC side, K^T y), balanced by
+// nonzeros. A Shard owns one row block and one column block; a session holds
+// either every shard (world = 1, or the in-process multi-shard mode) or the
+// one shard of its rank (one process per GPU, NCCL exchanges). Vectors live in
+// the padded index space of comm.cuh; full copies of x and y are rebuilt by
+// one all-gather after each half-step.
 #pragma once
 
 #include <chrono>
 #include <functional>
+#include <memory>
 #include <vector>
 
 #include "../../include/pdhg.h"
+#include "comm.cuh"
 #include "darray.cuh"
 #include "engine.cuh"
 
@@ -14,9 +24,17 @@ namespace pdhg {
 
 struct CheckOut;  // host mirror of the check reductions
 
+// How K is distributed (pdhg_shard_spec in include/pdhg.h).
+struct ShardSpec {
+  int world = 1;                  // number of shards
+  int rank = 0;                   // this process's shard (NCCL mode)
+  int local = 1;                  // shards held by this session: 1 or world
+  const void* nccl_id = nullptr;  // 128-byte ncclUniqueId (NCCL mode)
+};
+
 class Session {
  public:
-  Session(const pdhg_lp& lp, const pdhg_params& prm, int device);
+  Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const ShardSpec& spec = ShardSpec{});
   ~Session();
 
   void Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_result* out);
@@ -26,6 +44,7 @@ class Session {
   double OpNorm(int iters, uint64_t seed);
   void TimeKernels(int iters, double* ms_primal, double* ms_dual, double* ms_iter);
   void Stats(pdhg_session_stats* s) const;
+  void Blocks(int64_t* row_begin, int64_t* col_begin) const;
   void UnitPrimal(const double* x, const double* y, double eta, double omega, double* out);
   void UnitDual(const double* xn, const double* xo, const double* y, double eta, double omega, double* out);
   int device() const { return device_; }
@@ -40,7 +59,7 @@ class Session {
     int parity = 0;
     bool adapt = false;
   };
-  // Storage of one permuted layout (CSR of K or CSC of K).
+  // Storage of one permuted layout (CSR of a row block or CSC of a column block).
   struct Store {
     DArray<int32_t> ptr, idx;
     DArray<double> val;
@@ -48,6 +67,16 @@ class Session {
     DArray<double> head, tail;
     DArray<unsigned> cnt;
   };
+  struct Shard {
+    int block = 0;
+    int64_t roff = 0, coff = 0;  // padded offsets of the block's rows / columns
+    int64_t rows = 0, cols = 0;  // block sizes
+    Layout csr, csc;             // segment s of the block <-> vector index off + s
+    Store csr_st, csc_st;
+    RowKind rk{};                // equality rows of the block (local order)
+    DArray<double> red[2];       // reduction slots: [0] CSR passes, [1] CSC passes
+  };
+  static constexpr int kPack = 32;  // doubles per reduction pack (>= kRowRed + kColRed)
 
   void Upload(const pdhg_lp& lp, DArray<int32_t>& ptr0, DArray<int32_t>& idx0, DArray<double>& val0);
   void Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, const DArray<double>& val0);
@@ -59,9 +88,17 @@ class Session {
   void RunSteps(int parity, int count, bool adapt);
   void LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx);
   void ReadCheck(CheckOut* out);
+  void SumPacks(int n);  // red_out_ shard packs -> red_out_[0..n), all ranks
   void Copy(double* dst, const double* src, size_t n);
-  void ToInternal(const double* host, const DArray<int32_t>& perm, double* dev, int64_t n);
-  void ToHost(const double* dev, const double* scale, const DArray<int32_t>& inv, double* host, int64_t n);
+  void ToInternal(const double* host, const DArray<int32_t>& pad, double* dev, int64_t n, int64_t padded);
+  void ToHost(const double* dev, const double* scale, const DArray<int32_t>& pad, double* host, int64_t n);
+  void GatherX(double* v) { comm_->AllGather(v, pn_, st_); }
+  void GatherY(double* v) { comm_->AllGather(v, pm_, st_); }
+  bool nccl() const { return !comm_->local(); }
+  int parts_csr() const;
+  int parts_csc() const;
+  int launches_csr() const;
+  int launches_csc() const;
 
   int device_ = 0;
   cudaStream_t st_ = nullptr;
@@ -72,23 +109,26 @@ class Session {
   bool scaled_ = false;
   bool l2_resident_ = false;
 
-  // K_s in both layouts, rows / columns permuted into length classes.
-  Layout csr_, csc_;
-  Store csr_st_, csc_st_;
-  RowKind rk_{};
-  DArray<int32_t> perm_r_, inv_r_, perm_c_, inv_c_;  // new->old, old->new
-  DArray<int32_t> ptr0_;                             // original CSR row_ptr (probe only)
+  // Distribution: blocks in original order, padded slice sizes.
+  int world_ = 1, rank_ = 0;
+  std::vector<int64_t> row_begin_, col_begin_;
+  int64_t pm_ = 0, pn_ = 0;      // padded slice (rows / columns per block)
+  int64_t mp_ = 0, np_ = 0;      // padded vector lengths world * pm_, world * pn_
+  std::unique_ptr<Comm> comm_;
+  std::vector<Shard> shards_;
+  DArray<int32_t> pad_r_, pad_c_;  // original row / column -> padded index
+  DArray<int32_t> ptr0_;           // original CSR row_ptr (probe only)
 
-  // Problem vectors (permuted order): scaled (loop) and original (termination).
-  DArray<double> c_s_, l_s_, u_s_, c_o_, l_o_, u_o_, cs_;  // n
-  DArray<double> q_s_, q_o_, rs_;                          // m
+  // Problem vectors (padded order): scaled (loop) and original (termination).
+  DArray<double> c_s_, l_s_, u_s_, c_o_, l_o_, u_o_, cs_;  // np_
+  DArray<double> q_s_, q_o_, rs_;                          // mp_
   double c_norm_s_ = 0, q_norm_s_ = 0, c_norm_o_ = 0, q_norm_o_ = 0;
 
   // Iterates (ping-pong x/y/kx), averages, loop start, best, scratch.
-  DArray<double> x_[2], xbar_, xstart_, xbest_, nvec_;            // n
-  DArray<double> y_[2], ybar_, ystart_, ybest_, kx_[2], kxavg_;  // m
+  DArray<double> x_[2], xbar_, xstart_, xbest_, nvec_;            // np_
+  DArray<double> y_[2], ybar_, ystart_, ybest_, kx_[2], kxavg_;  // mp_
   DArray<Scalars> scal_;
-  DArray<double> red_[2], red_out_;
+  DArray<double> red_out_;  // per-shard packs; pack 0 holds the reduced result
   double* host_red_ = nullptr;  // pinned
 
   std::vector<Graph> graphs_;

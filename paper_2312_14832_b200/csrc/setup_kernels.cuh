@@ -73,13 +73,53 @@ __global__ void k_csc_gather(const int32_t* perm, const int32_t* row_of, const d
 }
 
 // ------------------------------------------------------- class permutation
-// key = class(len) * 2 + (row is an inequality row); columns use eq_end = n.
-__global__ void k_class_keys(const int32_t* p, int64_t nseg, int64_t eq_end, int32_t* key) {
+// Block of original segment s (blocks contiguous in original order, P <= 64).
+__device__ __forceinline__ int block_of(const int64_t* begin, int P, int64_t s) {
+  int b = 0;
+  while (b + 1 < P && begin[b + 1] <= s) ++b;
+  return b;
+}
+
+// key = block * 8 + class(len) * 2 + (row is an inequality row); columns use
+// eq_end = n. A stable sort by key puts every block's segments contiguously
+// (in block order) and, inside a block, class by class with equality rows
+// first, each run keeping the original order.
+__global__ void k_class_keys(const int32_t* p, int64_t nseg, int64_t eq_end, const int64_t* begin, int P,
+                             int warp_max, int cta_max, int32_t* key) {
   GRID_STRIDE(s, nseg) {
     const int len = p[s + 1] - p[s];
-    const int cls = len <= kSeqMax ? 0 : (len <= kWarpMax ? 1 : (len <= kCtaMax ? 2 : 3));
-    key[s] = cls * 2 + (s >= eq_end ? 1 : 0);
+    const int cls = len <= kSeqMax ? 0 : (len <= warp_max ? 1 : (len <= cta_max ? 2 : 3));
+    key[s] = block_of(begin, P, s) * 8 + cls * 2 + (s >= eq_end ? 1 : 0);
   }
+}
+
+// Padded index of original segment s: block b's segments occupy
+// [b * slice, b * slice + size_b) in class order (inv = compact position).
+__global__ void k_pad_index(const int32_t* inv, const int64_t* begin, int P, int64_t slice, int32_t* pad, int64_t n) {
+  GRID_STRIDE(s, n) {
+    const int b = block_of(begin, P, s);
+    pad[s] = static_cast<int32_t>(b * slice + (inv[s] - begin[b]));
+  }
+}
+
+// out[pad[i]] = in[i] (original -> padded order).
+__global__ void k_scatter(const double* in, const int32_t* pad, double* out, int64_t n) {
+  GRID_STRIDE(i, n) out[pad[i]] = in[i];
+}
+
+// Shard-local row_ptr: out[s] = ptr[s] - ptr[0] for s <= nseg.
+__global__ void k_rebase(const int32_t* ptr, int64_t nseg, int32_t* out) {
+  const int32_t base = ptr[0];
+  GRID_STRIDE(s, nseg + 1) out[s] = ptr[s] - base;
+}
+
+// Sum of `count` reduction packs (fixed shard order) into pack 0.
+__global__ void k_sum_packs(double* packs, int count, int stride, int n) {
+  const int i = threadIdx.x;
+  if (i >= n) return;
+  double v = packs[i];
+  for (int k = 1; k < count; ++k) v += packs[static_cast<int64_t>(k) * stride + i];
+  packs[i] = v;
 }
 
 __global__ void k_key_hist(const int32_t* key, int64_t n, int32_t* hist) {
@@ -107,12 +147,7 @@ __global__ void k_perm_nnz(const int32_t* p0, const int32_t* seg_of, const int32
   }
 }
 
-// out[i'] = in[perm[i']] (original -> permuted order).
-__global__ void k_gather(const double* in, const int32_t* perm, double* out, int64_t n) {
-  GRID_STRIDE(i, n) out[i] = in[perm[i]];
-}
-
-// out[i] = in[inv[i]] * (scale ? scale[inv[i]] : 1)  (permuted -> original).
+// out[i] = in[inv[i]] * (scale ? scale[inv[i]] : 1)  (padded -> original).
 __global__ void k_unpermute(const double* in, const double* scale, const int32_t* inv, double* out, int64_t n) {
   GRID_STRIDE(i, n) {
     const int32_t j = inv[i];
@@ -122,11 +157,12 @@ __global__ void k_unpermute(const double* in, const double* scale, const int32_t
 
 // ------------------------------------------------------------- vectors
 // Scaled (sparse_matrix.cpp:213, :218): (row_scale * v) * col_scale.
+// seg_of is shard-local; `soff` moves it into the padded vector space.
 __global__ void k_scale_vals(const int32_t* seg_of, const int32_t* idx, const double* vin, double* vout,
-                             const double* rs, const double* cs, int64_t nnz, int csr_role) {
+                             const double* rs, const double* cs, int64_t nnz, int csr_role, int64_t soff) {
   GRID_STRIDE(k, nnz) {
-    const int32_t r = csr_role ? seg_of[k] : idx[k];
-    const int32_t c = csr_role ? idx[k] : seg_of[k];
+    const int64_t r = csr_role ? soff + seg_of[k] : idx[k];
+    const int64_t c = csr_role ? idx[k] : soff + seg_of[k];
     vout[k] = rs[r] * vin[k] * cs[c];
   }
 }
@@ -166,12 +202,14 @@ __device__ int64_t seg_end_pos(const int32_t* p, int64_t s, int64_t nz1) {
   return pos < nz1 - 1 ? pos : nz1 - 1;
 }
 
-// K_s values in the ORIGINAL CSR order (for the parity probe).
-__global__ void k_values_orig(const int32_t* p0, int64_t m, const int32_t* inv_r, const int32_t* p1,
-                              const double* v1, double* out, int64_t nnz) {
-  GRID_STRIDE(k, nnz) {
+// K_s values in the ORIGINAL CSR order (parity probe), one row block at a
+// time: original row r of the block is local segment pad[r] - roff.
+__global__ void k_values_orig(const int32_t* p0, int64_t m, int64_t k0, int64_t k1, const int32_t* pad_r,
+                              int64_t roff, const int32_t* p1, const double* v1, double* out) {
+  GRID_STRIDE(q, k1 - k0) {
+    const int64_t k = k0 + q;
     const int64_t r = upper_bound_i32(p0, m + 1, k) - 1;
-    out[k] = v1[p1[inv_r[r]] + (k - p0[r])];
+    out[k] = v1[p1[pad_r[r] - roff] + (k - p0[r])];
   }
 }
 
@@ -278,8 +316,10 @@ __global__ void k_power_norm(const double* sum, Scalars* sc) {
   }
 }
 
-// AdaptStepSize (solver.cpp:310-328) from the per-iteration partials.
-__global__ void k_adapt(const double* cred, int cn, const double* rred, int rn, Scalars* sc, int j) {
+// AdaptStepSize (solver.cpp:310-328) from the per-iteration partials:
+// k_adapt_sum folds one shard's tile partials into (|dx|^2, |dy|^2, dy.K dx),
+// k_adapt_apply updates eta from the (shard- and rank-summed) triple.
+__global__ void k_adapt_sum(const double* cred, int cn, const double* rred, int rn, double* out) {
   __shared__ double sh[3][kBlock / 32];
   double a[3] = {0.0, 0.0, 0.0};
   for (int t = threadIdx.x; t < cn; t += blockDim.x) a[0] += cred[t];
@@ -299,7 +339,14 @@ __global__ void k_adapt(const double* cred, int cn, const double* rred, int rn, 
     dy += sh[1][w];
     it += sh[2][w];
   }
-  it = fabs(it);
+  out[0] = dx;
+  out[1] = dy;
+  out[2] = it;
+}
+
+__global__ void k_adapt_apply(const double* sum, Scalars* sc, int j) {
+  const double dx = sum[0], dy = sum[1];
+  const double it = fabs(sum[2]);
   if (it <= 0.0) return;
   const double om = sc->omega;
   const double lim = (om * dx + dy / om) / (2.0 * it);

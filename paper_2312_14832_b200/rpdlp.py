@@ -279,16 +279,65 @@ def _pack(res, x, y, lam) -> SolveResult:
                        res.restarts, res.solve_seconds, res.scaling_seconds)
 
 
+@dataclass
+class Shards:
+    """How K is distributed (pdhg_shard_spec).
+
+    Shards(world=P, local=True): all P shards in this process on one device
+    (exchanges are in-place no-ops) -- the sharded path on a single GPU.
+    Shards.from_process_group(): one shard per torch.distributed rank (one
+    process per GPU); rank 0 creates the NCCL id and broadcasts it over the
+    group, the solver then all-gathers x / y slices with NCCL itself."""
+    world: int = 1
+    rank: int = 0
+    local: bool = True
+    nccl_id: Optional[bytes] = None
+
+    @staticmethod
+    def from_process_group(group=None) -> "Shards":
+        import torch
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        if world == 1:
+            return Shards()
+        uid = bytearray(128)
+        if rank == 0:
+            buf = C.create_string_buffer(128)
+            err = C.create_string_buffer(abi.ERRLEN)
+            raise_for(abi.load().pdhg_nccl_unique_id(buf, err, abi.ERRLEN), err)
+            uid = bytearray(buf.raw)
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, src=0, group=group)
+        return Shards(world, rank, False, bytes(t.cpu().tolist()))
+
+    def to_c(self):
+        spec = abi.ShardSpec(self.world, self.rank, self.world if self.local else 1, None)
+        keep = None
+        if not self.local:
+            if self.nccl_id is None or len(self.nccl_id) != 128:
+                raise ValueError("one-shard-per-process mode needs a 128-byte NCCL id")
+            keep = C.create_string_buffer(self.nccl_id, 128)
+            spec.nccl_id = C.cast(keep, C.c_void_p)
+        return spec, keep
+
+
 def Solve(problem: LpProblem, params: Optional[SolverParams] = None, observer: Optional[EvalObserver] = None,
-          device: int = 0) -> SolveResult:
-    """rpdlp::Solve (solver.cpp:521-543) on a B200 through pdhg_solve."""
+          device: int = 0, shards: Optional[Shards] = None) -> SolveResult:
+    """rpdlp::Solve (solver.cpp:521-543) on a B200 through pdhg_solve_on, or
+    pdhg_solve_sharded when `shards` distributes K."""
     lib = abi.load()
     params = params or SolverParams()
     lp, prm = problem.to_c(), params.to_c()
     res, x, y, lam = _result(problem)
     obs = _Observer(observer)
     err = C.create_string_buffer(abi.ERRLEN)
-    code = lib.pdhg_solve_on(C.byref(lp), C.byref(prm), device, obs.c, None, C.byref(res), err, abi.ERRLEN)
+    if shards is None or shards.world == 1:
+        code = lib.pdhg_solve_on(C.byref(lp), C.byref(prm), device, obs.c, None, C.byref(res), err, abi.ERRLEN)
+    else:
+        spec, _keep = shards.to_c()
+        code = lib.pdhg_solve_sharded(C.byref(lp), C.byref(prm), device, C.byref(spec), obs.c, None, C.byref(res),
+                                      err, abi.ERRLEN)
     raise_for(code, err, obs.error)
     return _pack(res, x, y, lam)
 
@@ -296,15 +345,22 @@ def Solve(problem: LpProblem, params: Optional[SolverParams] = None, observer: O
 class Session:
     """Problem resident in HBM (upload + CSC build + device scaling once)."""
 
-    def __init__(self, problem: LpProblem, params: Optional[SolverParams] = None, device: int = 0):
+    def __init__(self, problem: LpProblem, params: Optional[SolverParams] = None, device: int = 0,
+                 shards: Optional[Shards] = None):
         self.lib = abi.load()
         self.problem = problem
         self.params = params or SolverParams()
+        self.shards = shards or Shards()
         lp, prm = problem.to_c(), self.params.to_c()
         self.h = C.c_void_p()
         err = C.create_string_buffer(abi.ERRLEN)
-        raise_for(self.lib.pdhg_session_create(C.byref(lp), C.byref(prm), device, C.byref(self.h), err,
-                                               abi.ERRLEN), err)
+        if self.shards.world == 1:
+            code = self.lib.pdhg_session_create(C.byref(lp), C.byref(prm), device, C.byref(self.h), err, abi.ERRLEN)
+        else:
+            spec, _keep = self.shards.to_c()
+            code = self.lib.pdhg_session_create_sharded(C.byref(lp), C.byref(prm), device, C.byref(spec),
+                                                        C.byref(self.h), err, abi.ERRLEN)
+        raise_for(code, err)
 
     def close(self):
         if self.h:
@@ -349,6 +405,13 @@ class Session:
         s = abi.SessionStats()
         self.lib.pdhg_session_stats_get(self.h, C.byref(s))
         return s
+
+    def blocks(self):
+        """(row_begin, col_begin): the balanced blocks in original order."""
+        w = self.shards.world
+        rb, cb = np.empty(w + 1, np.int64), np.empty(w + 1, np.int64)
+        raise_for(self.lib.pdhg_session_blocks(self.h, _i64p(rb), _i64p(cb)), b"")
+        return rb, cb
 
     def scaling(self):
         rs, cs = np.empty(self.problem.num_rows()), np.empty(self.problem.num_vars())
@@ -431,25 +494,55 @@ def CheckTermination(report: ResidualReport, eps: float) -> bool:
     return bool(abi.load().pdhg_check_termination(C.byref(r), eps))
 
 
+def PartitionBlocks(ptr, parts: int, seg_weight: int = 6) -> np.ndarray:
+    """The balanced contiguous split every rank computes (host_logic.h)."""
+    p = _i64(ptr)
+    out = np.empty(parts + 1, np.int64)
+    code = abi.load().pdhg_partition_blocks(_i64p(p), len(p) - 1, parts, seg_weight, _i64p(out))
+    raise_for(code, b"invalid partition arguments")
+    return out
+
+
 # ------------------------------------------------------------ generators
+class _InstanceOwner:
+    """Frees a generated pdhg_instance once no array view into it is alive."""
+
+    def __init__(self, h: C.c_void_p):
+        self.h = h
+
+    def __del__(self):
+        if self.h:
+            abi.load().pdhg_instance_free(self.h)
+            self.h = None
+
+
 def _from_instance(h: C.c_void_p, name: str) -> LpProblem:
+    """Zero-copy view of a generated instance: every array's buffer keeps the
+    owner alive, so multi-GB instances are never duplicated on the host."""
     lib = abi.load()
+    owner = _InstanceOwner(h)
     v = abi.Lp()
     lib.pdhg_instance_view(h, C.byref(v))
 
-    def arr(p, n, dt):
-        return np.ctypeslib.as_array(p, shape=(n,)).astype(dt, copy=True) if n else np.zeros(0, dt)
+    def arr(p, n, ct, dt):
+        if not n:
+            return np.zeros(0, dt)
+        buf = (ct * n).from_address(C.cast(p, C.c_void_p).value)
+        buf._owner = owner
+        return np.frombuffer(buf, dtype=dt)
 
     def csr(m: abi.Csr) -> CsrMatrix:
-        ptr = arr(m.row_ptr, m.rows + 1, np.int64)
+        ptr = arr(m.row_ptr, m.rows + 1, C.c_int64, np.int64)
         nz = int(ptr[-1])
-        return CsrMatrix(m.rows, m.cols, ptr, arr(m.col_idx, nz, np.int64), arr(m.values, nz, np.float64))
+        return CsrMatrix(m.rows, m.cols, ptr, arr(m.col_idx, nz, C.c_int64, np.int64),
+                         arr(m.values, nz, C.c_double, np.float64))
 
+    d = lambda p, n: arr(p, n, C.c_double, np.float64)  # noqa: E731
     a, g = csr(v.a), csr(v.g)
-    p = LpProblem(a, g, arr(v.c, v.n, np.float64), arr(v.b, a.rows, np.float64), arr(v.h, g.rows, np.float64),
-                  arr(v.l, v.n, np.float64), arr(v.u, v.n, np.float64), v.objective_offset, False, name)
+    p = LpProblem(a, g, d(v.c, v.n), d(v.b, a.rows), d(v.h, g.rows), d(v.l, v.n), d(v.u, v.n),
+                  v.objective_offset, False, name)
     w = lib.pdhg_instance_witness(h)
-    p.witness = arr(w, v.n, np.float64) if w else None
+    p.witness = d(w, v.n) if w else None
     return p
 
 
@@ -466,30 +559,38 @@ def GenRandomLp(m: int, n: int, density: float, seed: int, equality_rows: int = 
     A with b = A x_hat."""
     lib = abi.load()
     h = _gen("pdhg_gen_random_lp", m, n, density, seed)
-    try:
-        if equality_rows:
-            err = C.create_string_buffer(abi.ERRLEN)
-            raise_for(lib.pdhg_instance_make_equalities(h, equality_rows, err, abi.ERRLEN), err)
-        return _from_instance(h, f"rand_{m}x{n}_s{seed}")
-    finally:
-        lib.pdhg_instance_free(h)
+    if equality_rows:
+        err = C.create_string_buffer(abi.ERRLEN)
+        code = lib.pdhg_instance_make_equalities(h, equality_rows, err, abi.ERRLEN)
+        if code:
+            lib.pdhg_instance_free(h)
+            raise_for(code, err)
+    return _from_instance(h, f"rand_{m}x{n}_s{seed}")
 
 
 def GenPagerank(n_nodes: int, damping: float = 0.85, attachment: int = 3, seed: int = 0) -> LpProblem:
     """instance_gen.cpp:27-64, 90-141."""
-    lib = abi.load()
-    h = _gen("pdhg_gen_pagerank", n_nodes, damping, attachment, seed)
-    try:
-        return _from_instance(h, "pagerank")
-    finally:
-        lib.pdhg_instance_free(h)
+    return _from_instance(_gen("pdhg_gen_pagerank", n_nodes, damping, attachment, seed), "pagerank")
 
 
 def GenTransport(sources: int, sinks: int, seed: int = 1) -> LpProblem:
     """Transportation LP of SURVEY §8d config 2."""
-    lib = abi.load()
-    h = _gen("pdhg_gen_transport", sources, sinks, seed)
-    try:
-        return _from_instance(h, f"transport_{sources}x{sinks}_s{seed}")
-    finally:
-        lib.pdhg_instance_free(h)
+    return _from_instance(_gen("pdhg_gen_transport", sources, sinks, seed), f"transport_{sources}x{sinks}_s{seed}")
+
+
+def GenMcf(nodes: int, arcs: int, commodities: int, seed: int = 1) -> LpProblem:
+    """Multicommodity network flow LP of SURVEY §8d config 3 (heavy-tailed
+    conservation rows, capacity rows of length `commodities`, columns of 3)."""
+    return _from_instance(_gen("pdhg_gen_mcf", nodes, arcs, commodities, seed),
+                          f"mcf_{nodes}v_{arcs}a_{commodities}k_s{seed}")
+
+
+def GenStaircase(stages: int, rows_per_stage: int, cols_per_stage: int, nnz_per_row: int = 20,
+                 linking_per_row: int = 5, eq_rows_per_stage: Optional[int] = None, seed: int = 1,
+                 threads: int = 0) -> LpProblem:
+    """Block-angular staircase LP of SURVEY §8d config 5; bit-identical per
+    seed for any `threads` (0 = all host cores)."""
+    req = rows_per_stage // 2 if eq_rows_per_stage is None else eq_rows_per_stage
+    return _from_instance(_gen("pdhg_gen_staircase", stages, rows_per_stage, cols_per_stage, nnz_per_row,
+                               linking_per_row, req, seed, threads),
+                          f"staircase_{stages}x{rows_per_stage}x{cols_per_stage}_d{nnz_per_row}_s{seed}")

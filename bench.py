@@ -58,6 +58,15 @@ def make_problem(cfg: str, args):
     elif cfg == "random":
         p = rpdlp.GenRandomLp(1000, 2000, 0.005, 1, equality_rows=300)
         wl = f"random LP 1000x2000 0.5% (300 eq rows, boxed), eps={args.eps:g}"
+    elif cfg == "mcf":
+        V, E, K = args.mcf
+        p = rpdlp.GenMcf(V, E, K, 1)
+        wl = f"multicommodity flow LP V={V} E={E} K={K} ({E * K} vars, {3 * E * K} nnz), eps={args.eps:g}"
+    elif cfg == "staircase":
+        T, R, D = args.staircase
+        p = rpdlp.GenStaircase(T, R, R, D, max(1, D // 4), seed=1)
+        wl = (f"block-angular staircase LP {T} stages x {R} rows x {R} cols, {D} nnz/row "
+              f"({T * R * D} nnz), eps={args.eps:g}")
     else:
         raise SystemExit(f"unknown config {cfg}")
     return p, wl
@@ -271,7 +280,9 @@ def run_ours(args, world, rank, local, dist):
     params = SolverParams(eps=args.eps)
     m, n, nnz = problem.num_rows(), problem.num_vars(), problem.nnz()
 
-    sess = Session(problem, params, device=local)
+    sharded = world > 1 and args.mode == "sharded"
+    shards = rpdlp.Shards.from_process_group() if sharded else None
+    sess = Session(problem, params, device=local, shards=shards)
     st = sess.stats()
     log(f"[rank {rank}] session: upload {st.upload_seconds:.3f}s scaling {st.scaling_seconds:.3f}s "
         f"tiles csr={st.csr_tiles} csc={st.csc_tiles} device bytes={st.device_bytes / 1e9:.2f} GB")
@@ -297,12 +308,31 @@ def run_ours(args, world, rank, local, dist):
     clk = clocks.stop()
 
     t_max = max_over_ranks(dist, local, dev_ms / 1e3)
-    tot_iters = sum_over_ranks(dist, local, float(iters))
+    # Sharded: every rank runs the same iterations of ONE solve; replicas:
+    # each rank solves its own copy.
+    tot_iters = float(iters) if sharded else sum_over_ranks(dist, local, float(iters))
     value = tot_iters / t_max
+
+    tight = None
+    if args.eps_tight > 0:
+        tp = SolverParams(eps=args.eps_tight, time_limit=args.tight_time_limit)
+        sess.flush_l2()
+        barrier(dist, local)
+        rt = sess.solve(tp)
+        ms_t, _ = sess.last_solve()
+        t_t = max_over_ranks(dist, local, ms_t / 1e3)
+        tight = {"eps": args.eps_tight, "status": int(rt.status), "iterations": rt.iterations,
+                 "restarts": rt.restarts, "seconds": t_t, "it_per_s": rt.iterations / t_t,
+                 "rel_primal": rt.report.rel_primal, "rel_dual": rt.report.rel_dual, "rel_gap": rt.report.rel_gap,
+                 "primal_obj": rt.report.primal_obj}
+        log(f"[rank {rank}] tight solve eps={args.eps_tight:g}: status={int(rt.status)} it={rt.iterations} "
+            f"{t_t:.3f}s")
 
     # Per-kernel roofline (K-CSC primal / K-CSR dual), events on the solver stream.
     ms_p, ms_d, ms_it = sess.time_kernels(args.kernel_iters)
     b_p, b_d, b_it = algorithmic_bytes(m, n, nnz)
+    if sharded:  # each rank streams its own blocks (x / y all-gathers ride on NVLink)
+        b_p, b_d, b_it = b_p / world, b_d / world, b_it / world
     dom = "pdhg_primal_csc" if ms_p >= ms_d else "pdhg_dual_csr"
     b_dom, ms_dom = (b_p, ms_p) if ms_p >= ms_d else (b_d, ms_d)
     achieved = b_dom / (ms_dom * 1e-3) / 1e9
@@ -321,11 +351,11 @@ def run_ours(args, world, rank, local, dist):
     e2e_t, e2e_it = 0.0, 0
     for _ in range(max(1, args.e2e_steps)):
         ts = time.perf_counter()
-        r = rpdlp.Solve(pinned, params, device=local)
+        r = rpdlp.Solve(pinned, params, device=local, shards=shards)
         e2e_t += time.perf_counter() - ts
         e2e_it += r.iterations
     e2e_t = max_over_ranks(dist, local, e2e_t)
-    e2e_it = sum_over_ranks(dist, local, float(e2e_it))
+    e2e_it = float(e2e_it) if sharded else sum_over_ranks(dist, local, float(e2e_it))
     h2d = sum(a.nbytes for a in (problem.a.row_ptr, problem.a.col_idx, problem.a.values, problem.g.row_ptr,
                                  problem.g.col_idx, problem.g.values, problem.c, problem.b, problem.h, problem.l,
                                  problem.u))
@@ -340,14 +370,16 @@ def run_ours(args, world, rank, local, dist):
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload, "m": m, "n": n, "nnz": nnz, "eps": args.eps,
                    "step": "one full solve to eps on the resident scaled problem (power iteration included)",
                    "l2_flush": "2x L2 written between timed steps",
-                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "parallelism": (f"K sharded {world} ways (row/column blocks, NCCL all-gather of x/y slices)"
+                                   if sharded else ("replicas" if world > 1 else "single GPU")),
                    "iterations_per_solve": iters // max(args.steps, 1),
                    "statuses": sorted(set(statuses))},
         "time_to_eps_s": t_max / args.steps,
+        "tight_solve": tight,
         "e2e": {"value": e2e_it / e2e_t, "unit": "it/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": d2h,
                 "seconds_per_solve": e2e_t / max(1, args.e2e_steps), "entry": "pdhg_solve_on (C-ABI)"},
         "roofline": roofline,
@@ -365,7 +397,14 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="transport", choices=["transport", "pagerank", "random"])
+    ap.add_argument("--config", default="transport", choices=["transport", "pagerank", "random", "mcf", "staircase"])
+    ap.add_argument("--mcf", type=int, nargs=3, default=[50_000, 330_000, 50], metavar=("V", "E", "K"))
+    ap.add_argument("--staircase", type=int, nargs=3, default=[100, 100_000, 20], metavar=("T", "R", "D"))
+    ap.add_argument("--mode", choices=["sharded", "replicas"], default="sharded",
+                    help="N>1: shard K across the ranks (NCCL all-gathers) or run independent replicas")
+    ap.add_argument("--eps-tight", type=float, default=1e-8,
+                    help="also time one solve to this eps (0 disables)")
+    ap.add_argument("--tight-time-limit", type=float, default=60.0)
     ap.add_argument("--eps", type=float, default=1e-4)
     ap.add_argument("--transport", type=int, default=1000)
     ap.add_argument("--pagerank-n", type=int, default=1_000_000)

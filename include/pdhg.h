@@ -211,6 +211,12 @@ int pdhg_session_blocks(pdhg_session* s, int64_t* row_begin,
 int pdhg_partition_blocks(const int64_t* ptr, int64_t nseg, int parts,
                           int64_t seg_weight, int64_t* begin);
 void pdhg_session_destroy(pdhg_session* s);
+/* The power-iteration start vector of EstimateOpNorm (solver.cpp:88-97):
+ * n draws of std::normal_distribution<double>(0,1) over
+ * std::mt19937_64(seed). threads < 0: the sequential libstdc++ draw;
+ * otherwise the bit-identical multi-threaded replica the solver uses
+ * (0 = all host threads). */
+int pdhg_normal_vector(uint64_t seed, int64_t n, int threads, double* out);
 int pdhg_session_stats_get(pdhg_session* s, pdhg_session_stats* out);
 /* SolveLoop(...).Run() (solver.cpp:232-267) on the resident scaled problem.
  * out->scaling_seconds reports the session's device scaling time. */

@@ -10,6 +10,7 @@
 #include <string>
 
 #include "host_logic.h"
+#include "normal_rng.h"
 #include "session.cuh"
 
 struct pdhg_session {
@@ -185,6 +186,13 @@ int pdhg_partition_blocks(const int64_t* ptr, int64_t nseg, int parts, int64_t s
 }
 
 void pdhg_session_destroy(pdhg_session* s) { delete s; }
+
+int pdhg_normal_vector(uint64_t seed, int64_t n, int threads, double* out) {
+  if (n < 0 || (n && !out)) return PDHG_INVALID_ARGUMENT;
+  if (threads < 0) pdhg::NormalVectorSequential(seed, n, out);
+  else pdhg::NormalVector(seed, n, out, threads);
+  return PDHG_OK;
+}
 
 int pdhg_session_stats_get(pdhg_session* s, pdhg_session_stats* out) {
   return Guard(nullptr, 0, [&] { S(s).Stats(out); });

@@ -113,34 +113,41 @@ __global__ void __launch_bounds__(kBlock) seg_thread_kernel(const int32_t* __res
   block_reduce_out<Op>(red, red_out);
 }
 
-// Lane-strided partial sum of [b, e) with kUnroll loads in flight per lane.
+// Lane-strided partial sum of [b, e): batches of kStrideUnroll predicated
+// loads per lane, so even the last partial batch keeps every load of the
+// lane in flight at once (a sequential tail loop would serialise one
+// idx -> gather latency chain per element). Masked-off slots contribute 0,
+// the identity of both combines (sums, and max over |v| >= 0).
+constexpr int kStrideUnroll = 8;
 template <class Op, int kStride>
 __device__ __forceinline__ void strided_sum(const Op& op, const int32_t* __restrict__ idx,
                                             const double* __restrict__ val, int b, int e, int t,
                                             double (&acc)[Op::kRhs]) {
   constexpr int R = Op::kRhs;
   constexpr bool MX = Op::kMax;
-  int k = b + t;
-  for (; k + kStride * (kUnroll - 1) < e; k += kStride * kUnroll) {
-    int32_t j[kUnroll];
-    double v[kUnroll], p[kUnroll][R];
+  constexpr int U = kStrideUnroll;
+  for (int k = b + t; k < e; k += kStride * U) {
+    int32_t j[U];
+    double v[U], p[U][R];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      j[u] = ld_stream(idx + k + kStride * u);
-      v[u] = ld_stream(val + k + kStride * u);
+    for (int u = 0; u < U; ++u) {
+      const bool in = k + kStride * u < e;
+      j[u] = in ? ld_stream(idx + k + kStride * u) : 0;
+      v[u] = in ? ld_stream(val + k + kStride * u) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) op.map(j[u], v[u], p[u]);
+    for (int u = 0; u < U; ++u) {
+      if (k + kStride * u < e) {
+        op.map(j[u], v[u], p[u]);
+      } else {
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
+        for (int r = 0; r < R; ++r) p[u][r] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[u][r]);
-  }
-  for (; k < e; k += kStride) {
-    double p[R];
-    op.map(ld_stream(idx + k), ld_stream(val + k), p);
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[r]);
   }
 }
 
@@ -217,6 +224,56 @@ inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, cudaStr
   if (L.s3 > L.s2) seg_cta_kernel<Op><<<L.nb_l(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s2, op, red.at(slot, nr));
   slot += L.nb_l();
   if (L.nseg > L.s3) launch_tiles(L.lng, op, red.at(slot, nr), red.at(slot + L.nt_x(), nr), st);
+}
+
+// A main stream plus side streams: the class kernels of one pass are
+// independent (disjoint segments, disjoint reduction slots), so with more
+// than one class present they run as parallel branches (fork/join events;
+// inside a captured graph these become parallel graph nodes) instead of
+// serialising their tails.
+struct Fork {
+  cudaStream_t main = nullptr;
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t join[3] = {nullptr, nullptr, nullptr};
+};
+
+template <class Op>
+inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, const Fork& f) {
+  constexpr int nr = Op::kRed > 0 ? Op::kRed : 1;
+  const bool has[4] = {L.s1 > 0, L.s2 > L.s1, L.s3 > L.s2, L.nseg > L.s3};
+  const int nclass = has[0] + has[1] + has[2] + has[3];
+  if (nclass <= 1 || !f.side[0]) {
+    run_pass(L, op, red, f.main);
+    return;
+  }
+  cudaEventRecord(f.fork, f.main);
+  cudaStream_t on[4];
+  int k = 0;
+  for (int c = 0; c < 4; ++c) {
+    if (!has[c]) continue;
+    on[c] = k == 0 ? f.main : f.side[k - 1];
+    if (k > 0) cudaStreamWaitEvent(on[c], f.fork, 0);
+    ++k;
+  }
+  int64_t slot = 0;
+  if (has[0]) seg_thread_kernel<Op><<<L.nb_s(), kBlock, 0, on[0]>>>(L.ptr, L.idx, L.val, L.s1, op, red.at(slot, nr));
+  slot += L.nb_s();
+  if (has[1])
+    seg_warp_kernel<Op><<<L.nb_m(), kBlock, 0, on[1]>>>(L.ptr, L.idx, L.val, L.s1, L.s2, op, red.at(slot, nr));
+  slot += L.nb_m();
+  if (has[2]) seg_cta_kernel<Op><<<L.nb_l(), kBlock, 0, on[2]>>>(L.ptr, L.idx, L.val, L.s2, op, red.at(slot, nr));
+  slot += L.nb_l();
+  if (has[3]) launch_tiles(L.lng, op, red.at(slot, nr), red.at(slot + L.nt_x(), nr), on[3]);
+  k = 0;
+  for (int c = 0; c < 4; ++c) {
+    if (!has[c]) continue;
+    if (k > 0) {
+      cudaEventRecord(f.join[k - 1], on[c]);
+      cudaStreamWaitEvent(f.main, f.join[k - 1], 0);
+    }
+    ++k;
+  }
 }
 
 // Number of kernels run_pass launches.

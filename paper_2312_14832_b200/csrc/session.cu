@@ -25,6 +25,7 @@
 #include <random>
 
 #include "host_logic.h"
+#include "normal_rng.h"
 #include "ops.cuh"
 #include "setup_kernels.cuh"
 
@@ -66,16 +67,34 @@ void segment_ids(const int32_t* ptr, int64_t nseg, int64_t nnz, DArray<int32_t>&
 }
 
 // Stable sort of segment keys (values < 2^bits) -> permutation new -> old.
-void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, int bits, cudaStream_t st) {
-  DArray<int32_t> iota, kout;
+// With `ptr` given, segments of equal key are ordered by length, longest
+// first (then original order): a segment with L nonzeros is the target of L
+// gathers in the other layout's pass, so this packs the hottest vector
+// entries (hub rows / columns) into few cache lines and makes the lengths
+// inside a warp uniform. Segment-internal nonzero order is untouched, so
+// every segment sum is unchanged.
+void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, int bits, cudaStream_t st,
+                  const int32_t* ptr = nullptr) {
+  DArray<int32_t> iota, kout, first, k2;
   iota.alloc(std::max<int64_t>(n, 1));
   kout.alloc(std::max<int64_t>(n, 1));
   k_iota<<<ew_grid(n), kEw, 0, st>>>(iota.p, n);
+  const int32_t* vals = iota.p;
+  const int32_t* pkeys = keys;
   size_t tb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, bits, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, 31, st);
   DArray<char> tmp;
   tmp.alloc(tb);
-  PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, bits, st));
+  if (ptr) {
+    first.alloc(std::max<int64_t>(n, 1));
+    k2.alloc(std::max<int64_t>(n, 1));
+    k_len_desc_key<<<ew_grid(n), kEw, 0, st>>>(ptr, n, k2.p);
+    PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k2.p, kout.p, iota.p, first.p, (int)n, 0, 31, st));
+    k_gather_i32<<<ew_grid(n), kEw, 0, st>>>(keys, first.p, k2.p, n);
+    vals = first.p;
+    pkeys = k2.p;
+  }
+  PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, pkeys, kout.p, vals, perm.p, (int)n, 0, bits, st));
   PDHG_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -101,6 +120,12 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
   rank_ = spec.local == spec.world ? 0 : spec.rank;
   PDHG_CUDA(cudaSetDevice(device_));
   PDHG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  fork_.main = st_;
+  PDHG_CUDA(cudaEventCreateWithFlags(&fork_.fork, cudaEventDisableTiming));
+  for (int k = 0; k < 3; ++k) {
+    PDHG_CUDA(cudaStreamCreateWithFlags(&fork_.side[k], cudaStreamNonBlocking));
+    PDHG_CUDA(cudaEventCreateWithFlags(&fork_.join[k], cudaEventDisableTiming));
+  }
   PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&host_red_), kPack * sizeof(double) + 64));
   if (world_ > 1 && spec.local == 1) {
     if (!spec.nccl_id) throw Error(PDHG_INVALID_ARGUMENT, "a one-shard-per-process session needs an NCCL id");
@@ -185,6 +210,11 @@ Session::~Session() {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (host_red_) cudaFreeHost(host_red_);
   comm_.reset();
+  if (fork_.fork) cudaEventDestroy(fork_.fork);
+  for (int k = 0; k < 3; ++k) {
+    if (fork_.side[k]) cudaStreamDestroy(fork_.side[k]);
+    if (fork_.join[k]) cudaEventDestroy(fork_.join[k]);
+  }
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -335,23 +365,30 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     kc.alloc(std::max<int64_t>(n_, 1));
     hist.alloc(2 * nkeys);
     PDHG_CUDA(cudaMemsetAsync(hist.p, 0, 2 * nkeys * sizeof(int32_t), st_));
-    // Class bounds: kWarpMax / kCtaMax unless overridden (PDHG_WARP_MAX,
-    // PDHG_CTA_MAX; tuning experiments only -- the one-thread class is fixed
-    // at kSeqMax so short segments keep the reference's summation order).
+    // Class bounds: kSeqMax / kWarpMax / kCtaMax unless overridden
+    // (PDHG_THREAD_MAX <= 32, PDHG_WARP_MAX, PDHG_CTA_MAX; tuning experiments).
+    // Segments of <= 32 nonzeros keep the reference's summation order in the
+    // thread class and in the tile engine; the warp / CTA classes only get
+    // them if PDHG_WARP_MAX is lowered below 32 by hand.
     auto env_int = [](const char* k, int d) {
       const char* v = std::getenv(k);
-      return v ? std::max(kSeqMax, std::atoi(v)) : d;
+      return v ? std::max(0, std::atoi(v)) : d;
     };
-    const int warp_max = env_int("PDHG_WARP_MAX", kWarpMax);
+    const int thread_max = std::min(kSeqMax, env_int("PDHG_THREAD_MAX", kSeqMax));
+    const int warp_max = std::max(thread_max, env_int("PDHG_WARP_MAX", kWarpMax));
     const int cta_max = std::max(warp_max, env_int("PDHG_CTA_MAX", kCtaMax));
-    k_class_keys<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, m1_, rbeg.p, world_, warp_max, cta_max, kr.p);
-    k_class_keys<<<ew_grid(n_), kEw, 0, st_>>>(cptr0.p, n_, n_, cbeg.p, world_, warp_max, cta_max, kc.p);
+    k_class_keys<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, m1_, rbeg.p, world_, thread_max, warp_max, cta_max,
+                                               kr.p);
+    k_class_keys<<<ew_grid(n_), kEw, 0, st_>>>(cptr0.p, n_, n_, cbeg.p, world_, thread_max, warp_max, cta_max,
+                                               kc.p);
     k_key_hist<<<ew_grid(m_), kEw, 0, st_>>>(kr.p, m_, hist.p);
     k_key_hist<<<ew_grid(n_), kEw, 0, st_>>>(kc.p, n_, hist.p + nkeys);
     int bits = 3;
     while ((1 << bits) < nkeys) ++bits;
-    if (m_) stable_order(kr.p, m_, perm_r, bits, st_);
-    if (n_) stable_order(kc.p, n_, perm_c, bits, st_);
+    const char* dord = std::getenv("PDHG_DEGREE_ORDER");
+    const bool by_len = !(dord && dord[0] == '0');
+    if (m_) stable_order(kr.p, m_, perm_r, bits, st_, by_len ? ptr0.p : nullptr);
+    if (n_) stable_order(kc.p, n_, perm_c, bits, st_, by_len ? cptr0.p : nullptr);
     std::vector<int> h(2 * nkeys);
     PDHG_CUDA(cudaMemcpyAsync(h.data(), hist.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st_));
     Sync();
@@ -657,12 +694,12 @@ void Session::LaunchStep(int parity, int j, bool adapt) {
       run_pass(h.csc,
                OpPrimal<true>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
                               scal_.p, j},
-               RedSlots{h.red[1].p}, st_);
+               RedSlots{h.red[1].p}, fork_);
     else
       run_pass(h.csc,
                OpPrimal<false>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
                                scal_.p, j},
-               RedSlots{}, st_);
+               RedSlots{}, fork_);
   }
   GatherX(x_[b].p);
   for (Shard& h : shards_) {
@@ -671,12 +708,12 @@ void Session::LaunchStep(int parity, int j, bool adapt) {
       run_pass(h.csr,
                OpDual<true>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
                             h.rk, scal_.p, j},
-               RedSlots{h.red[0].p}, st_);
+               RedSlots{h.red[0].p}, fork_);
     else
       run_pass(h.csr,
                OpDual<false>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
                              h.rk, scal_.p, j},
-               RedSlots{}, st_);
+               RedSlots{}, fork_);
   }
   GatherY(y_[b].p);
   if (adapt) {
@@ -741,10 +778,10 @@ void Session::LaunchCheck(const double* x, const double* y, const double* xb, co
     Shard& h = shards_[k];
     const int64_t r = h.roff, c = h.coff;
     OpCheckRow row{xb, kxavg_.p + r, kx + r, y + r, yb + r, ystart_.p + r, q_s_.p + r, q_o_.p + r, rs_.p + r, h.rk};
-    run_pass(h.csr, row, RedSlots{h.red[0].p}, st_);
+    run_pass(h.csr, row, RedSlots{h.red[0].p}, fork_);
     OpCheckCol col{y, yb, x + c, xb + c, xstart_.p + c, c_s_.p + c, l_s_.p + c, u_s_.p + c, c_o_.p + c,
                    l_o_.p + c, u_o_.p + c, cs_.p + c};
-    run_pass(h.csc, col, RedSlots{h.red[1].p}, st_);
+    run_pass(h.csc, col, RedSlots{h.red[1].p}, fork_);
     double* pk = red_out_.p + k * kPack;
     k_reduce_tiles<<<kRowRed, kBlock, 0, st_>>>(h.red[0].p, nullptr, h.csr.parts(), kRowRed, pk);
     k_reduce_tiles<<<kColRed, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), kColRed, pk + kRowRed);
@@ -773,6 +810,9 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 
   // eta = 0.9 / ||K|| (solver.cpp:233-234), omega0 = ||c_s|| / ||q_s|| (:235-238).
   const double op = OpNorm(100, prm.seed);
+  const double t_opnorm = secs();
+  double t_checks = 0.0;
+  int64_t nchecks = 0;
   Scalars sc{};
   sc.eta = op > 0.0 ? 0.9 / op : 1.0;
   sc.omega = 1.0;
@@ -878,6 +918,8 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     if (iters % prm.check_every != 0) continue;
 
     // ---- Check (solver.cpp:390-428).
+    const double tc0 = secs();
+    ++nchecks;
     LaunchCheck(x_[par].p, y_[par].p, xbar_.p, ybar_.p, kx_[par].p);
     if (nccl()) {  // rank 0's clock, summed into slot kPack - 1 of every rank
       host_red_[kPack - 1] = (rank_ == 0 && secs() >= prm.time_limit) ? 1.0 : 0.0;
@@ -889,6 +931,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     }
     if (adapt) PDHG_CUDA(cudaMemcpyAsync(&sc.eta, &scal_.p->eta, sizeof(double), cudaMemcpyDeviceToHost, st_));
     ReadCheck(&ck);
+    t_checks += secs() - tc0;  // includes the wait for the block before it
     if (nccl()) time_up = host_red_[kPack - 1] > 0.0;
     if (ck.row[2 * kRowPer] > 0.0 || ck.col[2 * kColPer] > 0.0)
       throw Error(PDHG_NUMERICAL_FAILURE, "non-finite iterate at iteration " + std::to_string(iters));
@@ -979,6 +1022,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   }
 
   // Finish (solver.cpp:473-481): unscale best, lambda on the original problem.
+  const double t_loop = secs();
   ToHost(xbest_.p, cs_.p, pad_c_, out->x, n_);
   ToHost(ybest_.p, rs_.p, pad_r_, out->y, m_);
   if (out->lambda) {
@@ -1001,6 +1045,12 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   out->restarts = restarts;
   out->solve_seconds = secs();
   out->scaling_seconds = scaling_s_;
+  if (std::getenv("PDHG_TRACE"))
+    std::fprintf(stderr,
+                 "[pdhg] solve %.4fs: opnorm %.4fs | loop %.4fs (%lld its, %lld checks, host-side check wait %.4fs) "
+                 "| finish %.4fs | device %.4fs | graphs %zu\n",
+                 out->solve_seconds, t_opnorm, t_loop - t_opnorm, (long long)iters, (long long)nchecks, t_checks,
+                 out->solve_seconds - t_loop, ms * 1e-3, graphs_.size());
 }
 
 // EstimateOpNorm (solver.cpp:84-110) with the host start vector drawn from the
@@ -1010,10 +1060,8 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 double Session::OpNorm(int iters, uint64_t seed) {
   PDHG_CUDA(cudaSetDevice(device_));
   if (nnz_ == 0) return 0.0;
-  std::mt19937_64 rng(seed);
-  std::normal_distribution<double> gauss(0.0, 1.0);
   std::vector<double> v(static_cast<size_t>(n_));
-  for (double& e : v) e = gauss(rng);
+  NormalVector(seed, n_, v.data(), 0);  // == std::normal_distribution draws, all host threads
   double acc = 0.0;
   for (double e : v) acc += e * e;
   double vnorm = std::sqrt(acc);
@@ -1119,7 +1167,7 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   k_clamp0<<<ew_grid(np_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, np_);
   if (mp_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, mp_ * sizeof(double), st_));
-  for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, st_);
+  for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, fork_);
   cudaEvent_t e0, e1, e2;
   PDHG_CUDA(cudaEventCreate(&e0));
   PDHG_CUDA(cudaEventCreate(&e1));
@@ -1134,7 +1182,7 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
       run_pass(h.csc,
                OpPrimal<false>{y_[0].p, x_[0].p + o, x_[1].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
                                scal_.p, i + 1},
-               RedSlots{}, st_);
+               RedSlots{}, fork_);
     }
     GatherX(x_[1].p);
   }
@@ -1145,7 +1193,7 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
       run_pass(h.csr,
                OpDual<false>{x_[1].p, y_[0].p + o, y_[1].p + o, ybar_.p + o, kx_[0].p + o, kx_[1].p + o, q_s_.p + o,
                              h.rk, scal_.p, i + 1},
-               RedSlots{}, st_);
+               RedSlots{}, fork_);
     }
     GatherY(y_[1].p);
   }

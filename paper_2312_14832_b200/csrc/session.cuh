@@ -102,6 +102,7 @@ class Session {
 
   int device_ = 0;
   cudaStream_t st_ = nullptr;
+  Fork fork_;  // st_ + side streams for parallel class kernels
   Arena arena_;
   int64_t m1_ = 0, m2_ = 0, m_ = 0, n_ = 0, nnz_ = 0;
   double offset_ = 0.0;

@@ -85,10 +85,10 @@ __device__ __forceinline__ int block_of(const int64_t* begin, int P, int64_t s) 
 // (in block order) and, inside a block, class by class with equality rows
 // first, each run keeping the original order.
 __global__ void k_class_keys(const int32_t* p, int64_t nseg, int64_t eq_end, const int64_t* begin, int P,
-                             int warp_max, int cta_max, int32_t* key) {
+                             int thread_max, int warp_max, int cta_max, int32_t* key) {
   GRID_STRIDE(s, nseg) {
     const int len = p[s + 1] - p[s];
-    const int cls = len <= kSeqMax ? 0 : (len <= warp_max ? 1 : (len <= cta_max ? 2 : 3));
+    const int cls = len <= thread_max ? 0 : (len <= warp_max ? 1 : (len <= cta_max ? 2 : 3));
     key[s] = block_of(begin, P, s) * 8 + cls * 2 + (s >= eq_end ? 1 : 0);
   }
 }
@@ -120,6 +120,15 @@ __global__ void k_sum_packs(double* packs, int count, int stride, int n) {
   double v = packs[i];
   for (int k = 1; k < count; ++k) v += packs[static_cast<int64_t>(k) * stride + i];
   packs[i] = v;
+}
+
+// Sort key putting longer segments first: INT32_MAX - length.
+__global__ void k_len_desc_key(const int32_t* p, int64_t nseg, int32_t* key) {
+  GRID_STRIDE(s, nseg) key[s] = INT32_MAX - (p[s + 1] - p[s]);
+}
+
+__global__ void k_gather_i32(const int32_t* in, const int32_t* perm, int32_t* out, int64_t n) {
+  GRID_STRIDE(i, n) out[i] = in[perm[i]];
 }
 
 __global__ void k_key_hist(const int32_t* key, int64_t n, int32_t* hist) {

@@ -223,3 +223,21 @@ def test_gloo_two_rank_sharded_iteration(tmp_path):
         np.testing.assert_array_equal(r[k]["ys"], r[k]["y1"])
         np.testing.assert_allclose(r[k]["ss"], r[k]["s1"], rtol=1e-12)
     np.testing.assert_array_equal(r[0]["ss"], r[1]["ss"])  # all-reduced sums agree across ranks
+
+
+# ------------------------------------------- power-iteration start vector
+@pytest.mark.parametrize("seed", [0, 1, 12345])
+@pytest.mark.parametrize("n", [1, 7, 40000, 100001])
+def test_parallel_normal_vector_is_bit_exact(seed, n):
+    """The multi-threaded start vector equals the sequential libstdc++
+    std::normal_distribution / std::mt19937_64 draw bit for bit."""
+    import ctypes as C
+    from paper_2312_14832_b200 import abi
+    lib = abi.load()
+    a, b, c = np.empty(n), np.empty(n), np.empty(n)
+    dp = lambda v: v.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    assert lib.pdhg_normal_vector(seed, n, -1, dp(a)) == 0
+    assert lib.pdhg_normal_vector(seed, n, 8, dp(b)) == 0
+    assert lib.pdhg_normal_vector(seed, n, 3, dp(c)) == 0
+    np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
+    np.testing.assert_array_equal(a.view(np.uint64), c.view(np.uint64))

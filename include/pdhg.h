@@ -35,7 +35,9 @@ enum {
   PDHG_NUMERICAL_FAILURE = 2, /* rpdlp::NumericalFailure (solver.cpp:391-394) */
   PDHG_CUDA_ERROR = 3,
   PDHG_NCCL_ERROR = 4,
-  PDHG_ABORTED = 5 /* the eval callback asked to stop */
+  PDHG_ABORTED = 5, /* the eval callback asked to stop */
+  PDHG_PARSE_ERROR = 6, /* rpdlp::MpsParseError (mps.hpp:26-36); line in err_line */
+  PDHG_IO_ERROR = 7     /* std::runtime_error from file access (mps_reader.cpp:453-468) */
 };
 
 /* rpdlp::SolveStatus (solver.hpp:57). */
@@ -142,7 +144,8 @@ typedef struct {
   int32_t world;        /* shards K is split into */
   int32_t local_shards; /* shards held by this session (1 or world) */
   int32_t rank;         /* this session's shard when local_shards == 1 */
-  int32_t pad;
+  int32_t uniform_bounds; /* bit 0: all scaled l equal, bit 1: all u equal
+                             (those streams are skipped by the primal step) */
 } pdhg_session_stats;
 
 /* Distribution of K over shards: `world` balanced row blocks
@@ -321,6 +324,28 @@ int pdhg_instance_view(const pdhg_instance* inst, pdhg_lp* out);
 /* Witness x_hat (GenRandomLp, MCF, staircase; length n) or NULL. */
 const double* pdhg_instance_witness(const pdhg_instance* inst);
 void pdhg_instance_free(pdhg_instance* inst);
+/* NAME of an instance read from MPS ("" otherwise). */
+const char* pdhg_instance_name(const pdhg_instance* inst);
+
+/* ---- MPS ingestion (mps.hpp:50-56; reader mps_reader.cpp, writer
+ * mps_writer.cpp): same normalisations, errors and messages as the
+ * reference's ParseMps / WriteMps. Read results are instances (view them with
+ * pdhg_instance_view, free with pdhg_instance_free). Parse failures return
+ * PDHG_PARSE_ERROR with "mps parse error at line N: ..." in err and N in
+ * *err_line; unreadable files PDHG_IO_ERROR; an invalid LP (e.g. an infinite
+ * cost) PDHG_INVALID_ARGUMENT. Paths ending in .gz are read through zlib. */
+int pdhg_mps_read_file(const char* path, int fixed_format, pdhg_instance** out,
+                       char* err, size_t errlen, int* err_line);
+int pdhg_mps_read_string(const char* text, size_t len, int fixed_format,
+                         pdhg_instance** out, char* err, size_t errlen,
+                         int* err_line);
+/* WriteMps / WriteMpsFile: free format, %.17g numbers. The string variant
+ * returns a malloc'ed buffer released with pdhg_free_string. */
+int pdhg_mps_write_file(const pdhg_lp* lp, const char* name, const char* path,
+                        char* err, size_t errlen);
+int pdhg_mps_write_string(const pdhg_lp* lp, const char* name, char** out,
+                          size_t* out_len, char* err, size_t errlen);
+void pdhg_free_string(char* s);
 
 #ifdef __cplusplus
 }

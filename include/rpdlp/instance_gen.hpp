@@ -21,6 +21,12 @@ LpProblem GenPagerank(const PagerankConfig& cfg);
 LpProblem GenRandomLp(Index m, Index n, double density, std::uint64_t seed, std::vector<double>* witness = nullptr);
 // SURVEY §8d config 2 (not in the reference).
 LpProblem GenTransport(Index sources, Index sinks, std::uint64_t seed);
+// SURVEY §8d configs 3 (multicommodity flow) and 5 (block-angular staircase).
+LpProblem GenMcf(Index nodes, Index arcs, Index commodities, std::uint64_t seed,
+                 std::vector<double>* witness = nullptr);
+LpProblem GenStaircase(Index stages, Index rows_per_stage, Index cols_per_stage, Index nnz_per_row,
+                       Index linking_per_row, Index eq_rows_per_stage, std::uint64_t seed,
+                       std::vector<double>* witness = nullptr);
 
 }  // namespace rpdlp
 

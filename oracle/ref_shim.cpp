@@ -10,12 +10,15 @@
 
 #include <cstdio>
 #include <cstring>
+#include <sstream>
+#include <string>
 #include <stdexcept>
 #include <vector>
 
 #include "rpdlp/instance_gen.hpp"
 #include "rpdlp/kkt.hpp"
 #include "rpdlp/lp_problem.hpp"
+#include "rpdlp/mps.hpp"
 #include "rpdlp/scaling.hpp"
 #include "rpdlp/solver.hpp"
 #include "../include/pdhg.h"
@@ -246,5 +249,51 @@ void ref_instance_view(const ref_instance* r, pdhg_lp* v) {
 }
 const double* ref_instance_witness(const ref_instance* r) { return r->witness.empty() ? nullptr : r->witness.data(); }
 void ref_instance_free(ref_instance* r) { delete r; }
+const char* ref_instance_name(const ref_instance* r) { return r->p.name.c_str(); }
+
+// ParseMpsString / WriteMps (mps_reader.cpp, mps_writer.cpp) for pinning the
+// product's MPS reader and writer. Returns 0, or 6 with *line set on
+// MpsParseError, 1 on std::invalid_argument (Validate), 7 otherwise.
+int ref_parse_mps(const char* text, size_t len, int fixed, ref_instance** out, char* err, size_t errlen, int* line) {
+  *line = 0;
+  try {
+    auto* r = new ref_instance;
+    try {
+      MpsOptions o;
+      o.fixed_format = fixed != 0;
+      r->p = ParseMpsString(std::string(text, len), o);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    *out = r;
+    return 0;
+  } catch (const MpsParseError& e) {
+    std::snprintf(err, errlen, "%s", e.what());
+    *line = e.line();
+    return 6;
+  } catch (const std::invalid_argument& e) {
+    std::snprintf(err, errlen, "%s", e.what());
+    return 1;
+  } catch (const std::exception& e) {
+    std::snprintf(err, errlen, "%s", e.what());
+    return 7;
+  }
+}
+
+int ref_write_mps(const pdhg_lp* lp, const char* name, char* out, size_t cap, size_t* len) {
+  try {
+    LpProblem p = ToProblem(*lp);
+    p.name = name ? name : "";
+    std::ostringstream os;
+    WriteMps(p, os);
+    const std::string s = os.str();
+    *len = s.size();
+    if (out && cap >= s.size()) std::memcpy(out, s.data(), s.size());
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
 
 }  // extern "C"

@@ -18,6 +18,8 @@ PDHG_NUMERICAL_FAILURE = 2
 PDHG_CUDA_ERROR = 3
 PDHG_NCCL_ERROR = 4
 PDHG_ABORTED = 5
+PDHG_PARSE_ERROR = 6
+PDHG_IO_ERROR = 7
 
 PDHG_OPTIMAL = 0
 PDHG_ITER_LIMIT = 1
@@ -68,7 +70,7 @@ class SessionStats(C.Structure):
                 ("csr_tiles", C.c_int64), ("csc_tiles", C.c_int64), ("device_bytes", C.c_int64),
                 ("upload_seconds", C.c_double), ("scaling_seconds", C.c_double), ("device", C.c_int32),
                 ("l2_resident", C.c_int32), ("world", C.c_int32), ("local_shards", C.c_int32),
-                ("rank", C.c_int32), ("pad", C.c_int32)]
+                ("rank", C.c_int32), ("uniform_bounds", C.c_int32)]
 
 
 class ShardSpec(C.Structure):
@@ -132,6 +134,15 @@ SIGNATURES = {
     "pdhg_instance_view": (C.c_int, [C.c_void_p, C.POINTER(Lp)]),
     "pdhg_instance_witness": (dptr, [C.c_void_p]),
     "pdhg_instance_free": (None, [C.c_void_p]),
+    "pdhg_instance_name": (C.c_char_p, [C.c_void_p]),
+    "pdhg_mps_read_file": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t,
+                                     C.POINTER(C.c_int)]),
+    "pdhg_mps_read_string": (C.c_int, [C.c_char_p, C.c_size_t, C.c_int, C.POINTER(C.c_void_p), C.c_char_p,
+                                       C.c_size_t, C.POINTER(C.c_int)]),
+    "pdhg_mps_write_file": (C.c_int, [C.POINTER(Lp), C.c_char_p, C.c_char_p, C.c_char_p, C.c_size_t]),
+    "pdhg_mps_write_string": (C.c_int, [C.POINTER(Lp), C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                                        C.c_char_p, C.c_size_t]),
+    "pdhg_free_string": (None, [C.c_void_p]),
 }
 
 _lib = None

@@ -34,7 +34,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "--expt-relax
 CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-pthread", "-Wall", "-Wextra", "-I", str(ROOT / "include")]
 
 CU_SRCS = ["session.cu", "abi.cu"]
-CPP_SRCS = ["instance_gen.cpp", "rpdlp_api.cpp"]
+CPP_SRCS = ["instance_gen.cpp", "rpdlp_api.cpp", "mps.cpp"]
 DROPIN_TEST = ROOT / "tests" / "cpp" / "drop_in_test.cpp"
 DROPIN_BIN = BUILD / "drop_in_test"
 HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh", "tma.cuh", "host_logic.h", "engine.cuh", "setup_kernels.cuh", "comm.cuh", "normal_rng.h"]
@@ -68,7 +68,8 @@ def build_product(force: bool = False, ptxas_verbose: bool = False) -> Path:
     for s in CPP_SRCS:
         o = BUILD / (s + ".o")
         objs.append(o)
-        if force or not _newer(o, [CSRC / s, ROOT / "include" / "pdhg.h"] + sorted((ROOT / "include" / "rpdlp").glob("*.hpp"))):
+        if force or not _newer(o, [CSRC / s, ROOT / "include" / "pdhg.h", CSRC / "host_logic.h", CSRC / "instance.h"]
+                               + sorted((ROOT / "include" / "rpdlp").glob("*.hpp"))):
             jobs.append([CXX] + CXXFLAGS + ["-c", str(CSRC / s), "-o", str(o)])
     logs = []
     with cf.ThreadPoolExecutor(max_workers=max(1, len(jobs))) as ex:
@@ -77,7 +78,7 @@ def build_product(force: bool = False, ptxas_verbose: bool = False) -> Path:
     if ptxas_verbose:
         print("\n".join(l for l in logs if l.strip()))
     if force or jobs or not _newer(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", str(LIB)] + [str(o) for o in objs] + ["-lcuda", "-lpthread"])
+        _run([NVCC] + ARCH + ["-shared", "-o", str(LIB)] + [str(o) for o in objs] + ["-lcuda", "-lpthread", "-lz"])
     # Reference-style C++ caller linked against the drop-in headers + library.
     if force or not _newer(DROPIN_BIN, [DROPIN_TEST, LIB]):
         _run([CXX] + CXXFLAGS + [str(DROPIN_TEST), "-o", str(DROPIN_BIN), "-L", str(PKG), "-lpdhg_b200",

@@ -2,7 +2,9 @@
 // every entry maps pdhg::Error / std::invalid_argument onto a return code and
 // a message, which the C++ shim (include/rpdlp/) rethrows as the reference's
 // exception types.
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -48,25 +50,7 @@ int Guard(char* err, size_t len, F&& f) {
 void Invalid(const std::string& m) { throw Error(PDHG_INVALID_ARGUMENT, m); }
 
 // LpProblem::Validate (lp_problem.cpp:22-58), same checks and messages.
-void ValidateLp(const pdhg_lp& lp) {
-  const int64_t n = lp.n;
-  if (n < 0 || lp.a.rows < 0 || lp.g.rows < 0) Invalid("negative matrix dimension");
-  if (lp.a.cols != n || lp.g.cols != n) Invalid("matrix column count does not match c");
-  if ((lp.a.rows && !lp.a.row_ptr) || (lp.g.rows && !lp.g.row_ptr)) Invalid("missing row_ptr");
-  if ((n && (!lp.c || !lp.l || !lp.u)) || (lp.a.rows && !lp.b) || (lp.g.rows && !lp.h)) Invalid("missing vector");
-  for (int64_t i = 0; i < n; ++i)
-    if (std::isnan(lp.c[i])) Invalid("NaN in c");
-  for (int64_t i = 0; i < lp.a.rows; ++i)
-    if (std::isnan(lp.b[i])) Invalid("NaN in b");
-  for (int64_t i = 0; i < lp.g.rows; ++i)
-    if (std::isnan(lp.h[i])) Invalid("NaN in h");
-  for (int64_t i = 0; i < n; ++i)
-    if (std::isinf(lp.c[i])) Invalid("infinite entry in c");
-  for (int64_t i = 0; i < n; ++i) {
-    if (std::isnan(lp.l[i]) || std::isnan(lp.u[i])) Invalid("NaN bound");
-    if (lp.l[i] > lp.u[i]) Invalid("crossed bounds: l > u at index " + std::to_string(i));
-  }
-}
+void ValidateLp(const pdhg_lp& lp) { pdhg::ValidateLpHost(lp); }
 
 // SolverParams::Validate (solver.cpp:59-70).
 void ValidateParams(const pdhg_params& p) {
@@ -210,10 +194,24 @@ int pdhg_solve_on(const pdhg_lp* lp, const pdhg_params* prm, int device, pdhg_ev
                   pdhg_result* out, char* err, size_t errlen) {
   return Guard(err, errlen, [&] {
     if (!lp || !prm || !out) Invalid("null argument");
+    const auto t0 = std::chrono::steady_clock::now();
     ValidateLp(*lp);
     ValidateParams(*prm);
-    pdhg::Session sess(*lp, *prm, device);
-    sess.Solve(*prm, cb, user, out);
+    const auto t1 = std::chrono::steady_clock::now();
+    double t2s = 0.0, t3s = 0.0;
+    {
+      pdhg::Session sess(*lp, *prm, device);
+      const auto t2 = std::chrono::steady_clock::now();
+      sess.Solve(*prm, cb, user, out);
+      t2s = std::chrono::duration<double>(t2 - t1).count();
+      t3s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
+    }
+    if (std::getenv("PDHG_TRACE")) {
+      const auto t4 = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[pdhg] pdhg_solve_on %.4fs: validate %.4fs | session %.4fs | solve %.4fs | teardown %.4fs\n",
+                   std::chrono::duration<double>(t4 - t0).count(), std::chrono::duration<double>(t1 - t0).count(),
+                   t2s, t3s, std::chrono::duration<double>(t4 - t1).count() - t2s - t3s);
+    }
   });
 }
 

@@ -67,6 +67,7 @@ struct Scalars {
   int32_t pw_zero;    // power iteration hit a zero vector
   int32_t pad;
   double adapt_iter;  // iterations_ at the start of the block (adaptive step)
+  double lb, ub;      // the common scaled bound when every column shares it
 };
 
 // Clamp with the reference's NaN behaviour: std::min(std::max(v, lo), hi)

@@ -38,6 +38,7 @@ struct Layout {
   int32_t* idx = nullptr;
   double* val = nullptr;
   int32_t s1 = 0, s2 = 0, s3 = 0;  // class bounds S | M | L | XL
+  bool s_staged = false;           // class S uses seg_thread_staged_kernel
   CMat lng;                        // tile-engine view of [s3, nseg)
   int nb_s() const { return ceil_div(s1, kBlock); }
   int nb_m() const { return ceil_div(static_cast<int64_t>(s2 - s1) * 32, kBlock); }
@@ -65,9 +66,13 @@ __device__ __forceinline__ void block_reduce_out(double (&red)[Op::kRed > 0 ? Op
   }
 }
 
-// Class S: one thread per segment, direct loads (consecutive threads read
-// adjacent ranges, so L1 turns the per-thread streams into full-line use),
-// sum in storage order -- bit-identical to the reference's serial loops.
+// Class S: one thread per segment, sum in storage order -- bit-identical to
+// the reference's serial `acc += v * x[j]` loops. Two variants, chosen per
+// layout from the class's mean segment length (Layout::s_staged):
+//
+// direct (very short segments, e.g. transport / MCF / PageRank columns of 2,
+// 3, 8): each thread loads its own few entries; consecutive threads read
+// adjacent ranges, so each warp load touches a couple of lines.
 template <class Op>
 __global__ void __launch_bounds__(kBlock) seg_thread_kernel(const int32_t* __restrict__ ptr,
                                                             const int32_t* __restrict__ idx,
@@ -109,6 +114,80 @@ __global__ void __launch_bounds__(kBlock) seg_thread_kernel(const int32_t* __res
       for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[r]);
     }
     op.finish(s, acc, pre, red);
+  }
+  block_reduce_out<Op>(red, red_out);
+}
+
+// staged (longer short segments, e.g. 20-nonzero staircase rows): the 32
+// segments of a warp are contiguous in the nonzero stream, so the warp
+// streams that range in chunks of kSChunk entries with fully coalesced
+// lane-strided loads (all loads and gathers of a chunk in flight at once),
+// stages the rounded products in shared memory, and every lane then adds up
+// the part of its own segment inside the chunk, chunk after chunk -- i.e. in
+// storage order, exactly like the direct variant.
+constexpr int kSChunk = 256;
+
+template <class Op>
+__global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int32_t* __restrict__ ptr,
+                                                                      const int32_t* __restrict__ idx,
+                                                                      const double* __restrict__ val,
+                                                                      int32_t s_end, const Op op,
+                                                                      double* __restrict__ red_out) {
+  constexpr int R = Op::kRhs;
+  constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
+  constexpr bool MX = Op::kMax;
+  constexpr int C = kSChunk;
+  constexpr int U = C / 32;
+  __shared__ double sprod[kWarps][R][C];
+  double red[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) red[i] = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int s = blockIdx.x * kBlock + threadIdx.x;
+  const int s0 = blockIdx.x * kBlock + warp * 32;
+  if (s0 < s_end) {  // warp-uniform
+    const bool own = s < s_end;
+    int b = 0, e = 0;
+    typename Op::Pre pre{};
+    if (own) {
+      b = ptr[s];
+      e = ptr[s + 1];
+      pre = op.prefetch(s);
+    }
+    const int wb = ptr[s0];
+    const int we = ptr[s0 + 32 < s_end ? s0 + 32 : s_end];
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    double(*sp)[C] = sprod[warp];
+    for (int c0 = wb; c0 < we; c0 += C) {
+      int32_t j[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = c0 + lane + 32 * u;
+        j[u] = k < we ? ld_stream(idx + k) : 0;
+        v[u] = k < we ? ld_stream(val + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (c0 + lane + 32 * u < we) {
+          double p[R];
+          op.map(j[u], v[u], p);
+#pragma unroll
+          for (int r = 0; r < R; ++r) sp[r][lane + 32 * u] = p[r];
+        }
+      }
+      __syncwarp();
+      const int lo = (b > c0 ? b : c0) - c0;
+      const int hi = (e < c0 + C ? e : c0 + C) - c0;
+      for (int q = lo; q < hi; ++q) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], sp[r][q]);  // storage order
+      }
+      __syncwarp();
+    }
+    if (own) op.finish(s, acc, pre, red);
   }
   block_reduce_out<Op>(red, red_out);
 }
@@ -206,6 +285,14 @@ __global__ void __launch_bounds__(kBlock) seg_cta_kernel(const int32_t* __restri
   block_reduce_out<Op>(red, red_out);
 }
 
+template <class Op>
+inline void launch_thread_class(const Layout& L, const Op& op, double* red, cudaStream_t st) {
+  if (L.s_staged)
+    seg_thread_staged_kernel<Op><<<L.nb_s(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, op, red);
+  else
+    seg_thread_kernel<Op><<<L.nb_s(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, op, red);
+}
+
 // Reduction slots of one pass: [S blocks | M blocks | L CTAs | XL tiles | XL spans].
 struct RedSlots {
   double* base = nullptr;
@@ -216,7 +303,7 @@ template <class Op>
 inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, cudaStream_t st) {
   constexpr int nr = Op::kRed > 0 ? Op::kRed : 1;
   int64_t slot = 0;
-  if (L.s1 > 0) seg_thread_kernel<Op><<<L.nb_s(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, op, red.at(slot, nr));
+  if (L.s1 > 0) launch_thread_class(L, op, red.at(slot, nr), st);
   slot += L.nb_s();
   if (L.s2 > L.s1)
     seg_warp_kernel<Op><<<L.nb_m(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, L.s2, op, red.at(slot, nr));
@@ -257,7 +344,7 @@ inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, const F
     ++k;
   }
   int64_t slot = 0;
-  if (has[0]) seg_thread_kernel<Op><<<L.nb_s(), kBlock, 0, on[0]>>>(L.ptr, L.idx, L.val, L.s1, op, red.at(slot, nr));
+  if (has[0]) launch_thread_class(L, op, red.at(slot, nr), on[0]);
   slot += L.nb_s();
   if (has[1])
     seg_warp_kernel<Op><<<L.nb_m(), kBlock, 0, on[1]>>>(L.ptr, L.idx, L.val, L.s1, L.s2, op, red.at(slot, nr));

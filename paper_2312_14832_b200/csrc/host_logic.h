@@ -4,10 +4,34 @@
 
 #include <cmath>
 #include <cstdint>
+#include <stdexcept>
+#include <string>
 
 #include "../../include/pdhg.h"
 
 namespace pdhg {
+
+// LpProblem::Validate (lp_problem.cpp:22-58): same checks, same messages.
+inline void ValidateLpHost(const pdhg_lp& lp) {
+  auto bad = [](const std::string& m) { throw std::invalid_argument(m); };
+  const int64_t n = lp.n;
+  if (n < 0 || lp.a.rows < 0 || lp.g.rows < 0) bad("negative matrix dimension");
+  if (lp.a.cols != n || lp.g.cols != n) bad("matrix column count does not match c");
+  if ((lp.a.rows && !lp.a.row_ptr) || (lp.g.rows && !lp.g.row_ptr)) bad("missing row_ptr");
+  if ((n && (!lp.c || !lp.l || !lp.u)) || (lp.a.rows && !lp.b) || (lp.g.rows && !lp.h)) bad("missing vector");
+  for (int64_t i = 0; i < n; ++i)
+    if (std::isnan(lp.c[i])) bad("NaN in c");
+  for (int64_t i = 0; i < lp.a.rows; ++i)
+    if (std::isnan(lp.b[i])) bad("NaN in b");
+  for (int64_t i = 0; i < lp.g.rows; ++i)
+    if (std::isnan(lp.h[i])) bad("NaN in h");
+  for (int64_t i = 0; i < n; ++i)
+    if (std::isinf(lp.c[i])) bad("infinite entry in c");
+  for (int64_t i = 0; i < n; ++i) {
+    if (std::isnan(lp.l[i]) || std::isnan(lp.u[i])) bad("NaN bound");
+    if (lp.l[i] > lp.u[i]) bad("crossed bounds: l > u at index " + std::to_string(i));
+  }
+}
 
 // KktError (kkt.cpp:153-157).
 inline double KktError(double p, double d, double g, double w) {

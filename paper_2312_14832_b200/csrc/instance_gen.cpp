@@ -20,14 +20,7 @@
 #include <vector>
 
 #include "../../include/pdhg.h"
-
-struct pdhg_instance {
-  int64_t n = 0;
-  int64_t a_rows = 0, g_rows = 0;
-  std::vector<int64_t> a_ptr{0}, a_idx, g_ptr{0}, g_idx;
-  std::vector<double> a_val, g_val, c, b, h, l, u, witness;
-  double offset = 0.0;
-};
+#include "instance.h"
 
 namespace {
 
@@ -487,7 +480,7 @@ int pdhg_instance_view(const pdhg_instance* p, pdhg_lp* v) {
   v->l = p->l.data();
   v->u = p->u.data();
   v->objective_offset = p->offset;
-  v->negated_objective = 0;
+  v->negated_objective = p->negated;
   return PDHG_OK;
 }
 

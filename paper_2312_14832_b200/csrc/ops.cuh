@@ -106,10 +106,15 @@ struct OpPowerSumScale {
 // --------------------------------------------------------- PDHG step kernels
 // K-CSC: kty = K^T y, x+ = proj_[l,u](x - (eta/omega)(c - kty)), running
 // average of x (solver.cpp:285-290, RunningAverage::Add x-half :159).
-template <bool kAdapt>
+// kBnd: bit 0 -- every scaled lower bound equals sc->lb, bit 1 -- every upper
+// bound equals sc->ub (e.g. x >= 0: l_s = 0 / cs = 0, u_s = inf / cs = inf),
+// so those arrays are never streamed (16 of the 56 vector bytes per column).
+template <bool kAdapt, int kBnd = 0>
 struct OpPrimal {
   static constexpr int kRhs = 1, kRed = kAdapt ? 1 : 0;
   static constexpr bool kMax = false;
+  static constexpr bool kL = !(kBnd & 1), kU = !(kBnd & 2);  // streamed?
+  static constexpr int kIL = 2, kIU = 2 + kL, kIB = 2 + kL + kU;  // operand slots
   struct Pre {
     double x, c, l, u, xbar, w, step;
   };
@@ -124,10 +129,13 @@ struct OpPrimal {
   int j_in_block;
   __device__ void map(int32_t i, double v, double (&p)[1]) const { p[0] = v * y[i]; }
   static constexpr int kOcc = 5;
-  static constexpr int kOps = 5;
+  static constexpr int kOps = 3 + kL + kU;
   __device__ const double* operand(int k) const {
-    const double* a[5] = {x, c, l, u, xbar};
-    return a[k];
+    if (k == 0) return x;
+    if (k == 1) return c;
+    if (kL && k == kIL) return l;
+    if (kU && k == kIU) return u;
+    return xbar;
   }
   __device__ Pre staged(int32_t, const double* st, int ld) const {
     Pre p;
@@ -135,9 +143,9 @@ struct OpPrimal {
     p.step = sc->eta / sc->omega;
     p.x = st[0];
     p.c = st[ld];
-    p.l = st[2 * ld];
-    p.u = st[3 * ld];
-    p.xbar = (p.w == 0.0) ? 0.0 : st[4 * ld];
+    p.l = kL ? st[kIL * ld] : sc->lb;
+    p.u = kU ? st[kIU * ld] : sc->ub;
+    p.xbar = (p.w == 0.0) ? 0.0 : st[kIB * ld];
     return p;
   }
   __device__ Pre prefetch(int32_t s) const {
@@ -146,8 +154,8 @@ struct OpPrimal {
     p.step = sc->eta / sc->omega;
     p.x = x[s];
     p.c = c[s];
-    p.l = l[s];
-    p.u = u[s];
+    p.l = kL ? l[s] : sc->lb;
+    p.u = kU ? u[s] : sc->ub;
     p.xbar = (p.w == 0.0) ? 0.0 : xbar[s];  // Reset() zeroes the average
     return p;
   }

@@ -372,6 +372,8 @@ LpProblem Take(pdhg_instance* inst, std::vector<double>* witness) {
   pdhg_lp v{};
   pdhg_instance_view(inst, &v);
   LpProblem p;
+  p.name = pdhg_instance_name(inst);
+  p.negated_objective = v.negated_objective != 0;
   p.a = FromCsr(v.a);
   p.g = FromCsr(v.g);
   p.c.assign(v.c, v.c + v.n);
@@ -414,6 +416,93 @@ LpProblem GenTransport(Index sources, Index sinks, std::uint64_t seed) {
   char err[512] = {0};
   if (pdhg_gen_transport(sources, sinks, seed, &inst, err, sizeof(err)) != PDHG_OK) throw std::invalid_argument(err);
   return Take(inst, nullptr);
+}
+
+}  // namespace rpdlp
+
+// ------------------------------------------------------------------- MPS
+#include <fstream>
+#include <iterator>
+#include <sstream>
+
+#include "rpdlp/mps.hpp"
+
+namespace rpdlp {
+namespace {
+
+LpProblem FromMps(int code, pdhg_instance* inst, const char* err, int line) {
+  if (code == PDHG_OK) return Take(inst, nullptr);
+  std::string msg(err);
+  if (code == PDHG_PARSE_ERROR) {
+    const std::string prefix = "mps parse error at line " + std::to_string(line) + ": ";
+    if (msg.compare(0, prefix.size(), prefix) == 0) msg = msg.substr(prefix.size());
+    throw MpsParseError(line, msg);
+  }
+  if (code == PDHG_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+}  // namespace
+
+LpProblem ParseMpsString(const std::string& text, const MpsOptions& o) {
+  pdhg_instance* inst = nullptr;
+  char err[512] = {0};
+  int line = 0;
+  const int code = pdhg_mps_read_string(text.data(), text.size(), o.fixed_format, &inst, err, sizeof(err), &line);
+  return FromMps(code, inst, err, line);
+}
+
+LpProblem ParseMps(std::istream& in, const MpsOptions& o) {
+  std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  return ParseMpsString(text, o);
+}
+
+LpProblem ParseMpsFile(const std::string& path, const MpsOptions& o) {
+  pdhg_instance* inst = nullptr;
+  char err[512] = {0};
+  int line = 0;
+  const int code = pdhg_mps_read_file(path.c_str(), o.fixed_format, &inst, err, sizeof(err), &line);
+  return FromMps(code, inst, err, line);
+}
+
+void WriteMps(const LpProblem& problem, std::ostream& out) {
+  const pdhg_lp v = View(problem);
+  char* s = nullptr;
+  size_t n = 0;
+  char err[512] = {0};
+  const int code = pdhg_mps_write_string(&v, problem.name.c_str(), &s, &n, err, sizeof(err));
+  if (code == PDHG_INVALID_ARGUMENT) throw std::invalid_argument(err);
+  if (code != PDHG_OK) throw std::runtime_error(err);
+  out.write(s, static_cast<std::streamsize>(n));
+  pdhg_free_string(s);
+}
+
+void WriteMpsFile(const LpProblem& problem, const std::string& path) {
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot open " + path + " for writing");
+  WriteMps(problem, out);
+  out.flush();
+  if (!out) throw std::runtime_error("write failed for " + path);
+}
+
+// SURVEY §8d configs 3 and 5 (not in the reference).
+LpProblem GenMcf(Index nodes, Index arcs, Index commodities, std::uint64_t seed, std::vector<double>* witness) {
+  pdhg_instance* inst = nullptr;
+  char err[512] = {0};
+  if (pdhg_gen_mcf(nodes, arcs, commodities, seed, &inst, err, sizeof(err)) != PDHG_OK)
+    throw std::invalid_argument(err);
+  return Take(inst, witness);
+}
+
+LpProblem GenStaircase(Index stages, Index rows_per_stage, Index cols_per_stage, Index nnz_per_row,
+                       Index linking_per_row, Index eq_rows_per_stage, std::uint64_t seed,
+                       std::vector<double>* witness) {
+  pdhg_instance* inst = nullptr;
+  char err[512] = {0};
+  if (pdhg_gen_staircase(stages, rows_per_stage, cols_per_stage, nnz_per_row, linking_per_row, eq_rows_per_stage,
+                         seed, 0, &inst, err, sizeof(err)) != PDHG_OK)
+    throw std::invalid_argument(err);
+  return Take(inst, witness);
 }
 
 }  // namespace rpdlp

@@ -102,6 +102,9 @@ void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, int bit
 // vector traffic per row / column against 12 bytes per nonzero.
 constexpr int64_t kSegWeight = 6;
 
+// Mean class-S segment length from which the warp-staged S kernel is used.
+constexpr double kStagedMin = 6.0;
+
 }  // namespace
 
 // Host mirror of the check reductions (26 doubles).
@@ -197,9 +200,13 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
   Sync();
   scaling_s_ = now_s() - t1;
   DeviceNorms();
+  UniformBounds();
   const double iter_bytes = (24.0 * nnz_ + 68.0 * (m_ + n_)) / world_;
   l2_resident_ = iter_bytes < 100e6;
   Sync();
+  if (std::getenv("PDHG_TRACE"))
+    std::fprintf(stderr, "[pdhg] session %.4fs: upload+csc+permute+partition %.4fs | scaling %.4fs | %.2f GB\n",
+                 now_s() - t0, upload_s_, scaling_s_, arena_.bytes / 1e9);
 }
 
 Session::~Session() {
@@ -208,7 +215,9 @@ Session::~Session() {
     if (e) cudaEventDestroy(e);
   for (Graph& g : graphs_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (power_graph_) cudaGraphExecDestroy(power_graph_);
   if (host_red_) cudaFreeHost(host_red_);
+  if (hstage_) cudaFreeHost(hstage_);
   comm_.reset();
   if (fork_.fork) cudaEventDestroy(fork_.fork);
   for (int k = 0; k < 3; ++k) {
@@ -386,7 +395,7 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     int bits = 3;
     while ((1 << bits) < nkeys) ++bits;
     const char* dord = std::getenv("PDHG_DEGREE_ORDER");
-    const bool by_len = !(dord && dord[0] == '0');
+    const bool by_len = dord && dord[0] == '1';  // off by default: it breaks stage locality (staircase)
     if (m_) stable_order(kr.p, m_, perm_r, bits, st_, by_len ? ptr0.p : nullptr);
     if (n_) stable_order(kc.p, n_, perm_c, bits, st_, by_len ? cptr0.p : nullptr);
     std::vector<int> h(2 * nkeys);
@@ -418,6 +427,8 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       k_perm_nnz<<<ew_grid(nnz_), kEw, 0, st_>>>(p0.p, seg_of.p, i0.p, v0.p, inv_seg.p, pad_other.p, ptr.p, idx.p,
                                                   val.p, nnz_);
   };
+  const char* smin = std::getenv("PDHG_STAGED_MIN");
+  const double staged_min = smin ? std::atof(smin) : kStagedMin;
   // One layout's block slice -> shard storage (ownership moves when the
   // session holds the whole matrix in one shard).
   auto slice = [&](Layout& L, Store& S, DArray<int32_t>& ptr, DArray<int32_t>& idx, DArray<double>& val, int64_t b0,
@@ -449,6 +460,14 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     L.s1 = hist[0] + hist[1];
     L.s2 = L.s1 + hist[2] + hist[3];
     L.s3 = L.s2 + hist[4] + hist[5];
+    // Class S kernel variant from the class's mean length (setup-time D2H
+    // of one offset): warp-staged once segments average >= kStagedMin.
+    int32_t se = 0;
+    if (L.s1 > 0) {
+      PDHG_CUDA(cudaMemcpyAsync(&se, L.ptr + L.s1, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+      Sync();
+    }
+    L.s_staged = L.s1 > 0 && static_cast<double>(se) >= staged_min * L.s1;
   };
   {
     DArray<int32_t> fptr, fidx;
@@ -639,6 +658,30 @@ void Session::ComputeScaling(const pdhg_params& prm) {
   check_launch("apply scaling");
 }
 
+// Common scaled bounds: bit 0 when every l_s is bitwise one value, bit 1 for
+// u_s (the primal kernels then skip those streams). PDHG_UNIFORM_BOUNDS=0
+// disables it (A/B timing).
+void Session::UniformBounds() {
+  bnd_ = 0;
+  lb_ = ub_ = 0.0;
+  const char* env = std::getenv("PDHG_UNIFORM_BOUNDS");
+  if (n_ == 0 || (env && env[0] == '0')) return;
+  DArray<int> diff;
+  diff.alloc(2);
+  PDHG_CUDA(cudaMemsetAsync(diff.p, 0, 2 * sizeof(int), st_));
+  k_uniform<<<ew_grid(n_), kEw, 0, st_>>>(l_s_.p, pad_c_.p, n_, diff.p);
+  k_uniform<<<ew_grid(n_), kEw, 0, st_>>>(u_s_.p, pad_c_.p, n_, diff.p + 1);
+  int h[2];
+  int32_t p0 = 0;
+  PDHG_CUDA(cudaMemcpyAsync(h, diff.p, sizeof(h), cudaMemcpyDeviceToHost, st_));
+  PDHG_CUDA(cudaMemcpyAsync(&p0, pad_c_.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+  Sync();
+  PDHG_CUDA(cudaMemcpyAsync(&lb_, l_s_.p + p0, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  PDHG_CUDA(cudaMemcpyAsync(&ub_, u_s_.p + p0, sizeof(double), cudaMemcpyDeviceToHost, st_));
+  Sync();
+  bnd_ = (h[0] ? 0 : 1) | (h[1] ? 0 : 2);
+}
+
 // ||c||, ||q|| in both spaces (kkt.cpp:45-56), deterministic device sums over
 // the full (padded, zero-filled) vectors every rank holds.
 void Session::DeviceNorms() {
@@ -661,46 +704,77 @@ void Session::DeviceNorms() {
   q_norm_o_ = std::sqrt(h[3]);
 }
 
+// Session-lifetime staging: one device vector and one pinned host vector of
+// max(m, n) doubles, so no solve-path call allocates (cudaMalloc / cudaFree
+// synchronise the device and were the largest non-kernel cost of a solve).
+double* Session::DevStage() {
+  const size_t need = static_cast<size_t>(std::max<int64_t>(std::max(m_, n_), 1));
+  if (dstage_.n < need) dstage_.alloc(need, &arena_);
+  return dstage_.p;
+}
+
+double* Session::HostStage() {
+  const size_t need = static_cast<size_t>(std::max<int64_t>(std::max(m_, n_), 1));
+  if (hstage_n_ < need) {
+    if (hstage_) cudaFreeHost(hstage_);
+    hstage_ = nullptr;
+    PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hstage_), need * sizeof(double)));
+    hstage_n_ = need;
+  }
+  return hstage_;
+}
+
 // Host vector (original order) -> device (padded order); padding zeroed.
+// `host` may already be the pinned stage.
 void Session::ToInternal(const double* host, const DArray<int32_t>& pad, double* dev, int64_t n, int64_t padded) {
   if (padded) PDHG_CUDA(cudaMemsetAsync(dev, 0, padded * sizeof(double), st_));
   if (!n) return;
-  DArray<double> tmp;
-  tmp.alloc(n);
-  PDHG_CUDA(cudaMemcpyAsync(tmp.p, host, n * sizeof(double), cudaMemcpyHostToDevice, st_));
-  k_scatter<<<ew_grid(n), kEw, 0, st_>>>(tmp.p, pad.p, dev, n);
+  double* d = DevStage();
+  PDHG_CUDA(cudaMemcpyAsync(d, host, n * sizeof(double), cudaMemcpyHostToDevice, st_));
+  k_scatter<<<ew_grid(n), kEw, 0, st_>>>(d, pad.p, dev, n);
   Sync();
 }
 
 void Session::ToHost(const double* dev, const double* scale, const DArray<int32_t>& pad, double* host, int64_t n) {
   if (!n || !host) return;
-  DArray<double> tmp;
-  tmp.alloc(n);
-  k_unpermute<<<ew_grid(n), kEw, 0, st_>>>(dev, scale, pad.p, tmp.p, n);
-  PDHG_CUDA(cudaMemcpyAsync(host, tmp.p, n * sizeof(double), cudaMemcpyDeviceToHost, st_));
+  double* d = DevStage();
+  double* h = HostStage();
+  k_unpermute<<<ew_grid(n), kEw, 0, st_>>>(dev, scale, pad.p, d, n);
+  PDHG_CUDA(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, st_));
   Sync();
+  std::memcpy(host, h, n * sizeof(double));
 }
 
 // ================================================================== kernels
 // One PDHG iteration (solver.cpp:284-306): every local shard's K-CSC primal
 // pass writes its slice of x+, one all-gather rebuilds x+ everywhere, then the
 // K-CSR dual passes and the all-gather of y+.
+template <bool kAdapt, int kBnd>
+void Session::PrimalPass(Shard& h, int a, int b, int j) {
+  const int64_t o = h.coff;
+  run_pass(h.csc,
+           OpPrimal<kAdapt, kBnd>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
+                                  scal_.p, j},
+           RedSlots{kAdapt ? h.red[1].p : nullptr}, fork_);
+}
+
+void Session::LaunchPrimal(Shard& h, int a, int b, int j, bool adapt) {
+  switch (bnd_ + 4 * adapt) {
+    case 0: PrimalPass<false, 0>(h, a, b, j); break;
+    case 1: PrimalPass<false, 1>(h, a, b, j); break;
+    case 2: PrimalPass<false, 2>(h, a, b, j); break;
+    case 3: PrimalPass<false, 3>(h, a, b, j); break;
+    case 4: PrimalPass<true, 0>(h, a, b, j); break;
+    case 5: PrimalPass<true, 1>(h, a, b, j); break;
+    case 6: PrimalPass<true, 2>(h, a, b, j); break;
+    default: PrimalPass<true, 3>(h, a, b, j); break;
+  }
+}
+
 void Session::LaunchStep(int parity, int j, bool adapt) {
   const int a = parity, b = 1 - parity;
   launches_ += launches_csc() + launches_csr();
-  for (Shard& h : shards_) {
-    const int64_t o = h.coff;
-    if (adapt)
-      run_pass(h.csc,
-               OpPrimal<true>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
-                              scal_.p, j},
-               RedSlots{h.red[1].p}, fork_);
-    else
-      run_pass(h.csc,
-               OpPrimal<false>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
-                               scal_.p, j},
-               RedSlots{}, fork_);
-  }
+  for (Shard& h : shards_) LaunchPrimal(h, a, b, j, adapt);
   GatherX(x_[b].p);
   for (Shard& h : shards_) {
     const int64_t o = h.roff;
@@ -819,6 +893,8 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   if (c_norm_s_ > 1e-10 && q_norm_s_ > 1e-10) sc.omega = c_norm_s_ / q_norm_s_;
   sc.inner_base = 0.0;
   sc.pw_norm = 1.0;
+  sc.lb = lb_;
+  sc.ub = ub_;
   const bool adapt = prm.adaptive_step != 0;
 
   // x0 = proj(0), y0 = 0, kx = K x0 (solver.cpp:240-245).
@@ -1060,44 +1136,60 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 double Session::OpNorm(int iters, uint64_t seed) {
   PDHG_CUDA(cudaSetDevice(device_));
   if (nnz_ == 0) return 0.0;
-  std::vector<double> v(static_cast<size_t>(n_));
-  NormalVector(seed, n_, v.data(), 0);  // == std::normal_distribution draws, all host threads
+  double* v = HostStage();
+  NormalVector(seed, n_, v, 0);  // == std::normal_distribution draws, all host threads
   double acc = 0.0;
-  for (double e : v) acc += e * e;
+  for (int64_t j = 0; j < n_; ++j) acc += v[j] * v[j];
   double vnorm = std::sqrt(acc);
   if (vnorm == 0.0) {
     v[0] = 1.0;
     vnorm = 1.0;
   }
-  DArray<double> u, kv;
-  u.alloc(np_);
-  kv.alloc(mp_);
-  PDHG_CUDA(cudaMemsetAsync(kv.p, 0, mp_ * sizeof(double), st_));
-  ToInternal(v.data(), pad_c_, u.p, n_, np_);
+  // Scratch: x_[1] and kx_[1] are free until the loop starts.
+  double* u = x_[1].p;
+  double* kv = kx_[1].p;
+  PDHG_CUDA(cudaMemsetAsync(kv, 0, mp_ * sizeof(double), st_));
+  ToInternal(v, pad_c_, u, n_, np_);
   Scalars sc{};
   sc.pw_norm = vnorm;
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   const int64_t ns = static_cast<int64_t>(shards_.size());
   launches_ += static_cast<int64_t>(iters) * (launches_csr() + launches_csc() + ns + (ns > 1) + 1) + launches_csr() +
                ns + (ns > 1);
-  for (int it = 0; it < iters; ++it) {
-    for (Shard& h : shards_) run_pass(h.csr, OpPowerStep<false>{u.p, scal_.p, 1, kv.p + h.roff}, RedSlots{}, st_);
-    GatherY(kv.p);
+  // The 100 power steps (+ the final K u pass) are one captured graph per
+  // session, replayed on every solve: no per-step launch latency.
+  auto body = [&] {
+    for (int it = 0; it < iters; ++it) {
+      for (Shard& h : shards_) run_pass(h.csr, OpPowerStep<false>{u, scal_.p, 1, kv + h.roff}, RedSlots{}, fork_);
+      GatherY(kv);
+      for (size_t k = 0; k < shards_.size(); ++k) {
+        Shard& h = shards_[k];
+        run_pass(h.csc, OpPowerStep<true>{kv, scal_.p, 0, u + h.coff}, RedSlots{h.red[1].p}, fork_);
+        k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), 1, red_out_.p + k * kPack);
+      }
+      SumPacks(1);
+      k_power_norm<<<1, 1, 0, st_>>>(red_out_.p, scal_.p);
+      GatherX(u);
+    }
     for (size_t k = 0; k < shards_.size(); ++k) {
       Shard& h = shards_[k];
-      run_pass(h.csc, OpPowerStep<true>{kv.p, scal_.p, 0, u.p + h.coff}, RedSlots{h.red[1].p}, st_);
-      k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), 1, red_out_.p + k * kPack);
+      run_pass(h.csr, OpPowerStep<true>{u, scal_.p, 1, kv + h.roff}, RedSlots{h.red[0].p}, fork_);
+      k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[0].p, nullptr, h.csr.parts(), 1, red_out_.p + k * kPack);
     }
     SumPacks(1);
-    k_power_norm<<<1, 1, 0, st_>>>(red_out_.p, scal_.p);
-    GatherX(u.p);
+  };
+  if (power_iters_ != iters) {
+    if (power_graph_) cudaGraphExecDestroy(power_graph_);
+    power_graph_ = nullptr;
+    cudaGraph_t graph;
+    PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    body();
+    PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
+    PDHG_CUDA(cudaGraphInstantiate(&power_graph_, graph, 0));
+    cudaGraphDestroy(graph);
+    power_iters_ = iters;
   }
-  for (size_t k = 0; k < shards_.size(); ++k) {
-    Shard& h = shards_[k];
-    run_pass(h.csr, OpPowerStep<true>{u.p, scal_.p, 1, kv.p + h.roff}, RedSlots{h.red[0].p}, st_);
-    k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[0].p, nullptr, h.csr.parts(), 1, red_out_.p + k * kPack);
-  }
-  SumPacks(1);
+  PDHG_CUDA(cudaGraphLaunch(power_graph_, st_));
   check_launch("power iteration");
   double sum = 0.0;
   Scalars hs{};
@@ -1164,6 +1256,8 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   sc.eta = 1e-3;
   sc.omega = 1.0;
   sc.inner_base = 1.0;
+  sc.lb = lb_;
+  sc.ub = ub_;
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   k_clamp0<<<ew_grid(np_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, np_);
   if (mp_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, mp_ * sizeof(double), st_));
@@ -1177,13 +1271,7 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   float t_p = 0, t_d = 0, t_i = 0;
   PDHG_CUDA(cudaEventRecord(e0, st_));
   for (int i = 0; i < iters; ++i) {
-    for (Shard& h : shards_) {
-      const int64_t o = h.coff;
-      run_pass(h.csc,
-               OpPrimal<false>{y_[0].p, x_[0].p + o, x_[1].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
-                               scal_.p, i + 1},
-               RedSlots{}, fork_);
-    }
+    for (Shard& h : shards_) LaunchPrimal(h, 0, 1, i + 1, false);
     GatherX(x_[1].p);
   }
   PDHG_CUDA(cudaEventRecord(e1, st_));
@@ -1283,6 +1371,7 @@ void Session::Stats(pdhg_session_stats* s) const {
   s->world = world_;
   s->local_shards = static_cast<int32_t>(shards_.size());
   s->rank = rank_;
+  s->uniform_bounds = bnd_;
 }
 
 void Session::Blocks(int64_t* row_begin, int64_t* col_begin) const {

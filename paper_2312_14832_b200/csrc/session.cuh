@@ -85,6 +85,10 @@ class Session {
   void DeviceNorms();
   void Sync();
   void LaunchStep(int parity, int j, bool adapt);
+  template <bool kAdapt, int kBnd>
+  void PrimalPass(Shard& h, int a, int b, int j);
+  void LaunchPrimal(Shard& h, int a, int b, int j, bool adapt);
+  void UniformBounds();
   void RunSteps(int parity, int count, bool adapt);
   void LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx);
   void ReadCheck(CheckOut* out);
@@ -92,6 +96,8 @@ class Session {
   void Copy(double* dst, const double* src, size_t n);
   void ToInternal(const double* host, const DArray<int32_t>& pad, double* dev, int64_t n, int64_t padded);
   void ToHost(const double* dev, const double* scale, const DArray<int32_t>& pad, double* host, int64_t n);
+  double* DevStage();
+  double* HostStage();
   void GatherX(double* v) { comm_->AllGather(v, pn_, st_); }
   void GatherY(double* v) { comm_->AllGather(v, pm_, st_); }
   bool nccl() const { return !comm_->local(); }
@@ -124,6 +130,8 @@ class Session {
   DArray<double> c_s_, l_s_, u_s_, c_o_, l_o_, u_o_, cs_;  // np_
   DArray<double> q_s_, q_o_, rs_;                          // mp_
   double c_norm_s_ = 0, q_norm_s_ = 0, c_norm_o_ = 0, q_norm_o_ = 0;
+  int bnd_ = 0;               // uniform-bound bits (UniformBounds)
+  double lb_ = 0.0, ub_ = 0.0;
 
   // Iterates (ping-pong x/y/kx), averages, loop start, best, scratch.
   DArray<double> x_[2], xbar_, xstart_, xbest_, nvec_;            // np_
@@ -131,8 +139,13 @@ class Session {
   DArray<Scalars> scal_;
   DArray<double> red_out_;  // per-shard packs; pack 0 holds the reduced result
   double* host_red_ = nullptr;  // pinned
+  DArray<double> dstage_;       // max(m, n) device staging
+  double* hstage_ = nullptr;    // max(m, n) pinned host staging
+  size_t hstage_n_ = 0;
 
   std::vector<Graph> graphs_;
+  cudaGraphExec_t power_graph_ = nullptr;  // EstimateOpNorm steps (OpNorm)
+  int power_iters_ = 0;
   DArray<char> flush_;
   cudaEvent_t ev_[2] = {nullptr, nullptr};
   double last_ms_ = 0.0;

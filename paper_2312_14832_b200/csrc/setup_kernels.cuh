@@ -176,6 +176,14 @@ __global__ void k_scale_vals(const int32_t* seg_of, const int32_t* idx, const do
   }
 }
 
+// *diff = 1 unless v[pad[j]] is bitwise equal to v[pad[0]] for every j.
+__global__ void k_uniform(const double* v, const int32_t* pad, int64_t n, int* diff) {
+  const unsigned long long ref = __double_as_longlong(v[pad[0]]);
+  GRID_STRIDE(j, n) {
+    if (static_cast<unsigned long long>(__double_as_longlong(v[pad[j]])) != ref) *diff = 1;
+  }
+}
+
 __global__ void k_fill(double* v, double a, int64_t n) {
   GRID_STRIDE(i, n) v[i] = a;
 }

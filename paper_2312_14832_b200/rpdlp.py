@@ -32,6 +32,14 @@ class NumericalFailure(RuntimeError):
     """Non-finite iterate (solver.cpp:391-394)."""
 
 
+class MpsParseError(RuntimeError):
+    """rpdlp::MpsParseError (mps.hpp:26-36): message carries the line."""
+
+    def __init__(self, message: str, line: int):
+        super().__init__(message)
+        self.line = line
+
+
 class CudaError(RuntimeError):
     pass
 
@@ -503,7 +511,7 @@ def PartitionBlocks(ptr, parts: int, seg_weight: int = 6) -> np.ndarray:
     return out
 
 
-# ------------------------------------------------------------ generators
+# ---------------------------------------------- host-owned instances
 class _InstanceOwner:
     """Frees a generated pdhg_instance once no array view into it is alive."""
 
@@ -539,8 +547,9 @@ def _from_instance(h: C.c_void_p, name: str) -> LpProblem:
 
     d = lambda p, n: arr(p, n, C.c_double, np.float64)  # noqa: E731
     a, g = csr(v.a), csr(v.g)
+    own_name = (lib.pdhg_instance_name(h) or b"").decode()
     p = LpProblem(a, g, d(v.c, v.n), d(v.b, a.rows), d(v.h, g.rows), d(v.l, v.n), d(v.u, v.n),
-                  v.objective_offset, False, name)
+                  v.objective_offset, bool(v.negated_objective), own_name or name)
     w = lib.pdhg_instance_witness(h)
     p.witness = d(w, v.n) if w else None
     return p
@@ -554,6 +563,58 @@ def _gen(fn, *args, name=""):
     return h
 
 
+# ------------------------------------------------------------------ MPS
+def _mps_result(code, h, err, line):
+    if code == abi.PDHG_PARSE_ERROR:
+        raise MpsParseError(err.value.decode(errors="replace"), line.value)
+    if code == abi.PDHG_IO_ERROR:
+        raise OSError(err.value.decode(errors="replace"))
+    raise_for(code, err)
+    return _from_instance(h, "")
+
+
+def ParseMpsString(text, fixed_format: bool = False) -> LpProblem:
+    """ParseMpsString (mps.hpp:53, mps_reader.cpp) -- same normalisations and
+    errors; MpsParseError carries the line number."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h, err, line = C.c_void_p(), C.create_string_buffer(abi.ERRLEN), C.c_int(0)
+    code = abi.load().pdhg_mps_read_string(data, len(data), int(fixed_format), C.byref(h), err, abi.ERRLEN,
+                                           C.byref(line))
+    return _mps_result(code, h, err, line)
+
+
+def ParseMpsFile(path, fixed_format: bool = False) -> LpProblem:
+    """ParseMpsFile (mps.hpp:55): plain or .gz (zlib)."""
+    h, err, line = C.c_void_p(), C.create_string_buffer(abi.ERRLEN), C.c_int(0)
+    code = abi.load().pdhg_mps_read_file(str(path).encode(), int(fixed_format), C.byref(h), err, abi.ERRLEN,
+                                         C.byref(line))
+    return _mps_result(code, h, err, line)
+
+
+def WriteMps(problem: LpProblem) -> str:
+    """WriteMps (mps_writer.cpp:37-107): free format, %.17g."""
+    lib = abi.load()
+    lp = problem.to_c()
+    out, n, err = C.c_void_p(), C.c_size_t(0), C.create_string_buffer(abi.ERRLEN)
+    raise_for(lib.pdhg_mps_write_string(C.byref(lp), (problem.name or "").encode(), C.byref(out), C.byref(n), err,
+                                        abi.ERRLEN), err)
+    try:
+        return C.string_at(out, n.value).decode()
+    finally:
+        lib.pdhg_free_string(out)
+
+
+def WriteMpsFile(problem: LpProblem, path) -> None:
+    lp = problem.to_c()
+    err = C.create_string_buffer(abi.ERRLEN)
+    code = abi.load().pdhg_mps_write_file(C.byref(lp), (problem.name or "").encode(), str(path).encode(), err,
+                                          abi.ERRLEN)
+    if code == abi.PDHG_IO_ERROR:
+        raise OSError(err.value.decode(errors="replace"))
+    raise_for(code, err)
+
+
+# ------------------------------------------------------------ generators
 def GenRandomLp(m: int, n: int, density: float, seed: int, equality_rows: int = 0) -> LpProblem:
     """instance_gen.cpp:143-188; `equality_rows` moves the first rows of G into
     A with b = A x_hat."""

@@ -10,7 +10,10 @@
 #include <string>
 #include <vector>
 
+#include <sstream>
+
 #include "rpdlp/instance_gen.hpp"
+#include "rpdlp/mps.hpp"
 #include "rpdlp/solver.hpp"
 
 using namespace rpdlp;
@@ -158,6 +161,37 @@ int main() {
     LpProblem p = GenRandomLp(6, 8, 0.5, 55);
     SolveResult a = Solve(p, prm), b = Solve(p, prm);
     CHECK(a.iterations == b.iterations && a.x == b.x && a.y == b.y);
+  }
+  {  // MPS ingestion (mps.hpp / test_mps.cpp): parse, errors, write round trip, solve
+    const std::string text =
+        "NAME T\nROWS\n N obj\n E e1\n L l1\nCOLUMNS\n x obj 1 e1 1\n x l1 1\n y obj 2 e1 1\n"
+        "RHS\n RHS e1 2 l1 1.5\nBOUNDS\n UP B y 3\nENDATA\n";
+    LpProblem p = ParseMpsString(text);
+    CHECK(p.name == "T" && p.num_vars() == 2 && p.num_eq_rows() == 1 && p.num_ineq_rows() == 1);
+    CHECK(p.h[0] == -1.5 && p.u[1] == 3.0);
+    bool threw = false;
+    try {
+      ParseMpsString("NAME\nROWS\n N o\n Q r\n");
+    } catch (const MpsParseError& e) {
+      threw = e.line() == 4 && std::string(e.what()) == "mps parse error at line 4: unknown row type 'Q'";
+    }
+    CHECK(threw);
+    std::ostringstream os;
+    WriteMps(p, os);
+    LpProblem q = ParseMpsString(os.str());
+    CHECK(q.c == p.c && q.b == p.b && q.h == p.h && q.l == p.l && q.u == p.u);
+    SolverParams prm;
+    prm.eps = 1e-8;
+    SolveResult r = Solve(q, prm);
+    CHECK(r.status == SolveStatus::kOptimal && Near(r.report.primal_obj, 2.0, 1e-6));
+  }
+  {  // the new SURVEY §8d shapes through the drop-in generators
+    SolverParams prm;
+    prm.eps = 1e-4;
+    SolveResult r = Solve(GenMcf(40, 200, 3, 1), prm);
+    CHECK(r.status == SolveStatus::kOptimal);
+    SolveResult s = Solve(GenStaircase(4, 20, 25, 6, 2, 10, 1), prm);
+    CHECK(s.status == SolveStatus::kOptimal);
   }
   std::printf("drop_in_test: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail;

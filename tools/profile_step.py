@@ -23,6 +23,6 @@ def problem(name):
 if __name__ == "__main__":
     p = problem(sys.argv[1] if len(sys.argv) > 1 else "transport")
     with rpdlp.Session(p) as s:
-        iters = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+        iters = int(sys.argv[3]) if len(sys.argv) > 3 else 2
         ms_p, ms_d, ms_it = s.time_kernels(iters)
         print(f"primal {ms_p * 1e3:.1f} us  dual {ms_d * 1e3:.1f} us  iteration {ms_it * 1e3:.1f} us")

@@ -72,18 +72,23 @@ def make_problem(cfg: str, args):
     return p, wl
 
 
-def algorithmic_bytes(m: int, n: int, nnz: int, uniform_bounds: int = 0):
+def algorithmic_bytes(m: int, n: int, nnz: int, uniform_bounds: int = 0, csr_uniform: int = 0,
+                      csc_uniform: int = 0):
     """per-kernel algorithmic bytes (int32 idx, f64 values).
     K-CSC primal: 12 nnz (idx+val) + 4(n+1) ptr + 8 m (y gathered once)
                   + 56 n (x, c, l, u, xbar read; x+, xbar written),
                   less 8 n for each bound vector that is one common value
-                  (uniform_bounds bits; the step then never needs it).
+                  (uniform_bounds bits; the step then never needs it), and
+                  less the 4(n+1) offsets when every column has one common
+                  length (csc_uniform: offsets are implicit).
     K-CSR dual:   12 nnz + 4(m+1) + 8 n (x+ gathered once)
                   + 56 m (y, kx, q, ybar read; y+, kx+, ybar written)."""
     skip = 8 * n * (bin(uniform_bounds & 3).count("1"))
-    primal = 12 * nnz + 4 * (n + 1) + 8 * m + 56 * n - skip
-    dual = 12 * nnz + 4 * (m + 1) + 8 * n + 56 * m
-    return primal, dual, 24 * nnz + 68 * (m + n) + 8 - skip
+    pp = 0 if csc_uniform else 4 * (n + 1)
+    pd = 0 if csr_uniform else 4 * (m + 1)
+    primal = 12 * nnz + pp + 8 * m + 56 * n - skip
+    dual = 12 * nnz + pd + 8 * n + 56 * m
+    return primal, dual, primal + dual
 
 
 # ------------------------------------------------------------------- clocks
@@ -333,7 +338,7 @@ def run_ours(args, world, rank, local, dist):
 
     # Per-kernel roofline (K-CSC primal / K-CSR dual), events on the solver stream.
     ms_p, ms_d, ms_it = sess.time_kernels(args.kernel_iters)
-    b_p, b_d, b_it = algorithmic_bytes(m, n, nnz, st.uniform_bounds)
+    b_p, b_d, b_it = algorithmic_bytes(m, n, nnz, st.uniform_bounds, st.csr_uniform_len, st.csc_uniform_len)
     if sharded:  # each rank streams its own blocks (x / y all-gathers ride on NVLink)
         b_p, b_d, b_it = b_p / world, b_d / world, b_it / world
     dom = "pdhg_primal_csc" if ms_p >= ms_d else "pdhg_dual_csr"

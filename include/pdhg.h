@@ -146,6 +146,9 @@ typedef struct {
   int32_t rank;         /* this session's shard when local_shards == 1 */
   int32_t uniform_bounds; /* bit 0: all scaled l equal, bit 1: all u equal
                              (those streams are skipped by the primal step) */
+  int32_t csr_uniform_len; /* every short row has this many nonzeros (offsets
+                              implicit, never read), else 0 */
+  int32_t csc_uniform_len; /* same for short columns */
 } pdhg_session_stats;
 
 /* Distribution of K over shards: `world` balanced row blocks

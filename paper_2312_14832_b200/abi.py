@@ -70,7 +70,8 @@ class SessionStats(C.Structure):
                 ("csr_tiles", C.c_int64), ("csc_tiles", C.c_int64), ("device_bytes", C.c_int64),
                 ("upload_seconds", C.c_double), ("scaling_seconds", C.c_double), ("device", C.c_int32),
                 ("l2_resident", C.c_int32), ("world", C.c_int32), ("local_shards", C.c_int32),
-                ("rank", C.c_int32), ("uniform_bounds", C.c_int32)]
+                ("rank", C.c_int32), ("uniform_bounds", C.c_int32),
+                ("csr_uniform_len", C.c_int32), ("csc_uniform_len", C.c_int32)]
 
 
 class ShardSpec(C.Structure):

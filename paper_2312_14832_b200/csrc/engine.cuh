@@ -15,6 +15,8 @@
 // a fixed order, so every pass stays bitwise reproducible.
 #pragma once
 
+#include <type_traits>
+
 #include "tile_spmv.cuh"
 
 namespace pdhg {
@@ -39,10 +41,12 @@ struct Layout {
   double* val = nullptr;
   int32_t s1 = 0, s2 = 0, s3 = 0;  // class bounds S | M | L | XL
   bool s_staged = false;           // class S uses seg_thread_staged_kernel
+  int l_rpc = 1;                   // class L segments per CTA (1 or 4)
+  int s_len = 0;                   // common class-S length (1,2,3,4,8) or 0
   CMat lng;                        // tile-engine view of [s3, nseg)
   int nb_s() const { return ceil_div(s1, kBlock); }
   int nb_m() const { return ceil_div(static_cast<int64_t>(s2 - s1) * 32, kBlock); }
-  int nb_l() const { return s3 - s2; }
+  int nb_l() const { return ceil_div(s3 - s2, l_rpc); }
   int nt_x() const { return nseg > s3 ? lng.ntiles : 0; }
   int parts() const { return nb_s() + nb_m() + nb_l() + 2 * nt_x(); }  // reduction slots
 };
@@ -113,6 +117,72 @@ __global__ void __launch_bounds__(kBlock) seg_thread_kernel(const int32_t* __res
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[r]);
     }
+    op.finish(s, acc, pre, red);
+  }
+  block_reduce_out<Op>(red, red_out);
+}
+
+// uniform (every class-S segment has the same length L in {1,2,3,4,8}, e.g.
+// the columns of transportation / MCF / PageRank LPs): segment s occupies
+// [s*L, (s+1)*L) of the layout (class S starts at nonzero 0), so the offsets
+// array is never read and the L entries come in with vector loads. Only Ops
+// that declare kUniform (the per-iteration step kernels) are instantiated.
+template <class T, class = void>
+struct UniformOk : std::false_type {};
+template <class T>
+struct UniformOk<T, std::void_t<decltype(T::kUniform)>> : std::integral_constant<bool, T::kUniform> {};
+
+template <int L>
+__device__ __forceinline__ void load_uniform(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                             int64_t b, int32_t (&j)[L], double (&v)[L]) {
+  if constexpr (L == 2) {
+    const int2 jj = __ldcs(reinterpret_cast<const int2*>(idx + b));
+    const double2 vv = __ldcs(reinterpret_cast<const double2*>(val + b));
+    j[0] = jj.x, j[1] = jj.y, v[0] = vv.x, v[1] = vv.y;
+  } else if constexpr (L == 4 || L == 8) {
+#pragma unroll
+    for (int q = 0; q < L / 4; ++q) {
+      const int4 jj = __ldcs(reinterpret_cast<const int4*>(idx + b) + q);
+      const double2 v0 = __ldcs(reinterpret_cast<const double2*>(val + b) + 2 * q);
+      const double2 v1 = __ldcs(reinterpret_cast<const double2*>(val + b) + 2 * q + 1);
+      j[4 * q] = jj.x, j[4 * q + 1] = jj.y, j[4 * q + 2] = jj.z, j[4 * q + 3] = jj.w;
+      v[4 * q] = v0.x, v[4 * q + 1] = v0.y, v[4 * q + 2] = v1.x, v[4 * q + 3] = v1.y;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < L; ++u) {
+      j[u] = ld_stream(idx + b + u);
+      v[u] = ld_stream(val + b + u);
+    }
+  }
+}
+
+template <class Op, int L>
+__global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_t* __restrict__ idx,
+                                                                    const double* __restrict__ val, int32_t s_end,
+                                                                    const Op op, double* __restrict__ red_out) {
+  constexpr int R = Op::kRhs;
+  constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
+  constexpr bool MX = Op::kMax;
+  double red[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) red[i] = 0.0;
+  const int s = blockIdx.x * kBlock + threadIdx.x;
+  if (s < s_end) {
+    const typename Op::Pre pre = op.prefetch(s);
+    int32_t j[L];
+    double v[L];
+    load_uniform<L>(idx, val, static_cast<int64_t>(s) * L, j, v);
+    double p[L][R];
+#pragma unroll
+    for (int u = 0; u < L; ++u) op.map(j[u], v[u], p[u]);
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+#pragma unroll
+    for (int u = 0; u < L; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[u][r]);  // storage order
     op.finish(s, acc, pre, red);
   }
   block_reduce_out<Op>(red, red_out);
@@ -259,38 +329,79 @@ __global__ void __launch_bounds__(kBlock) seg_warp_kernel(const int32_t* __restr
   block_reduce_out<Op>(red, red_out);
 }
 
-// Class L: one CTA per segment (fixed tree over the block).
-template <class Op>
+// Class L: a CTA per RPC segments, kBlock / RPC threads per segment (fixed
+// trees). RPC = 4 for moderately long segments: the 4 consecutive segments of
+// a CTA typically gather neighbouring vector entries (transportation demand
+// rows j..j+3 read x[i*T + j..j+3]), so they share L1 sectors instead of each
+// pulling its own 32-byte sector per 8-byte gather from L2.
+template <class Op, int RPC>
 __global__ void __launch_bounds__(kBlock) seg_cta_kernel(const int32_t* __restrict__ ptr,
                                                          const int32_t* __restrict__ idx,
                                                          const double* __restrict__ val, int32_t s_begin,
-                                                         const Op op, double* __restrict__ red_out) {
+                                                         int32_t s_end, const Op op, double* __restrict__ red_out) {
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   constexpr bool MX = Op::kMax;
+  constexpr int T = kBlock / RPC;  // threads per segment
+  constexpr int W = T / 32;        // warps per segment
   __shared__ double sh[kWarps][R];
   double red[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
-  const int s = s_begin + blockIdx.x;
-  const int b = ptr[s], e = ptr[s + 1];
+  const int sub = threadIdx.x / T, t = threadIdx.x % T;
+  const int s = s_begin + blockIdx.x * RPC + sub;
+  const bool own = s < s_end;
   typename Op::Pre pre{};
-  if (threadIdx.x == 0) pre = op.prefetch(s);
   double acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = 0.0;
-  strided_sum<Op, kBlock>(op, idx, val, b, e, threadIdx.x, acc);
-  block_combine<R, MX, R>(acc, sh);
-  if (threadIdx.x == 0) op.finish(s, acc, pre, red);
+  if (own) {
+    if (t == 0) pre = op.prefetch(s);
+    strided_sum<Op, T>(op, idx, val, ptr[s], ptr[s + 1], t, acc);
+  }
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    acc[r] = warp_combine<MX>(acc[r]);
+    if ((threadIdx.x & 31) == 0) sh[warp][r] = acc[r];
+  }
+  __syncthreads();
+  if (own && t == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double v = sh[sub * W][r];
+      for (int w = 1; w < W; ++w) v = combine<MX>(v, sh[sub * W + w][r]);
+      acc[r] = v;
+    }
+    op.finish(s, acc, pre, red);
+  }
   block_reduce_out<Op>(red, red_out);
 }
 
 template <class Op>
 inline void launch_thread_class(const Layout& L, const Op& op, double* red, cudaStream_t st) {
+  if constexpr (UniformOk<Op>::value) {
+    switch (L.s_len) {
+      case 1: seg_thread_uniform_kernel<Op, 1><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
+      case 2: seg_thread_uniform_kernel<Op, 2><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
+      case 3: seg_thread_uniform_kernel<Op, 3><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
+      case 4: seg_thread_uniform_kernel<Op, 4><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
+      case 8: seg_thread_uniform_kernel<Op, 8><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
+      default: break;
+    }
+  }
   if (L.s_staged)
     seg_thread_staged_kernel<Op><<<L.nb_s(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, op, red);
   else
     seg_thread_kernel<Op><<<L.nb_s(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, op, red);
+}
+
+template <class Op>
+inline void launch_cta_class(const Layout& L, const Op& op, double* red, cudaStream_t st) {
+  if (L.l_rpc == 4)
+    seg_cta_kernel<Op, 4><<<L.nb_l(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s2, L.s3, op, red);
+  else
+    seg_cta_kernel<Op, 1><<<L.nb_l(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s2, L.s3, op, red);
 }
 
 // Reduction slots of one pass: [S blocks | M blocks | L CTAs | XL tiles | XL spans].
@@ -308,7 +419,7 @@ inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, cudaStr
   if (L.s2 > L.s1)
     seg_warp_kernel<Op><<<L.nb_m(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, L.s2, op, red.at(slot, nr));
   slot += L.nb_m();
-  if (L.s3 > L.s2) seg_cta_kernel<Op><<<L.nb_l(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s2, op, red.at(slot, nr));
+  if (L.s3 > L.s2) launch_cta_class(L, op, red.at(slot, nr), st);
   slot += L.nb_l();
   if (L.nseg > L.s3) launch_tiles(L.lng, op, red.at(slot, nr), red.at(slot + L.nt_x(), nr), st);
 }
@@ -349,7 +460,7 @@ inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, const F
   if (has[1])
     seg_warp_kernel<Op><<<L.nb_m(), kBlock, 0, on[1]>>>(L.ptr, L.idx, L.val, L.s1, L.s2, op, red.at(slot, nr));
   slot += L.nb_m();
-  if (has[2]) seg_cta_kernel<Op><<<L.nb_l(), kBlock, 0, on[2]>>>(L.ptr, L.idx, L.val, L.s2, op, red.at(slot, nr));
+  if (has[2]) launch_cta_class(L, op, red.at(slot, nr), on[2]);
   slot += L.nb_l();
   if (has[3]) launch_tiles(L.lng, op, red.at(slot, nr), red.at(slot + L.nt_x(), nr), on[3]);
   k = 0;

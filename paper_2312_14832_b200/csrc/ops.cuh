@@ -114,6 +114,7 @@ struct OpPrimal {
   static constexpr int kRhs = 1, kRed = kAdapt ? 1 : 0;
   static constexpr bool kMax = false;
   static constexpr bool kL = !(kBnd & 1), kU = !(kBnd & 2);  // streamed?
+  static constexpr bool kUniform = true;                     // per-iteration: specialise
   static constexpr int kIL = 2, kIU = 2 + kL, kIB = 2 + kL + kU;  // operand slots
   struct Pre {
     double x, c, l, u, xbar, w, step;
@@ -177,6 +178,7 @@ template <bool kAdapt>
 struct OpDual {
   static constexpr int kRhs = 1, kRed = kAdapt ? 2 : 0;
   static constexpr bool kMax = false;
+  static constexpr bool kUniform = true;
   struct Pre {
     double kx, y, q, ybar, w, step;
   };

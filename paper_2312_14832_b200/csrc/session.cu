@@ -105,6 +105,9 @@ constexpr int64_t kSegWeight = 6;
 // Mean class-S segment length from which the warp-staged S kernel is used.
 constexpr double kStagedMin = 6.0;
 
+// Mean class-L segment length up to which a CTA takes 4 segments.
+constexpr double kRpc4Max = 2048.0;
+
 }  // namespace
 
 // Host mirror of the check reductions (26 doubles).
@@ -427,6 +430,10 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       k_perm_nnz<<<ew_grid(nnz_), kEw, 0, st_>>>(p0.p, seg_of.p, i0.p, v0.p, inv_seg.p, pad_other.p, ptr.p, idx.p,
                                                   val.p, nnz_);
   };
+  const char* uenv = std::getenv("PDHG_UNIFORM_S");
+  const bool uniform_s = !(uenv && uenv[0] == '0');
+  const char* rmax = std::getenv("PDHG_RPC4_MAX");
+  const double rpc4_max = rmax ? std::atof(rmax) : kRpc4Max;
   const char* smin = std::getenv("PDHG_STAGED_MIN");
   const double staged_min = smin ? std::atof(smin) : kStagedMin;
   // One layout's block slice -> shard storage (ownership moves when the
@@ -468,6 +475,41 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       Sync();
     }
     L.s_staged = L.s1 > 0 && static_cast<double>(se) >= staged_min * L.s1;
+    // Class S of one common length (and starting at nonzero 0): offsets implicit.
+    L.s_len = 0;
+    if (L.s1 > 0 && uniform_s) {
+      DArray<int> mm;
+      mm.alloc(2);
+      const int init[2] = {INT32_MAX, 0};
+      PDHG_CUDA(cudaMemcpyAsync(mm.p, init, sizeof(init), cudaMemcpyHostToDevice, st_));
+      k_len_minmax<<<ew_grid(L.s1), kEw, 0, st_>>>(L.ptr, L.s1, mm.p);
+      int h[2];
+      int32_t p0 = 1;
+      PDHG_CUDA(cudaMemcpyAsync(h, mm.p, sizeof(h), cudaMemcpyDeviceToHost, st_));
+      PDHG_CUDA(cudaMemcpyAsync(&p0, L.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+      Sync();
+      if (p0 == 0 && h[0] == h[1] && (h[0] == 1 || h[0] == 2 || h[0] == 3 || h[0] == 4 || h[0] == 8))
+        L.s_len = h[0];
+    }
+    // Class L: 4 segments per CTA when they average <= kRpc4Max nonzeros and
+    // most neighbours start gathering in the same sector (shared L1 lines).
+    L.l_rpc = 1;
+    if (L.s3 > L.s2) {
+      int32_t lb = 0, le = 0;
+      PDHG_CUDA(cudaMemcpyAsync(&lb, L.ptr + L.s2, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+      PDHG_CUDA(cudaMemcpyAsync(&le, L.ptr + L.s3, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+      Sync();
+      int adj = 0;
+      if (L.s3 - L.s2 > 1 && static_cast<double>(le - lb) <= rpc4_max * (L.s3 - L.s2)) {
+        DArray<int> cnt;
+        cnt.alloc(1);
+        PDHG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st_));
+        k_adjacent_count<<<ew_grid(L.s3 - L.s2), kEw, 0, st_>>>(L.ptr, L.idx, L.s2, L.s3, cnt.p);
+        PDHG_CUDA(cudaMemcpyAsync(&adj, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+        Sync();
+      }
+      if (4 * adj >= L.s3 - L.s2 - 1 && adj > 0) L.l_rpc = 4;  // >= 25% adjacent pairs
+    }
   };
   {
     DArray<int32_t> fptr, fidx;
@@ -1372,6 +1414,19 @@ void Session::Stats(pdhg_session_stats* s) const {
   s->local_shards = static_cast<int32_t>(shards_.size());
   s->rank = rank_;
   s->uniform_bounds = bnd_;
+  // Uniform only if every local shard's whole layout is one uniform class S.
+  auto all_uniform = [&](bool csr) {
+    int len = -1;
+    for (const Shard& h : shards_) {
+      const Layout& L = csr ? h.csr : h.csc;
+      if (L.nseg == 0) continue;
+      if (L.s1 != L.nseg || L.s_len == 0 || (len >= 0 && L.s_len != len)) return 0;
+      len = L.s_len;
+    }
+    return len > 0 ? len : 0;
+  };
+  s->csr_uniform_len = all_uniform(true);
+  s->csc_uniform_len = all_uniform(false);
 }
 
 void Session::Blocks(int64_t* row_begin, int64_t* col_begin) const {

@@ -122,6 +122,34 @@ __global__ void k_sum_packs(double* packs, int count, int stride, int n) {
   packs[i] = v;
 }
 
+// Min / max segment length over [0, nseg) (out[0] = min, out[1] = max;
+// initialise to INT32_MAX / 0).
+__global__ void k_len_minmax(const int32_t* p, int64_t nseg, int* out) {
+  int mn = INT32_MAX, mx = 0;
+  GRID_STRIDE(s, nseg) {
+    const int len = p[s + 1] - p[s];
+    mn = len < mn ? len : mn;
+    mx = len > mx ? len : mx;
+  }
+  atomicMin(out, mn);
+  atomicMax(out + 1, mx);
+}
+
+// Neighbouring segments whose first entries gather from the same 32-byte
+// sector (|first index difference| <= 3): the transportation pattern that
+// makes several segments per CTA share L1 sectors.
+__global__ void k_adjacent_count(const int32_t* p, const int32_t* idx, int32_t lo, int32_t hi, int* out) {
+  int c = 0;
+  GRID_STRIDE(s, (int64_t)(hi - lo - 1)) {
+    const int32_t a = lo + static_cast<int32_t>(s);
+    if (p[a + 1] > p[a] && p[a + 2] > p[a + 1]) {
+      const int d = idx[p[a + 1]] - idx[p[a]];
+      c += (d >= -3 && d <= 3) ? 1 : 0;
+    }
+  }
+  atomicAdd(out, c);
+}
+
 // Sort key putting longer segments first: INT32_MAX - length.
 __global__ void k_len_desc_key(const int32_t* p, int64_t nseg, int32_t* key) {
   GRID_STRIDE(s, nseg) key[s] = INT32_MAX - (p[s + 1] - p[s]);

@@ -34,9 +34,10 @@ for name in which:
     with rpdlp.Session(p, shards=sp) as s:
         st = s.stats()
         ms_p, ms_d, ms_it = s.time_kernels(256)
-        bp, bd, bi = algorithmic_bytes(p.num_rows(), p.num_vars(), p.nnz(), st.uniform_bounds)
+        bp, bd, bi = algorithmic_bytes(p.num_rows(), p.num_vars(), p.nnz(), st.uniform_bounds, st.csr_uniform_len,
+                                       st.csc_uniform_len)
         print(f"{name}: m={p.num_rows()} n={p.num_vars()} nnz={p.nnz()} gen {tg:.1f}s upload {st.upload_seconds:.3f}s "
-              f"scaling {st.scaling_seconds:.3f}s bnd {st.uniform_bounds} tiles {st.csr_tiles}/{st.csc_tiles} dev {st.device_bytes / 1e9:.2f} GB"
+              f"scaling {st.scaling_seconds:.3f}s bnd {st.uniform_bounds} ulen {st.csr_uniform_len}/{st.csc_uniform_len} tiles {st.csr_tiles}/{st.csc_tiles} dev {st.device_bytes / 1e9:.2f} GB"
               f"\n   primal {ms_p*1e3:.1f}us {bp/ms_p/1e6:.0f} GB/s | dual {ms_d*1e3:.1f}us "
               f"{bd/ms_d/1e6:.0f} GB/s | iter {ms_it*1e3:.1f}us {bi/ms_it/1e6:.0f} GB/s -> {1e3 / ms_it:.0f} it/s",
               flush=True)

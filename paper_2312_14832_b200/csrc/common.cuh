@@ -65,7 +65,7 @@ struct Scalars {
   double inner_base;  // RunningAverage weight at the start of the block
   double pw_norm;     // power iteration: norm of the current vector
   int32_t pw_zero;    // power iteration hit a zero vector
-  int32_t pad;
+  int32_t halt;       // pipelined loop: skip queued blocks until the host clears it
   double adapt_iter;  // iterations_ at the start of the block (adaptive step)
   double lb, ub;      // the common scaled bound when every column shares it
 };

@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kBlock) seg_thread_kernel(const int32_t* __res
                                                             const int32_t* __restrict__ idx,
                                                             const double* __restrict__ val, int32_t s_end,
                                                             const Op op, double* __restrict__ red_out) {
+  if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   constexpr bool MX = Op::kMax;
@@ -161,6 +162,7 @@ template <class Op, int L>
 __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_t* __restrict__ idx,
                                                                     const double* __restrict__ val, int32_t s_end,
                                                                     const Op op, double* __restrict__ red_out) {
+  if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   constexpr bool MX = Op::kMax;
@@ -203,6 +205,7 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
                                                                       const double* __restrict__ val,
                                                                       int32_t s_end, const Op op,
                                                                       double* __restrict__ red_out) {
+  if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   constexpr bool MX = Op::kMax;
@@ -306,6 +309,7 @@ __global__ void __launch_bounds__(kBlock) seg_warp_kernel(const int32_t* __restr
                                                           const int32_t* __restrict__ idx,
                                                           const double* __restrict__ val, int32_t s_begin,
                                                           int32_t s_end, const Op op, double* __restrict__ red_out) {
+  if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   constexpr bool MX = Op::kMax;
@@ -339,6 +343,7 @@ __global__ void __launch_bounds__(kBlock) seg_cta_kernel(const int32_t* __restri
                                                          const int32_t* __restrict__ idx,
                                                          const double* __restrict__ val, int32_t s_begin,
                                                          int32_t s_end, const Op op, double* __restrict__ red_out) {
+  if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   constexpr bool MX = Op::kMax;

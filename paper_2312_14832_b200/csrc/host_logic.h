@@ -9,6 +9,12 @@
 
 #include "../../include/pdhg.h"
 
+#if defined(__CUDACC__)
+#define PDHG_HD __host__ __device__
+#else
+#define PDHG_HD
+#endif
+
 namespace pdhg {
 
 // LpProblem::Validate (lp_problem.cpp:22-58): same checks, same messages.
@@ -34,22 +40,29 @@ inline void ValidateLpHost(const pdhg_lp& lp) {
 }
 
 // KktError (kkt.cpp:153-157).
-inline double KktError(double p, double d, double g, double w) {
-  return std::sqrt(w * w * p * p + d * d / (w * w) + g * g);
+// The decision helpers below are PDHG_HD: the pipelined loop evaluates them on
+// the device (csrc/decide.cuh) with the same IEEE operations (sqrt, fabs,
+// compares; no FMA on either side), hence bit-identical decisions.
+PDHG_HD inline double KktError(double p, double d, double g, double w) {
+  return sqrt(w * w * p * p + d * d / (w * w) + g * g);
 }
-inline double Kkt1(const pdhg_report& r) { return KktError(r.primal_res, r.dual_res, r.gap_abs, 1.0); }
+PDHG_HD inline double Kkt1(const pdhg_report& r) { return KktError(r.primal_res, r.dual_res, r.gap_abs, 1.0); }
 
 // CheckTermination (kkt.cpp:147-151).
-inline bool Terminated(const pdhg_report& r, double eps) {
+PDHG_HD inline bool Terminated(const pdhg_report& r, double eps) {
   return r.rel_primal <= eps && r.rel_dual <= eps && r.rel_gap <= eps;
 }
 
 // ShouldRestart (solver.cpp:178-189): sufficient decay; necessary decay with
 // no local progress; long inner loop.
+PDHG_HD inline bool ShouldRestartV(double suff, double nec, double frac, int64_t t, int64_t k, double cand,
+                                    double start, double prev) {
+  if (cand <= suff * start) return true;
+  if (cand <= nec * start && cand > prev) return true;
+  return static_cast<double>(t) >= frac * static_cast<double>(k);
+}
 inline bool ShouldRestart(const pdhg_params& p, int64_t t, int64_t k, double cand, double start, double prev) {
-  if (cand <= p.sufficient_decay * start) return true;
-  if (cand <= p.necessary_decay * start && cand > prev) return true;
-  return static_cast<double>(t) >= p.long_loop_frac * static_cast<double>(k);
+  return ShouldRestartV(p.sufficient_decay, p.necessary_decay, p.long_loop_frac, t, k, cand, start, prev);
 }
 
 // UpdatePrimalWeight (solver.cpp:191-196).
@@ -60,17 +73,17 @@ inline double UpdatePrimalWeight(double w, double dx, double dy) {
 }
 
 // ResidualReport from reduced sums (kkt.cpp:80-118).
-inline pdhg_report MakeReport(double pr2, double du2, double bound, double cx, double qy, double off, double qn,
-                              double cn) {
+PDHG_HD inline pdhg_report MakeReport(double pr2, double du2, double bound, double cx, double qy, double off,
+                                      double qn, double cn) {
   pdhg_report r{};
-  r.primal_res = std::sqrt(pr2);
-  r.dual_res = std::sqrt(du2);
+  r.primal_res = sqrt(pr2);
+  r.dual_res = sqrt(du2);
   r.primal_obj = off + cx;
   r.dual_obj = off + bound + qy;
-  r.gap_abs = std::abs(r.dual_obj - r.primal_obj);
+  r.gap_abs = fabs(r.dual_obj - r.primal_obj);
   r.rel_primal = r.primal_res / (1.0 + qn);
   r.rel_dual = r.dual_res / (1.0 + cn);
-  r.rel_gap = r.gap_abs / (1.0 + std::abs(r.dual_obj) + std::abs(r.primal_obj));
+  r.rel_gap = r.gap_abs / (1.0 + fabs(r.dual_obj) + fabs(r.primal_obj));
   return r;
 }
 

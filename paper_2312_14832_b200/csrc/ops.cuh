@@ -18,6 +18,7 @@ namespace pdhg {
 struct OpSpmv {
   static constexpr int kRhs = 1, kRed = 0;
   static constexpr bool kMax = false;
+  static constexpr bool kUniform = true;
   using Pre = Nil;
   const double* x;
   double* y;
@@ -38,6 +39,7 @@ template <bool kSumSq>
 struct OpPowerStep {
   static constexpr int kRhs = 1, kRed = kSumSq ? 1 : 0;
   static constexpr bool kMax = false;
+  static constexpr bool kUniform = true;
   using Pre = Nil;
   const double* x;
   const Scalars* sc;  // pw_norm divides the gathered operand
@@ -128,6 +130,7 @@ struct OpPrimal {
   const double* u;
   const Scalars* sc;
   int j_in_block;
+  __device__ bool skip() const { return sc->halt != 0; }  // pipelined loop: block discarded
   __device__ void map(int32_t i, double v, double (&p)[1]) const { p[0] = v * y[i]; }
   static constexpr int kOcc = 5;
   static constexpr int kOps = 3 + kL + kU;
@@ -192,6 +195,7 @@ struct OpDual {
   RowKind rk;  // equality rows (permuted order)
   const Scalars* sc;
   int j_in_block;
+  __device__ bool skip() const { return sc->halt != 0; }
   __device__ void map(int32_t j, double v, double (&p)[1]) const { p[0] = v * xn[j]; }
   static constexpr int kOcc = 5;
   static constexpr int kOps = 4;
@@ -249,6 +253,7 @@ constexpr int kColRed = 2 * kColPer + 1;
 struct OpCheckRow {
   static constexpr int kRhs = 1, kRed = kRowRed;
   static constexpr bool kMax = false;
+  static constexpr bool kUniform = true;
   struct Pre {
     double kx, y, yb, y0, qs, qo, r;
   };
@@ -262,6 +267,8 @@ struct OpCheckRow {
   const double* q_o;
   const double* rs;
   RowKind rk;  // equality rows (permuted order)
+  const Scalars* sc;  // null outside the pipelined loop
+  __device__ bool skip() const { return sc && sc->halt != 0; }
   __device__ void map(int32_t j, double v, double (&p)[1]) const { p[0] = v * xbar[j]; }
   static constexpr int kOcc = 2;
   static constexpr int kOps = 7;
@@ -300,9 +307,13 @@ struct OpCheckRow {
 // term, c'x for both points and both spaces; dx for the primal weight
 // (solver.cpp:433-436); finite test of x (solver.cpp:391). Two gathered
 // operands: K^T [y_cur, ybar] from one pass over the matrix.
+// kUB: every column shares its scaled and original bounds (x >= 0: l_s = l_o = 0,
+// u_s = u_o = inf), carried in lb/ub instead of four streamed arrays.
+template <bool kUB = false>
 struct OpCheckCol {
   static constexpr int kRhs = 2, kRed = kColRed;
   static constexpr bool kMax = false;
+  static constexpr bool kUniform = true;
   struct Pre {
     double x, xb, x0, cS, lS, uS, cO, lO, uO, f;
   };
@@ -318,22 +329,36 @@ struct OpCheckCol {
   const double* l_o;
   const double* u_o;
   const double* cs;
+  const Scalars* sc;  // null outside the pipelined loop
+  double lb = 0.0, ub = 0.0;  // kUB: the common bounds (both spaces)
+  __device__ bool skip() const { return sc && sc->halt != 0; }
   __device__ void map(int32_t i, double v, double (&p)[2]) const {
     p[0] = v * y_cur[i];
     p[1] = v * ybar[i];
   }
   static constexpr int kOcc = 2;
-  static constexpr int kOps = 10;
+  static constexpr int kOps = kUB ? 6 : 10;
   __device__ const double* operand(int k) const {
-    const double* a[10] = {x_cur, xbar, x_start, c_s, l_s, u_s, c_o, l_o, u_o, cs};
-    return a[k];
+    if constexpr (kUB) {
+      const double* a[6] = {x_cur, xbar, x_start, c_s, c_o, cs};
+      return a[k];
+    } else {
+      const double* a[10] = {x_cur, xbar, x_start, c_s, l_s, u_s, c_o, l_o, u_o, cs};
+      return a[k];
+    }
   }
   __device__ Pre staged(int32_t, const double* st, int ld) const {
-    return {st[0], st[ld], st[2 * ld], st[3 * ld], st[4 * ld], st[5 * ld], st[6 * ld], st[7 * ld], st[8 * ld],
-            st[9 * ld]};
+    if constexpr (kUB)
+      return {st[0], st[ld], st[2 * ld], st[3 * ld], lb, ub, st[4 * ld], lb, ub, st[5 * ld]};
+    else
+      return {st[0], st[ld], st[2 * ld], st[3 * ld], st[4 * ld], st[5 * ld], st[6 * ld], st[7 * ld], st[8 * ld],
+              st[9 * ld]};
   }
   __device__ Pre prefetch(int32_t s) const {
-    return {x_cur[s], xbar[s], x_start[s], c_s[s], l_s[s], u_s[s], c_o[s], l_o[s], u_o[s], cs[s]};
+    if constexpr (kUB)
+      return {x_cur[s], xbar[s], x_start[s], c_s[s], lb, ub, c_o[s], lb, ub, cs[s]};
+    else
+      return {x_cur[s], xbar[s], x_start[s], c_s[s], l_s[s], u_s[s], c_o[s], l_o[s], u_o[s], cs[s]};
   }
   __device__ void finish(int32_t s, const double (&a)[2], const Pre& p, double* red) const {
     const int cls = bound_class(p.lO, p.uO);
@@ -367,6 +392,7 @@ struct OpCheckCol {
 struct OpLambda {
   static constexpr int kRhs = 1, kRed = 0;
   static constexpr bool kMax = false;
+  static constexpr bool kUniform = true;
   struct Pre {
     double c, l, u, f;
   };

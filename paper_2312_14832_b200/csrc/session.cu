@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <limits>
 #include <random>
 
@@ -28,6 +29,7 @@
 #include "normal_rng.h"
 #include "ops.cuh"
 #include "setup_kernels.cuh"
+#include "decide.cuh"
 
 namespace pdhg {
 
@@ -139,88 +141,100 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
   } else {
     comm_ = std::make_unique<LocalComm>();
   }
+  n_ = lp.n;
+  if (n_ > 0) start_ = std::thread([this, seed = prm.seed] { DrawStart(seed); });
   shards_ = std::vector<Shard>(spec.local);
   for (int k = 0; k < spec.local; ++k) shards_[k].block = spec.local == 1 ? rank_ : k;
   m1_ = lp.a.rows;
   m2_ = lp.g.rows;
   m_ = m1_ + m2_;
-  n_ = lp.n;
   offset_ = lp.objective_offset;
-  const double t0 = now_s();
-  {
-    DArray<int32_t> ptr0, idx0;
-    DArray<double> val0;
-    Upload(lp, ptr0, idx0, val0);
-    Permute(ptr0, idx0, val0);
+  try {
+    const double t0 = now_s();
+    {
+      DArray<int32_t> ptr0, idx0;
+      DArray<double> val0;
+      Upload(lp, ptr0, idx0, val0);
+      Permute(ptr0, idx0, val0);
+    }
+    for (Shard& h : shards_) {
+      PartitionLong(h.csr, h.csr_st);
+      PartitionLong(h.csc, h.csc_st);
+    }
+    // Original-space problem vectors into padded order.
+    c_o_.alloc(np_, &arena_);
+    l_o_.alloc(np_, &arena_);
+    u_o_.alloc(np_, &arena_);
+    q_o_.alloc(mp_, &arena_);
+    ToInternal(lp.c, pad_c_, c_o_.p, n_, np_);
+    ToInternal(lp.l, pad_c_, l_o_.p, n_, np_);
+    ToInternal(lp.u, pad_c_, u_o_.p, n_, np_);
+    {
+      std::vector<double> q(static_cast<size_t>(m_));
+      if (m1_) std::memcpy(q.data(), lp.b, m1_ * sizeof(double));
+      if (m2_) std::memcpy(q.data() + m1_, lp.h, m2_ * sizeof(double));
+      ToInternal(q.data(), pad_r_, q_o_.p, m_, mp_);
+    }
+    Sync();
+    upload_s_ = now_s() - t0;
+    for (int p = 0; p < 2; ++p) {
+      x_[p].alloc(np_, &arena_);
+      y_[p].alloc(mp_, &arena_);
+      kx_[p].alloc(mp_, &arena_);
+    }
+    xbar_.alloc(np_, &arena_);
+    xstart_.alloc(np_, &arena_);
+    xbest_.alloc(np_, &arena_);
+    nvec_.alloc(np_, &arena_);
+    ybar_.alloc(mp_, &arena_);
+    ystart_.alloc(mp_, &arena_);
+    ybest_.alloc(mp_, &arena_);
+    kxavg_.alloc(mp_, &arena_);
+    // Padding entries are never addressed by an index but travel with the
+    // all-gathers: keep them zero.
+    for (DArray<double>* v : {&x_[0], &x_[1], &xbar_, &xstart_, &xbest_, &nvec_, &y_[0], &y_[1], &ybar_, &ystart_,
+                              &ybest_, &kx_[0], &kx_[1], &kxavg_})
+      if (v->n) PDHG_CUDA(cudaMemsetAsync(v->p, 0, v->n * sizeof(double), st_));
+    scal_.alloc(1, &arena_);
+    const int nred = std::max(kRowRed, kColRed);
+    for (Shard& h : shards_) {
+      h.red[0].alloc(static_cast<size_t>(std::max(h.csr.parts(), 1)) * nred, &arena_);
+      h.red[1].alloc(static_cast<size_t>(std::max(h.csc.parts(), 1)) * nred, &arena_);
+    }
+    red_out_.alloc(static_cast<size_t>(kPack) * shards_.size(), &arena_);
+    const double t1 = now_s();
+    ComputeScaling(prm);
+    Sync();
+    scaling_s_ = now_s() - t1;
+    DeviceNorms();
+    UniformBounds();
+    const double iter_bytes = (24.0 * nnz_ + 68.0 * (m_ + n_)) / world_;
+    l2_resident_ = iter_bytes < 100e6;
+    Sync();
+    if (std::getenv("PDHG_TRACE"))
+      std::fprintf(stderr, "[pdhg] session %.4fs: upload+csc+permute+partition %.4fs | scaling %.4fs | %.2f GB\n",
+                   now_s() - t0, upload_s_, scaling_s_, arena_.bytes / 1e9);
+  } catch (...) {
+    if (start_.joinable()) start_.join();
+    throw;
   }
-  for (Shard& h : shards_) {
-    PartitionLong(h.csr, h.csr_st);
-    PartitionLong(h.csc, h.csc_st);
-  }
-  // Original-space problem vectors into padded order.
-  c_o_.alloc(np_, &arena_);
-  l_o_.alloc(np_, &arena_);
-  u_o_.alloc(np_, &arena_);
-  q_o_.alloc(mp_, &arena_);
-  ToInternal(lp.c, pad_c_, c_o_.p, n_, np_);
-  ToInternal(lp.l, pad_c_, l_o_.p, n_, np_);
-  ToInternal(lp.u, pad_c_, u_o_.p, n_, np_);
-  {
-    std::vector<double> q(static_cast<size_t>(m_));
-    if (m1_) std::memcpy(q.data(), lp.b, m1_ * sizeof(double));
-    if (m2_) std::memcpy(q.data() + m1_, lp.h, m2_ * sizeof(double));
-    ToInternal(q.data(), pad_r_, q_o_.p, m_, mp_);
-  }
-  Sync();
-  upload_s_ = now_s() - t0;
-  for (int p = 0; p < 2; ++p) {
-    x_[p].alloc(np_, &arena_);
-    y_[p].alloc(mp_, &arena_);
-    kx_[p].alloc(mp_, &arena_);
-  }
-  xbar_.alloc(np_, &arena_);
-  xstart_.alloc(np_, &arena_);
-  xbest_.alloc(np_, &arena_);
-  nvec_.alloc(np_, &arena_);
-  ybar_.alloc(mp_, &arena_);
-  ystart_.alloc(mp_, &arena_);
-  ybest_.alloc(mp_, &arena_);
-  kxavg_.alloc(mp_, &arena_);
-  // Padding entries are never addressed by an index but travel with the
-  // all-gathers: keep them zero.
-  for (DArray<double>* v : {&x_[0], &x_[1], &xbar_, &xstart_, &xbest_, &nvec_, &y_[0], &y_[1], &ybar_, &ystart_,
-                            &ybest_, &kx_[0], &kx_[1], &kxavg_})
-    if (v->n) PDHG_CUDA(cudaMemsetAsync(v->p, 0, v->n * sizeof(double), st_));
-  scal_.alloc(1, &arena_);
-  const int nred = std::max(kRowRed, kColRed);
-  for (Shard& h : shards_) {
-    h.red[0].alloc(static_cast<size_t>(std::max(h.csr.parts(), 1)) * nred, &arena_);
-    h.red[1].alloc(static_cast<size_t>(std::max(h.csc.parts(), 1)) * nred, &arena_);
-  }
-  red_out_.alloc(static_cast<size_t>(kPack) * shards_.size(), &arena_);
-  const double t1 = now_s();
-  ComputeScaling(prm);
-  Sync();
-  scaling_s_ = now_s() - t1;
-  DeviceNorms();
-  UniformBounds();
-  const double iter_bytes = (24.0 * nnz_ + 68.0 * (m_ + n_)) / world_;
-  l2_resident_ = iter_bytes < 100e6;
-  Sync();
-  if (std::getenv("PDHG_TRACE"))
-    std::fprintf(stderr, "[pdhg] session %.4fs: upload+csc+permute+partition %.4fs | scaling %.4fs | %.2f GB\n",
-                 now_s() - t0, upload_s_, scaling_s_, arena_.bytes / 1e9);
 }
 
 Session::~Session() {
+  if (start_.joinable()) start_.join();
   cudaSetDevice(device_);
   for (cudaEvent_t e : ev_)
     if (e) cudaEventDestroy(e);
   for (Graph& g : graphs_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (Graph& g : blocks_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (power_graph_) cudaGraphExecDestroy(power_graph_);
   if (host_red_) cudaFreeHost(host_red_);
   if (hstage_) cudaFreeHost(hstage_);
+  if (hstate_) cudaFreeHost(hstate_);
+  for (cudaEvent_t e : pev_)
+    if (e) cudaEventDestroy(e);
   comm_.reset();
   if (fork_.fork) cudaEventDestroy(fork_.fork);
   for (int k = 0; k < 3; ++k) {
@@ -722,6 +736,21 @@ void Session::UniformBounds() {
   PDHG_CUDA(cudaMemcpyAsync(&ub_, u_s_.p + p0, sizeof(double), cudaMemcpyDeviceToHost, st_));
   Sync();
   bnd_ = (h[0] ? 0 : 1) | (h[1] ? 0 : 2);
+  // The check may drop all four bound arrays when the original bounds are
+  // the same common values as the scaled ones (l in {0, -inf}, u in {0, +inf}).
+  bnd_all_ = false;
+  if (bnd_ == 3) {
+    PDHG_CUDA(cudaMemsetAsync(diff.p, 0, 2 * sizeof(int), st_));
+    k_uniform<<<ew_grid(n_), kEw, 0, st_>>>(l_o_.p, pad_c_.p, n_, diff.p);
+    k_uniform<<<ew_grid(n_), kEw, 0, st_>>>(u_o_.p, pad_c_.p, n_, diff.p + 1);
+    double lo = 0.0, uo = 0.0;
+    PDHG_CUDA(cudaMemcpyAsync(h, diff.p, sizeof(h), cudaMemcpyDeviceToHost, st_));
+    PDHG_CUDA(cudaMemcpyAsync(&lo, l_o_.p + p0, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    PDHG_CUDA(cudaMemcpyAsync(&uo, u_o_.p + p0, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    Sync();
+    bnd_all_ = !h[0] && !h[1] && std::memcmp(&lo, &lb_, sizeof(double)) == 0 &&
+               std::memcmp(&uo, &ub_, sizeof(double)) == 0;
+  }
 }
 
 // ||c||, ||q|| in both spaces (kkt.cpp:45-56), deterministic device sums over
@@ -759,6 +788,9 @@ double* Session::HostStage() {
   const size_t need = static_cast<size_t>(std::max<int64_t>(std::max(m_, n_), 1));
   if (hstage_n_ < need) {
     if (hstage_) cudaFreeHost(hstage_);
+  if (hstate_) cudaFreeHost(hstate_);
+  for (cudaEvent_t e : pev_)
+    if (e) cudaEventDestroy(e);
     hstage_ = nullptr;
     PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hstage_), need * sizeof(double)));
     hstage_n_ = need;
@@ -835,17 +867,19 @@ void Session::LaunchStep(int parity, int j, bool adapt) {
   if (adapt) {
     for (size_t k = 0; k < shards_.size(); ++k) {
       Shard& h = shards_[k];
-      k_adapt_sum<<<1, kBlock, 0, st_>>>(h.red[1].p, h.csc.parts(), h.red[0].p, h.csr.parts(), red_out_.p + k * kPack);
+      k_adapt_sum<<<1, kBlock, 0, st_>>>(h.red[1].p, h.csc.parts(), h.red[0].p, h.csr.parts(), red_out_.p + k * kPack,
+                                         scal_.p);
     }
-    SumPacks(3);
+    SumPacks(3, scal_.p);
     k_adapt_apply<<<1, 1, 0, st_>>>(red_out_.p, scal_.p, j);
     launches_ += static_cast<int64_t>(shards_.size()) + 1 + (shards_.size() > 1);
   }
 }
 
 // Shard packs -> pack 0 (fixed shard order), then the sum over ranks.
-void Session::SumPacks(int n) {
-  if (shards_.size() > 1) k_sum_packs<<<1, kPack, 0, st_>>>(red_out_.p, static_cast<int>(shards_.size()), kPack, n);
+void Session::SumPacks(int n, const Scalars* guard) {
+  if (shards_.size() > 1)
+    k_sum_packs<<<1, kPack, 0, st_>>>(red_out_.p, static_cast<int>(shards_.size()), kPack, n, guard);
   comm_->AllReduceSum(red_out_.p, n, st_);
 }
 
@@ -882,27 +916,86 @@ void Session::RunSteps(int parity, int count, bool adapt) {
   check_launch("pdhg steps");
 }
 
+// Pipelined loop: one captured graph per (length, parity, adapt, check,
+// slot) holding the block's steps, the counter advance and -- at check
+// iterations -- the check passes, k_decide, the best copy, the halt settle
+// and the D2H of the decision state into pinned slot `slot`.
+void Session::RunBlock(int parity, int count, bool adapt, bool check, int slot) {
+  const int key_par = parity + 2 * (check ? 1 + slot : 0);
+  Graph* g = nullptr;
+  for (Graph& gg : blocks_)
+    if (gg.steps == count && gg.parity == key_par && gg.adapt == adapt) g = &gg;
+  const int pa = (parity + count) & 1;
+  auto body = [&] {
+    for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
+    k_advance<<<1, 1, 0, st_>>>(scal_.p, dstate_.p, count);
+    if (check) {
+      LaunchCheck(x_[pa].p, y_[pa].p, xbar_.p, ybar_.p, kx_[pa].p, scal_.p);
+      k_decide<<<1, 1, 0, st_>>>(red_out_.p, scal_.p, dstate_.p);
+      k_copy_best<<<ew_grid(np_ + mp_), kEw, 0, st_>>>(scal_.p, dstate_.p, x_[pa].p, xbar_.p, xbest_.p, np_,
+                                                        y_[pa].p, ybar_.p, ybest_.p, mp_);
+      k_settle<<<1, 1, 0, st_>>>(scal_.p);
+      PDHG_CUDA(cudaMemcpyAsync(hstate_ + slot, dstate_.p, sizeof(DecideState), cudaMemcpyDeviceToHost, st_));
+    }
+  };
+  const int64_t before = launches_;
+  if (!g) {
+    cudaGraph_t graph;
+    PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    body();
+    PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
+    Graph ng;
+    ng.steps = count;
+    ng.parity = key_par;
+    ng.adapt = adapt;
+    PDHG_CUDA(cudaGraphInstantiate(&ng.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    blocks_.push_back(ng);
+    g = &blocks_.back();
+  }
+  launches_ = before;
+  const int64_t per = launches_csc() + launches_csr() +
+                      (adapt ? static_cast<int64_t>(shards_.size()) + 1 + (shards_.size() > 1) : 0);
+  launches_ += static_cast<int64_t>(count) * per + 1;
+  if (check)
+    launches_ += launches_csr() + launches_csc() + static_cast<int64_t>(shards_.size()) + (shards_.size() > 1) + 3;
+  PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
+  check_launch("pdhg block");
+}
+
 // The check (solver.cpp:390-428) as two matrix passes per shard: the row
 // side gathers x_bar (K x_bar), the column side gathers [y, y_bar]. Both
 // gathered operands are all-gathered first; the 26 sums are reduced per
 // shard, over local shards and over ranks.
-void Session::LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx) {
+void Session::LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx,
+                          const Scalars* guard) {
   if (xb != x) GatherX(const_cast<double*>(xb));
   if (yb != y) GatherY(const_cast<double*>(yb));
-  launches_ += launches_csr() + launches_csc() + 2 * static_cast<int64_t>(shards_.size()) + (shards_.size() > 1);
+  launches_ += launches_csr() + launches_csc() + static_cast<int64_t>(shards_.size()) + (shards_.size() > 1);
   for (size_t k = 0; k < shards_.size(); ++k) {
     Shard& h = shards_[k];
     const int64_t r = h.roff, c = h.coff;
-    OpCheckRow row{xb, kxavg_.p + r, kx + r, y + r, yb + r, ystart_.p + r, q_s_.p + r, q_o_.p + r, rs_.p + r, h.rk};
+    OpCheckRow row{xb, kxavg_.p + r, kx + r, y + r, yb + r, ystart_.p + r, q_s_.p + r, q_o_.p + r, rs_.p + r, h.rk,
+                   guard};
     run_pass(h.csr, row, RedSlots{h.red[0].p}, fork_);
-    OpCheckCol col{y, yb, x + c, xb + c, xstart_.p + c, c_s_.p + c, l_s_.p + c, u_s_.p + c, c_o_.p + c,
-                   l_o_.p + c, u_o_.p + c, cs_.p + c};
-    run_pass(h.csc, col, RedSlots{h.red[1].p}, fork_);
+    if (bnd_all_) {
+      OpCheckCol<true> col{y, yb, x + c, xb + c, xstart_.p + c, c_s_.p + c, l_s_.p + c, u_s_.p + c, c_o_.p + c,
+                           l_o_.p + c, u_o_.p + c, cs_.p + c, guard, lb_, ub_};
+      run_pass(h.csc, col, RedSlots{h.red[1].p}, fork_);
+    } else {
+      OpCheckCol<false> col{y, yb, x + c, xb + c, xstart_.p + c, c_s_.p + c, l_s_.p + c, u_s_.p + c, c_o_.p + c,
+                            l_o_.p + c, u_o_.p + c, cs_.p + c, guard};
+      run_pass(h.csc, col, RedSlots{h.red[1].p}, fork_);
+    }
     double* pk = red_out_.p + k * kPack;
-    k_reduce_tiles<<<kRowRed, kBlock, 0, st_>>>(h.red[0].p, nullptr, h.csr.parts(), kRowRed, pk);
-    k_reduce_tiles<<<kColRed, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), kColRed, pk + kRowRed);
+    if (guard)
+      k_reduce_two_guarded<<<kRowRed + kColRed, kBlock, 0, st_>>>(guard, h.red[0].p, h.csr.parts(), kRowRed,
+                                                                  h.red[1].p, h.csc.parts(), kColRed, pk);
+    else
+      k_reduce_two<<<kRowRed + kColRed, kBlock, 0, st_>>>(h.red[0].p, h.csr.parts(), kRowRed, h.red[1].p,
+                                                          h.csc.parts(), kColRed, pk);
   }
-  SumPacks(kRowRed + kColRed);
+  SumPacks(kRowRed + kColRed, guard);
   check_launch("check");
 }
 
@@ -1006,6 +1099,174 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   } else {
     record_best(0, o_cur);
     last_rep = o_cur;
+  }
+
+  // ---- Pipelined loop (one process, no NCCL): the next block is queued
+  // before the host looks at the previous check; decisions run on the
+  // device (decide.cuh), the host only steps in for restarts, termination,
+  // limits and the observer. Identical trajectory to the synchronous loop.
+  const char* penv = std::getenv("PDHG_PIPELINE");
+  const bool pipelined = !finished && !nccl() && !(penv && penv[0] == '0');
+  if (pipelined) {
+    DecideState ds{};
+    ds.eps = prm.eps;
+    ds.suff = prm.sufficient_decay;
+    ds.nec = prm.necessary_decay;
+    ds.frac = prm.long_loop_frac;
+    ds.offset = offset_;
+    ds.qn_s = q_norm_s_;
+    ds.cn_s = c_norm_s_;
+    ds.qn_o = q_norm_o_;
+    ds.cn_o = c_norm_o_;
+    ds.restart_enabled = prm.restart_enabled;
+    ds.kkt_start = kkt_start;
+    ds.kkt_prev = kkt_prev;
+    ds.best_k1 = best_k1;
+    ds.have_best = have_best;
+    ds.checks = 0;
+    ds.best_from = -1;
+    ds.best_rep = best_rep;
+    ds.last_rep = last_rep;
+    if (!dstate_.p) dstate_.alloc(1, &arena_);
+    if (!hstate_) PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hstate_), 2 * sizeof(DecideState)));
+    if (!pev_[0])
+      for (cudaEvent_t& e : pev_) PDHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    sc.halt = 0;
+    push_scalars();
+    PDHG_CUDA(cudaMemcpyAsync(dstate_.p, &ds, sizeof(DecideState), cudaMemcpyHostToDevice, st_));
+    struct Pend {
+      int64_t count, iters_after;
+      int par_after, slot, id;
+      bool check;
+    };
+    std::deque<Pend> q;
+    int64_t it_enq = 0;
+    int par_enq = par, next_id = 0, checks_base = 0;
+    bool stop_enq = false;
+    int limit_status = PDHG_ITER_LIMIT;
+    int hslot = 0;
+    while (true) {
+      while (!stop_enq && q.size() < 2) {
+        if (it_enq >= prm.iter_limit) {
+          stop_enq = true;
+          limit_status = PDHG_ITER_LIMIT;
+          break;
+        }
+        if (secs() >= prm.time_limit) {
+          stop_enq = true;
+          limit_status = PDHG_TIME_LIMIT;
+          break;
+        }
+        const int64_t count = std::min<int64_t>(prm.check_every - (it_enq % prm.check_every), prm.iter_limit - it_enq);
+        if (adapt) {
+          sc.adapt_iter = static_cast<double>(it_enq);
+          PDHG_CUDA(cudaMemcpyAsync(&scal_.p->adapt_iter, &sc.adapt_iter, sizeof(double), cudaMemcpyHostToDevice,
+                                    st_));
+        }
+        Pend pd{count, it_enq + count, static_cast<int>((par_enq + count) & 1), hslot, -1, false};
+        pd.check = pd.iters_after % prm.check_every == 0;
+        if (pd.check) pd.id = next_id++;
+        RunBlock(par_enq, static_cast<int>(count), adapt, pd.check, hslot);
+        PDHG_CUDA(cudaEventRecord(pev_[hslot], st_));
+        hslot ^= 1;
+        q.push_back(pd);
+        it_enq = pd.iters_after;
+        par_enq = pd.par_after;
+      }
+      if (q.empty()) {
+        status = limit_status;
+        break;
+      }
+      const Pend pd = q.front();
+      q.pop_front();
+      const double tc0 = secs();
+      PDHG_CUDA(cudaEventSynchronize(pev_[pd.slot]));
+      iters = pd.iters_after;
+      inner += pd.count;
+      par = pd.par_after;
+      sc.inner_base += static_cast<double>(pd.count);
+      if (!pd.check) continue;
+      ++nchecks;
+      t_checks += secs() - tc0;
+      const DecideState& h = hstate_[pd.slot];
+      if (h.checks != pd.id + 1 + checks_base)
+        throw Error(PDHG_CUDA_ERROR, "pipelined loop: check skipped unexpectedly");
+      have_best = h.have_best != 0;
+      best_k1 = h.best_k1;
+      best_rep = h.best_rep;
+      last_rep = h.last_rep;
+      if (adapt) sc.eta = h.eta;
+      if (h.action == kNonFinite)
+        throw Error(PDHG_NUMERICAL_FAILURE, "non-finite iterate at iteration " + std::to_string(iters));
+      if (h.action == kOptimalCur || h.action == kOptimalAvg) {
+        status = PDHG_OPTIMAL;  // best copied on the device; queued block skipped
+        break;
+      }
+      pdhg_eval_info info{};
+      info.iteration = iters;
+      info.inner_iteration = inner;
+      info.restarts = restarts;
+      info.omega = sc.omega;
+      info.eta = sc.eta;
+      info.kkt_candidate = h.kkt_cand;
+      info.kkt_loop_start = kkt_start;
+      info.candidate_is_current = h.take_cur;
+      info.original_report = last_rep;
+      info.seconds = secs();
+      if (h.action == kRestart) {
+        // Queued blocks were skipped: requeue from here after the restart.
+        for (const Pend& dropped : q)
+          if (dropped.check) --checks_base;  // ids handed out to skipped checks
+        q.clear();
+        it_enq = iters;
+        par_enq = par;
+        stop_enq = false;
+        info.restarted = 1;
+        // Restart (solver.cpp:430-446), as in the synchronous loop.
+        const bool take_cur = h.take_cur != 0;
+        const pdhg_report& ps = take_cur ? h.s_cur : h.s_avg;
+        // dx, dy from the check pack (still in red_out_: nothing ran after it).
+        double pack[kRowRed + kColRed];
+        PDHG_CUDA(cudaMemcpyAsync(pack, red_out_.p, sizeof(pack), cudaMemcpyDeviceToHost, st_));
+        Sync();
+        const int P = take_cur ? 0 : 1;
+        const double dx = std::sqrt(pack[kRowRed + P * kColPer + kDx2]);
+        const double dy = std::sqrt(pack[P * kRowPer + kDy2]);
+        sc.omega = UpdatePrimalWeight(sc.omega, dx, dy);
+        if (!take_cur) {
+          Copy(x_[par].p, xbar_.p, np_);
+          Copy(y_[par].p, ybar_.p, mp_);
+          Copy(kx_[par].p, kxavg_.p, mp_);
+        }
+        start_loop(ps);
+        ++restarts;
+        sc.halt = 0;
+        push_scalars();
+        DecideState reset = h;
+        reset.kkt_start = kkt_start;
+        reset.kkt_prev = kkt_prev;
+        reset.inner = 0;
+        reset.iters = iters;
+        PDHG_CUDA(cudaMemcpyAsync(dstate_.p, &reset, sizeof(DecideState), cudaMemcpyHostToDevice, st_));
+      } else {
+        kkt_prev = h.kkt_cand;
+      }
+      if (prm.log_every > 0 && (info.iteration - last_log >= prm.log_every || info.iteration == 0)) {
+        last_log = info.iteration;
+        std::printf("iter=%lld time=%.3f rel_primal=%.3e rel_dual=%.3e rel_gap=%.3e omega=%.3e restarts=%lld\n",
+                    (long long)info.iteration, info.seconds, info.original_report.rel_primal,
+                    info.original_report.rel_dual, info.original_report.rel_gap, info.omega,
+                    (long long)info.restarts);
+      }
+      if (cb && cb(&info, user) != 0) {
+        Sync();
+        throw Error(PDHG_ABORTED, "aborted by observer");
+      }
+    }
+    Sync();  // queued (skipped) blocks drain
+    sc.halt = 0;
+    push_scalars();
+    finished = true;
   }
 
   // Time limit: one clock decides for every rank (rank 0's, shipped in the
@@ -1178,11 +1439,14 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 double Session::OpNorm(int iters, uint64_t seed) {
   PDHG_CUDA(cudaSetDevice(device_));
   if (nnz_ == 0) return 0.0;
+  // Start vector (solver.cpp:88-97): drawn on a host thread while the
+  // session was being built (upload, CSC, scaling) for the seed the session
+  // was created with; another seed is drawn here.
+  if (start_.joinable()) start_.join();
+  if (start_seed_ != seed || start_vec_.size() != static_cast<size_t>(n_)) DrawStart(seed);
   double* v = HostStage();
-  NormalVector(seed, n_, v, 0);  // == std::normal_distribution draws, all host threads
-  double acc = 0.0;
-  for (int64_t j = 0; j < n_; ++j) acc += v[j] * v[j];
-  double vnorm = std::sqrt(acc);
+  std::memcpy(v, start_vec_.data(), n_ * sizeof(double));
+  double vnorm = start_norm_;
   if (vnorm == 0.0) {
     v[0] = 1.0;
     vnorm = 1.0;
@@ -1240,6 +1504,20 @@ double Session::OpNorm(int iters, uint64_t seed) {
   Sync();
   if (hs.pw_zero) return 0.0;
   return std::sqrt(sum);
+}
+
+// n draws of std::normal_distribution(0,1) over std::mt19937_64(seed) and
+// the sequential sum of squares (solver.cpp:88-97). The libstdc++ draw is
+// faster than the bit-identical threaded replica (normal_rng.h) on these
+// hosts -- the engine itself is the serial part -- so the session overlaps
+// it with setup instead.
+void Session::DrawStart(uint64_t seed) {
+  start_vec_.resize(static_cast<size_t>(n_));
+  NormalVectorSequential(seed, n_, start_vec_.data());
+  double acc = 0.0;
+  for (int64_t j = 0; j < n_; ++j) acc += start_vec_[j] * start_vec_[j];
+  start_norm_ = std::sqrt(acc);
+  start_seed_ = seed;
 }
 
 // ============================================================ kernel probes

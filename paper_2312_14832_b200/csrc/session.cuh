@@ -13,6 +13,7 @@
 #include <chrono>
 #include <functional>
 #include <memory>
+#include <thread>
 #include <vector>
 
 #include "../../include/pdhg.h"
@@ -22,7 +23,8 @@
 
 namespace pdhg {
 
-struct CheckOut;  // host mirror of the check reductions
+struct CheckOut;     // host mirror of the check reductions
+struct DecideState;  // device-side check decisions (decide.cuh)
 
 // How K is distributed (pdhg_shard_spec in include/pdhg.h).
 struct ShardSpec {
@@ -89,10 +91,13 @@ class Session {
   void PrimalPass(Shard& h, int a, int b, int j);
   void LaunchPrimal(Shard& h, int a, int b, int j, bool adapt);
   void UniformBounds();
+  void DrawStart(uint64_t seed);
   void RunSteps(int parity, int count, bool adapt);
-  void LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx);
+  void RunBlock(int parity, int count, bool adapt, bool check, int slot);
+  void LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx,
+                   const Scalars* guard = nullptr);
   void ReadCheck(CheckOut* out);
-  void SumPacks(int n);  // red_out_ shard packs -> red_out_[0..n), all ranks
+  void SumPacks(int n, const Scalars* guard = nullptr);  // shard packs -> red_out_[0..n), all ranks
   void Copy(double* dst, const double* src, size_t n);
   void ToInternal(const double* host, const DArray<int32_t>& pad, double* dev, int64_t n, int64_t padded);
   void ToHost(const double* dev, const double* scale, const DArray<int32_t>& pad, double* host, int64_t n);
@@ -131,6 +136,7 @@ class Session {
   DArray<double> q_s_, q_o_, rs_;                          // mp_
   double c_norm_s_ = 0, q_norm_s_ = 0, c_norm_o_ = 0, q_norm_o_ = 0;
   int bnd_ = 0;               // uniform-bound bits (UniformBounds)
+  bool bnd_all_ = false;      // original bounds equal the common scaled ones too
   double lb_ = 0.0, ub_ = 0.0;
 
   // Iterates (ping-pong x/y/kx), averages, loop start, best, scratch.
@@ -143,7 +149,19 @@ class Session {
   double* hstage_ = nullptr;    // max(m, n) pinned host staging
   size_t hstage_n_ = 0;
 
+  // Power-iteration start vector, drawn on a host thread during setup.
+  std::thread start_;
+  std::vector<double> start_vec_;
+  uint64_t start_seed_ = ~uint64_t(0);
+  double start_norm_ = 0.0;
+
+  // Pipelined loop: device decision state, its pinned host mirrors, events.
+  DArray<DecideState> dstate_;
+  DecideState* hstate_ = nullptr;
+  cudaEvent_t pev_[2] = {nullptr, nullptr};
+
   std::vector<Graph> graphs_;
+  std::vector<Graph> blocks_;  // pipelined-loop block graphs
   cudaGraphExec_t power_graph_ = nullptr;  // EstimateOpNorm steps (OpNorm)
   int power_iters_ = 0;
   DArray<char> flush_;

@@ -114,7 +114,8 @@ __global__ void k_rebase(const int32_t* ptr, int64_t nseg, int32_t* out) {
 }
 
 // Sum of `count` reduction packs (fixed shard order) into pack 0.
-__global__ void k_sum_packs(double* packs, int count, int stride, int n) {
+__global__ void k_sum_packs(double* packs, int count, int stride, int n, const Scalars* guard) {
+  if (guard && guard->halt) return;
   const int i = threadIdx.x;
   if (i >= n) return;
   double v = packs[i];
@@ -135,15 +136,18 @@ __global__ void k_len_minmax(const int32_t* p, int64_t nseg, int* out) {
   atomicMax(out + 1, mx);
 }
 
-// Neighbouring segments whose first entries gather from the same 32-byte
-// sector (|first index difference| <= 3): the transportation pattern that
-// makes several segments per CTA share L1 sectors.
+// Neighbouring segments whose middle entries gather from the same 32-byte
+// sector (|index difference| <= 3): the transportation pattern (demand rows
+// j, j+1 read x[i*T + j], x[i*T + j + 1] at every position) that makes
+// several segments per CTA share L1 sectors. Middle, not first, entries: the
+// first in-neighbours of PageRank hub rows are the same few early nodes.
 __global__ void k_adjacent_count(const int32_t* p, const int32_t* idx, int32_t lo, int32_t hi, int* out) {
   int c = 0;
   GRID_STRIDE(s, (int64_t)(hi - lo - 1)) {
     const int32_t a = lo + static_cast<int32_t>(s);
-    if (p[a + 1] > p[a] && p[a + 2] > p[a + 1]) {
-      const int d = idx[p[a + 1]] - idx[p[a]];
+    const int32_t l0 = p[a + 1] - p[a], l1 = p[a + 2] - p[a + 1];
+    if (l0 > 0 && l1 > 0) {
+      const int d = idx[p[a + 1] + l1 / 2] - idx[p[a] + l0 / 2];
       c += (d >= -3 && d <= 3) ? 1 : 0;
     }
   }
@@ -336,6 +340,27 @@ __global__ void k_reduce_tiles(const double* tile, const double* span, int ntile
   }
 }
 
+// Both check reductions in one launch: blocks [0, n0) reduce layout 0's
+// slots (n0 sums), blocks [n0, n0 + n1) layout 1's; same fixed order as
+// k_reduce_tiles.
+__global__ void k_reduce_two(const double* t0, int nt0, int n0, const double* t1, int nt1, int n1, double* out) {
+  __shared__ double sh[kBlock / 32];
+  const bool second = static_cast<int>(blockIdx.x) >= n0;
+  const int i = second ? blockIdx.x - n0 : blockIdx.x;
+  const double* tile = second ? t1 : t0;
+  const int ntiles = second ? nt1 : nt0, nred = second ? n1 : n0;
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) acc += tile[(int64_t)t * nred + i];
+  acc = warp_combine<false>(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = sh[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v += sh[w];
+    out[blockIdx.x] = v;
+  }
+}
+
 __global__ void k_sumsq_partial(const double* v, int64_t n, double* part) {
   __shared__ double sh[kEw / 32];
   double acc = 0.0;
@@ -364,7 +389,8 @@ __global__ void k_power_norm(const double* sum, Scalars* sc) {
 // AdaptStepSize (solver.cpp:310-328) from the per-iteration partials:
 // k_adapt_sum folds one shard's tile partials into (|dx|^2, |dy|^2, dy.K dx),
 // k_adapt_apply updates eta from the (shard- and rank-summed) triple.
-__global__ void k_adapt_sum(const double* cred, int cn, const double* rred, int rn, double* out) {
+__global__ void k_adapt_sum(const double* cred, int cn, const double* rred, int rn, double* out, const Scalars* sc) {
+  if (sc->halt) return;
   __shared__ double sh[3][kBlock / 32];
   double a[3] = {0.0, 0.0, 0.0};
   for (int t = threadIdx.x; t < cn; t += blockDim.x) a[0] += cred[t];
@@ -390,6 +416,7 @@ __global__ void k_adapt_sum(const double* cred, int cn, const double* rred, int 
 }
 
 __global__ void k_adapt_apply(const double* sum, Scalars* sc, int j) {
+  if (sc->halt) return;
   const double dx = sum[0], dy = sum[1];
   const double it = fabs(sum[2]);
   if (it <= 0.0) return;

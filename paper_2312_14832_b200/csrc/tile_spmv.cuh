@@ -31,12 +31,28 @@
 //    kernels sum tiles in a fixed order.
 #pragma once
 
+#include <type_traits>
+#include <utility>
+
 #include "common.cuh"
 #include "tma.cuh"
 
 namespace pdhg {
 
 struct Nil {};
+
+// Ops with `bool skip()` abandon the whole launch when it returns true (the
+// pipelined loop's discarded blocks); evaluated before any barrier.
+template <class T, class = void>
+struct HasSkip : std::false_type {};
+template <class T>
+struct HasSkip<T, std::void_t<decltype(std::declval<T>().skip())>> : std::true_type {};
+template <class Op>
+__device__ __forceinline__ bool skip_launch(const Op& op) {
+  if constexpr (HasSkip<Op>::value) return op.skip();
+  else return false;
+}
+
 
 __device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ int32_t ld_stream(const int32_t* p) { return __ldcs(p); }
@@ -107,6 +123,7 @@ __host__ __device__ constexpr int smem_bytes(int rhs, int ops) { return smem_off
 template <class Op>
 __global__ void __launch_bounds__(kBlock, Op::kOcc) tile_kernel(const CMat M, const Op op, double* __restrict__ tile_red,
                                                          double* __restrict__ span_red) {
+  if (skip_launch(op)) return;
   using Pre = typename Op::Pre;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;

@@ -178,3 +178,28 @@ def test_check_every(check_every, restatement):
 
 def test_empty_rows(restatement):
     parity(empty_rows_lp(), SolverParams(eps=1e-8), restatement)
+
+
+@pytest.mark.parametrize("case", ["config1", "transport", "pagerank", "limits", "adaptive"])
+def test_pipelined_loop_matches_synchronous(case, monkeypatch):
+    """Device-side check decisions with the next block queued (default) vs the
+    host-synchronous loop (PDHG_PIPELINE=0): identical trajectory -- same
+    iterations, restarts, observer trace, bitwise iterates."""
+    p = {"config1": lambda: config1(2), "transport": lambda: GenTransport(30, 40, 1),
+         "pagerank": lambda: GenPagerank(2000, 0.85, 3, 1), "limits": lambda: config1(3),
+         "adaptive": lambda: small_cases()["pagerank_200"]}[case]()
+    prm = {"limits": SolverParams(eps=1e-10, iter_limit=1000, check_every=48),
+           "adaptive": SolverParams(eps=1e-6, adaptive_step=True, iter_limit=5000)}.get(case, SolverParams(eps=1e-6))
+    runs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PDHG_PIPELINE", flag)
+        tr = []
+        r = rpdlp.Solve(p, prm, observer=tr.append)
+        runs.append((r, tr))
+    (a, ta), (b, tb) = runs
+    assert a.status == b.status and a.iterations == b.iterations and a.restarts == b.restarts
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
+    assert a.report.primal_obj == b.report.primal_obj
+    assert [(e.iteration, e.restarted, e.candidate_is_current, e.omega, e.kkt_candidate) for e in ta] == \
+        [(e.iteration, e.restarted, e.candidate_is_current, e.omega, e.kkt_candidate) for e in tb]

@@ -1105,8 +1105,11 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   // before the host looks at the previous check; decisions run on the
   // device (decide.cuh), the host only steps in for restarts, termination,
   // limits and the observer. Identical trajectory to the synchronous loop.
+  // Opt-in (PDHG_PIPELINE=1): measured on B200 it does not beat the
+  // synchronous loop -- a check costs ~80 us of GPU work either way, and a
+  // block queued behind a restarting check must still be launched (empty).
   const char* penv = std::getenv("PDHG_PIPELINE");
-  const bool pipelined = !finished && !nccl() && !(penv && penv[0] == '0');
+  const bool pipelined = !finished && !nccl() && (penv && penv[0] == '1');
   if (pipelined) {
     DecideState ds{};
     ds.eps = prm.eps;

@@ -182,9 +182,9 @@ def test_empty_rows(restatement):
 
 @pytest.mark.parametrize("case", ["config1", "transport", "pagerank", "limits", "adaptive"])
 def test_pipelined_loop_matches_synchronous(case, monkeypatch):
-    """Device-side check decisions with the next block queued (default) vs the
-    host-synchronous loop (PDHG_PIPELINE=0): identical trajectory -- same
-    iterations, restarts, observer trace, bitwise iterates."""
+    """Device-side check decisions with the next block queued
+    (PDHG_PIPELINE=1) vs the host-synchronous loop (default): identical
+    trajectory -- same iterations, restarts, observer trace, bitwise iterates."""
     p = {"config1": lambda: config1(2), "transport": lambda: GenTransport(30, 40, 1),
          "pagerank": lambda: GenPagerank(2000, 0.85, 3, 1), "limits": lambda: config1(3),
          "adaptive": lambda: small_cases()["pagerank_200"]}[case]()

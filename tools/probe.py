@@ -26,6 +26,7 @@ if "--shards" in args:
     del args[i:i + 2]
 which = args or ["transport", "pagerank1m", "random", "mcf"]
 full_solve = {"transport", "random"}
+short = {"pagerank10m", "staircase", "mcf"}
 for name in which:
     t = time.time()
     p = cases[name]()
@@ -33,7 +34,7 @@ for name in which:
     sp = rpdlp.Shards(world=shards) if shards > 1 else None
     with rpdlp.Session(p, shards=sp) as s:
         st = s.stats()
-        ms_p, ms_d, ms_it = s.time_kernels(256)
+        ms_p, ms_d, ms_it = s.time_kernels(64 if p.nnz() > 2e7 else 256)
         bp, bd, bi = algorithmic_bytes(p.num_rows(), p.num_vars(), p.nnz(), st.uniform_bounds, st.csr_uniform_len,
                                        st.csc_uniform_len)
         print(f"{name}: m={p.num_rows()} n={p.num_vars()} nnz={p.nnz()} gen {tg:.1f}s upload {st.upload_seconds:.3f}s "
@@ -47,7 +48,7 @@ for name in which:
             print(f"   solve: status {int(r.status)} it {r.iterations} restarts {r.restarts} device {ms:.1f} ms "
                   f"-> {r.iterations / ms * 1e3:.0f} it/s", flush=True)
         else:
-            r = s.solve(rpdlp.SolverParams(eps=1e-4, iter_limit=640))
+            r = s.solve(rpdlp.SolverParams(eps=1e-4, iter_limit=128 if name in short else 640))
             ms, nl = s.last_solve()
-            print(f"   640 its: device {ms:.1f} ms -> {r.iterations / ms * 1e3:.0f} it/s", flush=True)
+            print(f"   {r.iterations} its: device {ms:.1f} ms -> {r.iterations / ms * 1e3:.0f} it/s", flush=True)
     del p

@@ -51,10 +51,10 @@ struct Layout {
   int parts() const { return nb_s() + nb_m() + nb_l() + 2 * nt_x(); }  // reduction slots
 };
 
-template <class Op>
+template <class Op, int NW = kWarps>
 __device__ __forceinline__ void block_reduce_out(double (&red)[Op::kRed > 0 ? Op::kRed : 1], double* out) {
   if constexpr (Op::kRed > 0) {
-    __shared__ double sh[kWarps][Op::kRed];
+    __shared__ double sh[NW][Op::kRed];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int i = 0; i < Op::kRed; ++i) {
@@ -64,7 +64,7 @@ __device__ __forceinline__ void block_reduce_out(double (&red)[Op::kRed > 0 ? Op
     __syncthreads();
     if (threadIdx.x < Op::kRed) {
       double v = sh[0][threadIdx.x];
-      for (int w = 1; w < kWarps; ++w) v += sh[w][threadIdx.x];
+      for (int w = 1; w < NW; ++w) v += sh[w][threadIdx.x];
       out[static_cast<int64_t>(blockIdx.x) * Op::kRed + threadIdx.x] = v;
     }
   }
@@ -338,18 +338,18 @@ __global__ void __launch_bounds__(kBlock) seg_warp_kernel(const int32_t* __restr
 // a CTA typically gather neighbouring vector entries (transportation demand
 // rows j..j+3 read x[i*T + j..j+3]), so they share L1 sectors instead of each
 // pulling its own 32-byte sector per 8-byte gather from L2.
-template <class Op, int RPC>
-__global__ void __launch_bounds__(kBlock) seg_cta_kernel(const int32_t* __restrict__ ptr,
-                                                         const int32_t* __restrict__ idx,
-                                                         const double* __restrict__ val, int32_t s_begin,
-                                                         int32_t s_end, const Op op, double* __restrict__ red_out) {
+template <class Op, int RPC, int B = kBlock>
+__global__ void __launch_bounds__(B) seg_cta_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                                    const double* __restrict__ val, int32_t s_begin, int32_t s_end,
+                                                    const Op op, double* __restrict__ red_out) {
   if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   constexpr bool MX = Op::kMax;
-  constexpr int T = kBlock / RPC;  // threads per segment
-  constexpr int W = T / 32;        // warps per segment
-  __shared__ double sh[kWarps][R];
+  constexpr int T = B / RPC;  // threads per segment
+  constexpr int W = T / 32;   // warps per segment
+  constexpr int NW = B / 32;
+  __shared__ double sh[NW][R];
   double red[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
@@ -380,7 +380,7 @@ __global__ void __launch_bounds__(kBlock) seg_cta_kernel(const int32_t* __restri
     }
     op.finish(s, acc, pre, red);
   }
-  block_reduce_out<Op>(red, red_out);
+  block_reduce_out<Op, NW>(red, red_out);
 }
 
 template <class Op>

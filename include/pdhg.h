@@ -212,6 +212,13 @@ int pdhg_nccl_unique_id(void* out128, char* err, size_t errlen);
 /* Block boundaries in original row / column order (world + 1 each). */
 int pdhg_session_blocks(pdhg_session* s, int64_t* row_begin,
                         int64_t* col_begin);
+/* Ghost-exchange plan of a sharded session: x_counts[r * world + b] = number
+ * of distinct x entries (columns) of block b that row block r reads (b != r;
+ * the diagonal is 0), y_counts likewise for the column blocks' row reads;
+ * use[0] / use[1] = whether the x / y exchange sends only those entries
+ * (NCCL mode, ghost volume <= half an all-gather) instead of all-gathering. */
+int pdhg_session_ghost_counts(pdhg_session* s, int64_t* x_counts,
+                              int64_t* y_counts, int32_t* use);
 /* The balanced split every rank computes: `parts` contiguous blocks of the
  * `nseg` segments of a CSR/CSC offset array (`begin`: parts + 1 entries). */
 int pdhg_partition_blocks(const int64_t* ptr, int64_t nseg, int parts,

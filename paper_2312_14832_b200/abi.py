@@ -99,6 +99,7 @@ SIGNATURES = {
                                      C.c_void_p, C.POINTER(Result), C.c_char_p, C.c_size_t]),
     "pdhg_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
     "pdhg_session_blocks": (C.c_int, [C.c_void_p, i64ptr, i64ptr]),
+    "pdhg_session_ghost_counts": (C.c_int, [C.c_void_p, i64ptr, i64ptr, C.POINTER(C.c_int32)]),
     "pdhg_partition_blocks": (C.c_int, [i64ptr, C.c_int64, C.c_int, C.c_int64, i64ptr]),
     "pdhg_normal_vector": (C.c_int, [C.c_uint64, C.c_int64, C.c_int, dptr]),
     "pdhg_session_destroy": (None, [C.c_void_p]),

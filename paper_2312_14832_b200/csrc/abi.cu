@@ -163,6 +163,10 @@ int pdhg_session_blocks(pdhg_session* s, int64_t* row_begin, int64_t* col_begin)
   return Guard(nullptr, 0, [&] { S(s).Blocks(row_begin, col_begin); });
 }
 
+int pdhg_session_ghost_counts(pdhg_session* s, int64_t* x_counts, int64_t* y_counts, int32_t* use) {
+  return Guard(nullptr, 0, [&] { S(s).GhostCounts(x_counts, y_counts, use); });
+}
+
 int pdhg_partition_blocks(const int64_t* ptr, int64_t nseg, int parts, int64_t seg_weight, int64_t* begin) {
   if (!ptr || !begin || nseg < 0 || parts < 1 || seg_weight < 0) return PDHG_INVALID_ARGUMENT;
   pdhg::BalancedBlocks(ptr, nseg, parts, seg_weight, begin);

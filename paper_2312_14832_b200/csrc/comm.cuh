@@ -25,10 +25,36 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "common.cuh"
 
 namespace pdhg {
+
+// Ghost-only exchange of one gather pattern: instead of the
+// whole vector, each rank receives just the entries its matrix block reads
+// from other blocks (the staircase's one boundary stage), and sends the
+// entries of its own slice that other blocks read. Index lists are padded
+// positions; per-peer ranges in send/recv are [off[p], off[p + 1]).
+struct GhostPlan {
+  bool use = false;   // ghost exchange (all ranks agree) instead of all-gather
+  int64_t slice = 0;  // padded slice of the pattern's vector
+  int32_t* send_idx = nullptr;
+  int32_t* recv_idx = nullptr;
+  double* send_buf = nullptr;
+  double* recv_buf = nullptr;
+  std::vector<int64_t> send_off, recv_off;  // world + 1 each
+};
+
+static __global__ void k_ghost_pack(const double* __restrict__ buf, const int32_t* __restrict__ idx, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = buf[idx[i]];
+}
+static __global__ void k_ghost_unpack(double* __restrict__ buf, const int32_t* __restrict__ idx, const double* in, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[idx[i]] = in[i];
+}
 
 class Comm {
  public:
@@ -36,6 +62,8 @@ class Comm {
   virtual bool local() const = 0;
   // In place: this rank's slice is buf[rank * slice, (rank + 1) * slice).
   virtual void AllGather(double* buf, int64_t slice, cudaStream_t st) = 0;
+  // The entries this rank's block reads (ghost plan), or the full vector.
+  virtual void Exchange(double* buf, const GhostPlan& plan, cudaStream_t st) { AllGather(buf, plan.slice, st); }
   virtual void AllReduceSum(double* buf, int64_t n, cudaStream_t st) = 0;
   virtual void AllReduceMax(double* buf, int64_t n, cudaStream_t st) = 0;
 };
@@ -44,6 +72,7 @@ class LocalComm final : public Comm {
  public:
   bool local() const override { return true; }
   void AllGather(double*, int64_t, cudaStream_t) override {}
+  void Exchange(double*, const GhostPlan&, cudaStream_t) override {}
   void AllReduceSum(double*, int64_t, cudaStream_t) override {}
   void AllReduceMax(double*, int64_t, cudaStream_t) override {}
 };
@@ -55,6 +84,10 @@ struct NcclApi {
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
   static const NcclApi& Get() {
@@ -76,7 +109,12 @@ struct NcclApi {
     a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
     a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(dlsym(h, "ncclAllReduce"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    if (!a.GetUniqueId || !a.CommInitRank || !a.CommDestroy || !a.AllReduce || !a.GetErrorString)
+    a.Send = reinterpret_cast<decltype(a.Send)>(dlsym(h, "ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(h, "ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    if (!a.GetUniqueId || !a.CommInitRank || !a.CommDestroy || !a.AllReduce || !a.GetErrorString || !a.Send ||
+        !a.Recv || !a.GroupStart || !a.GroupEnd)
       a.AllGather = nullptr;
     return a;
   }
@@ -102,6 +140,27 @@ class NcclComm final : public Comm {
     if (slice <= 0) return;
     nccl_check(NcclApi::Get().AllGather(buf + rank_ * slice, buf, static_cast<size_t>(slice), ncclFloat64, comm_, st),
                "ncclAllGather");
+  }
+  // Pack the entries peers read from this slice, one grouped send/recv per
+  // peer pair (only pairs with a non-empty list), unpack into the gathered
+  // positions. Stream-ordered and graph-capturable like the collectives.
+  void Exchange(double* buf, const GhostPlan& plan, cudaStream_t st) override {
+    if (!plan.use) return AllGather(buf, plan.slice, st);
+    const NcclApi& api = NcclApi::Get();
+    const int world = static_cast<int>(plan.send_off.size()) - 1;
+    const int64_t ns = plan.send_off[world], nr = plan.recv_off[world];
+    if (ns) k_ghost_pack<<<static_cast<int>(std::min<int64_t>((ns + 255) / 256, 1184)), 256, 0, st>>>(
+        buf, plan.send_idx, plan.send_buf, ns);
+    nccl_check(api.GroupStart(), "ncclGroupStart");
+    for (int p = 0; p < world; ++p) {
+      if (p == rank_) continue;
+      const int64_t sc = plan.send_off[p + 1] - plan.send_off[p], rc = plan.recv_off[p + 1] - plan.recv_off[p];
+      if (sc) nccl_check(api.Send(plan.send_buf + plan.send_off[p], sc, ncclFloat64, p, comm_, st), "ncclSend");
+      if (rc) nccl_check(api.Recv(plan.recv_buf + plan.recv_off[p], rc, ncclFloat64, p, comm_, st), "ncclRecv");
+    }
+    nccl_check(api.GroupEnd(), "ncclGroupEnd");
+    if (nr) k_ghost_unpack<<<static_cast<int>(std::min<int64_t>((nr + 255) / 256, 1184)), 256, 0, st>>>(
+        buf, plan.recv_idx, plan.recv_buf, nr);
   }
   void AllReduceSum(double* buf, int64_t n, cudaStream_t st) override {
     nccl_check(NcclApi::Get().AllReduce(buf, buf, static_cast<size_t>(n), ncclFloat64, ncclSum, comm_, st),

@@ -363,12 +363,16 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     BalancedBlocks(hp.data(), n_, world_, kSegWeight, col_begin_.data());
   }
   pm_ = pn_ = 0;
+  gx_ = GhostPlan{};
+  gy_ = GhostPlan{};
   for (int b = 0; b < world_; ++b) {
     pm_ = std::max(pm_, row_begin_[b + 1] - row_begin_[b]);
     pn_ = std::max(pn_, col_begin_[b + 1] - col_begin_[b]);
   }
   mp_ = pm_ * world_;
   np_ = pn_ * world_;
+  gx_.slice = pn_;
+  gy_.slice = pm_;
   if (mp_ >= (int64_t(1) << 31) - 1 || np_ >= (int64_t(1) << 31) - 1)
     throw Error(PDHG_INVALID_ARGUMENT, "padded vectors too large for int32 device indices");
   DArray<int64_t> rbeg, cbeg;
@@ -529,6 +533,7 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     DArray<int32_t> fptr, fidx;
     DArray<double> fval;
     build(fptr, fidx, fval, ptr0, idx0, val0, row_of, m_, perm_r, inv_r, pad_c_);
+    if (world_ > 1) BuildGhostPlan(fptr.p, fidx.p, row_begin_, np_, pn_, gx_, gxs_, ghost_counts_x_);
     for (Shard& h : shards_) {
       const int b = h.block;
       const int* hb = hr.data() + 8 * b;
@@ -551,6 +556,7 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     DArray<double> fval;
     segment_ids(cptr0.p, n_, nnz_, col_of, st_);
     build(fptr, fidx, fval, cptr0, ridx0, cval0, col_of, n_, perm_c, inv_c, pad_r_);
+    if (world_ > 1) BuildGhostPlan(fptr.p, fidx.p, col_begin_, mp_, pm_, gy_, gys_, ghost_counts_y_);
     for (Shard& h : shards_) {
       const int b = h.block;
       h.coff = b * pn_;
@@ -564,6 +570,111 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
   PDHG_CUDA(cudaMemcpyAsync(ptr0_.p, ptr0.p, (m_ + 1) * sizeof(int32_t), cudaMemcpyDeviceToDevice, st_));
   Sync();
   check_launch("permute");
+}
+
+// Ghost plan of one gather pattern, from the full compact layout (every
+// block's segments, indices already padded) that every rank builds: for each
+// reader block r, the distinct padded indices its segments read outside its
+// own slice (sorted, hence grouped by source block). This rank receives its
+// own list and sends, to each peer r, the part of r's list inside its slice.
+// All ranks see the same counts, so they agree on ghost vs all-gather: ghosts
+// when the largest per-rank ghost volume is at most half an all-gather.
+void Session::BuildGhostPlan(const int32_t* ptr, const int32_t* idx, const std::vector<int64_t>& seg_begin,
+                             int64_t nvec, int64_t slice, GhostPlan& plan, GhostStore& store,
+                             std::vector<int64_t>& counts) {
+  const int P = world_;
+  counts.assign(static_cast<size_t>(P) * P, 0);
+  DArray<uint8_t> mark;
+  DArray<int32_t> list, nsel, bcount;
+  mark.alloc(std::max<int64_t>(nvec, 1));
+  list.alloc(std::max<int64_t>(nvec, 1));
+  nsel.alloc(1);
+  bcount.alloc(P);
+  std::vector<int32_t> hptr(static_cast<size_t>(P) + 1);
+  for (int r = 0; r <= P; ++r) {
+    PDHG_CUDA(cudaMemcpyAsync(&hptr[r], ptr + seg_begin[r], sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+  }
+  Sync();
+  size_t tb = 0;
+  cub::DeviceSelect::Flagged(nullptr, tb, static_cast<const int32_t*>(nullptr), static_cast<const uint8_t*>(nullptr),
+                             list.p, nsel.p, static_cast<int>(nvec), st_);
+  DArray<char> tmp;
+  DArray<int32_t> iota;
+  tmp.alloc(std::max<size_t>(tb, 1));
+  iota.alloc(std::max<int64_t>(nvec, 1));
+  k_iota<<<ew_grid(nvec), kEw, 0, st_>>>(iota.p, nvec);
+  std::vector<int32_t> send_host;  // this rank's send lists, peer by peer
+  std::vector<int64_t> send_off(P + 1, 0), recv_off(P + 1, 0);
+  for (int r = 0; r < P; ++r) {
+    PDHG_CUDA(cudaMemsetAsync(mark.p, 0, nvec, st_));
+    const int64_t k0 = hptr[r], k1 = hptr[r + 1];
+    if (k1 > k0) k_mark<<<ew_grid(k1 - k0), kEw, 0, st_>>>(idx + k0, k1 - k0, mark.p);
+    PDHG_CUDA(cudaMemsetAsync(mark.p + r * slice, 0, slice, st_));  // own slice: local
+    PDHG_CUDA(cub::DeviceSelect::Flagged(tmp.p, tb, iota.p, mark.p, list.p, nsel.p, static_cast<int>(nvec), st_));
+    PDHG_CUDA(cudaMemsetAsync(bcount.p, 0, P * sizeof(int32_t), st_));
+    int nl = 0;
+    PDHG_CUDA(cudaMemcpyAsync(&nl, nsel.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+    Sync();
+    if (nl) k_block_count<<<ew_grid(nl), kEw, 0, st_>>>(list.p, nl, slice, bcount.p);
+    std::vector<int32_t> bc(P);
+    PDHG_CUDA(cudaMemcpyAsync(bc.data(), bcount.p, P * sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+    Sync();
+    int64_t before = 0;
+    for (int b = 0; b < P; ++b) {
+      counts[static_cast<size_t>(r) * P + b] = bc[b];
+      if (b < rank_) before += bc[b];
+    }
+    if (r == rank_) {  // receive list: where the ghosts land
+      for (int b = 0; b < P; ++b) recv_off[b + 1] = recv_off[b] + bc[b];
+      store.recv_idx.alloc(std::max(nl, 1), &arena_);
+      if (nl) PDHG_CUDA(cudaMemcpyAsync(store.recv_idx.p, list.p, nl * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                        st_));
+    } else {  // what r reads from this rank's slice
+      const int64_t c = bc[rank_];
+      std::vector<int32_t> part(static_cast<size_t>(c));
+      if (c) PDHG_CUDA(cudaMemcpyAsync(part.data(), list.p + before, c * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                       st_));
+      Sync();
+      send_host.insert(send_host.end(), part.begin(), part.end());
+    }
+    send_off[r + 1] = static_cast<int64_t>(send_host.size());
+  }
+  int64_t worst = 0;
+  for (int r = 0; r < P; ++r) {
+    int64_t g = 0;
+    for (int b = 0; b < P; ++b)
+      if (b != r) g += counts[static_cast<size_t>(r) * P + b];
+    worst = std::max(worst, g);
+  }
+  const char* genv = std::getenv("PDHG_GHOST");
+  const bool allow = !(genv && genv[0] == '0');
+  plan.use = allow && !comm_->local() && 2 * worst <= static_cast<int64_t>(P - 1) * slice;
+  plan.slice = slice;
+  plan.send_off = send_off;
+  plan.recv_off = recv_off;
+  if (plan.use) {
+    const int64_t ns = send_off[P], nr = recv_off[P];
+    store.send_idx.alloc(std::max<int64_t>(ns, 1), &arena_);
+    if (ns) PDHG_CUDA(cudaMemcpyAsync(store.send_idx.p, send_host.data(), ns * sizeof(int32_t),
+                                      cudaMemcpyHostToDevice, st_));
+    store.send_buf.alloc(std::max<int64_t>(ns, 1), &arena_);
+    store.recv_buf.alloc(std::max<int64_t>(nr, 1), &arena_);
+    plan.send_idx = store.send_idx.p;
+    plan.recv_idx = store.recv_idx.p;
+    plan.send_buf = store.send_buf.p;
+    plan.recv_buf = store.recv_buf.p;
+    Sync();
+  } else {
+    store.recv_idx.release();
+  }
+  check_launch("ghost plan");
+}
+
+void Session::GhostCounts(int64_t* x_counts, int64_t* y_counts, int32_t* use) const {
+  std::copy(ghost_counts_x_.begin(), ghost_counts_x_.end(), x_counts);
+  std::copy(ghost_counts_y_.begin(), ghost_counts_y_.end(), y_counts);
+  use[0] = gx_.use;
+  use[1] = gy_.use;
 }
 
 // Tile partition of the extra-long class [s3, nseg) of one layout (tile_spmv.cuh):
@@ -690,8 +801,8 @@ void Session::ComputeScaling(const pdhg_params& prm) {
       GatherX(dc.p);
       rescale(false, dr.p, dc.p);
     }
-    GatherY(rs_.p);
-    GatherX(cs_.p);
+    GatherYFull(rs_.p);
+    GatherXFull(cs_.p);
     // PC on K.Scaled(ruiz) recomputed from the original values (scaling.cpp:89).
     rescale(true, rs_.p, cs_.p);
     auto mode_of = [](double p) { return p == 0.0 ? 0 : (p == 1.0 ? 1 : (p == 2.0 ? 2 : 3)); };
@@ -700,8 +811,8 @@ void Session::ComputeScaling(const pdhg_params& prm) {
       run_pass(h.csr, OpPowerSumScale{pr, mode_of(pr), rs_.p + h.roff}, none, st_);
       run_pass(h.csc, OpPowerSumScale{pc, mode_of(pc), cs_.p + h.coff}, none, st_);
     }
-    GatherY(rs_.p);
-    GatherX(cs_.p);
+    GatherYFull(rs_.p);
+    GatherXFull(cs_.p);
     // Final K_s from the original values (ApplyScaling, scaling.cpp:105-106).
     rescale(true, rs_.p, cs_.p);
     check_launch("scaling");
@@ -1405,6 +1516,8 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 
   // Finish (solver.cpp:473-481): unscale best, lambda on the original problem.
   const double t_loop = secs();
+  if (gx_.use) GatherXFull(xbest_.p);  // ghost exchange left only the read entries valid
+  if (gy_.use) GatherYFull(ybest_.p);
   ToHost(xbest_.p, cs_.p, pad_c_, out->x, n_);
   ToHost(ybest_.p, rs_.p, pad_r_, out->y, m_);
   if (out->lambda) {
@@ -1412,7 +1525,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
       const int64_t c = h.coff;
       run_pass(h.csc, OpLambda{ybest_.p, c_o_.p + c, l_o_.p + c, u_o_.p + c, cs_.p + c, nvec_.p + c}, RedSlots{}, st_);
     }
-    GatherX(nvec_.p);
+    GatherXFull(nvec_.p);
     ToHost(nvec_.p, nullptr, pad_c_, out->lambda, n_);
   }
   PDHG_CUDA(cudaEventRecord(ev_[1], st_));
@@ -1565,8 +1678,8 @@ void Session::Spmv(int transpose, const double* in, double* out) {
   ToInternal(in, transpose ? pad_r_ : pad_c_, a.p, nin, pin);
   for (Shard& h : shards_) run_pass(transpose ? h.csc : h.csr, OpSpmv{a.p, b.p + (transpose ? h.coff : h.roff)},
                                     RedSlots{}, st_);
-  if (transpose) GatherX(b.p);
-  else GatherY(b.p);
+  if (transpose) GatherXFull(b.p);
+  else GatherYFull(b.p);
   check_launch("spmv");
   ToHost(b.p, nullptr, transpose ? pad_c_ : pad_r_, out, nout);
 }
@@ -1642,7 +1755,7 @@ void Session::UnitPrimal(const double* x, const double* y, double eta, double om
     run_pass(h.csc, OpUnitPrimal{dy.p, dx.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o, eta / omega, dout.p + o},
              RedSlots{}, st_);
   }
-  GatherX(dout.p);
+  GatherXFull(dout.p);
   check_launch("primal step");
   ToHost(dout.p, nullptr, pad_c_, out, n_);
 }
@@ -1663,7 +1776,7 @@ void Session::UnitDual(const double* xn, const double* xo, const double* y, doub
     const int64_t o = h.roff;
     run_pass(h.csr, OpUnitDual{ext.p, dy.p + o, q_s_.p + o, h.rk, eta * omega, dout.p + o}, RedSlots{}, st_);
   }
-  GatherY(dout.p);
+  GatherYFull(dout.p);
   check_launch("dual step");
   ToHost(dout.p, nullptr, pad_r_, out, m_);
 }

@@ -47,6 +47,7 @@ class Session {
   void TimeKernels(int iters, double* ms_primal, double* ms_dual, double* ms_iter);
   void Stats(pdhg_session_stats* s) const;
   void Blocks(int64_t* row_begin, int64_t* col_begin) const;
+  void GhostCounts(int64_t* x_counts, int64_t* y_counts, int32_t* use) const;
   void UnitPrimal(const double* x, const double* y, double eta, double omega, double* out);
   void UnitDual(const double* xn, const double* xo, const double* y, double eta, double omega, double* out);
   int device() const { return device_; }
@@ -103,8 +104,18 @@ class Session {
   void ToHost(const double* dev, const double* scale, const DArray<int32_t>& pad, double* host, int64_t n);
   double* DevStage();
   double* HostStage();
-  void GatherX(double* v) { comm_->AllGather(v, pn_, st_); }
-  void GatherY(double* v) { comm_->AllGather(v, pm_, st_); }
+  // Gathers for the next matrix pass (ghost entries only when the plan says
+  // so) and full gathers for values leaving the session.
+  void GatherX(double* v) { comm_->Exchange(v, gx_, st_); }
+  void GatherY(double* v) { comm_->Exchange(v, gy_, st_); }
+  void GatherXFull(double* v) { comm_->AllGather(v, pn_, st_); }
+  void GatherYFull(double* v) { comm_->AllGather(v, pm_, st_); }
+  struct GhostStore {
+    DArray<int32_t> send_idx, recv_idx;
+    DArray<double> send_buf, recv_buf;
+  };
+  void BuildGhostPlan(const int32_t* ptr, const int32_t* idx, const std::vector<int64_t>& seg_begin, int64_t nvec,
+                      int64_t slice, GhostPlan& plan, GhostStore& store, std::vector<int64_t>& counts);
   bool nccl() const { return !comm_->local(); }
   int parts_csr() const;
   int parts_csc() const;
@@ -129,6 +140,9 @@ class Session {
   std::unique_ptr<Comm> comm_;
   std::vector<Shard> shards_;
   DArray<int32_t> pad_r_, pad_c_;  // original row / column -> padded index
+  GhostPlan gx_, gy_;               // x pattern (CSR reads), y pattern (CSC reads)
+  GhostStore gxs_, gys_;
+  std::vector<int64_t> ghost_counts_x_, ghost_counts_y_;  // [reader block][source block] entries
   DArray<int32_t> ptr0_;           // original CSR row_ptr (probe only)
 
   // Problem vectors (padded order): scaled (loop) and original (termination).

@@ -154,6 +154,14 @@ __global__ void k_adjacent_count(const int32_t* p, const int32_t* idx, int32_t l
   atomicAdd(out, c);
 }
 
+// Ghost plans: mark every gathered index; count marked indices per block.
+__global__ void k_mark(const int32_t* idx, int64_t n, uint8_t* mark) {
+  GRID_STRIDE(k, n) mark[idx[k]] = 1;
+}
+__global__ void k_block_count(const int32_t* list, int64_t n, int64_t slice, int32_t* count) {
+  GRID_STRIDE(i, n) atomicAdd(count + list[i] / slice, 1);
+}
+
 // Sort key putting longer segments first: INT32_MAX - length.
 __global__ void k_len_desc_key(const int32_t* p, int64_t nseg, int32_t* key) {
   GRID_STRIDE(s, nseg) key[s] = INT32_MAX - (p[s + 1] - p[s]);

@@ -421,6 +421,16 @@ class Session:
         raise_for(self.lib.pdhg_session_blocks(self.h, _i64p(rb), _i64p(cb)), b"")
         return rb, cb
 
+    def ghost_counts(self):
+        """(x_counts, y_counts, (use_x, use_y)): world x world matrices of the
+        ghost entries each block reads from each other block."""
+        w = self.shards.world
+        xc, yc = np.zeros((w, w), np.int64), np.zeros((w, w), np.int64)
+        use = (C.c_int32 * 2)()
+        if w > 1:
+            raise_for(self.lib.pdhg_session_ghost_counts(self.h, _i64p(xc), _i64p(yc), use), b"")
+        return xc, yc, (bool(use[0]), bool(use[1]))
+
     def scaling(self):
         rs, cs = np.empty(self.problem.num_rows()), np.empty(self.problem.num_vars())
         err = self._err()

@@ -127,3 +127,28 @@ def test_sharded_limits():
     assert r.status == SolveStatus.kIterLimit and r.iterations == 100
     r = rpdlp.Solve(p, SolverParams(eps=1e-10, time_limit=0.0), shards=Shards(world=3))
     assert r.status == SolveStatus.kTimeLimit and r.iterations == 0
+
+
+@pytest.mark.parametrize("gen", ["staircase", "pagerank", "transport"])
+def test_ghost_plan_counts(gen):
+    """The ghost plan (entries each block reads from every other block) equals
+    a numpy count from the original matrix and the balanced blocks."""
+    p = {"staircase": lambda: GenStaircase(8, 60, 70, 6, 2, seed=3),
+         "pagerank": lambda: GenPagerank(2000, 0.85, 3, 2),
+         "transport": lambda: GenTransport(20, 30, 1)}[gen]()
+    world = 4
+    K = np.vstack([p.a.to_dense(), p.g.to_dense()]) != 0
+    with rpdlp.Session(p, shards=Shards(world=world)) as s:
+        rb, cb = s.blocks()
+        xc, yc, use = s.ghost_counts()
+    assert use == (False, False)  # one process: exchanges are in place
+    for r in range(world):
+        for b in range(world):
+            rows, cols = slice(rb[r], rb[r + 1]), slice(cb[b], cb[b + 1])
+            want_x = 0 if r == b else int(K[rows, cols].any(axis=0).sum())
+            crow, ccol = slice(cb[r], cb[r + 1]), slice(rb[b], rb[b + 1])
+            want_y = 0 if r == b else int(K[ccol, crow].any(axis=1).sum())
+            assert xc[r, b] == want_x, (r, b)
+            assert yc[r, b] == want_y, (r, b)
+    if gen == "staircase":  # a stage block reads only its neighbour's boundary
+        assert xc.sum() < 0.5 * (world - 1) * K.shape[1]

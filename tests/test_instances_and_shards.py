@@ -241,3 +241,75 @@ def test_parallel_normal_vector_is_bit_exact(seed, n):
     assert lib.pdhg_normal_vector(seed, n, 3, dp(c)) == 0
     np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
     np.testing.assert_array_equal(a.view(np.uint64), c.view(np.uint64))
+
+
+# ------------------------------- gloo world_size-3 ghost-only exchange test
+def _ghost_lists(K, row_begin, col_begin, me):
+    """Entries block `me` reads from every other column block (recv) and the
+    entries of block `me`'s slice every other block reads (send) -- the
+    definition csrc/session.cu BuildGhostPlan implements."""
+    world = len(row_begin) - 1
+    nz = K != 0
+    recv, send = {}, {}
+    for b in range(world):
+        if b == me:
+            continue
+        cols = np.arange(col_begin[b], col_begin[b + 1])
+        recv[b] = cols[nz[row_begin[me]:row_begin[me + 1], col_begin[b]:col_begin[b + 1]].any(axis=0)]
+        mine = np.arange(col_begin[me], col_begin[me + 1])
+        send[b] = mine[nz[row_begin[b]:row_begin[b + 1], col_begin[me]:col_begin[me + 1]].any(axis=0)]
+    return recv, send
+
+
+def _ghost_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = GenStaircase(6, 14, 16, 5, 2, seed=11)
+        K = np.vstack([p.a.to_dense(), p.g.to_dense()])
+        kptr = np.concatenate([p.a.row_ptr[:-1], p.a.nnz + p.g.row_ptr])
+        rb = PartitionBlocks(kptr, world, 6)
+        cb = PartitionBlocks(np.concatenate([[0], np.cumsum(np.count_nonzero(K, axis=0))]), world, 6)
+        # K x with rows of block `rank`, x exchanged ghost-only (x_full NaN elsewhere)
+        rng = np.random.default_rng(3)
+        x = rng.standard_normal(K.shape[1])
+        x_full = np.full(K.shape[1], np.nan)
+        x_full[cb[rank]:cb[rank + 1]] = x[cb[rank]:cb[rank + 1]]
+        recv, send = _ghost_lists(K, rb, cb, rank)
+        reqs = []
+        bufs = {}
+        for b in range(world):
+            if b == rank:
+                continue
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(x_full[send[b]])), dst=b))
+            bufs[b] = torch.zeros(len(recv[b]), dtype=torch.float64)
+            reqs.append(dist.irecv(bufs[b], src=b))
+        for r in reqs:
+            r.wait()
+        for b, t in bufs.items():
+            x_full[recv[b]] = t.numpy()
+        rows = slice(rb[rank], rb[rank + 1])
+        sub = K[rows]
+        kx = np.array([np.sum(sub[i][sub[i] != 0] * x_full[sub[i] != 0]) for i in range(sub.shape[0])])
+        ghost = sum(len(v) for v in recv.values())
+        np.savez(os.path.join(out_dir, f"g{rank}.npz"), kx=kx, want=K[rows] @ x, ghost=ghost,
+                 full=(world - 1) * int(max(np.diff(cb))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_three_rank_ghost_exchange(tmp_path):
+    """Ghost-only exchange (send/recv of just the entries each row block
+    reads) reproduces the row products exactly; everything outside the own
+    slice and the ghost lists stays NaN, so a missing ghost would show."""
+    import torch.multiprocessing as mp
+    world = 3
+    mp.spawn(_ghost_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for k in range(world):
+        r = np.load(tmp_path / f"g{k}.npz")
+        assert np.all(np.isfinite(r["kx"]))
+        np.testing.assert_allclose(r["kx"], r["want"], rtol=1e-13, atol=1e-13)
+        assert r["ghost"] < r["full"]  # staircase: far less than an all-gather

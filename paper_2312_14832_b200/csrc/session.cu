@@ -135,7 +135,10 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
     PDHG_CUDA(cudaEventCreateWithFlags(&fork_.join[k], cudaEventDisableTiming));
   }
   PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&host_red_), kPack * sizeof(double) + 64));
-  if (world_ > 1 && spec.local == 1) {
+  // NCCL whenever a one-shard-per-process id is given -- also for world = 1,
+  // which runs the NCCL code path (collectives, graph capture, rank-0 clock,
+  // abort all-reduce) on a single GPU.
+  if (spec.local == 1 && (world_ > 1 || spec.nccl_id)) {
     if (!spec.nccl_id) throw Error(PDHG_INVALID_ARGUMENT, "a one-shard-per-process session needs an NCCL id");
     comm_ = std::make_unique<NcclComm>(spec.nccl_id, world_, rank_);
   } else {

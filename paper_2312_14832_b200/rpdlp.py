@@ -302,6 +302,14 @@ class Shards:
     nccl_id: Optional[bytes] = None
 
     @staticmethod
+    def nccl_single() -> "Shards":
+        """One rank, one GPU, through the NCCL exchange path (tests)."""
+        buf = C.create_string_buffer(128)
+        err = C.create_string_buffer(abi.ERRLEN)
+        raise_for(abi.load().pdhg_nccl_unique_id(buf, err, abi.ERRLEN), err)
+        return Shards(1, 0, False, bytes(buf.raw))
+
+    @staticmethod
     def from_process_group(group=None) -> "Shards":
         import torch
         import torch.distributed as dist
@@ -340,7 +348,7 @@ def Solve(problem: LpProblem, params: Optional[SolverParams] = None, observer: O
     res, x, y, lam = _result(problem)
     obs = _Observer(observer)
     err = C.create_string_buffer(abi.ERRLEN)
-    if shards is None or shards.world == 1:
+    if shards is None or (shards.world == 1 and shards.local):
         code = lib.pdhg_solve_on(C.byref(lp), C.byref(prm), device, obs.c, None, C.byref(res), err, abi.ERRLEN)
     else:
         spec, _keep = shards.to_c()
@@ -362,7 +370,7 @@ class Session:
         lp, prm = problem.to_c(), self.params.to_c()
         self.h = C.c_void_p()
         err = C.create_string_buffer(abi.ERRLEN)
-        if self.shards.world == 1:
+        if self.shards.world == 1 and self.shards.local:
             code = self.lib.pdhg_session_create(C.byref(lp), C.byref(prm), device, C.byref(self.h), err, abi.ERRLEN)
         else:
             spec, _keep = self.shards.to_c()

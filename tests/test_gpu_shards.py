@@ -152,3 +152,24 @@ def test_ghost_plan_counts(gen):
             assert yc[r, b] == want_y, (r, b)
     if gen == "staircase":  # a stage block reads only its neighbour's boundary
         assert xc.sum() < 0.5 * (world - 1) * K.shape[1]
+
+
+def test_nccl_path_single_rank(restatement):
+    """The one-shard-per-process NCCL path on one GPU (world = 1): in-place
+    all-gathers, the check all-reduce, rank 0's clock in the pack and the
+    observer-abort all-reduce, all captured in the block graphs -- same
+    trajectory as the default session."""
+    p = config1(1)
+    prm = SolverParams(eps=1e-6)
+    tr_a, tr_b = [], []
+    a = rpdlp.Solve(p, prm, observer=tr_a.append)
+    b = rpdlp.Solve(p, prm, observer=tr_b.append, shards=Shards.nccl_single())
+    assert a.status == b.status and a.iterations == b.iterations and a.restarts == b.restarts
+    np.testing.assert_array_equal(a.x, b.x)
+    assert [(e.iteration, e.restarted) for e in tr_a] == [(e.iteration, e.restarted) for e in tr_b]
+    r = rpdlp.Solve(p, SolverParams(eps=1e-10, iter_limit=200), shards=Shards.nccl_single())
+    assert r.iterations == 200
+    with pytest.raises(RuntimeError):
+        def stop(_):
+            raise RuntimeError("stop")
+        rpdlp.Solve(p, prm, observer=stop, shards=Shards.nccl_single())

@@ -13,7 +13,13 @@ pinned host buffers: H2D of the LP, int32 narrowing, CSC build, scaling, the
 solve and D2H of x, y, lambda all inside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config transport|pagerank|random] [--eps 1e-4]
+                    [--config transport|pagerank|random|mcf|staircase] [--eps 1e-4]
+                    [--mode sharded|replicas] [--eps-tight 1e-8]
+
+Under torchrun (N > 1) the default mode shards K over the ranks (row/column
+blocks, NCCL exchanges; strong scaling: value = iterations of the one solve
+per device second, max over ranks); --mode replicas runs N independent solves.
+`tight_solve` times one extra solve to --eps-tight (time-to-1e-8).
 
 --impl reference times the reference's own CPU implementation (oracle/_ref,
 the UNMODIFIED rpdlp sources compiled by oracle/Makefile; else the oracle

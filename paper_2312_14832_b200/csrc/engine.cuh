@@ -15,6 +15,7 @@
 // a fixed order, so every pass stays bitwise reproducible.
 #pragma once
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "tile_spmv.cuh"
@@ -90,9 +91,15 @@ __global__ void __launch_bounds__(kBlock) seg_thread_kernel(const int32_t* __res
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
   const int s = blockIdx.x * kBlock + threadIdx.x;
+  int b = 0, e = 0;
+  typename Op::Pre pre{};
   if (s < s_end) {
-    const int b = ptr[s], e = ptr[s + 1];
-    const typename Op::Pre pre = op.prefetch(s);
+    b = ptr[s];
+    e = ptr[s + 1];
+    pre = op.prefetch(s);
+  }
+  pdl_wait_trigger();
+  if (s < s_end) {
     double acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
@@ -170,11 +177,15 @@ __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
   const int s = blockIdx.x * kBlock + threadIdx.x;
+  typename Op::Pre pre{};
+  int32_t j[L];
+  double v[L];
   if (s < s_end) {
-    const typename Op::Pre pre = op.prefetch(s);
-    int32_t j[L];
-    double v[L];
+    pre = op.prefetch(s);
     load_uniform<L>(idx, val, static_cast<int64_t>(s) * L, j, v);
+  }
+  pdl_wait_trigger();
+  if (s < s_end) {
     double p[L][R];
 #pragma unroll
     for (int u = 0; u < L; ++u) op.map(j[u], v[u], p[u]);
@@ -218,15 +229,16 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int s = blockIdx.x * kBlock + threadIdx.x;
   const int s0 = blockIdx.x * kBlock + warp * 32;
+  const bool own = s < s_end;
+  int b = 0, e = 0;
+  typename Op::Pre pre{};
+  if (own) {
+    b = ptr[s];
+    e = ptr[s + 1];
+    pre = op.prefetch(s);
+  }
+  pdl_wait_trigger();
   if (s0 < s_end) {  // warp-uniform
-    const bool own = s < s_end;
-    int b = 0, e = 0;
-    typename Op::Pre pre{};
-    if (own) {
-      b = ptr[s];
-      e = ptr[s + 1];
-      pre = op.prefetch(s);
-    }
     const int wb = ptr[s0];
     const int we = ptr[s0 + 32 < s_end ? s0 + 32 : s_end];
     double acc[R];
@@ -271,13 +283,16 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
 // idx -> gather latency chain per element). Masked-off slots contribute 0,
 // the identity of both combines (sums, and max over |v| >= 0).
 constexpr int kStrideUnroll = 8;
-template <class Op, int kStride>
+// kPdl: issue the first batch of stream loads, then wait for the predecessor
+// grid (pdl_wait_trigger) before the first gather -- exactly once per thread.
+template <class Op, int kStride, bool kPdl = false>
 __device__ __forceinline__ void strided_sum(const Op& op, const int32_t* __restrict__ idx,
                                             const double* __restrict__ val, int b, int e, int t,
                                             double (&acc)[Op::kRhs]) {
   constexpr int R = Op::kRhs;
   constexpr bool MX = Op::kMax;
   constexpr int U = kStrideUnroll;
+  bool waited = !kPdl;
   for (int k = b + t; k < e; k += kStride * U) {
     int32_t j[U];
     double v[U], p[U][R];
@@ -286,6 +301,10 @@ __device__ __forceinline__ void strided_sum(const Op& op, const int32_t* __restr
       const bool in = k + kStride * u < e;
       j[u] = in ? ld_stream(idx + k + kStride * u) : 0;
       v[u] = in ? ld_stream(val + k + kStride * u) : 0.0;
+    }
+    if (!waited) {
+      pdl_wait_trigger();
+      waited = true;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -301,6 +320,7 @@ __device__ __forceinline__ void strided_sum(const Op& op, const int32_t* __restr
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[u][r]);
   }
+  if (!waited) pdl_wait_trigger();
 }
 
 // Class M: one warp per segment.
@@ -318,6 +338,7 @@ __global__ void __launch_bounds__(kBlock) seg_warp_kernel(const int32_t* __restr
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
   const int lane = threadIdx.x & 31;
   const int s = s_begin + blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (s >= s_end) pdl_wait_trigger();
   if (s < s_end) {  // warp-uniform
     const int b = ptr[s], e = ptr[s + 1];
     typename Op::Pre pre{};
@@ -325,7 +346,7 @@ __global__ void __launch_bounds__(kBlock) seg_warp_kernel(const int32_t* __restr
     double acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
-    strided_sum<Op, 32>(op, idx, val, b, e, lane, acc);
+    strided_sum<Op, 32, true>(op, idx, val, b, e, lane, acc);
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = warp_combine<MX>(acc[r]);
     if (lane == 0) op.finish(s, acc, pre, red);
@@ -362,7 +383,9 @@ __global__ void __launch_bounds__(B) seg_cta_kernel(const int32_t* __restrict__ 
   for (int r = 0; r < R; ++r) acc[r] = 0.0;
   if (own) {
     if (t == 0) pre = op.prefetch(s);
-    strided_sum<Op, T>(op, idx, val, ptr[s], ptr[s + 1], t, acc);
+    strided_sum<Op, T, true>(op, idx, val, ptr[s], ptr[s + 1], t, acc);
+  } else {
+    pdl_wait_trigger();
   }
   const int warp = threadIdx.x >> 5;
 #pragma unroll
@@ -384,29 +407,30 @@ __global__ void __launch_bounds__(B) seg_cta_kernel(const int32_t* __restrict__ 
 }
 
 template <class Op>
-inline void launch_thread_class(const Layout& L, const Op& op, double* red, cudaStream_t st) {
+inline void launch_thread_class(const Layout& L, const Op& op, double* red, cudaStream_t st, bool pdl = false) {
+  const int g = L.nb_s();
   if constexpr (UniformOk<Op>::value) {
     switch (L.s_len) {
-      case 1: seg_thread_uniform_kernel<Op, 1><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
-      case 2: seg_thread_uniform_kernel<Op, 2><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
-      case 3: seg_thread_uniform_kernel<Op, 3><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
-      case 4: seg_thread_uniform_kernel<Op, 4><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
-      case 8: seg_thread_uniform_kernel<Op, 8><<<L.nb_s(), kBlock, 0, st>>>(L.idx, L.val, L.s1, op, red); return;
+      case 1: return launch_k(seg_thread_uniform_kernel<Op, 1>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
+      case 2: return launch_k(seg_thread_uniform_kernel<Op, 2>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
+      case 3: return launch_k(seg_thread_uniform_kernel<Op, 3>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
+      case 4: return launch_k(seg_thread_uniform_kernel<Op, 4>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
+      case 8: return launch_k(seg_thread_uniform_kernel<Op, 8>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
       default: break;
     }
   }
   if (L.s_staged)
-    seg_thread_staged_kernel<Op><<<L.nb_s(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, op, red);
+    launch_k(seg_thread_staged_kernel<Op>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red);
   else
-    seg_thread_kernel<Op><<<L.nb_s(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, op, red);
+    launch_k(seg_thread_kernel<Op>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red);
 }
 
 template <class Op>
-inline void launch_cta_class(const Layout& L, const Op& op, double* red, cudaStream_t st) {
+inline void launch_cta_class(const Layout& L, const Op& op, double* red, cudaStream_t st, bool pdl = false) {
   if (L.l_rpc == 4)
-    seg_cta_kernel<Op, 4><<<L.nb_l(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s2, L.s3, op, red);
+    launch_k(seg_cta_kernel<Op, 4>, L.nb_l(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s2, L.s3, op, red);
   else
-    seg_cta_kernel<Op, 1><<<L.nb_l(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s2, L.s3, op, red);
+    launch_k(seg_cta_kernel<Op, 1>, L.nb_l(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s2, L.s3, op, red);
 }
 
 // Reduction slots of one pass: [S blocks | M blocks | L CTAs | XL tiles | XL spans].
@@ -415,18 +439,36 @@ struct RedSlots {
   double* at(int64_t slot, int nr) const { return base ? base + slot * nr : nullptr; }
 };
 
+// Programmatic dependent launch for a pass that is one kernel of an opted-in
+// Op (the per-iteration steps): its prologue overlaps the previous step's
+// drain. PDHG_PDL=0 disables it.
+inline bool& pdl_suspended() {  // per-kernel timing: launches must not overlap each other
+  static thread_local bool v = false;
+  return v;
+}
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PDHG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on && !pdl_suspended();
+}
+
 template <class Op>
 inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, cudaStream_t st) {
   constexpr int nr = Op::kRed > 0 ? Op::kRed : 1;
+  const int nclass = (L.s1 > 0) + (L.s2 > L.s1) + (L.s3 > L.s2) + (L.nseg > L.s3);
+  const bool pdl = PdlOk<Op>::value && nclass == 1 && pdl_enabled();
   int64_t slot = 0;
-  if (L.s1 > 0) launch_thread_class(L, op, red.at(slot, nr), st);
+  if (L.s1 > 0) launch_thread_class(L, op, red.at(slot, nr), st, pdl);
   slot += L.nb_s();
   if (L.s2 > L.s1)
-    seg_warp_kernel<Op><<<L.nb_m(), kBlock, 0, st>>>(L.ptr, L.idx, L.val, L.s1, L.s2, op, red.at(slot, nr));
+    launch_k(seg_warp_kernel<Op>, L.nb_m(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, L.s2, op,
+             red.at(slot, nr));
   slot += L.nb_m();
-  if (L.s3 > L.s2) launch_cta_class(L, op, red.at(slot, nr), st);
+  if (L.s3 > L.s2) launch_cta_class(L, op, red.at(slot, nr), st, pdl);
   slot += L.nb_l();
-  if (L.nseg > L.s3) launch_tiles(L.lng, op, red.at(slot, nr), red.at(slot + L.nt_x(), nr), st);
+  if (L.nseg > L.s3) launch_tiles(L.lng, op, red.at(slot, nr), red.at(slot + L.nt_x(), nr), st, pdl);
 }
 
 // A main stream plus side streams: the class kernels of one pass are

@@ -117,6 +117,7 @@ struct OpPrimal {
   static constexpr bool kMax = false;
   static constexpr bool kL = !(kBnd & 1), kU = !(kBnd & 2);  // streamed?
   static constexpr bool kUniform = true;                     // per-iteration: specialise
+  static constexpr bool kPdl = true;                         // programmatic dependent launch
   static constexpr int kIL = 2, kIU = 2 + kL, kIB = 2 + kL + kU;  // operand slots
   struct Pre {
     double x, c, l, u, xbar, w, step;
@@ -182,6 +183,7 @@ struct OpDual {
   static constexpr int kRhs = 1, kRed = kAdapt ? 2 : 0;
   static constexpr bool kMax = false;
   static constexpr bool kUniform = true;
+  static constexpr bool kPdl = true;
   struct Pre {
     double kx, y, q, ybar, w, step;
   };

@@ -1581,40 +1581,36 @@ double Session::OpNorm(int iters, uint64_t seed) {
   const int64_t ns = static_cast<int64_t>(shards_.size());
   launches_ += static_cast<int64_t>(iters) * (launches_csr() + launches_csc() + ns + (ns > 1) + 1) + launches_csr() +
                ns + (ns > 1);
-  // The 100 power steps (+ the final K u pass) are one captured graph per
-  // session, replayed on every solve: no per-step launch latency.
-  auto body = [&] {
-    for (int it = 0; it < iters; ++it) {
-      for (Shard& h : shards_) run_pass(h.csr, OpPowerStep<false>{u, scal_.p, 1, kv + h.roff}, RedSlots{}, fork_);
-      GatherY(kv);
-      for (size_t k = 0; k < shards_.size(); ++k) {
-        Shard& h = shards_[k];
-        run_pass(h.csc, OpPowerStep<true>{kv, scal_.p, 0, u + h.coff}, RedSlots{h.red[1].p}, fork_);
-        k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), 1, red_out_.p + k * kPack);
-      }
-      SumPacks(1);
-      k_power_norm<<<1, 1, 0, st_>>>(red_out_.p, scal_.p);
-      GatherX(u);
-    }
+  // One power step is a captured graph per session, replayed `iters` times
+  // (a 100-step graph costs more to instantiate than it saves for a
+  // one-shot solve); the final K u pass is launched directly.
+  auto step = [&] {
+    for (Shard& h : shards_) run_pass(h.csr, OpPowerStep<false>{u, scal_.p, 1, kv + h.roff}, RedSlots{}, fork_);
+    GatherY(kv);
     for (size_t k = 0; k < shards_.size(); ++k) {
       Shard& h = shards_[k];
-      run_pass(h.csr, OpPowerStep<true>{u, scal_.p, 1, kv + h.roff}, RedSlots{h.red[0].p}, fork_);
-      k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[0].p, nullptr, h.csr.parts(), 1, red_out_.p + k * kPack);
+      run_pass(h.csc, OpPowerStep<true>{kv, scal_.p, 0, u + h.coff}, RedSlots{h.red[1].p}, fork_);
+      k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), 1, red_out_.p + k * kPack);
     }
     SumPacks(1);
+    k_power_norm<<<1, 1, 0, st_>>>(red_out_.p, scal_.p);
+    GatherX(u);
   };
-  if (power_iters_ != iters) {
-    if (power_graph_) cudaGraphExecDestroy(power_graph_);
-    power_graph_ = nullptr;
+  if (!power_graph_) {
     cudaGraph_t graph;
     PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-    body();
+    step();
     PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
     PDHG_CUDA(cudaGraphInstantiate(&power_graph_, graph, 0));
     cudaGraphDestroy(graph);
-    power_iters_ = iters;
   }
-  PDHG_CUDA(cudaGraphLaunch(power_graph_, st_));
+  for (int it = 0; it < iters; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph_, st_));
+  for (size_t k = 0; k < shards_.size(); ++k) {
+    Shard& h = shards_[k];
+    run_pass(h.csr, OpPowerStep<true>{u, scal_.p, 1, kv + h.roff}, RedSlots{h.red[0].p}, fork_);
+    k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[0].p, nullptr, h.csr.parts(), 1, red_out_.p + k * kPack);
+  }
+  SumPacks(1);
   check_launch("power iteration");
   double sum = 0.0;
   Scalars hs{};
@@ -1708,6 +1704,10 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   for (int w = 0; w < 3; ++w) LaunchStep(w & 1, w, false);
   Sync();
   float t_p = 0, t_d = 0, t_i = 0;
+  // Per-kernel times: back-to-back launches of ONE kernel, without
+  // programmatic overlap between them (that overlap belongs to the
+  // primal -> dual chain, measured by the graph-launched block below).
+  pdl_suspended() = true;
   PDHG_CUDA(cudaEventRecord(e0, st_));
   for (int i = 0; i < iters; ++i) {
     for (Shard& h : shards_) LaunchPrimal(h, 0, 1, i + 1, false);
@@ -1725,6 +1725,7 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
     GatherY(y_[1].p);
   }
   PDHG_CUDA(cudaEventRecord(e2, st_));
+  pdl_suspended() = false;
   PDHG_CUDA(cudaEventSynchronize(e2));
   PDHG_CUDA(cudaEventElapsedTime(&t_p, e0, e1));
   PDHG_CUDA(cudaEventElapsedTime(&t_d, e1, e2));

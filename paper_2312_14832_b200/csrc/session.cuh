@@ -176,8 +176,7 @@ class Session {
 
   std::vector<Graph> graphs_;
   std::vector<Graph> blocks_;  // pipelined-loop block graphs
-  cudaGraphExec_t power_graph_ = nullptr;  // EstimateOpNorm steps (OpNorm)
-  int power_iters_ = 0;
+  cudaGraphExec_t power_graph_ = nullptr;  // one EstimateOpNorm step (OpNorm)
   DArray<char> flush_;
   cudaEvent_t ev_[2] = {nullptr, nullptr};
   double last_ms_ = 0.0;

@@ -43,6 +43,43 @@ struct Nil {};
 
 // Ops with `bool skip()` abandon the whole launch when it returns true (the
 // pipelined loop's discarded blocks); evaluated before any barrier.
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains. Each pass kernel runs its independent prologue (the
+// static matrix stream, per-segment operands written two kernels back), then
+// waits for the predecessor grid (griddepcontrol.wait) before touching the
+// gathered operand or writing anything, then lets its own successor launch.
+// Both instructions are no-ops for normally launched kernels.
+__device__ __forceinline__ void pdl_wait_trigger() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <class Kern, class... Args>
+inline void launch_k(Kern kernel, int grid, int block, size_t smem, cudaStream_t st, bool pdl, Args... args) {
+  if (!pdl) {
+    kernel<<<grid, block, smem, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// Ops that opt into programmatic dependent launch (the per-iteration steps).
+template <class T, class = void>
+struct PdlOk : std::false_type {};
+template <class T>
+struct PdlOk<T, std::void_t<decltype(T::kPdl)>> : std::integral_constant<bool, T::kPdl> {};
+
 template <class T, class = void>
 struct HasSkip : std::false_type {};
 template <class T>
@@ -179,6 +216,7 @@ __global__ void __launch_bounds__(kBlock, Op::kOcc) tile_kernel(const CMat M, co
     }
   }
   mbar_wait(bar, 0);
+  pdl_wait_trigger();
 
   // ---- Gather + rounded products, in place over the staged values.
   {
@@ -399,14 +437,15 @@ __global__ void __launch_bounds__(kBlock, Op::kOcc) tile_kernel(const CMat M, co
 }
 
 template <class Op>
-inline void launch_tiles(const CMat& M, const Op& op, double* tile_red, double* span_red, cudaStream_t st) {
+inline void launch_tiles(const CMat& M, const Op& op, double* tile_red, double* span_red, cudaStream_t st,
+                         bool pdl = false) {
   constexpr int bytes = smem_bytes(Op::kRhs, Op::kOps);
   static bool configured = false;  // per instantiation; attribute is per device function
   if (!configured) {
     cudaFuncSetAttribute(tile_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     configured = true;
   }
-  tile_kernel<Op><<<M.ntiles, kBlock, bytes, st>>>(M, op, tile_red, span_red);
+  launch_k(tile_kernel<Op>, M.ntiles, kBlock, bytes, st, pdl, M, op, tile_red, span_red);
 }
 
 }  // namespace pdhg

@@ -5,11 +5,26 @@ import numpy as np
 import pytest
 
 from paper_2312_14832_b200 import rpdlp
-from paper_2312_14832_b200.rpdlp import GenPagerank, GenRandomLp, GenTransport, Session, SolverParams
+from paper_2312_14832_b200.rpdlp import (CsrMatrix, GenMcf, GenPagerank, GenRandomLp, GenStaircase, GenTransport,
+                                         LpProblem, Session, SolverParams)
 
 from problems import config1, empty_rows_lp, hand_dual_lp, hand_primal_lp, long_row_lp, mixed_bounds_lp, small_cases
 
 pytestmark = pytest.mark.gpu
+
+
+def uniform_columns_lp(L, n=3000, m=500, seed=4):
+    """Every column holds exactly L nonzeros: the uniform-length class-S
+    kernel (implicit offsets, vector loads) for L in {1, 2, 3, 4, 8}."""
+    rng = np.random.default_rng(seed)
+    trips = []
+    for j in range(n):
+        for i in rng.choice(m, size=L, replace=False):
+            trips.append((int(i), j, float(rng.uniform(-1, 1)) or 0.5))
+    g = CsrMatrix.from_triplets(m, n, trips)
+    x = rng.uniform(0, 1, n)
+    h = g.to_dense() @ x - 0.1
+    return LpProblem(CsrMatrix.empty(0, n), g, rng.uniform(-1, 1, n), np.zeros(0), h, np.zeros(n), np.full(n, 2.0))
 
 
 def kernel_cases():
@@ -18,6 +33,12 @@ def kernel_cases():
     d["long_row"] = long_row_lp()
     d["pagerank_3k"] = GenPagerank(3000, 0.85, 6, 2)
     d["transport_60x70"] = GenTransport(60, 70, 3)
+    d["transport_600x40"] = GenTransport(600, 40, 2)  # 600-long demand rows: 4 rows per CTA
+    d["mcf"] = GenMcf(80, 600, 6, 3)                    # columns of exactly 3
+    d["staircase_d8"] = GenStaircase(5, 40, 60, 8, 2, seed=2)  # rows of exactly 8
+    d["staircase_d20"] = GenStaircase(4, 50, 70, 20, 5, seed=3)  # warp-staged rows
+    for L in (1, 4, 8):
+        d[f"cols_len{L}"] = uniform_columns_lp(L)
     return d
 
 

@@ -203,3 +203,11 @@ def test_pipelined_loop_matches_synchronous(case, monkeypatch):
     assert a.report.primal_obj == b.report.primal_obj
     assert [(e.iteration, e.restarted, e.candidate_is_current, e.omega, e.kkt_candidate) for e in ta] == \
         [(e.iteration, e.restarted, e.candidate_is_current, e.omega, e.kkt_candidate) for e in tb]
+
+
+@pytest.mark.parametrize("name", ["transport_600x40", "mcf", "staircase_d8", "staircase_d20", "cols_len4"])
+def test_kernel_variant_solves(name, restatement):
+    """Solve parity on the instances that route through the uniform-length,
+    warp-staged and 4-rows-per-CTA kernels (test_gpu_kernels.CASES)."""
+    from test_gpu_kernels import CASES
+    parity(CASES[name], SolverParams(eps=1e-6, iter_limit=40000), restatement)

@@ -105,7 +105,13 @@ void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, int bit
 constexpr int64_t kSegWeight = 6;
 
 // Mean class-S segment length from which the warp-staged S kernel is used.
-constexpr double kStagedMin = 6.0;
+constexpr double kStagedMin = 3.0;
+
+// Class S (one thread per segment, storage-order sums -- bit-exact with the
+// reference) takes segments up to this length; past 32 they go through the
+// warp-staged kernel, whose coalesced chunks beat a warp per 33..64 segment
+// (MCF capacity rows of 50: dual 497 -> 337 us).
+constexpr int kThreadMax = 64;
 
 // Mean class-L segment length up to which a CTA takes 4 segments.
 constexpr double kRpc4Max = 2048.0;
@@ -398,16 +404,15 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     kc.alloc(std::max<int64_t>(n_, 1));
     hist.alloc(2 * nkeys);
     PDHG_CUDA(cudaMemsetAsync(hist.p, 0, 2 * nkeys * sizeof(int32_t), st_));
-    // Class bounds: kSeqMax / kWarpMax / kCtaMax unless overridden
-    // (PDHG_THREAD_MAX <= 32, PDHG_WARP_MAX, PDHG_CTA_MAX; tuning experiments).
-    // Segments of <= 32 nonzeros keep the reference's summation order in the
-    // thread class and in the tile engine; the warp / CTA classes only get
-    // them if PDHG_WARP_MAX is lowered below 32 by hand.
+    // Class bounds: kThreadMax / kWarpMax / kCtaMax unless overridden
+    // (PDHG_THREAD_MAX <= 64, PDHG_WARP_MAX, PDHG_CTA_MAX; tuning experiments).
+    // Class S sums every segment in storage order (the reference's order);
+    // the tile engine does so for segments <= 32.
     auto env_int = [](const char* k, int d) {
       const char* v = std::getenv(k);
       return v ? std::max(0, std::atoi(v)) : d;
     };
-    const int thread_max = std::min(kSeqMax, env_int("PDHG_THREAD_MAX", kSeqMax));
+    const int thread_max = std::min(kThreadMax, env_int("PDHG_THREAD_MAX", kThreadMax));
     const int warp_max = std::max(thread_max, env_int("PDHG_WARP_MAX", kWarpMax));
     const int cta_max = std::max(warp_max, env_int("PDHG_CTA_MAX", kCtaMax));
     k_class_keys<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, m1_, rbeg.p, world_, thread_max, warp_max, cta_max,

@@ -412,7 +412,7 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       const char* v = std::getenv(k);
       return v ? std::max(0, std::atoi(v)) : d;
     };
-    const int thread_max = std::min(kThreadMax, env_int("PDHG_THREAD_MAX", kThreadMax));
+    const int thread_max = std::min(512, env_int("PDHG_THREAD_MAX", kThreadMax));
     const int warp_max = std::max(thread_max, env_int("PDHG_WARP_MAX", kWarpMax));
     const int cta_max = std::max(warp_max, env_int("PDHG_CTA_MAX", kCtaMax));
     k_class_keys<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, m1_, rbeg.p, world_, thread_max, warp_max, cta_max,

@@ -274,6 +274,23 @@ int pdhg_dual_step(const pdhg_lp* lp, const double* x_new,
                    const double* x_old, const double* y, double eta,
                    double omega, double* out, char* err, size_t errlen);
 
+/* ---- scaling and residual utilities (scaling.hpp:49-59, kkt.hpp:45-60) ----
+ * Device-backed; the device is $PDHG_DEVICE (default 0).
+ * pdhg_compute_scaling: stages 1 = RuizEquilibrate(k, ruiz_iters)
+ * (scaling.cpp:49-68), 2 = PockChambolleScale(k, pc_alpha) (:70-84),
+ * 3 = ComputeScaling (:86-91; Ruiz then PC on the Ruiz-scaled matrix,
+ * composed). row_scale has k->rows entries, col_scale k->cols. */
+int pdhg_compute_scaling(const pdhg_csr* k, int ruiz_iters, double pc_alpha,
+                         int stages, double* row_scale, double* col_scale,
+                         char* err, size_t errlen);
+/* ComputeResiduals(problem, {x, y}) (kkt.cpp:143-145) on the original
+ * problem. */
+int pdhg_residuals(const pdhg_lp* lp, const double* x, const double* y,
+                   pdhg_report* out, char* err, size_t errlen);
+/* DeriveLambda(problem, y) (kkt.cpp:127-141): lambda (n). */
+int pdhg_derive_lambda(const pdhg_lp* lp, const double* y, double* lambda,
+                       char* err, size_t errlen);
+
 /* ---- bench instrumentation ------------------------------------------------
  * flush_l2 writes a buffer of twice the L2 size on the session stream.
  * last_solve reports the device time of the most recent pdhg_session_solve

@@ -99,6 +99,10 @@ SIGNATURES = {
                                      C.c_void_p, C.POINTER(Result), C.c_char_p, C.c_size_t]),
     "pdhg_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
     "pdhg_session_blocks": (C.c_int, [C.c_void_p, i64ptr, i64ptr]),
+    "pdhg_compute_scaling": (C.c_int, [C.POINTER(Csr), C.c_int, C.c_double, C.c_int, dptr, dptr, C.c_char_p,
+                                       C.c_size_t]),
+    "pdhg_residuals": (C.c_int, [C.POINTER(Lp), dptr, dptr, C.POINTER(Report), C.c_char_p, C.c_size_t]),
+    "pdhg_derive_lambda": (C.c_int, [C.POINTER(Lp), dptr, dptr, C.c_char_p, C.c_size_t]),
     "pdhg_session_ghost_counts": (C.c_int, [C.c_void_p, i64ptr, i64ptr, C.POINTER(C.c_int32)]),
     "pdhg_partition_blocks": (C.c_int, [i64ptr, C.c_int64, C.c_int, C.c_int64, i64ptr]),
     "pdhg_normal_vector": (C.c_int, [C.c_uint64, C.c_int64, C.c_int, dptr]),

@@ -10,6 +10,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "host_logic.h"
 #include "normal_rng.h"
@@ -60,6 +61,13 @@ void ValidateParams(const pdhg_params& p) {
   if (!(0.0 < p.long_loop_frac && p.long_loop_frac < 1.0)) Invalid("long_loop_frac must lie in (0, 1)");
   if (p.check_every < 1) Invalid("check_every must be >= 1");
   if (p.iter_limit < 0) Invalid("negative iter_limit");
+}
+
+// Device for the unit-level entry points ($PDHG_DEVICE, default 0), as the
+// C++ shim chooses it for Solve.
+int DeviceFromEnv() {
+  const char* d = std::getenv("PDHG_DEVICE");
+  return d ? std::atoi(d) : 0;
 }
 
 pdhg::ShardSpec Spec(const pdhg_shard_spec& s) {
@@ -161,6 +169,57 @@ int pdhg_nccl_unique_id(void* out128, char* err, size_t errlen) {
 
 int pdhg_session_blocks(pdhg_session* s, int64_t* row_begin, int64_t* col_begin) {
   return Guard(nullptr, 0, [&] { S(s).Blocks(row_begin, col_begin); });
+}
+
+int pdhg_compute_scaling(const pdhg_csr* k, int ruiz_iters, double pc_alpha, int stages, double* row_scale,
+                         double* col_scale, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!k || stages < 1 || stages > 3 || ruiz_iters < 0) Invalid("invalid scaling request");
+    const int64_t n = k->cols, m = k->rows;
+    std::vector<double> zn(static_cast<size_t>(n), 0.0), zm(static_cast<size_t>(m), 0.0);
+    std::vector<int64_t> ap{0};
+    pdhg_lp lp{};
+    lp.a = {0, n, ap.data(), nullptr, nullptr};
+    lp.g = *k;
+    lp.n = n;
+    lp.c = zn.data();
+    lp.l = zn.data();
+    lp.u = zn.data();
+    lp.h = zm.data();
+    ValidateLp(lp);
+    pdhg_params p;
+    pdhg_params_default(&p);
+    p.scaling_enabled = 1;
+    p.ruiz_iters = (stages & 1) ? ruiz_iters : 0;
+    p.pc_alpha = pc_alpha;
+    pdhg::Session sess(lp, p, DeviceFromEnv(), pdhg::ShardSpec{}, !(stages & 2));
+    sess.Scaling(row_scale, col_scale);
+  });
+}
+
+int pdhg_residuals(const pdhg_lp* lp, const double* x, const double* y, pdhg_report* out, char* err,
+                   size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!lp || !x || !y || !out) Invalid("null argument");
+    ValidateLp(*lp);
+    pdhg_params p;
+    pdhg_params_default(&p);
+    p.scaling_enabled = 0;
+    pdhg::Session sess(*lp, p, DeviceFromEnv());
+    sess.Residuals(x, y, out);
+  });
+}
+
+int pdhg_derive_lambda(const pdhg_lp* lp, const double* y, double* lambda, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!lp || !y || !lambda) Invalid("null argument");
+    ValidateLp(*lp);
+    pdhg_params p;
+    pdhg_params_default(&p);
+    p.scaling_enabled = 0;
+    pdhg::Session sess(*lp, p, DeviceFromEnv());
+    sess.Lambda(y, lambda);
+  });
 }
 
 int pdhg_session_ghost_counts(pdhg_session* s, int64_t* x_counts, int64_t* y_counts, int32_t* use) {

@@ -125,7 +125,8 @@ struct CheckOut {
 };
 
 // ============================================================== construction
-Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const ShardSpec& spec) : device_(device) {
+Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const ShardSpec& spec, bool skip_pc)
+    : device_(device), skip_pc_(skip_pc) {
   if (spec.world < 1 || spec.world > 64) throw Error(PDHG_INVALID_ARGUMENT, "shard world must lie in [1, 64]");
   if (spec.local != 1 && spec.local != spec.world)
     throw Error(PDHG_INVALID_ARGUMENT, "a session holds either one shard or all of them");
@@ -419,8 +420,8 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
                                                kr.p);
     k_class_keys<<<ew_grid(n_), kEw, 0, st_>>>(cptr0.p, n_, n_, cbeg.p, world_, thread_max, warp_max, cta_max,
                                                kc.p);
-    k_key_hist<<<ew_grid(m_), kEw, 0, st_>>>(kr.p, m_, hist.p);
-    k_key_hist<<<ew_grid(n_), kEw, 0, st_>>>(kc.p, n_, hist.p + nkeys);
+    k_key_hist<<<ew_grid(m_), kEw, 0, st_>>>(kr.p, m_, hist.p, nkeys);
+    k_key_hist<<<ew_grid(n_), kEw, 0, st_>>>(kc.p, n_, hist.p + nkeys, nkeys);
     int bits = 3;
     while ((1 << bits) < nkeys) ++bits;
     const char* dord = std::getenv("PDHG_DEGREE_ORDER");
@@ -816,6 +817,7 @@ void Session::ComputeScaling(const pdhg_params& prm) {
     auto mode_of = [](double p) { return p == 0.0 ? 0 : (p == 1.0 ? 1 : (p == 2.0 ? 2 : 3)); };
     const double pr = 2.0 - prm.pc_alpha, pc = prm.pc_alpha;
     for (Shard& h : shards_) {
+      if (skip_pc_) break;  // RuizEquilibrate alone (pdhg_compute_scaling)
       run_pass(h.csr, OpPowerSumScale{pr, mode_of(pr), rs_.p + h.roff}, none, st_);
       run_pass(h.csc, OpPowerSumScale{pc, mode_of(pc), cs_.p + h.coff}, none, st_);
     }
@@ -1767,6 +1769,43 @@ void Session::UnitPrimal(const double* x, const double* y, double eta, double om
   GatherXFull(dout.p);
   check_launch("primal step");
   ToHost(dout.p, nullptr, pad_c_, out, n_);
+}
+
+// ComputeResiduals (kkt.cpp:143-145) of (x, y) on this session's problem in
+// its ORIGINAL space: one check pass with the point standing in for the
+// average, the "original" half of the pack.
+void Session::Residuals(const double* x, const double* y, pdhg_report* out) {
+  PDHG_CUDA(cudaSetDevice(device_));
+  ToInternal(x, pad_c_, x_[0].p, n_, np_);
+  ToInternal(y, pad_r_, y_[0].p, m_, mp_);
+  // The check works in the scaled space: map the original point into it.
+  k_div<<<ew_grid(np_), kEw, 0, st_>>>(x_[0].p, cs_.p, x_[0].p, np_);
+  k_div<<<ew_grid(mp_), kEw, 0, st_>>>(y_[0].p, rs_.p, y_[0].p, mp_);
+  GatherXFull(x_[0].p);
+  GatherYFull(y_[0].p);
+  for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, st_);
+  Copy(xstart_.p, x_[0].p, np_);
+  Copy(ystart_.p, y_[0].p, mp_);
+  LaunchCheck(x_[0].p, y_[0].p, x_[0].p, y_[0].p, kx_[0].p);
+  CheckOut ck;
+  ReadCheck(&ck);
+  *out = MakeReport(ck.row[kPrO], ck.col[kDuO], ck.col[kBdO], ck.col[kCxO], ck.row[kQyO], offset_, q_norm_o_,
+                    c_norm_o_);
+}
+
+// DeriveLambda (kkt.cpp:127-141) for an original-space y.
+void Session::Lambda(const double* y, double* out) {
+  PDHG_CUDA(cudaSetDevice(device_));
+  ToInternal(y, pad_r_, y_[0].p, m_, mp_);
+  k_div<<<ew_grid(mp_), kEw, 0, st_>>>(y_[0].p, rs_.p, y_[0].p, mp_);
+  GatherYFull(y_[0].p);
+  for (Shard& h : shards_) {
+    const int64_t c = h.coff;
+    run_pass(h.csc, OpLambda{y_[0].p, c_o_.p + c, l_o_.p + c, u_o_.p + c, cs_.p + c, nvec_.p + c}, RedSlots{}, st_);
+  }
+  GatherXFull(nvec_.p);
+  check_launch("lambda");
+  ToHost(nvec_.p, nullptr, pad_c_, out, n_);
 }
 
 void Session::UnitDual(const double* xn, const double* xo, const double* y, double eta, double omega, double* out) {

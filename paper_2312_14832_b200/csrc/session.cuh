@@ -36,7 +36,8 @@ struct ShardSpec {
 
 class Session {
  public:
-  Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const ShardSpec& spec = ShardSpec{});
+  Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const ShardSpec& spec = ShardSpec{},
+          bool skip_pc = false);
   ~Session();
 
   void Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_result* out);
@@ -49,6 +50,8 @@ class Session {
   void Blocks(int64_t* row_begin, int64_t* col_begin) const;
   void GhostCounts(int64_t* x_counts, int64_t* y_counts, int32_t* use) const;
   void UnitPrimal(const double* x, const double* y, double eta, double omega, double* out);
+  void Residuals(const double* x, const double* y, pdhg_report* out);
+  void Lambda(const double* y, double* out);
   void UnitDual(const double* xn, const double* xo, const double* y, double eta, double omega, double* out);
   int device() const { return device_; }
   void FlushL2();
@@ -123,6 +126,7 @@ class Session {
   int launches_csc() const;
 
   int device_ = 0;
+  bool skip_pc_ = false;  // scaling = Ruiz sweeps only (pdhg_compute_scaling)
   cudaStream_t st_ = nullptr;
   Fork fork_;  // st_ + side streams for parallel class kernels
   Arena arena_;

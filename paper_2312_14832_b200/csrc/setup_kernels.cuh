@@ -132,8 +132,14 @@ __global__ void k_len_minmax(const int32_t* p, int64_t nseg, int* out) {
     mn = len < mn ? len : mn;
     mx = len > mx ? len : mx;
   }
-  atomicMin(out, mn);
-  atomicMax(out + 1, mx);
+  for (int o = 16; o > 0; o >>= 1) {  // one atomic pair per warp
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, mn);
+    atomicMax(out + 1, mx);
+  }
 }
 
 // Neighbouring segments whose middle entries gather from the same 32-byte
@@ -151,7 +157,8 @@ __global__ void k_adjacent_count(const int32_t* p, const int32_t* idx, int32_t l
       c += (d >= -3 && d <= 3) ? 1 : 0;
     }
   }
-  atomicAdd(out, c);
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
 // Ghost plans: mark every gathered index; count marked indices per block.
@@ -171,8 +178,17 @@ __global__ void k_gather_i32(const int32_t* in, const int32_t* perm, int32_t* ou
   GRID_STRIDE(i, n) out[i] = in[perm[i]];
 }
 
-__global__ void k_key_hist(const int32_t* key, int64_t n, int32_t* hist) {
-  GRID_STRIDE(i, n) atomicAdd(hist + key[i], 1);
+// Histogram of class keys (< nkeys <= 512): per-block shared-memory counts,
+// one global atomic per non-empty bin and block (a global atomic per key
+// serialised on the few hot bins: 0.3 ms for 1M columns).
+__global__ void k_key_hist(const int32_t* key, int64_t n, int32_t* hist, int nkeys) {
+  __shared__ int32_t sh[512];
+  for (int i = threadIdx.x; i < nkeys; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  GRID_STRIDE(i, n) atomicAdd(sh + key[i], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nkeys; i += blockDim.x)
+    if (sh[i]) atomicAdd(hist + i, sh[i]);
 }
 
 __global__ void k_invert(const int32_t* perm, int32_t* inv, int64_t n) {

@@ -2,6 +2,7 @@
 #ifndef RPDLP_B200_KKT_HPP_
 #define RPDLP_B200_KKT_HPP_
 
+#include <span>
 #include <vector>
 
 #include "rpdlp/lp_problem.hpp"
@@ -27,6 +28,26 @@ struct ResidualReport {
 
 bool CheckTermination(const ResidualReport& report, double eps);
 double KktError(double primal_res, double dual_res, double gap, double omega);
+
+// Device-backed (pdhg_residuals / pdhg_derive_lambda; $PDHG_DEVICE).
+std::vector<double> DeriveLambda(const LpProblem& problem, std::span<const double> y);
+ResidualReport ComputeResiduals(const LpProblem& problem, const Iterate& z);
+double KktOmega(const LpProblem& problem, const Iterate& z, double omega);
+
+// kkt.hpp:59-77 interface; each Evaluate is one device residual pass.
+class ResidualEvaluator {
+ public:
+  explicit ResidualEvaluator(const LpProblem& problem);
+  ResidualReport Evaluate(std::span<const double> x, std::span<const double> y) const;
+  double KktOmega(std::span<const double> x, std::span<const double> y, double omega) const;
+  double q_norm() const { return q_norm_; }
+  double c_norm() const { return c_norm_; }
+
+ private:
+  const LpProblem& problem_;
+  double q_norm_;
+  double c_norm_;
+};
 
 }  // namespace rpdlp
 

@@ -506,3 +506,124 @@ LpProblem GenStaircase(Index stages, Index rows_per_stage, Index cols_per_stage,
 }
 
 }  // namespace rpdlp
+
+// --------------------------------------------- scaling / residual utilities
+#include "rpdlp/kkt.hpp"
+#include "rpdlp/scaling.hpp"
+
+namespace rpdlp {
+namespace {
+
+void Check(int code, const char* err) {
+  if (code == PDHG_OK) return;
+  if (code == PDHG_INVALID_ARGUMENT) throw std::invalid_argument(err);
+  throw DeviceError(std::string("libpdhg_b200: ") + err);
+}
+
+ScalingInfo Scales(const SparseMatrix& k, int iters, double alpha, int stages) {
+  ScalingInfo s{std::vector<double>(static_cast<size_t>(k.rows())), std::vector<double>(static_cast<size_t>(k.cols()))};
+  const pdhg_csr c = View(k);
+  char err[512] = {0};
+  Check(pdhg_compute_scaling(&c, iters, alpha, stages, s.row_scale.data(), s.col_scale.data(), err, sizeof(err)), err);
+  return s;
+}
+
+double Norm2(const std::vector<double>& v) {  // kkt.cpp:23-27 (sequential)
+  double acc = 0.0;
+  for (double e : v) acc += e * e;
+  return std::sqrt(acc);
+}
+
+}  // namespace
+
+ScalingInfo ScalingInfo::Identity(Index n_rows, Index n_cols) {
+  return {std::vector<double>(static_cast<size_t>(n_rows), 1.0), std::vector<double>(static_cast<size_t>(n_cols), 1.0)};
+}
+
+ScalingInfo ScalingInfo::Composed(const ScalingInfo& other) const {
+  ScalingInfo out = *this;
+  for (size_t i = 0; i < out.row_scale.size(); ++i) out.row_scale[i] *= other.row_scale[i];
+  for (size_t j = 0; j < out.col_scale.size(); ++j) out.col_scale[j] *= other.col_scale[j];
+  return out;
+}
+
+void ScalingInfo::UnscaleIterate(std::span<double> x, std::span<double> y) const {
+  for (size_t j = 0; j < x.size(); ++j) x[j] *= col_scale[j];
+  for (size_t i = 0; i < y.size(); ++i) y[i] *= row_scale[i];
+}
+
+ScalingInfo RuizEquilibrate(const SparseMatrix& k, int iters) { return Scales(k, iters, 1.0, 1); }
+
+ScalingInfo PockChambolleScale(const SparseMatrix& k, double alpha) {
+  if (alpha < 0.0 || alpha > 2.0) throw std::invalid_argument("pock-chambolle alpha must lie in [0, 2]");
+  return Scales(k, 0, alpha, 2);
+}
+
+ScalingInfo ComputeScaling(const SparseMatrix& k, const ScalingConfig& config) {
+  if (!config.enabled) return ScalingInfo::Identity(k.rows(), k.cols());
+  return Scales(k, config.ruiz_iters, config.pc_alpha, 3);
+}
+
+LpProblem ApplyScaling(const LpProblem& problem, const ScalingInfo& info) {
+  const Index m1 = problem.num_eq_rows(), m2 = problem.num_ineq_rows();
+  if (static_cast<Index>(info.row_scale.size()) != m1 + m2 ||
+      static_cast<Index>(info.col_scale.size()) != problem.num_vars())
+    throw std::invalid_argument("scaling dimensions do not match problem");
+  auto scaled = [&](const SparseMatrix& m, Index r0) {
+    std::vector<Triplet> t;
+    for (Index r = 0; r < m.rows(); ++r)
+      for (Index k = m.row_ptr()[r]; k < m.row_ptr()[r + 1]; ++k)
+        t.push_back({r, m.col_idx()[k], (info.row_scale[r0 + r] * m.csr_values()[k]) * info.col_scale[m.col_idx()[k]]});
+    return SparseMatrix::FromTriplets(m.rows(), m.cols(), std::move(t));
+  };
+  LpProblem out = problem;
+  out.a = scaled(problem.a, 0);
+  out.g = scaled(problem.g, m1);
+  for (Index i = 0; i < m1; ++i) out.b[i] = problem.b[i] * info.row_scale[i];
+  for (Index i = 0; i < m2; ++i) out.h[i] = problem.h[i] * info.row_scale[m1 + i];
+  for (size_t j = 0; j < out.c.size(); ++j) {
+    out.c[j] = problem.c[j] * info.col_scale[j];
+    out.l[j] = problem.l[j] / info.col_scale[j];
+    out.u[j] = problem.u[j] / info.col_scale[j];
+  }
+  return out;
+}
+
+std::vector<double> DeriveLambda(const LpProblem& problem, std::span<const double> y) {
+  std::vector<double> out(static_cast<size_t>(problem.num_vars()));
+  const pdhg_lp v = View(problem);
+  char err[512] = {0};
+  Check(pdhg_derive_lambda(&v, y.data(), out.data(), err, sizeof(err)), err);
+  return out;
+}
+
+ResidualReport ComputeResiduals(const LpProblem& problem, const Iterate& z) {
+  const pdhg_lp v = View(problem);
+  pdhg_report r{};
+  char err[512] = {0};
+  Check(pdhg_residuals(&v, z.x.data(), z.y.data(), &r, err, sizeof(err)), err);
+  return {r.primal_res, r.dual_res, r.gap_abs, r.primal_obj, r.dual_obj, r.rel_primal, r.rel_dual, r.rel_gap};
+}
+
+double KktOmega(const LpProblem& problem, const Iterate& z, double omega) {
+  const ResidualReport r = ComputeResiduals(problem, z);
+  return KktError(r.primal_res, r.dual_res, r.gap_abs, omega);
+}
+
+ResidualEvaluator::ResidualEvaluator(const LpProblem& problem) : problem_(problem) {
+  std::vector<double> q(problem.b);
+  q.insert(q.end(), problem.h.begin(), problem.h.end());
+  q_norm_ = Norm2(q);
+  c_norm_ = Norm2(problem.c);
+}
+
+ResidualReport ResidualEvaluator::Evaluate(std::span<const double> x, std::span<const double> y) const {
+  return ComputeResiduals(problem_, Iterate{std::vector<double>(x.begin(), x.end()), std::vector<double>(y.begin(), y.end())});
+}
+
+double ResidualEvaluator::KktOmega(std::span<const double> x, std::span<const double> y, double omega) const {
+  const ResidualReport r = Evaluate(x, y);
+  return KktError(r.primal_res, r.dual_res, r.gap_abs, omega);
+}
+
+}  // namespace rpdlp

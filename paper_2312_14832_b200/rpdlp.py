@@ -520,6 +520,94 @@ def CheckTermination(report: ResidualReport, eps: float) -> bool:
     return bool(abi.load().pdhg_check_termination(C.byref(r), eps))
 
 
+# --------------------------------------- scaling / residual utilities
+@dataclass
+class ScalingInfo:
+    """scaling.hpp:30-38: positive diagonal scales of K = [A; G]."""
+    row_scale: np.ndarray
+    col_scale: np.ndarray
+
+    @staticmethod
+    def Identity(n_rows: int, n_cols: int) -> "ScalingInfo":
+        return ScalingInfo(np.ones(n_rows), np.ones(n_cols))
+
+    def Composed(self, other: "ScalingInfo") -> "ScalingInfo":
+        return ScalingInfo(self.row_scale * other.row_scale, self.col_scale * other.col_scale)
+
+    def UnscaleIterate(self, x: np.ndarray, y: np.ndarray) -> None:
+        x *= self.col_scale
+        y *= self.row_scale
+
+
+def _scaling(k: CsrMatrix, iters: int, alpha: float, stages: int) -> ScalingInfo:
+    rs, cs = np.empty(k.rows), np.empty(k.cols)
+    csr = k.to_c()
+    err = C.create_string_buffer(abi.ERRLEN)
+    raise_for(abi.load().pdhg_compute_scaling(C.byref(csr), iters, alpha, stages, _dp(rs), _dp(cs), err,
+                                              abi.ERRLEN), err)
+    return ScalingInfo(rs, cs)
+
+
+def RuizEquilibrate(k: CsrMatrix, iters: int) -> ScalingInfo:
+    """scaling.cpp:49-68 (device)."""
+    return _scaling(k, iters, 1.0, 1)
+
+
+def PockChambolleScale(k: CsrMatrix, alpha: float) -> ScalingInfo:
+    """scaling.cpp:70-84 (device)."""
+    return _scaling(k, 0, alpha, 2)
+
+
+def ComputeScaling(k: CsrMatrix, config: Optional[ScalingConfig] = None) -> ScalingInfo:
+    """scaling.cpp:86-91: Ruiz sweeps, then PC on the Ruiz-scaled matrix, composed."""
+    config = config or ScalingConfig()
+    if not config.enabled:
+        return ScalingInfo.Identity(k.rows, k.cols)
+    return _scaling(k, config.ruiz_iters, config.pc_alpha, 3)
+
+
+def ApplyScaling(problem: LpProblem, info: ScalingInfo) -> LpProblem:
+    """scaling.cpp:93-116 (host; same operations and rounding order)."""
+    m1, m2 = problem.num_eq_rows(), problem.num_ineq_rows()
+    if len(info.row_scale) != m1 + m2 or len(info.col_scale) != problem.num_vars():
+        raise ValueError("scaling dimensions do not match problem")
+    er, ir = info.row_scale[:m1], info.row_scale[m1:]
+
+    def scaled(m: CsrMatrix, rs) -> CsrMatrix:  # Scaled: (rs * v) * cs (sparse_matrix.cpp:213)
+        rows = np.repeat(np.arange(m.rows), np.diff(m.row_ptr))
+        return CsrMatrix(m.rows, m.cols, m.row_ptr.copy(), m.col_idx.copy(),
+                         (rs[rows] * m.values) * info.col_scale[m.col_idx])
+
+    return LpProblem(scaled(problem.a, er), scaled(problem.g, ir), problem.c * info.col_scale, problem.b * er,
+                     problem.h * ir, problem.l / info.col_scale, problem.u / info.col_scale, problem.objective_offset,
+                     problem.negated_objective, problem.name)
+
+
+def ComputeResiduals(problem: LpProblem, x, y) -> ResidualReport:
+    """kkt.cpp:143-145 on the original problem (device)."""
+    lp = problem.to_c()
+    rep = abi.Report()
+    err = C.create_string_buffer(abi.ERRLEN)
+    raise_for(abi.load().pdhg_residuals(C.byref(lp), _dp(_f64(x)), _dp(_f64(y)), C.byref(rep), err, abi.ERRLEN),
+              err)
+    return ResidualReport.from_c(rep)
+
+
+def KktOmega(problem: LpProblem, x, y, omega: float) -> float:
+    """kkt.cpp:159-161."""
+    r = ComputeResiduals(problem, x, y)
+    return KktError(r.primal_res, r.dual_res, r.gap_abs, omega)
+
+
+def DeriveLambda(problem: LpProblem, y) -> np.ndarray:
+    """kkt.cpp:127-141 (device)."""
+    lp = problem.to_c()
+    out = np.empty(problem.num_vars())
+    err = C.create_string_buffer(abi.ERRLEN)
+    raise_for(abi.load().pdhg_derive_lambda(C.byref(lp), _dp(_f64(y)), _dp(out), err, abi.ERRLEN), err)
+    return out
+
+
 def PartitionBlocks(ptr, parts: int, seg_weight: int = 6) -> np.ndarray:
     """The balanced contiguous split every rank computes (host_logic.h)."""
     p = _i64(ptr)

@@ -13,7 +13,9 @@
 #include <sstream>
 
 #include "rpdlp/instance_gen.hpp"
+#include "rpdlp/kkt.hpp"
 #include "rpdlp/mps.hpp"
+#include "rpdlp/scaling.hpp"
 #include "rpdlp/solver.hpp"
 
 using namespace rpdlp;
@@ -183,7 +185,7 @@ int main() {
     SolverParams prm;
     prm.eps = 1e-8;
     SolveResult r = Solve(q, prm);
-    CHECK(r.status == SolveStatus::kOptimal && Near(r.report.primal_obj, 2.0, 1e-6));
+    CHECK(r.status == SolveStatus::kOptimal && Near(r.report.primal_obj, 2.5, 1e-6));  // x = 1.5, y = 0.5
   }
   {  // the new SURVEY §8d shapes through the drop-in generators
     SolverParams prm;
@@ -192,6 +194,30 @@ int main() {
     CHECK(r.status == SolveStatus::kOptimal);
     SolveResult s = Solve(GenStaircase(4, 20, 25, 6, 2, 10, 1), prm);
     CHECK(s.status == SolveStatus::kOptimal);
+  }
+  {  // scaling + residual API (test_scaling.cpp:27-180, test_kkt.cpp:65-101)
+    const SparseMatrix one = SparseMatrix::FromTriplets(1, 1, {{0, 0, 100.0}});
+    CHECK(Near(RuizEquilibrate(one, 10).row_scale[0], 0.1, 1e-15));
+    LpProblem p = GenRandomLp(20, 30, 0.3, 9);
+    const SparseMatrix& k = p.g;
+    ScalingInfo info = ComputeScaling(k, ScalingConfig{});
+    LpProblem s = ApplyScaling(p, info);
+    SolverParams prm;
+    prm.eps = 1e-8;
+    prm.scaling.enabled = false;
+    SolveResult rs = Solve(s, prm);
+    info.UnscaleIterate(rs.x, rs.y);
+    SolveResult ro = Solve(p, prm);
+    CHECK(std::abs(rs.report.primal_obj - ro.report.primal_obj) <= 1e-6 * (1.0 + std::abs(ro.report.primal_obj)));
+    const ResidualReport r = ComputeResiduals(p, Iterate{ro.x, ro.y});
+    CHECK(r.rel_primal <= 1e-8 && r.rel_dual <= 1e-8 && r.rel_gap <= 1e-8);
+    ResidualEvaluator ev(p);
+    CHECK(Near(ev.KktOmega(ro.x, ro.y, 1.0), KktError(r.primal_res, r.dual_res, r.gap_abs, 1.0), 1e-12));
+    const std::vector<double> lam = DeriveLambda(p, ro.y);
+    CHECK(lam.size() == ro.lambda.size());
+    double dl = 0.0;
+    for (size_t j = 0; j < lam.size(); ++j) dl = std::max(dl, std::abs(lam[j] - ro.lambda[j]));
+    CHECK(dl <= 1e-12);
   }
   std::printf("drop_in_test: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail;

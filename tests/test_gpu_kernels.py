@@ -175,3 +175,46 @@ def test_unit_steps_vs_reference(name, restatement):
                                rtol=1e-14, atol=1e-15)
     np.testing.assert_allclose(rpdlp.DualStep(p, x, xo, y, 0.3, 1.7), restatement.dual_step(p, x, xo, y, 0.3, 1.7),
                                rtol=1e-14, atol=1e-15)
+
+
+def test_scaling_api_matches_reference(restatement):
+    """ComputeScaling / RuizEquilibrate / PockChambolleScale / ApplyScaling
+    (scaling.hpp:49-59) through the device: the composed scales equal the
+    restatement's bit for bit (segments <= 64), ApplyScaling equals the
+    session's scaled problem; hand values of test_scaling.cpp:27-96."""
+    p = config1(2)
+    a, g = p.a, p.g  # K = [A; G] as one CSR
+    K = rpdlp.CsrMatrix(a.rows + g.rows, p.num_vars(), np.concatenate([a.row_ptr[:-1], a.nnz + g.row_ptr]),
+                        np.concatenate([a.col_idx, g.col_idx]), np.concatenate([a.values, g.values]))
+    info = rpdlp.ComputeScaling(K)
+    rs0, cs0 = restatement.scaling(p, SolverParams())
+    np.testing.assert_array_equal(info.row_scale, rs0)
+    np.testing.assert_array_equal(info.col_scale, cs0)
+    ruiz = rpdlp.RuizEquilibrate(K, 10)
+    pc = rpdlp.PockChambolleScale(K, 1.0)
+    assert np.all(ruiz.row_scale > 0) and np.all(pc.col_scale > 0)
+    sp = rpdlp.ApplyScaling(p, info)
+    with Session(p) as s:
+        kv, c, l, u, q = s.scaled()
+    np.testing.assert_array_equal(np.concatenate([sp.a.values, sp.g.values]), kv)
+    np.testing.assert_array_equal(sp.c, c)
+    np.testing.assert_array_equal(np.concatenate([sp.b, sp.h]), q)
+    one = rpdlp.CsrMatrix.from_triplets(1, 1, [(0, 0, 100.0)])
+    assert rpdlp.RuizEquilibrate(one, 10).row_scale[0] == pytest.approx(0.1, rel=1e-15)
+    pcs = rpdlp.PockChambolleScale(rpdlp.CsrMatrix.from_triplets(1, 2, [(0, 0, 4.0), (0, 1, 9.0)]), 1.0)
+    assert pcs.row_scale[0] == pytest.approx(1 / np.sqrt(13.0), rel=1e-15)
+    np.testing.assert_allclose(pcs.col_scale, [1 / 2.0, 1 / 3.0], rtol=1e-15)
+
+
+@pytest.mark.parametrize("name", ["mixed", "config1", "transport_60x70", "pagerank_3k"])
+def test_residuals_and_lambda_api(name, restatement):
+    """ComputeResiduals / DeriveLambda (kkt.hpp:45-57) on the device against
+    the reference: residuals of a CPU solution to 1e-12, lambda to 1e-12."""
+    p = CASES[name]
+    o = restatement.solve(p, SolverParams(eps=1e-6))
+    r = rpdlp.ComputeResiduals(p, o.x, o.y)
+    want = restatement.residuals(p, o.x, o.y)
+    for k in ("primal_res", "dual_res", "gap_abs", "primal_obj", "dual_obj", "rel_primal", "rel_dual", "rel_gap"):
+        assert getattr(r, k) == pytest.approx(getattr(want, k), rel=1e-12, abs=1e-12), k
+    lam = rpdlp.DeriveLambda(p, o.y)
+    np.testing.assert_allclose(lam, o.lambda_, rtol=1e-12, atol=1e-12)

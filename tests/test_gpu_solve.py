@@ -211,3 +211,15 @@ def test_kernel_variant_solves(name, restatement):
     warp-staged and 4-rows-per-CTA kernels (test_gpu_kernels.CASES)."""
     from test_gpu_kernels import CASES
     parity(CASES[name], SolverParams(eps=1e-6, iter_limit=40000), restatement)
+
+
+def test_cpp_drop_in_caller():
+    """tests/cpp/drop_in_test.cpp: reference-style C++ caller compiled against
+    include/rpdlp/*.hpp and linked to libpdhg_b200.so (built by build())."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parents[1] / "paper_2312_14832_b200" / "_build" / "drop_in_test"
+    assert exe.exists(), "run python -m paper_2312_14832_b200.build"
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout

@@ -223,3 +223,23 @@ def test_cpp_drop_in_caller():
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+def test_degenerate_shapes(restatement):
+    """No constraint rows (m = 0), no nonzeros at all, a single variable:
+    same status / objective / iterations as the reference restatement."""
+    from problems import lp
+    from paper_2312_14832_b200.rpdlp import CsrMatrix
+    INF = float("inf")
+    cases = [
+        lp(CsrMatrix.empty(0, 3), CsrMatrix.empty(0, 3), [1.0, -1.0, 0.5], [], [], [0.0, -2.0, -INF], [1.0, 3.0, INF]),
+        lp(CsrMatrix.empty(2, 3), CsrMatrix.empty(1, 3), [1.0, 2.0, 0.0], [0.0, 0.0], [-1.0], [0.0] * 3, [1.0] * 3),
+        lp(CsrMatrix.empty(0, 1), CsrMatrix.from_triplets(1, 1, [(0, 0, 2.0)]), [3.0], [], [4.0], [0.0], [INF]),
+    ]
+    for p in cases:
+        prm = SolverParams(eps=1e-8, iter_limit=5000)
+        g = rpdlp.Solve(p, prm)
+        o = restatement.solve(p, prm)
+        assert g.status == o.status and g.iterations == o.iterations
+        assert g.report.primal_obj == pytest.approx(o.report.primal_obj, rel=1e-9, abs=1e-12)
+        np.testing.assert_allclose(g.x, o.x, rtol=1e-9, atol=1e-12)

@@ -17,8 +17,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
+#include <deque>
 #include <limits>
+#include <mutex>
 #include <random>
 #include <thread>
 #include <vector>
@@ -37,65 +40,128 @@ inline void NormalVectorSequential(uint64_t seed, int64_t n, double* out) {
   for (int64_t i = 0; i < n; ++i) out[i] = gauss(rng);
 }
 
+// One accepted-attempt transform (random.tcc): y * mult, then x * mult.
+inline void PolarEmit(uint64_t r0, uint64_t r1, int64_t k, int64_t n, double* out) {
+  const double x = 2.0 * canonical53(r0) - 1.0;
+  const double y = 2.0 * canonical53(r1) - 1.0;
+  const double r2 = x * x + y * y;
+  const double mult = std::sqrt(-2 * std::log(r2) / r2);
+  out[2 * k] = y * mult * 1.0 + 0.0;  // __ret * stddev + mean
+  if (2 * k + 1 < n) out[2 * k + 1] = x * mult * 1.0 + 0.0;
+}
+
+inline bool PolarAccept(uint64_t r0, uint64_t r1) {
+  const double x = 2.0 * canonical53(r0) - 1.0;
+  const double y = 2.0 * canonical53(r1) - 1.0;
+  const double r2 = x * x + y * y;
+  return !(r2 > 1.0 || r2 == 0.0);
+}
+
+// Pipelined: the calling thread only runs the engine (the one inherently
+// sequential part), filling chunks of raw draws in a small ring of
+// cache-resident buffers. Workers test acceptance per chunk (publishing the
+// chunk's count), wait for the prefix of earlier chunks' counts -- the
+// chunk's output base -- and run the log / sqrt transforms. Counting never
+// blocks and chunks are taken in order, so the earliest chunk in flight can
+// always finish.
 inline void NormalVector(uint64_t seed, int64_t n, double* out, int threads) {
   if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  threads = std::min(threads, 32);
   if (threads == 1 || n < (int64_t(1) << 15)) {
     NormalVectorSequential(seed, n, out);
     return;
   }
   const int64_t need = (n + 1) / 2;  // accepted attempts
-  std::mt19937_64 rng(seed);
-  std::vector<uint64_t> raw;
-  std::vector<uint8_t> ok;
-  int64_t attempts = 0;
-  auto parallel = [&](int64_t count, auto&& fn) {  // fn(chunk, begin, end)
-    std::vector<std::thread> pool;
-    const int64_t per = (count + threads - 1) / threads;
-    for (int t = 0; t < threads; ++t) {
-      const int64_t b = std::min(count, t * per), e = std::min(count, b + per);
-      pool.emplace_back([&fn, t, b, e] { fn(t, b, e); });
-    }
-    for (auto& th : pool) th.join();
+  constexpr int kAttempts = 8192;    // per chunk (128 KB of raw draws)
+  const int workers = threads - 1;
+  const int ring = 4 * workers;
+  struct Chunk {
+    std::vector<uint64_t> raw;
+    std::vector<uint8_t> ok;
   };
-  std::vector<int64_t> counts(threads);
-  int64_t accepted = 0;
-  while (true) {
-    // Expected acceptance pi/4; a 3% + 4096 margin almost always suffices.
-    const int64_t want = attempts + static_cast<int64_t>((need - accepted) / 0.75) + 4096;
-    raw.resize(2 * want);
-    for (int64_t k = 2 * attempts; k < 2 * want; ++k) raw[k] = rng();
-    attempts = want;
-    ok.assign(attempts, 0);
-    parallel(attempts, [&](int t, int64_t b, int64_t e) {
-      int64_t c = 0;
-      for (int64_t i = b; i < e; ++i) {
-        const double x = 2.0 * canonical53(raw[2 * i]) - 1.0;
-        const double y = 2.0 * canonical53(raw[2 * i + 1]) - 1.0;
-        const double r2 = x * x + y * y;
-        ok[i] = !(r2 > 1.0 || r2 == 0.0);
-        c += ok[i];
-      }
-      counts[t] = c;
-    });
-    accepted = 0;
-    for (int64_t c : counts) accepted += c;
-    if (accepted >= need) break;
+  std::vector<Chunk> buf(ring);
+  for (Chunk& c : buf) {
+    c.raw.resize(2 * kAttempts);
+    c.ok.resize(kAttempts);
   }
-  std::vector<int64_t> base(threads, 0);
-  for (int t = 1; t < threads; ++t) base[t] = base[t - 1] + counts[t - 1];
-  parallel(attempts, [&](int t, int64_t b, int64_t e) {
-    int64_t k = base[t];
-    for (int64_t i = b; i < e && k < need; ++i) {
-      if (!ok[i]) continue;
-      const double x = 2.0 * canonical53(raw[2 * i]) - 1.0;
-      const double y = 2.0 * canonical53(raw[2 * i + 1]) - 1.0;
-      const double r2 = x * x + y * y;
-      const double mult = std::sqrt(-2 * std::log(r2) / r2);
-      out[2 * k] = y * mult * 1.0 + 0.0;  // __ret * stddev + mean
-      if (2 * k + 1 < n) out[2 * k + 1] = x * mult * 1.0 + 0.0;
-      ++k;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<std::pair<int64_t, int>> ready;  // (chunk sequence number, ring slot)
+  std::deque<int> avail;
+  for (int r = 0; r < ring; ++r) avail.push_back(r);
+  std::vector<int64_t> count, base{0};  // per chunk; base[c] valid for c < base.size()
+  std::vector<char> counted;
+  bool done = false;
+  std::vector<std::thread> pool;
+  for (int t = 0; t < workers; ++t)
+    pool.emplace_back([&] {
+      while (true) {
+        int64_t seq;
+        int r;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return done || !ready.empty(); });
+          if (ready.empty()) return;
+          seq = ready.front().first;
+          r = ready.front().second;
+          ready.pop_front();
+        }
+        Chunk& c = buf[r];
+        int64_t acc = 0;
+        for (int i = 0; i < kAttempts; ++i) acc += c.ok[i] = PolarAccept(c.raw[2 * i], c.raw[2 * i + 1]);
+        int64_t k;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          count[seq] = acc;
+          counted[seq] = 1;
+          for (size_t q = base.size() - 1; q < counted.size() && counted[q]; ++q) base.push_back(base.back() + count[q]);
+          cv.notify_all();
+          cv.wait(lk, [&] { return static_cast<int64_t>(base.size()) > seq; });
+          k = base[seq];
+        }
+        for (int i = 0; i < kAttempts && k < need; ++i)
+          if (c.ok[i]) PolarEmit(c.raw[2 * i], c.raw[2 * i + 1], k++, n, out);
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          avail.push_back(r);
+        }
+        cv.notify_all();
+      }
+    });
+  std::mt19937_64 rng(seed);
+  // Expected acceptance pi/4; 3% + one chunk of margin, more chunks if short.
+  int64_t target = static_cast<int64_t>(need / 0.75) / kAttempts + 2;
+  int64_t issued = 0;
+  while (true) {
+    for (; issued < target; ++issued) {
+      int r;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return !avail.empty(); });
+        r = avail.front();
+        avail.pop_front();
+      }
+      uint64_t* raw = buf[r].raw.data();
+      for (int i = 0; i < 2 * kAttempts; ++i) raw[i] = rng();
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        count.push_back(0);
+        counted.push_back(0);
+        ready.emplace_back(issued, r);
+      }
+      cv.notify_all();
     }
-  });
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return static_cast<int64_t>(base.size()) > issued; });
+    if (base[issued] >= need) break;
+    target += (need - base[issued]) / kAttempts + 2;
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    done = true;
+  }
+  cv.notify_all();
+  for (auto& th : pool) th.join();
 }
 
 }  // namespace pdhg

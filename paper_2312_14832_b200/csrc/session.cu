@@ -133,15 +133,31 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
   if (spec.rank < 0 || spec.rank >= spec.world) throw Error(PDHG_INVALID_ARGUMENT, "shard rank out of range");
   world_ = spec.world;
   rank_ = spec.local == spec.world ? 0 : spec.rank;
+  const char* tenv = std::getenv("PDHG_TRACE");
+  const bool fine = tenv && tenv[0] == '2';  // per-phase construction trace
+  double tp = now_s();
+  auto phase = [&](const char* what) {
+    if (!fine) return;
+    Sync();
+    const double t = now_s();
+    std::fprintf(stderr, "[pdhg]   ctor %-28s %.4fs\n", what, t - tp);
+    tp = t;
+  };
   PDHG_CUDA(cudaSetDevice(device_));
   PDHG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  streams_.st = st_;
   fork_.main = st_;
   PDHG_CUDA(cudaEventCreateWithFlags(&fork_.fork, cudaEventDisableTiming));
+  streams_.fork.fork = fork_.fork;
   for (int k = 0; k < 3; ++k) {
     PDHG_CUDA(cudaStreamCreateWithFlags(&fork_.side[k], cudaStreamNonBlocking));
     PDHG_CUDA(cudaEventCreateWithFlags(&fork_.join[k], cudaEventDisableTiming));
+    streams_.fork.side[k] = fork_.side[k];
+    streams_.fork.join[k] = fork_.join[k];
   }
-  PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&host_red_), kPack * sizeof(double) + 64));
+  AllocScope scope(st_);  // setup arrays are ordered on the session stream
+  host_red_ = static_cast<double*>(pinned_get(kPack * sizeof(double) + 64, &host_red_bytes_));
+  phase("streams+events+pinned");
   // NCCL whenever a one-shard-per-process id is given -- also for world = 1,
   // which runs the NCCL code path (collectives, graph capture, rank-0 clock,
   // abort all-reduce) on a single GPU.
@@ -165,12 +181,16 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
       DArray<int32_t> ptr0, idx0;
       DArray<double> val0;
       Upload(lp, ptr0, idx0, val0);
+      phase("upload");
       Permute(ptr0, idx0, val0);
+      phase("csc+permute");
     }
+    phase("free setup temporaries");
     for (Shard& h : shards_) {
       PartitionLong(h.csr, h.csr_st);
       PartitionLong(h.csc, h.csc_st);
     }
+    phase("partition");
     // Original-space problem vectors into padded order.
     c_o_.alloc(np_, &arena_);
     l_o_.alloc(np_, &arena_);
@@ -186,6 +206,7 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
       ToInternal(q.data(), pad_r_, q_o_.p, m_, mp_);
     }
     Sync();
+    phase("problem vectors");
     upload_s_ = now_s() - t0;
     for (int p = 0; p < 2; ++p) {
       x_[p].alloc(np_, &arena_);
@@ -212,12 +233,15 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
       h.red[1].alloc(static_cast<size_t>(std::max(h.csc.parts(), 1)) * nred, &arena_);
     }
     red_out_.alloc(static_cast<size_t>(kPack) * shards_.size(), &arena_);
+    phase("iterate vectors");
     const double t1 = now_s();
     ComputeScaling(prm);
     Sync();
     scaling_s_ = now_s() - t1;
+    phase("scaling");
     DeviceNorms();
     UniformBounds();
+    phase("norms+bounds");
     const double iter_bytes = (24.0 * nnz_ + 68.0 * (m_ + n_)) / world_;
     l2_resident_ = iter_bytes < 100e6;
     Sync();
@@ -231,8 +255,12 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
 }
 
 Session::~Session() {
+  const double t0 = now_s();
   if (start_.joinable()) start_.join();
   cudaSetDevice(device_);
+  cudaStreamSynchronize(st_);
+  const char* tenv = std::getenv("PDHG_TRACE");
+  if (tenv && tenv[0] == '2') std::fprintf(stderr, "[pdhg]   dtor join+sync %.4fs\n", now_s() - t0);
   for (cudaEvent_t e : ev_)
     if (e) cudaEventDestroy(e);
   for (Graph& g : graphs_)
@@ -240,18 +268,16 @@ Session::~Session() {
   for (Graph& g : blocks_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (power_graph_) cudaGraphExecDestroy(power_graph_);
-  if (host_red_) cudaFreeHost(host_red_);
-  if (hstage_) cudaFreeHost(hstage_);
-  if (hstate_) cudaFreeHost(hstate_);
+  pinned_put(host_red_, host_red_bytes_);
+  pinned_put(hstage_, hstage_bytes_);
+  pinned_put(hstate_, hstate_bytes_);
+  pinned_put(start_host_, start_host_bytes_);
   for (cudaEvent_t e : pev_)
     if (e) cudaEventDestroy(e);
   comm_.reset();
-  if (fork_.fork) cudaEventDestroy(fork_.fork);
-  for (int k = 0; k < 3; ++k) {
-    if (fork_.side[k]) cudaStreamDestroy(fork_.side[k]);
-    if (fork_.join[k]) cudaEventDestroy(fork_.join[k]);
-  }
-  if (st_) cudaStreamDestroy(st_);
+  // Streams outlive the arrays (streams_ is destroyed last): each array's
+  // release synchronises the stream that used it.
+  if (tenv && tenv[0] == '2') std::fprintf(stderr, "[pdhg]   dtor body %.4fs\n", now_s() - t0);
 }
 
 void Session::Sync() { PDHG_CUDA(cudaStreamSynchronize(st_)); }
@@ -908,13 +934,10 @@ double* Session::DevStage() {
 double* Session::HostStage() {
   const size_t need = static_cast<size_t>(std::max<int64_t>(std::max(m_, n_), 1));
   if (hstage_n_ < need) {
-    if (hstage_) cudaFreeHost(hstage_);
-  if (hstate_) cudaFreeHost(hstate_);
-  for (cudaEvent_t e : pev_)
-    if (e) cudaEventDestroy(e);
+    pinned_put(hstage_, hstage_bytes_);
     hstage_ = nullptr;
-    PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hstage_), need * sizeof(double)));
-    hstage_n_ = need;
+    hstage_ = static_cast<double*>(pinned_get(need * sizeof(double), &hstage_bytes_));
+    hstage_n_ = hstage_bytes_ / sizeof(double);
   }
   return hstage_;
 }
@@ -1129,6 +1152,7 @@ void Session::ReadCheck(CheckOut* out) {
 // ================================================================ solve loop
 void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_result* out) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   if (!ev_[0]) {
     PDHG_CUDA(cudaEventCreate(&ev_[0]));
     PDHG_CUDA(cudaEventCreate(&ev_[1]));
@@ -1252,7 +1276,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     ds.best_rep = best_rep;
     ds.last_rep = last_rep;
     if (!dstate_.p) dstate_.alloc(1, &arena_);
-    if (!hstate_) PDHG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&hstate_), 2 * sizeof(DecideState)));
+    if (!hstate_) hstate_ = static_cast<DecideState*>(pinned_get(2 * sizeof(DecideState), &hstate_bytes_));
     if (!pev_[0])
       for (cudaEvent_t& e : pev_) PDHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     sc.halt = 0;
@@ -1564,14 +1588,14 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
 // partials -> normalisation from the shard/rank sum -> all-gather u.
 double Session::OpNorm(int iters, uint64_t seed) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   if (nnz_ == 0) return 0.0;
   // Start vector (solver.cpp:88-97): drawn on a host thread while the
   // session was being built (upload, CSC, scaling) for the seed the session
   // was created with; another seed is drawn here.
   if (start_.joinable()) start_.join();
-  if (start_seed_ != seed || start_vec_.size() != static_cast<size_t>(n_)) DrawStart(seed);
-  double* v = HostStage();
-  std::memcpy(v, start_vec_.data(), n_ * sizeof(double));
+  if (start_seed_ != seed || !start_host_) DrawStart(seed);
+  double* v = start_host_;  // pinned: ToInternal copies it straight to the device
   double vnorm = start_norm_;
   if (vnorm == 0.0) {
     v[0] = 1.0;
@@ -1634,10 +1658,13 @@ double Session::OpNorm(int iters, uint64_t seed) {
 // hosts -- the engine itself is the serial part -- so the session overlaps
 // it with setup instead.
 void Session::DrawStart(uint64_t seed) {
-  start_vec_.resize(static_cast<size_t>(n_));
-  NormalVectorSequential(seed, n_, start_vec_.data());
+  if (!start_host_) start_host_ = static_cast<double*>(pinned_get(n_ * sizeof(double), &start_host_bytes_));
+  // Bit-identical to the sequential draw; engine on this thread, transforms
+  // on workers (normal_rng.h).
+  const int hw = static_cast<int>(std::thread::hardware_concurrency());
+  NormalVector(seed, n_, start_host_, n_ >= (int64_t(1) << 17) ? std::min(std::max(hw, 1), 16) : 1);
   double acc = 0.0;
-  for (int64_t j = 0; j < n_; ++j) acc += start_vec_[j] * start_vec_[j];
+  for (int64_t j = 0; j < n_; ++j) acc += start_host_[j] * start_host_[j];
   start_norm_ = std::sqrt(acc);
   start_seed_ = seed;
 }
@@ -1645,12 +1672,14 @@ void Session::DrawStart(uint64_t seed) {
 // ============================================================ kernel probes
 void Session::Scaling(double* rs, double* cs) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   ToHost(rs_.p, nullptr, pad_r_, rs, m_);
   ToHost(cs_.p, nullptr, pad_c_, cs, n_);
 }
 
 void Session::ScaledProblem(double* kv, double* c, double* l, double* u, double* q) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   if (kv && nnz_) {
     if (nccl()) throw Error(PDHG_INVALID_ARGUMENT, "scaled values are only available when all shards are local");
     std::vector<int32_t> hp(static_cast<size_t>(m_) + 1);
@@ -1675,6 +1704,7 @@ void Session::ScaledProblem(double* kv, double* c, double* l, double* u, double*
 
 void Session::Spmv(int transpose, const double* in, double* out) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   const int64_t nin = transpose ? m_ : n_, nout = transpose ? n_ : m_;
   const int64_t pin = transpose ? mp_ : np_, pout = transpose ? np_ : mp_;
   DArray<double> a, b;
@@ -1694,6 +1724,7 @@ void Session::Spmv(int transpose, const double* in, double* out) {
 // included) and of a graph-launched 64-iteration block, on the solver stream.
 void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double* ms_iter) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   Scalars sc{};
   sc.eta = 1e-3;
   sc.omega = 1.0;
@@ -1755,6 +1786,7 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
 
 void Session::UnitPrimal(const double* x, const double* y, double eta, double omega, double* out) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   DArray<double> dx, dy, dout;
   dx.alloc(std::max<int64_t>(np_, 1));
   dy.alloc(std::max<int64_t>(mp_, 1));
@@ -1776,6 +1808,7 @@ void Session::UnitPrimal(const double* x, const double* y, double eta, double om
 // average, the "original" half of the pack.
 void Session::Residuals(const double* x, const double* y, pdhg_report* out) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   ToInternal(x, pad_c_, x_[0].p, n_, np_);
   ToInternal(y, pad_r_, y_[0].p, m_, mp_);
   // The check works in the scaled space: map the original point into it.
@@ -1796,6 +1829,7 @@ void Session::Residuals(const double* x, const double* y, pdhg_report* out) {
 // DeriveLambda (kkt.cpp:127-141) for an original-space y.
 void Session::Lambda(const double* y, double* out) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   ToInternal(y, pad_r_, y_[0].p, m_, mp_);
   k_div<<<ew_grid(mp_), kEw, 0, st_>>>(y_[0].p, rs_.p, y_[0].p, mp_);
   GatherYFull(y_[0].p);
@@ -1810,6 +1844,7 @@ void Session::Lambda(const double* y, double* out) {
 
 void Session::UnitDual(const double* xn, const double* xo, const double* y, double eta, double omega, double* out) {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   DArray<double> a, b, ext, dy, dout;
   a.alloc(std::max<int64_t>(np_, 1));
   b.alloc(std::max<int64_t>(np_, 1));
@@ -1832,6 +1867,7 @@ void Session::UnitDual(const double* xn, const double* xo, const double* y, doub
 // Evict the working set between benchmark steps: write 2x the L2 capacity.
 void Session::FlushL2() {
   PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
   int l2 = 0;
   PDHG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device_));
   const size_t bytes = std::max<size_t>(2 * static_cast<size_t>(l2), 64u << 20);

@@ -125,6 +125,24 @@ class Session {
   int launches_csr() const;
   int launches_csc() const;
 
+  // Owns the session stream and the fork streams / events. Declared first so
+  // it is destroyed last, after every DArray member has been released on it.
+  struct StreamOwner {
+    cudaStream_t st = nullptr;
+    Fork fork;
+    StreamOwner() = default;
+    StreamOwner(const StreamOwner&) = delete;
+    StreamOwner& operator=(const StreamOwner&) = delete;
+    ~StreamOwner() {
+      if (fork.fork) cudaEventDestroy(fork.fork);
+      for (int k = 0; k < 3; ++k) {
+        if (fork.side[k]) cudaStreamDestroy(fork.side[k]);
+        if (fork.join[k]) cudaEventDestroy(fork.join[k]);
+      }
+      if (st) cudaStreamDestroy(st);
+    }
+  };
+  StreamOwner streams_;
   int device_ = 0;
   bool skip_pc_ = false;  // scaling = Ruiz sweeps only (pdhg_compute_scaling)
   cudaStream_t st_ = nullptr;
@@ -162,20 +180,23 @@ class Session {
   DArray<double> y_[2], ybar_, ystart_, ybest_, kx_[2], kxavg_;  // mp_
   DArray<Scalars> scal_;
   DArray<double> red_out_;  // per-shard packs; pack 0 holds the reduced result
-  double* host_red_ = nullptr;  // pinned
+  double* host_red_ = nullptr;  // pinned (darray.cuh pinned cache)
+  size_t host_red_bytes_ = 0;
   DArray<double> dstage_;       // max(m, n) device staging
   double* hstage_ = nullptr;    // max(m, n) pinned host staging
-  size_t hstage_n_ = 0;
+  size_t hstage_n_ = 0, hstage_bytes_ = 0;
 
   // Power-iteration start vector, drawn on a host thread during setup.
   std::thread start_;
-  std::vector<double> start_vec_;
+  double* start_host_ = nullptr;  // pinned, n doubles
+  size_t start_host_bytes_ = 0;
   uint64_t start_seed_ = ~uint64_t(0);
   double start_norm_ = 0.0;
 
   // Pipelined loop: device decision state, its pinned host mirrors, events.
   DArray<DecideState> dstate_;
   DecideState* hstate_ = nullptr;
+  size_t hstate_bytes_ = 0;
   cudaEvent_t pev_[2] = {nullptr, nullptr};
 
   std::vector<Graph> graphs_;

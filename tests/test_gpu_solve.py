@@ -205,6 +205,26 @@ def test_pipelined_loop_matches_synchronous(case, monkeypatch):
         [(e.iteration, e.restarted, e.candidate_is_current, e.omega, e.kkt_candidate) for e in tb]
 
 
+def test_pipelined_session_reuse(monkeypatch):
+    """Three pipelined solves on one session, with the sync loop between them:
+    the pinned decision state and its events live as long as the session
+    (a host-stage resize must not release them)."""
+    p = GenTransport(30, 40, 1)
+    prm = SolverParams(eps=1e-6)
+    sess = rpdlp.Session(p, prm)
+    try:
+        out = []
+        for flag in ("1", "0", "1", "1"):
+            monkeypatch.setenv("PDHG_PIPELINE", flag)
+            out.append(sess.solve(prm))
+        for r in out[1:]:
+            assert (r.status, r.iterations, r.restarts) == (out[0].status, out[0].iterations, out[0].restarts)
+            np.testing.assert_array_equal(r.x, out[0].x)
+            np.testing.assert_array_equal(r.y, out[0].y)
+    finally:
+        sess.close()
+
+
 @pytest.mark.parametrize("name", ["transport_600x40", "mcf", "staircase_d8", "staircase_d20", "cols_len4"])
 def test_kernel_variant_solves(name, restatement):
     """Solve parity on the instances that route through the uniform-length,

@@ -263,6 +263,14 @@ int pdhg_session_time_kernels(pdhg_session* s, int iters, double* ms_primal,
                               double* ms_dual, double* ms_iteration,
                               char* err, size_t errlen);
 
+/* Times the termination / restart check (SolveLoop::Check, solver.cpp:390-428:
+ * residual passes over K for the current and average iterates plus their
+ * reductions): mean device milliseconds per check from `iters` back-to-back
+ * checks bracketed by CUDA events, and mean wall milliseconds per check
+ * including the device -> host read the host loop waits on. */
+int pdhg_session_time_check(pdhg_session* s, int iters, double* ms_device,
+                            double* ms_wall, char* err, size_t errlen);
+
 /* ---- unit-level exports (solver.hpp:81-125), device-backed ---------------
  * PrimalStep (solver.cpp:112-129): out(n) = proj_[l,u](x - eta/omega (c - K'y))
  * DualStep (solver.cpp:131-154): out(m) = proj_Y(y + eta*omega (q - K(2x_new - x_old)))

@@ -311,6 +311,14 @@ int pdhg_session_time_kernels(pdhg_session* s, int iters, double* ms_primal, dou
   });
 }
 
+int pdhg_session_time_check(pdhg_session* s, int iters, double* ms_device, double* ms_wall, char* err,
+                            size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (iters < 1) Invalid("iters must be >= 1");
+    S(s).TimeCheck(iters, ms_device, ms_wall);
+  });
+}
+
 int pdhg_session_flush_l2(pdhg_session* s, char* err, size_t errlen) {
   return Guard(err, errlen, [&] { S(s).FlushL2(); });
 }

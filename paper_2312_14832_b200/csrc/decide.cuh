@@ -66,8 +66,7 @@ __global__ void k_reduce_two_guarded(const Scalars* sc, const double* t0, int nt
   const int i = second ? blockIdx.x - n0 : blockIdx.x;
   const double* tile = second ? t1 : t0;
   const int ntiles = second ? nt1 : nt0, nred = second ? n1 : n0;
-  double acc = 0.0;
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) acc += tile[(int64_t)t * nred + i];
+  double acc = slot_sum(tile, nullptr, ntiles, nred, i);
   acc = warp_combine<false>(acc);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
   __syncthreads();

@@ -52,15 +52,55 @@ struct Layout {
   int parts() const { return nb_s() + nb_m() + nb_l() + 2 * nt_x(); }  // reduction slots
 };
 
+constexpr int pow2_ceil(int k) { return k <= 1 ? 1 : 2 * pow2_ceil((k + 1) / 2); }
+
+// Warp sums of K <= 32 per-lane values by recursive halving: at each step a
+// lane trades the half of its remaining values that its partner keeps, so a
+// warp issues ~P = pow2_ceil(K) shuffles instead of 5K (the check passes
+// carry 11 and 15 sums per thread and were shuffle-bound). After the halving
+// steps the lanes of one group (equal above bit 32/P) share a value index;
+// plain xor steps finish the sums inside the group. Every lane ends with the
+// total of value index *idx; a fixed, deterministic tree.
+template <int K>
+__device__ __forceinline__ double warp_reduce_scatter(const double (&v)[K], int* idx) {
+  constexpr int P = pow2_ceil(K);
+  static_assert(P <= 32, "at most 32 values per lane");
+  const int lane = threadIdx.x & 31;
+  double w[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) w[j] = j < K ? v[j] : 0.0;
+  int base = 0;
+#pragma unroll
+  for (int c = P, o = 16; c > 1; c >>= 1, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int j = 0; j < c / 2; ++j) {
+      const double send = up ? w[j] : w[j + c / 2];
+      const double keep = up ? w[j + c / 2] : w[j];
+      w[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+    base += up ? c / 2 : 0;
+  }
+  double r = w[0];
+#pragma unroll
+  for (int o = 16 / P; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  *idx = base;
+  return r;
+}
+
 template <class Op, int NW = kWarps>
 __device__ __forceinline__ void block_reduce_out(double (&red)[Op::kRed > 0 ? Op::kRed : 1], double* out) {
   if constexpr (Op::kRed > 0) {
     __shared__ double sh[NW][Op::kRed];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int i = 0; i < Op::kRed; ++i) {
-      const double v = warp_combine<false>(red[i]);
-      if (lane == 0) sh[warp][i] = v;
+    if constexpr (Op::kRed == 1) {
+      const double v = warp_combine<false>(red[0]);
+      if (lane == 0) sh[warp][0] = v;
+    } else {
+      int i;
+      const double v = warp_reduce_scatter<Op::kRed>(red, &i);
+      constexpr int G = 32 / pow2_ceil(Op::kRed);  // lanes per value index
+      if ((lane & (G - 1)) == 0 && i < Op::kRed) sh[warp][i] = v;
     }
     __syncthreads();
     if (threadIdx.x < Op::kRed) {

@@ -1784,6 +1784,34 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   cudaEventDestroy(e2);
 }
 
+// Check cost probe: distinct current / average iterates so both halves of
+// every check pass are live, as in the loop.
+void Session::TimeCheck(int iters, double* ms_device, double* ms_wall) {
+  PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
+  for (int w = 0; w < 2; ++w) LaunchCheck(x_[0].p, y_[0].p, x_[1].p, y_[1].p, kx_[0].p);
+  Sync();
+  cudaEvent_t e0, e1;
+  PDHG_CUDA(cudaEventCreate(&e0));
+  PDHG_CUDA(cudaEventCreate(&e1));
+  PDHG_CUDA(cudaEventRecord(e0, st_));
+  for (int i = 0; i < iters; ++i) LaunchCheck(x_[0].p, y_[0].p, x_[1].p, y_[1].p, kx_[0].p);
+  PDHG_CUDA(cudaEventRecord(e1, st_));
+  PDHG_CUDA(cudaEventSynchronize(e1));
+  float t = 0.f;
+  PDHG_CUDA(cudaEventElapsedTime(&t, e0, e1));
+  *ms_device = t / iters;
+  CheckOut ck;
+  const double w0 = now_s();
+  for (int i = 0; i < iters; ++i) {
+    LaunchCheck(x_[0].p, y_[0].p, x_[1].p, y_[1].p, kx_[0].p);
+    ReadCheck(&ck);
+  }
+  *ms_wall = (now_s() - w0) * 1e3 / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
 void Session::UnitPrimal(const double* x, const double* y, double eta, double omega, double* out) {
   PDHG_CUDA(cudaSetDevice(device_));
   AllocScope scope(st_);

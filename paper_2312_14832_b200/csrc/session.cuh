@@ -46,6 +46,7 @@ class Session {
   void Spmv(int transpose, const double* in, double* out);
   double OpNorm(int iters, uint64_t seed);
   void TimeKernels(int iters, double* ms_primal, double* ms_dual, double* ms_iter);
+  void TimeCheck(int iters, double* ms_device, double* ms_wall);
   void Stats(pdhg_session_stats* s) const;
   void Blocks(int64_t* row_begin, int64_t* col_begin) const;
   void GhostCounts(int64_t* x_counts, int64_t* y_counts, int32_t* use) const;

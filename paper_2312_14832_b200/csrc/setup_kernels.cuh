@@ -348,12 +348,32 @@ __global__ void k_part_span(const int32_t* p, int32_t hi, int64_t nz1, int32_t n
 
 // --------------------------------------------------------------- reductions
 // out[i] = sum over slots (fixed order); one CTA per output.
+// Thread-strided sum of slot i over ntiles partials (t = tid, tid + B, ...),
+// in that order; loads are issued 8 at a time so a thread's whole chain is
+// not one dependent DRAM round trip per partial.
+__device__ __forceinline__ double slot_sum(const double* tile, const double* span, int ntiles, int nred, int i) {
+  constexpr int U = 8;
+  const int B = blockDim.x;
+  double acc = 0.0;
+  int t = threadIdx.x;
+  for (; t + (U - 1) * B < ntiles; t += U * B) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t o = (int64_t)(t + u * B) * nred + i;
+      v[u] = tile[o] + (span ? span[o] : 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u];
+  }
+  for (; t < ntiles; t += B) acc += tile[(int64_t)t * nred + i] + (span ? span[(int64_t)t * nred + i] : 0.0);
+  return acc;
+}
+
 __global__ void k_reduce_tiles(const double* tile, const double* span, int ntiles, int nred, double* out) {
   __shared__ double sh[kBlock / 32];
   const int i = blockIdx.x;
-  double acc = 0.0;
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x)
-    acc += tile[(int64_t)t * nred + i] + (span ? span[(int64_t)t * nred + i] : 0.0);
+  double acc = slot_sum(tile, span, ntiles, nred, i);
   acc = warp_combine<false>(acc);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
   __syncthreads();
@@ -373,8 +393,7 @@ __global__ void k_reduce_two(const double* t0, int nt0, int n0, const double* t1
   const int i = second ? blockIdx.x - n0 : blockIdx.x;
   const double* tile = second ? t1 : t0;
   const int ntiles = second ? nt1 : nt0, nred = second ? n1 : n0;
-  double acc = 0.0;
-  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) acc += tile[(int64_t)t * nred + i];
+  double acc = slot_sum(tile, nullptr, ntiles, nred, i);
   acc = warp_combine<false>(acc);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
   __syncthreads();

@@ -474,6 +474,13 @@ class Session:
                                                      abi.ERRLEN), err)
         return a.value, b.value, c.value
 
+    def time_check(self, iters: int = 50):
+        """(device ms, wall ms) per termination/restart check (solver.cpp:390-428)."""
+        a, b = C.c_double(), C.c_double()
+        err = self._err()
+        raise_for(self.lib.pdhg_session_time_check(self.h, iters, C.byref(a), C.byref(b), err, abi.ERRLEN), err)
+        return a.value, b.value
+
 
 def PrimalStep(problem: LpProblem, x, y, eta: float, omega: float) -> np.ndarray:
     """solver.cpp:112-129 on the unscaled problem (device)."""

@@ -42,6 +42,9 @@ for name in which:
               f"\n   primal {ms_p*1e3:.1f}us {bp/ms_p/1e6:.0f} GB/s | dual {ms_d*1e3:.1f}us "
               f"{bd/ms_d/1e6:.0f} GB/s | iter {ms_it*1e3:.1f}us {bi/ms_it/1e6:.0f} GB/s -> {1e3 / ms_it:.0f} it/s",
               flush=True)
+        cd, cw = s.time_check(20 if p.nnz() > 2e7 else 100)
+        print(f"   check: device {cd*1e3:.1f}us, with host read {cw*1e3:.1f}us (= {cd / ms_it:.1f} / {cw / ms_it:.1f} "
+              f"iterations)", flush=True)
         if name in full_solve:
             r = s.solve(rpdlp.SolverParams(eps=1e-4))
             ms, nl = s.last_solve()

@@ -1,6 +1,7 @@
 """Drive the fused PDHG step kernels for an ncu capture (one GPU).
 
     ncu --set full -k regex:"OpPrimal|OpDual" -s 4 -c 2 python tools/profile_step.py transport
+    ncu --set full -k regex:"OpCheck|k_reduce_two" -s 6 -c 3 python tools/profile_step.py transport - 2 --check
 """
 import sys
 from pathlib import Path
@@ -26,5 +27,9 @@ if __name__ == "__main__":
     p = problem(sys.argv[1] if len(sys.argv) > 1 else "transport")
     with rpdlp.Session(p) as s:
         iters = int(sys.argv[3]) if len(sys.argv) > 3 else 2
-        ms_p, ms_d, ms_it = s.time_kernels(iters)
-        print(f"primal {ms_p * 1e3:.1f} us  dual {ms_d * 1e3:.1f} us  iteration {ms_it * 1e3:.1f} us")
+        if "--check" in sys.argv:  # drive the check kernels instead (OpCheckRow|OpCheckCol|k_reduce_two)
+            cd, cw = s.time_check(iters)
+            print(f"check {cd * 1e3:.1f} us device, {cw * 1e3:.1f} us with the host read")
+        else:
+            ms_p, ms_d, ms_it = s.time_kernels(iters)
+            print(f"primal {ms_p * 1e3:.1f} us  dual {ms_d * 1e3:.1f} us  iteration {ms_it * 1e3:.1f} us")

@@ -69,14 +69,17 @@ void segment_ids(const int32_t* ptr, int64_t nseg, int64_t nnz, DArray<int32_t>&
 }
 
 // Stable sort of segment keys (values < 2^bits) -> permutation new -> old.
-// With `ptr` given, segments of equal key are ordered by length, longest
-// first (then original order): a segment with L nonzeros is the target of L
-// gathers in the other layout's pass, so this packs the hottest vector
-// entries (hub rows / columns) into few cache lines and makes the lengths
-// inside a warp uniform. Segment-internal nonzero order is untouched, so
-// every segment sum is unchanged.
+// Secondary order inside equal keys (`order`, with the segment offsets `ptr`
+// and indices `idx`): kOrderLength -- longest first (a segment with L
+// nonzeros is the target of L gathers in the other layout's pass, so hub rows
+// / columns pack into few cache lines); kOrderFirst -- by first index in the
+// other dimension (k_first_index_key). Ties keep the original order.
+// Segment-internal nonzero order is untouched, so every segment sum is
+// unchanged whatever the order.
+enum SegOrder { kOrderNatural = 0, kOrderLength = 1, kOrderFirst = 2 };
+
 void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, int bits, cudaStream_t st,
-                  const int32_t* ptr = nullptr) {
+                  SegOrder order = kOrderNatural, const int32_t* ptr = nullptr, const int32_t* idx = nullptr) {
   DArray<int32_t> iota, kout, first, k2;
   iota.alloc(std::max<int64_t>(n, 1));
   kout.alloc(std::max<int64_t>(n, 1));
@@ -87,10 +90,11 @@ void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, int bit
   cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout.p, iota.p, perm.p, (int)n, 0, 31, st);
   DArray<char> tmp;
   tmp.alloc(tb);
-  if (ptr) {
+  if (order != kOrderNatural) {
     first.alloc(std::max<int64_t>(n, 1));
     k2.alloc(std::max<int64_t>(n, 1));
-    k_len_desc_key<<<ew_grid(n), kEw, 0, st>>>(ptr, n, k2.p);
+    if (order == kOrderLength) k_len_desc_key<<<ew_grid(n), kEw, 0, st>>>(ptr, n, k2.p);
+    else k_first_index_key<<<ew_grid(n), kEw, 0, st>>>(ptr, idx, n, k2.p);
     PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, k2.p, kout.p, iota.p, first.p, (int)n, 0, 31, st));
     k_gather_i32<<<ew_grid(n), kEw, 0, st>>>(keys, first.p, k2.p, n);
     vals = first.p;
@@ -103,6 +107,15 @@ void stable_order(const int32_t* keys, int64_t n, DArray<int32_t>& perm, int bit
 // Per-segment charge of the block balance (in nonzeros): the ~68 bytes of
 // vector traffic per row / column against 12 bytes per nonzero.
 constexpr int64_t kSegWeight = 6;
+
+// Default secondary segment orders (stable_order). Rows by first column:
+// MCF conservation rows of one node across commodities become neighbours
+// (iteration 574 -> 500 us, primal at 95% of HBM); transport, PageRank,
+// staircase and random LPs are unchanged (profiles/r01/order_r01z.md).
+// Columns by first row split multicommodity arcs apart (MCF dual 311 ->
+// 433 us), so they keep their natural order.
+constexpr SegOrder kRowOrder = kOrderFirst;
+constexpr SegOrder kColOrder = kOrderNatural;
 
 // Mean class-S segment length from which the warp-staged S kernel is used.
 constexpr double kStagedMin = 3.0;
@@ -450,10 +463,19 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     k_key_hist<<<ew_grid(n_), kEw, 0, st_>>>(kc.p, n_, hist.p + nkeys, nkeys);
     int bits = 3;
     while ((1 << bits) < nkeys) ++bits;
-    const char* dord = std::getenv("PDHG_DEGREE_ORDER");
-    const bool by_len = dord && dord[0] == '1';  // off by default: it breaks stage locality (staircase)
-    if (m_) stable_order(kr.p, m_, perm_r, bits, st_, by_len ? ptr0.p : nullptr);
-    if (n_) stable_order(kc.p, n_, perm_c, bits, st_, by_len ? cptr0.p : nullptr);
+    // Secondary segment order (tuning: PDHG_ROW_ORDER / PDHG_COL_ORDER =
+    // natural | length | first; PDHG_DEGREE_ORDER=1 = length for both).
+    auto seg_order = [](const char* var, SegOrder def) {
+      const char* d = std::getenv("PDHG_DEGREE_ORDER");
+      if (d && d[0] == '1') return kOrderLength;
+      const char* v = std::getenv(var);
+      if (!v) return def;
+      const std::string s(v);
+      return s == "length" ? kOrderLength : (s == "first" ? kOrderFirst : kOrderNatural);
+    };
+    const SegOrder ro = seg_order("PDHG_ROW_ORDER", kRowOrder), co = seg_order("PDHG_COL_ORDER", kColOrder);
+    if (m_) stable_order(kr.p, m_, perm_r, bits, st_, ro, ptr0.p, idx0.p);
+    if (n_) stable_order(kc.p, n_, perm_c, bits, st_, co, cptr0.p, ridx0.p);
     std::vector<int> h(2 * nkeys);
     PDHG_CUDA(cudaMemcpyAsync(h.data(), hist.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st_));
     Sync();

@@ -174,6 +174,14 @@ __global__ void k_len_desc_key(const int32_t* p, int64_t nseg, int32_t* key) {
   GRID_STRIDE(s, nseg) key[s] = INT32_MAX - (p[s + 1] - p[s]);
 }
 
+// Secondary order key: the segment's first index in the other dimension
+// (INT32_MAX for an empty segment). Segments whose patterns are shifted
+// copies of each other (e.g. one node's conservation rows across
+// commodities) become neighbours, so thread-per-segment gathers coalesce.
+__global__ void k_first_index_key(const int32_t* p, const int32_t* idx, int64_t nseg, int32_t* key) {
+  GRID_STRIDE(s, nseg) key[s] = p[s + 1] > p[s] ? idx[p[s]] : INT32_MAX;
+}
+
 __global__ void k_gather_i32(const int32_t* in, const int32_t* perm, int32_t* out, int64_t n) {
   GRID_STRIDE(i, n) out[i] = in[perm[i]];
 }

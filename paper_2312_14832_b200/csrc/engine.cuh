@@ -395,10 +395,12 @@ __global__ void __launch_bounds__(kBlock) seg_warp_kernel(const int32_t* __restr
 }
 
 // Class L: a CTA per RPC segments, kBlock / RPC threads per segment (fixed
-// trees). RPC = 4 for moderately long segments: the 4 consecutive segments of
-// a CTA typically gather neighbouring vector entries (transportation demand
-// rows j..j+3 read x[i*T + j..j+3]), so they share L1 sectors instead of each
-// pulling its own 32-byte sector per 8-byte gather from L2.
+// trees). RPC = 4 for moderately long segments whose neighbours gather
+// neighbouring vector entries (transportation demand rows j..j+3 read
+// x[i*T + j..j+3]): the lanes of a warp are interleaved across the 4
+// segments (lane -> segment lane % 4, entry position warp * 8 + lane / 4), so
+// one warp-wide gather reads 8 sectors of 4 adjacent entries instead of 32
+// scattered sectors, and the stream loads stay 8-entry contiguous runs.
 template <class Op, int RPC, int B = kBlock>
 __global__ void __launch_bounds__(B) seg_cta_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                                     const double* __restrict__ val, int32_t s_begin, int32_t s_end,
@@ -407,14 +409,17 @@ __global__ void __launch_bounds__(B) seg_cta_kernel(const int32_t* __restrict__ 
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   constexpr bool MX = Op::kMax;
-  constexpr int T = B / RPC;  // threads per segment
-  constexpr int W = T / 32;   // warps per segment
+  constexpr bool IL = RPC > 1;  // interleaved lanes
+  constexpr int T = B / RPC;    // threads per segment
+  constexpr int W = T / 32;     // warps per segment (non-interleaved)
   constexpr int NW = B / 32;
-  __shared__ double sh[NW][R];
+  __shared__ double sh[NW][RPC][R];
   double red[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
-  const int sub = threadIdx.x / T, t = threadIdx.x % T;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = IL ? lane % RPC : threadIdx.x / T;
+  const int t = IL ? warp * (32 / RPC) + lane / RPC : threadIdx.x % T;
   const int s = s_begin + blockIdx.x * RPC + sub;
   const bool own = s < s_end;
   typename Op::Pre pre{};
@@ -427,18 +432,30 @@ __global__ void __launch_bounds__(B) seg_cta_kernel(const int32_t* __restrict__ 
   } else {
     pdl_wait_trigger();
   }
-  const int warp = threadIdx.x >> 5;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    acc[r] = warp_combine<MX>(acc[r]);
-    if ((threadIdx.x & 31) == 0) sh[warp][r] = acc[r];
+    double v = acc[r];
+    if constexpr (IL) {
+#pragma unroll
+      for (int o = 16; o >= RPC; o >>= 1) v = combine<MX>(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (lane < RPC) sh[warp][lane][r] = v;
+    } else {
+      v = warp_combine<MX>(v);
+      if (lane == 0) sh[warp][0][r] = v;
+    }
   }
   __syncthreads();
   if (own && t == 0) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      double v = sh[sub * W][r];
-      for (int w = 1; w < W; ++w) v = combine<MX>(v, sh[sub * W + w][r]);
+      double v;
+      if constexpr (IL) {
+        v = sh[0][sub][r];
+        for (int w = 1; w < NW; ++w) v = combine<MX>(v, sh[w][sub][r]);
+      } else {
+        v = sh[sub * W][0][r];
+        for (int w = 1; w < W; ++w) v = combine<MX>(v, sh[sub * W + w][0][r]);
+      }
       acc[r] = v;
     }
     op.finish(s, acc, pre, red);

@@ -6,6 +6,9 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
+#include <algorithm>
 
 #include "../../include/pdhg.h"
 
@@ -17,7 +20,31 @@
 
 namespace pdhg {
 
-// LpProblem::Validate (lp_problem.cpp:22-58): same checks, same messages.
+// LpProblem::Validate (lp_problem.cpp:22-58): same checks, same messages,
+// same precedence (NaN in c, b, h; then infinite c; then the first index
+// with a NaN or crossed bound). The element scans run on up to 8 threads for
+// large n -- each chunk reports flags / its first bad index, merged in
+// index order -- since they sit in front of every one-shot solve.
+struct LpScan {
+  bool nan_c = false, inf_c = false;
+  int64_t bad_bound = -1;  // first index with a NaN or crossed bound
+};
+
+inline void ScanLp(const pdhg_lp& lp, int64_t b, int64_t e, LpScan* out) {
+  bool nan_c = false, inf_c = false;
+  for (int64_t i = b; i < e; ++i) {
+    nan_c |= std::isnan(lp.c[i]);
+    inf_c |= std::isinf(lp.c[i]);
+  }
+  out->nan_c = nan_c;
+  out->inf_c = inf_c;
+  for (int64_t i = b; i < e; ++i)
+    if (std::isnan(lp.l[i]) || std::isnan(lp.u[i]) || lp.l[i] > lp.u[i]) {
+      out->bad_bound = i;
+      break;
+    }
+}
+
 inline void ValidateLpHost(const pdhg_lp& lp) {
   auto bad = [](const std::string& m) { throw std::invalid_argument(m); };
   const int64_t n = lp.n;
@@ -25,17 +52,34 @@ inline void ValidateLpHost(const pdhg_lp& lp) {
   if (lp.a.cols != n || lp.g.cols != n) bad("matrix column count does not match c");
   if ((lp.a.rows && !lp.a.row_ptr) || (lp.g.rows && !lp.g.row_ptr)) bad("missing row_ptr");
   if ((n && (!lp.c || !lp.l || !lp.u)) || (lp.a.rows && !lp.b) || (lp.g.rows && !lp.h)) bad("missing vector");
-  for (int64_t i = 0; i < n; ++i)
-    if (std::isnan(lp.c[i])) bad("NaN in c");
+  const int threads = n >= (int64_t(1) << 18)
+                          ? static_cast<int>(std::min<unsigned>(8, std::max(1u, std::thread::hardware_concurrency())))
+                          : 1;
+  std::vector<LpScan> part(threads);
+  {
+    std::vector<std::thread> pool;
+    const int64_t per = (n + threads - 1) / threads;
+    for (int t = 1; t < threads; ++t)
+      pool.emplace_back(ScanLp, std::cref(lp), std::min(n, t * per), std::min(n, (t + 1) * per), &part[t]);
+    ScanLp(lp, 0, std::min(n, per), &part[0]);
+    for (auto& th : pool) th.join();
+  }
+  LpScan all;
+  for (const LpScan& p : part) {
+    all.nan_c |= p.nan_c;
+    all.inf_c |= p.inf_c;
+    if (all.bad_bound < 0) all.bad_bound = p.bad_bound;
+  }
+  if (all.nan_c) bad("NaN in c");
   for (int64_t i = 0; i < lp.a.rows; ++i)
     if (std::isnan(lp.b[i])) bad("NaN in b");
   for (int64_t i = 0; i < lp.g.rows; ++i)
     if (std::isnan(lp.h[i])) bad("NaN in h");
-  for (int64_t i = 0; i < n; ++i)
-    if (std::isinf(lp.c[i])) bad("infinite entry in c");
-  for (int64_t i = 0; i < n; ++i) {
+  if (all.inf_c) bad("infinite entry in c");
+  if (all.bad_bound >= 0) {
+    const int64_t i = all.bad_bound;
     if (std::isnan(lp.l[i]) || std::isnan(lp.u[i])) bad("NaN bound");
-    if (lp.l[i] > lp.u[i]) bad("crossed bounds: l > u at index " + std::to_string(i));
+    bad("crossed bounds: l > u at index " + std::to_string(i));
   }
 }
 

@@ -263,3 +263,22 @@ def test_degenerate_shapes(restatement):
         assert g.status == o.status and g.iterations == o.iterations
         assert g.report.primal_obj == pytest.approx(o.report.primal_obj, rel=1e-9, abs=1e-12)
         np.testing.assert_allclose(g.x, o.x, rtol=1e-9, atol=1e-12)
+
+
+def test_one_shot_solves_reuse_pooled_memory():
+    """Sessions allocate from a per-device pool (csrc/darray.cuh) and release
+    into it: 20 one-shot solves leave device usage where the second left it,
+    and return identical results."""
+    import torch
+    p = GenTransport(200, 300, 1)
+    prm = SolverParams(eps=1e-6)
+    first = rpdlp.Solve(p, prm)
+    rpdlp.Solve(p, prm)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(18):
+        r = rpdlp.Solve(p, prm)
+        np.testing.assert_array_equal(r.x, first.x)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < (64 << 20)

@@ -227,20 +227,21 @@ def test_gloo_two_rank_sharded_iteration(tmp_path):
 
 # ------------------------------------------- power-iteration start vector
 @pytest.mark.parametrize("seed", [0, 1, 12345])
-@pytest.mark.parametrize("n", [1, 7, 40000, 100001])
+@pytest.mark.parametrize("n", [1, 7, 32768, 40000, 100001, 262147])
 def test_parallel_normal_vector_is_bit_exact(seed, n):
-    """The multi-threaded start vector equals the sequential libstdc++
-    std::normal_distribution / std::mt19937_64 draw bit for bit."""
+    """The pipelined multi-threaded start vector (csrc/normal_rng.h) equals the
+    sequential libstdc++ std::normal_distribution / std::mt19937_64 draw bit
+    for bit, for every worker count (1 worker, odd counts, the host's)."""
     import ctypes as C
     from paper_2312_14832_b200 import abi
     lib = abi.load()
-    a, b, c = np.empty(n), np.empty(n), np.empty(n)
     dp = lambda v: v.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
-    assert lib.pdhg_normal_vector(seed, n, -1, dp(a)) == 0
-    assert lib.pdhg_normal_vector(seed, n, 8, dp(b)) == 0
-    assert lib.pdhg_normal_vector(seed, n, 3, dp(c)) == 0
-    np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
-    np.testing.assert_array_equal(a.view(np.uint64), c.view(np.uint64))
+    ref = np.empty(n)
+    assert lib.pdhg_normal_vector(seed, n, 1, dp(ref)) == 0
+    for threads in (-1, 2, 3, 8):
+        out = np.full(n, np.nan)
+        assert lib.pdhg_normal_vector(seed, n, threads, dp(out)) == 0
+        np.testing.assert_array_equal(out.view(np.uint64), ref.view(np.uint64))
 
 
 # ------------------------------- gloo world_size-3 ghost-only exchange test
@@ -313,3 +314,36 @@ def test_gloo_three_rank_ghost_exchange(tmp_path):
         assert np.all(np.isfinite(r["kx"]))
         np.testing.assert_allclose(r["kx"], r["want"], rtol=1e-13, atol=1e-13)
         assert r["ghost"] < r["full"]  # staircase: far less than an all-gather
+
+
+# ------------------------------------------------ LpProblem::Validate (C-ABI)
+def _big_lp(n=600_000):
+    """A 1-row LP large enough for the threaded validation scan."""
+    from paper_2312_14832_b200.rpdlp import CsrMatrix, LpProblem
+    a = CsrMatrix(0, n, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0))
+    g = CsrMatrix(1, n, np.array([0, 2], np.int64), np.array([0, n - 1], np.int64), np.ones(2))
+    return LpProblem(a, g, np.ones(n), np.zeros(0), np.zeros(1), np.zeros(n), np.ones(n))
+
+
+@pytest.mark.parametrize("where", [0, 299_999, 599_999])
+def test_validation_precedence_on_large_inputs(where):
+    """lp_problem.cpp:22-58 order and messages, through the threaded scan the
+    C-ABI runs before any device work (no GPU needed): NaN in c beats an
+    infinite c and a crossed bound anywhere; the FIRST bad bound index is
+    reported; NaN bound beats crossed at the same index."""
+    from paper_2312_14832_b200 import rpdlp
+    p = _big_lp()
+    n = p.c.size
+    p.l[n - 1] = 5.0  # a crossed bound at the end ...
+    p.l[where] = 3.0  # ... and the first one here
+    with pytest.raises(ValueError, match=f"crossed bounds: l > u at index {where}$"):
+        rpdlp.Solve(p)
+    p.u[where] = np.nan
+    with pytest.raises(ValueError, match="NaN bound"):
+        rpdlp.Solve(p)
+    p.c[n - 1 - where] = np.inf
+    with pytest.raises(ValueError, match="infinite entry in c"):
+        rpdlp.Solve(p)
+    p.c[where // 2] = np.nan
+    with pytest.raises(ValueError, match="NaN in c"):
+        rpdlp.Solve(p)

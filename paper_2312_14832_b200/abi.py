@@ -170,8 +170,28 @@ def load():
         if not LIB_PATH.exists():
             raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2312_14832_b200.build` "
                                "(there is no CPU fallback)")
+        _point_at_torch_nccl()
         _lib = bind(C.CDLL(str(LIB_PATH)), SIGNATURES)
     return _lib
+
+
+def _point_at_torch_nccl():
+    """The sharded path dlopens NCCL on first use. If that were the system
+    libnccl.so.2 while PyTorch bundles a newer one, a later `import torch` in
+    the same process would bind to the older library (same soname) and fail
+    on missing symbols; so name PyTorch's copy (without importing torch)."""
+    if os.environ.get("PDHG_NCCL_LIB"):
+        return
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["PDHG_NCCL_LIB"] = cand
+            return
 
 
 def default_params() -> Params:

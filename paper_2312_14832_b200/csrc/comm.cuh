@@ -20,6 +20,8 @@
 #pragma once
 
 #include <dlfcn.h>
+
+#include <cstdlib>
 #include <nccl.h>
 
 #include <cstring>
@@ -99,7 +101,13 @@ struct NcclApi {
  private:
   static NcclApi Load() {
     NcclApi a;
+    // Already in the process (e.g. PyTorch's) -> that one; else the library
+    // PDHG_NCCL_LIB names (the Python layer points it at the NCCL PyTorch
+    // ships, so a later `import torch` resolves against the same build);
+    // else the system's.
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    const char* path = std::getenv("PDHG_NCCL_LIB");
+    if (!h && path && path[0]) h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return a;

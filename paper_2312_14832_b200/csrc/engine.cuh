@@ -401,8 +401,8 @@ __global__ void __launch_bounds__(kBlock) seg_warp_kernel(const int32_t* __restr
 // segments (lane -> segment lane % 4, entry position warp * 8 + lane / 4), so
 // one warp-wide gather reads 8 sectors of 4 adjacent entries instead of 32
 // scattered sectors, and the stream loads stay 8-entry contiguous runs.
-template <class Op, int RPC, int B = kBlock>
-__global__ void __launch_bounds__(B) seg_cta_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+template <class Op, int RPC, int B = kBlock, int MINB = 1>
+__global__ void __launch_bounds__(B, MINB) seg_cta_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                                     const double* __restrict__ val, int32_t s_begin, int32_t s_end,
                                                     const Op op, double* __restrict__ red_out) {
   if (skip_launch(op)) return;
@@ -482,12 +482,21 @@ inline void launch_thread_class(const Layout& L, const Op& op, double* red, cuda
     launch_k(seg_thread_kernel<Op>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red);
 }
 
+// Residency: kBlock-thread CTAs capped at 64 registers (4 CTAs = 1024
+// threads per SM). The 4-segments-per-CTA kernel runs one CTA per four rows
+// of a short class-L (transportation: 500 CTAs); without the cap the compiler
+// takes 66 registers, 3 CTAs fit per SM and the pass needs a second wave
+// (transport dual 12.3 us vs 10.3 us).
+constexpr int kCtaMinBlocks = 4;
+
 template <class Op>
 inline void launch_cta_class(const Layout& L, const Op& op, double* red, cudaStream_t st, bool pdl = false) {
   if (L.l_rpc == 4)
-    launch_k(seg_cta_kernel<Op, 4>, L.nb_l(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s2, L.s3, op, red);
+    launch_k(seg_cta_kernel<Op, 4, kBlock, kCtaMinBlocks>, L.nb_l(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s2,
+             L.s3, op, red);
   else
-    launch_k(seg_cta_kernel<Op, 1>, L.nb_l(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s2, L.s3, op, red);
+    launch_k(seg_cta_kernel<Op, 1, kBlock, kCtaMinBlocks>, L.nb_l(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s2,
+             L.s3, op, red);
 }
 
 // Reduction slots of one pass: [S blocks | M blocks | L CTAs | XL tiles | XL spans].

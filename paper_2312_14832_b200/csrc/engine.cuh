@@ -43,6 +43,7 @@ struct Layout {
   int32_t s1 = 0, s2 = 0, s3 = 0;  // class bounds S | M | L | XL
   bool s_staged = false;           // class S uses seg_thread_staged_kernel
   int l_rpc = 1;                   // class L segments per CTA (1 or 4)
+  int l_stage = 0;                 // > 0: RPC-4 stream staged by TMA, dynamic smem bytes
   int s_len = 0;                   // common class-S length (1,2,3,4,8) or 0
   CMat lng;                        // tile-engine view of [s3, nseg)
   int nb_s() const { return ceil_div(s1, kBlock); }
@@ -489,14 +490,129 @@ inline void launch_thread_class(const Layout& L, const Op& op, double* red, cuda
 // (transport dual 12.3 us vs 10.3 us).
 constexpr int kCtaMinBlocks = 4;
 
+// Dynamic shared memory cap of the TMA-staged variant: 4 CTAs per SM.
+constexpr int kCtaStageMax = 50 * 1024;
+
+// Class L, 4 segments per CTA (interleaved lanes as above), with the CTA's
+// whole contiguous (idx, val) range -- the 4 segments are adjacent in the
+// stream -- bulk-copied into shared memory by TMA BEFORE the programmatic
+// wait: the stream then arrives while the predecessor kernel drains, and
+// after the wait only the gathers, the sums and the epilogue remain. Same
+// per-thread order (k = b + t, b + t + T, ...) and the same trees as
+// seg_cta_kernel<Op, 4>, hence bit-identical results. Used when every
+// 4-segment group fits kCtaStageMax (Layout::l_stage).
+template <class Op>
+__global__ void __launch_bounds__(kBlock, kCtaMinBlocks)
+    seg_cta4_staged_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                           const double* __restrict__ val, int32_t s_begin, int32_t s_end, const Op op,
+                           double* __restrict__ red_out) {
+  if (skip_launch(op)) return;
+  constexpr int RPC = 4;
+  constexpr int R = Op::kRhs;
+  constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
+  constexpr bool MX = Op::kMax;
+  constexpr int T = kBlock / RPC;
+  constexpr int NW = kBlock / 32;
+  constexpr int U = kStrideUnroll;
+  extern __shared__ __align__(16) unsigned char stage[];
+  __shared__ uint64_t bar;
+  __shared__ double sh[NW][RPC][R];
+  double red[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) red[i] = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane % RPC, t = warp * (32 / RPC) + lane / RPC;
+  const int g0 = s_begin + blockIdx.x * RPC;
+  const int g1 = min(g0 + RPC, s_end);
+  const int32_t lo = ptr[g0], hi = ptr[g1];
+  uint32_t bv = 0, bi = 0;
+  const int64_t av = widen16<double>(lo, hi, &bv);
+  const int64_t ai = widen16<int32_t>(lo, hi, &bi);
+  double* sval = reinterpret_cast<double*>(stage);
+  int32_t* sidx = reinterpret_cast<int32_t*>(stage + bv);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, hi > lo ? bv + bi : 0);
+    if (hi > lo) {
+      bulk_g2s(sval, val + av, bv, &bar);
+      bulk_g2s(sidx, idx + ai, bi, &bar);
+    }
+  }
+  const int s = g0 + sub;
+  const bool own = s < s_end;
+  typename Op::Pre pre{};
+  int b = 0, e = 0;
+  if (own) {
+    b = ptr[s];
+    e = ptr[s + 1];
+    if (t == 0) pre = op.prefetch(s);
+  }
+  __syncthreads();  // barrier initialised
+  pdl_wait_trigger();
+  mbar_wait(&bar, 0);
+  double acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.0;
+  for (int k = b + t; k < e; k += T * U) {
+    int32_t j[U];
+    double v[U], p[U][R];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool in = k + T * u < e;
+      j[u] = in ? sidx[k + T * u - ai] : 0;
+      v[u] = in ? sval[k + T * u - av] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (k + T * u < e) {
+        op.map(j[u], v[u], p[u]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) p[u][r] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[u][r]);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double v = acc[r];
+#pragma unroll
+    for (int o = 16; o >= RPC; o >>= 1) v = combine<MX>(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane < RPC) sh[warp][lane][r] = v;
+  }
+  __syncthreads();
+  if (own && t == 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double v = sh[0][sub][r];
+      for (int w = 1; w < NW; ++w) v = combine<MX>(v, sh[w][sub][r]);
+      acc[r] = v;
+    }
+    op.finish(s, acc, pre, red);
+  }
+  block_reduce_out<Op, NW>(red, red_out);
+}
+
 template <class Op>
 inline void launch_cta_class(const Layout& L, const Op& op, double* red, cudaStream_t st, bool pdl = false) {
-  if (L.l_rpc == 4)
+  if (L.l_rpc == 4 && L.l_stage > 0) {
+    static const bool attr = [] {
+      cudaFuncSetAttribute(seg_cta4_staged_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaStageMax);
+      return true;
+    }();
+    (void)attr;
+    launch_k(seg_cta4_staged_kernel<Op>, L.nb_l(), kBlock, static_cast<size_t>(L.l_stage), st, pdl, L.ptr, L.idx,
+             L.val, L.s2, L.s3, op, red);
+  } else if (L.l_rpc == 4) {
     launch_k(seg_cta_kernel<Op, 4, kBlock, kCtaMinBlocks>, L.nb_l(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s2,
              L.s3, op, red);
-  else
+  } else {
     launch_k(seg_cta_kernel<Op, 1, kBlock, kCtaMinBlocks>, L.nb_l(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s2,
              L.s3, op, red);
+  }
 }
 
 // Reduction slots of one pass: [S blocks | M blocks | L CTAs | XL tiles | XL spans].

@@ -585,6 +585,20 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       }
       if (4 * adj >= L.s3 - L.s2 - 1 && adj > 0) L.l_rpc = 4;  // >= 25% adjacent pairs
     }
+    // RPC 4: stage each CTA's stream in shared memory when every group fits.
+    L.l_stage = 0;
+    const char* ts = std::getenv("PDHG_CTA_STAGE");
+    if (L.l_rpc == 4 && !(ts && ts[0] == '0')) {
+      DArray<int> mx;
+      mx.alloc(1);
+      PDHG_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), st_));
+      k_group_max<<<ew_grid((L.s3 - L.s2 + 3) / 4), kEw, 0, st_>>>(L.ptr, L.s2, L.s3, 4, mx.p);
+      int gmax = 0;
+      PDHG_CUDA(cudaMemcpyAsync(&gmax, mx.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      Sync();
+      const int64_t bytes = 12 * static_cast<int64_t>(gmax) + 64;  // + 16-byte widening of both ranges
+      if (bytes <= kCtaStageMax) L.l_stage = static_cast<int>(bytes);
+    }
   };
   {
     DArray<int32_t> fptr, fidx;

@@ -182,6 +182,20 @@ __global__ void k_first_index_key(const int32_t* p, const int32_t* idx, int64_t 
   GRID_STRIDE(s, nseg) key[s] = p[s + 1] > p[s] ? idx[p[s]] : INT32_MAX;
 }
 
+// Largest nonzero count of a group of `g` consecutive segments in [s0, s1)
+// (groups aligned at s0), into *out (initialised to 0).
+__global__ void k_group_max(const int32_t* ptr, int32_t s0, int32_t s1, int g, int* out) {
+  const int64_t ng = (static_cast<int64_t>(s1) - s0 + g - 1) / g;
+  int mx = 0;
+  GRID_STRIDE(q, ng) {
+    const int64_t a = s0 + q * g, b = a + g < s1 ? a + g : s1;
+    const int n = ptr[b] - ptr[a];
+    mx = n > mx ? n : mx;
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
 __global__ void k_gather_i32(const int32_t* in, const int32_t* perm, int32_t* out, int64_t n) {
   GRID_STRIDE(i, n) out[i] = in[perm[i]];
 }

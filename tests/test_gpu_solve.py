@@ -282,3 +282,21 @@ def test_one_shot_solves_reuse_pooled_memory():
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < (64 << 20)
+
+
+@pytest.mark.parametrize("shape", [(1000, 1000), (600, 40), (64, 900)])
+def test_staged_cta_kernel_bit_identical(shape, monkeypatch):
+    """The TMA-staged 4-segments-per-CTA kernel (engine.cuh
+    seg_cta4_staged_kernel) keeps the register path's per-thread order and
+    trees: whole trajectories are bitwise identical (PDHG_CTA_STAGE=0 forces
+    the register path)."""
+    p = GenTransport(shape[0], shape[1], 3)
+    prm = SolverParams(eps=1e-6, iter_limit=2000)
+    runs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PDHG_CTA_STAGE", flag)
+        runs.append(rpdlp.Solve(p, prm))
+    a, b = runs
+    assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)

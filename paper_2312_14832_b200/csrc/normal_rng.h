@@ -28,11 +28,74 @@
 
 namespace pdhg {
 
+// double(raw) rounded to nearest-even, without the data-dependent branch of
+// the compiler's unsigned conversion (half of all draws have bit 63 set):
+// above 2^63 the halved value with a sticky low bit rounds identically.
+inline double u64_to_double(uint64_t raw) {
+  const double lo = static_cast<double>(static_cast<int64_t>(raw));
+  const double hi = static_cast<double>(static_cast<int64_t>((raw >> 1) | (raw & 1))) * 2.0;
+  return static_cast<int64_t>(raw) >= 0 ? lo : hi;
+}
+
 inline double canonical53(uint64_t raw) {
-  double r = static_cast<double>(raw) / 18446744073709551616.0;  // 2^64
+  double r = u64_to_double(raw) / 18446744073709551616.0;  // 2^64
   if (r >= 1.0) r = std::nextafter(1.0, 0.0);
   return r;
 }
+
+// std::mt19937_64 (the C++ standard's parameters; libstdc++'s seeding,
+// twist and tempering) producing whole blocks: the twist of all 312 words
+// and the tempering are plain array loops the compiler vectorises, unlike
+// the engine's one-value operator(). Same sequence as std::mt19937_64(seed)
+// (tests/test_instances_and_shards.py checks it against the standard engine).
+class Mt64Block {
+ public:
+  static constexpr int kN = 312, kM = 156;
+  explicit Mt64Block(uint64_t seed) {
+    mt_[0] = seed;
+    for (int i = 1; i < kN; ++i) mt_[i] = 6364136223846793005ULL * (mt_[i - 1] ^ (mt_[i - 1] >> 62)) + i;
+    pos_ = kN;
+  }
+  // Next `count` outputs.
+  void Fill(uint64_t* out, int64_t count) {
+    while (count > 0) {
+      if (pos_ == kN) Twist();
+      const int take = static_cast<int>(std::min<int64_t>(count, kN - pos_));
+      Temper(mt_ + pos_, out, take);
+      pos_ += take;
+      out += take;
+      count -= take;
+    }
+  }
+
+ private:
+  static constexpr uint64_t kA = 0xB5026F5AA96619E9ULL, kUp = ~uint64_t(0) << 31, kLo = ~kUp;
+  static void Temper(const uint64_t* in, uint64_t* out, int n) {
+    for (int i = 0; i < n; ++i) {
+      uint64_t y = in[i];
+      y ^= (y >> 29) & 0x5555555555555555ULL;
+      y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+      y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+      y ^= y >> 43;
+      out[i] = y;
+    }
+  }
+  void Twist() {
+    for (int i = 0; i < kN - kM; ++i) {
+      const uint64_t y = (mt_[i] & kUp) | (mt_[i + 1] & kLo);
+      mt_[i] = mt_[i + kM] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+    }
+    for (int i = kN - kM; i < kN - 1; ++i) {
+      const uint64_t y = (mt_[i] & kUp) | (mt_[i + 1] & kLo);
+      mt_[i] = mt_[i + kM - kN] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+    }
+    const uint64_t y = (mt_[kN - 1] & kUp) | (mt_[0] & kLo);
+    mt_[kN - 1] = mt_[kM - 1] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+    pos_ = 0;
+  }
+  uint64_t mt_[kN];
+  int pos_;
+};
 
 inline void NormalVectorSequential(uint64_t seed, int64_t n, double* out) {
   std::mt19937_64 rng(seed);
@@ -128,7 +191,7 @@ inline void NormalVector(uint64_t seed, int64_t n, double* out, int threads) {
         cv.notify_all();
       }
     });
-  std::mt19937_64 rng(seed);
+  Mt64Block rng(seed);
   // Expected acceptance pi/4; 3% + one chunk of margin, more chunks if short.
   int64_t target = static_cast<int64_t>(need / 0.75) / kAttempts + 2;
   int64_t issued = 0;
@@ -142,7 +205,7 @@ inline void NormalVector(uint64_t seed, int64_t n, double* out, int threads) {
         avail.pop_front();
       }
       uint64_t* raw = buf[r].raw.data();
-      for (int i = 0; i < 2 * kAttempts; ++i) raw[i] = rng();
+      rng.Fill(raw, 2 * kAttempts);
       {
         std::lock_guard<std::mutex> lk(mu);
         count.push_back(0);

@@ -989,6 +989,28 @@ void Session::ToInternal(const double* host, const DArray<int32_t>& pad, double*
   Sync();
 }
 
+// Host copy of a staged result. Destinations are usually fresh pageable
+// buffers (numpy / std::vector): the copy is dominated by first-touch page
+// faults, which the kernel serves in parallel -- so large copies are split
+// over up to 8 threads.
+static void CopyOut(double* dst, const double* src, int64_t n) {
+  constexpr int64_t kChunk = int64_t(1) << 18;  // doubles per thread, at least
+  const int hw = static_cast<int>(std::thread::hardware_concurrency());
+  const int threads = static_cast<int>(std::min<int64_t>(std::min(std::max(hw, 1), 8), n / kChunk));
+  if (threads <= 1) {
+    std::memcpy(dst, src, n * sizeof(double));
+    return;
+  }
+  std::vector<std::thread> pool;
+  const int64_t per = (n + threads - 1) / threads;
+  for (int t = 1; t < threads; ++t) {
+    const int64_t b = std::min(n, t * per), e = std::min(n, b + per);
+    pool.emplace_back([=] { std::memcpy(dst + b, src + b, (e - b) * sizeof(double)); });
+  }
+  std::memcpy(dst, src, std::min(n, per) * sizeof(double));
+  for (auto& th : pool) th.join();
+}
+
 void Session::ToHost(const double* dev, const double* scale, const DArray<int32_t>& pad, double* host, int64_t n) {
   if (!n || !host) return;
   double* d = DevStage();
@@ -996,7 +1018,7 @@ void Session::ToHost(const double* dev, const double* scale, const DArray<int32_
   k_unpermute<<<ew_grid(n), kEw, 0, st_>>>(dev, scale, pad.p, d, n);
   PDHG_CUDA(cudaMemcpyAsync(h, d, n * sizeof(double), cudaMemcpyDeviceToHost, st_));
   Sync();
-  std::memcpy(host, h, n * sizeof(double));
+  CopyOut(host, h, n);
 }
 
 // ================================================================== kernels

@@ -1118,6 +1118,41 @@ void Session::RunSteps(int parity, int count, bool adapt) {
   check_launch("pdhg steps");
 }
 
+// Synchronous loop, block ending at a check: ONE captured graph holds the
+// block's steps, the inner_base advance, the check passes and the D2H of the
+// reduced pack into pinned host memory, so a check costs one graph launch and
+// one stream synchronisation instead of eager launches and a separate copy.
+void Session::RunChecked(int parity, int count) {
+  const int key = parity + 8;  // graphs_ key space: plain blocks use 0 / 1
+  Graph* g = nullptr;
+  for (Graph& gg : graphs_)
+    if (gg.steps == count && gg.parity == key && !gg.adapt) g = &gg;
+  const int pa = (parity + count) & 1;
+  if (!g) {
+    cudaGraph_t graph;
+    const int64_t before = launches_;
+    PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, false);
+    k_inner_add<<<1, 1, 0, st_>>>(scal_.p, count);
+    LaunchCheck(x_[pa].p, y_[pa].p, xbar_.p, ybar_.p, kx_[pa].p);
+    PDHG_CUDA(cudaMemcpyAsync(host_red_, red_out_.p, sizeof(CheckOut), cudaMemcpyDeviceToHost, st_));
+    PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
+    launches_ = before;
+    Graph ng;
+    ng.steps = count;
+    ng.parity = key;
+    ng.adapt = false;
+    PDHG_CUDA(cudaGraphInstantiate(&ng.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    graphs_.push_back(ng);
+    g = &graphs_.back();
+  }
+  launches_ += static_cast<int64_t>(count) * (launches_csc() + launches_csr()) + 1 + launches_csr() + launches_csc() +
+               static_cast<int64_t>(shards_.size()) + (shards_.size() > 1);
+  PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
+  check_launch("pdhg block + check");
+}
+
 // Pipelined loop: one captured graph per (length, parity, adapt, check,
 // slot) holding the block's steps, the counter advance and -- at check
 // iterations -- the check passes, k_decide, the best copy, the halt settle
@@ -1478,6 +1513,10 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   // Time limit: one clock decides for every rank (rank 0's, shipped in the
   // check pack), so all ranks leave the loop after the same block.
   bool time_up = !(prm.time_limit > 0.0);
+  static const bool fused_check = [] {  // PDHG_FUSED_CHECK=0: eager checks (A/B)
+    const char* e = std::getenv("PDHG_FUSED_CHECK");
+    return !(e && e[0] == '0');
+  }();
   while (!finished) {
     if (iters >= prm.iter_limit) {
       status = PDHG_ITER_LIMIT;
@@ -1490,23 +1529,37 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     }
     const int64_t to_check = prm.check_every - (iters % prm.check_every);
     const int64_t count = std::min<int64_t>(to_check, prm.iter_limit - iters);
-    if (adapt) {
-      sc.adapt_iter = static_cast<double>(iters);
-      PDHG_CUDA(cudaMemcpyAsync(&scal_.p->adapt_iter, &sc.adapt_iter, sizeof(double), cudaMemcpyHostToDevice, st_));
+    // A block ending at a check runs as one graph with the check (RunChecked);
+    // adaptive steps and NCCL sessions keep the eager check.
+    const bool fused = fused_check && !adapt && !nccl() && count == to_check && count >= 4;
+    if (fused) {
+      RunChecked(par, static_cast<int>(count));
+    } else {
+      if (adapt) {
+        sc.adapt_iter = static_cast<double>(iters);
+        PDHG_CUDA(
+            cudaMemcpyAsync(&scal_.p->adapt_iter, &sc.adapt_iter, sizeof(double), cudaMemcpyHostToDevice, st_));
+      }
+      RunSteps(par, static_cast<int>(count), adapt);
     }
-    RunSteps(par, static_cast<int>(count), adapt);
     par = static_cast<int>((par + count) & 1);
     iters += count;
     inner += count;
     sc.inner_base += static_cast<double>(count);
-    PDHG_CUDA(cudaMemcpyAsync(&scal_.p->inner_base, &sc.inner_base, sizeof(double), cudaMemcpyHostToDevice, st_));
+    if (!fused)
+      PDHG_CUDA(cudaMemcpyAsync(&scal_.p->inner_base, &sc.inner_base, sizeof(double), cudaMemcpyHostToDevice, st_));
     if (iters % prm.check_every != 0) continue;
 
     // ---- Check (solver.cpp:390-428).
     const double tc0 = secs();
     ++nchecks;
-    LaunchCheck(x_[par].p, y_[par].p, xbar_.p, ybar_.p, kx_[par].p);
-    if (nccl()) {  // rank 0's clock, summed into slot kPack - 1 of every rank
+    if (fused) {
+      Sync();
+      std::memcpy(&ck, host_red_, sizeof(CheckOut));
+    } else {
+      LaunchCheck(x_[par].p, y_[par].p, xbar_.p, ybar_.p, kx_[par].p);
+    }
+    if (!fused && nccl()) {  // rank 0's clock, summed into slot kPack - 1 of every rank
       host_red_[kPack - 1] = (rank_ == 0 && secs() >= prm.time_limit) ? 1.0 : 0.0;
       PDHG_CUDA(cudaMemcpyAsync(red_out_.p + kPack - 1, host_red_ + kPack - 1, sizeof(double), cudaMemcpyHostToDevice,
                                 st_));
@@ -1514,8 +1567,10 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
       PDHG_CUDA(cudaMemcpyAsync(host_red_ + kPack - 1, red_out_.p + kPack - 1, sizeof(double), cudaMemcpyDeviceToHost,
                                 st_));
     }
-    if (adapt) PDHG_CUDA(cudaMemcpyAsync(&sc.eta, &scal_.p->eta, sizeof(double), cudaMemcpyDeviceToHost, st_));
-    ReadCheck(&ck);
+    if (!fused) {
+      if (adapt) PDHG_CUDA(cudaMemcpyAsync(&sc.eta, &scal_.p->eta, sizeof(double), cudaMemcpyDeviceToHost, st_));
+      ReadCheck(&ck);
+    }
     t_checks += secs() - tc0;  // includes the wait for the block before it
     if (nccl()) time_up = host_red_[kPack - 1] > 0.0;
     if (ck.row[2 * kRowPer] > 0.0 || ck.col[2 * kColPer] > 0.0)

@@ -99,6 +99,7 @@ class Session {
   void DrawStart(uint64_t seed);
   void RunSteps(int parity, int count, bool adapt);
   void RunBlock(int parity, int count, bool adapt, bool check, int slot);
+  void RunChecked(int parity, int count);
   void LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx,
                    const Scalars* guard = nullptr);
   void ReadCheck(CheckOut* out);

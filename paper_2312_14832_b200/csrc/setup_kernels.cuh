@@ -196,6 +196,10 @@ __global__ void k_group_max(const int32_t* ptr, int32_t s0, int32_t s1, int g, i
   if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
+// RunningAverage weight base after a block of `count` steps (graph-resident
+// update of Scalars::inner_base).
+__global__ void k_inner_add(Scalars* sc, int count) { sc->inner_base += static_cast<double>(count); }
+
 __global__ void k_gather_i32(const int32_t* in, const int32_t* perm, int32_t* out, int64_t n) {
   GRID_STRIDE(i, n) out[i] = in[perm[i]];
 }

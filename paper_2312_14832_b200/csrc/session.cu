@@ -281,6 +281,7 @@ Session::~Session() {
   for (Graph& g : blocks_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   if (power_graph_) cudaGraphExecDestroy(power_graph_);
+  if (power_graph1_) cudaGraphExecDestroy(power_graph1_);
   pinned_put(host_red_, host_red_bytes_);
   pinned_put(hstage_, hstage_bytes_);
   pinned_put(hstate_, hstate_bytes_);
@@ -1723,32 +1724,48 @@ double Session::OpNorm(int iters, uint64_t seed) {
   sc.pw_norm = vnorm;
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   const int64_t ns = static_cast<int64_t>(shards_.size());
-  launches_ += static_cast<int64_t>(iters) * (launches_csr() + launches_csc() + ns + (ns > 1) + 1) + launches_csr() +
-               ns + (ns > 1);
-  // One power step is a captured graph per session, replayed `iters` times
-  // (a 100-step graph costs more to instantiate than it saves for a
-  // one-shot solve); the final K u pass is launched directly.
+  const bool single = shards_.size() == 1 && !nccl();
+  launches_ += static_cast<int64_t>(iters) * (launches_csr() + launches_csc() + (single ? 1 : ns + (ns > 1) + 1)) +
+               launches_csr() + ns + (ns > 1);
+  // Power steps run as captured graphs per session (a 100-step graph costs
+  // more to instantiate than it saves for a one-shot solve; kPowerSteps-step
+  // graphs do not); the final K u pass is launched directly.
   auto step = [&] {
     for (Shard& h : shards_) run_pass(h.csr, OpPowerStep<false>{u, scal_.p, 1, kv + h.roff}, RedSlots{}, fork_);
     GatherY(kv);
     for (size_t k = 0; k < shards_.size(); ++k) {
       Shard& h = shards_[k];
       run_pass(h.csc, OpPowerStep<true>{kv, scal_.p, 0, u + h.coff}, RedSlots{h.red[1].p}, fork_);
-      k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), 1, red_out_.p + k * kPack);
+      if (single)  // the reduction and the normalisation in one launch
+        k_reduce_power_norm<<<1, kBlock, 0, st_>>>(h.red[1].p, h.csc.parts(), red_out_.p, scal_.p);
+      else
+        k_reduce_tiles<<<1, kBlock, 0, st_>>>(h.red[1].p, nullptr, h.csc.parts(), 1, red_out_.p + k * kPack);
     }
-    SumPacks(1);
-    k_power_norm<<<1, 1, 0, st_>>>(red_out_.p, scal_.p);
+    if (!single) {
+      SumPacks(1);
+      k_power_norm<<<1, 1, 0, st_>>>(red_out_.p, scal_.p);
+    }
     GatherX(u);
   };
-  if (!power_graph_) {
+  // kPowerSteps steps per graph (PDHG_POWER_GRAPH_STEPS; 4 measured equal to
+  // 1 on transport, so 1), single-step graph for the remainder.
+  auto capture = [&](int steps, cudaGraphExec_t* exec) {
     cudaGraph_t graph;
     PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-    step();
+    for (int s = 0; s < steps; ++s) step();
     PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
-    PDHG_CUDA(cudaGraphInstantiate(&power_graph_, graph, 0));
+    PDHG_CUDA(cudaGraphInstantiate(exec, graph, 0));
     cudaGraphDestroy(graph);
-  }
-  for (int it = 0; it < iters; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph_, st_));
+  };
+  static const int kPowerSteps = [] {
+    const char* e = std::getenv("PDHG_POWER_GRAPH_STEPS");
+    return e ? std::max(1, std::atoi(e)) : 1;
+  }();
+  const int many = iters / kPowerSteps, rest = iters % kPowerSteps;
+  if (many && !power_graph_) capture(kPowerSteps, &power_graph_);
+  if (rest && !power_graph1_) capture(1, &power_graph1_);
+  for (int it = 0; it < many; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph_, st_));
+  for (int it = 0; it < rest; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph1_, st_));
   for (size_t k = 0; k < shards_.size(); ++k) {
     Shard& h = shards_[k];
     run_pass(h.csr, OpPowerStep<true>{u, scal_.p, 1, kv + h.roff}, RedSlots{h.red[0].p}, fork_);

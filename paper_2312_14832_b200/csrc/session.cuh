@@ -203,7 +203,8 @@ class Session {
 
   std::vector<Graph> graphs_;
   std::vector<Graph> blocks_;  // pipelined-loop block graphs
-  cudaGraphExec_t power_graph_ = nullptr;  // one EstimateOpNorm step (OpNorm)
+  cudaGraphExec_t power_graph_ = nullptr;   // kPowerSteps EstimateOpNorm steps (OpNorm)
+  cudaGraphExec_t power_graph1_ = nullptr;  // one step (remainder)
   DArray<char> flush_;
   cudaEvent_t ev_[2] = {nullptr, nullptr};
   double last_ms_ = 0.0;

@@ -445,6 +445,28 @@ __global__ void k_sumsq_partial(const double* v, int64_t n, double* part) {
 }
 
 // Power-iteration normalisation (solver.cpp:103-105).
+// k_reduce_tiles for one sum (ntiles slots of stride 1) followed by
+// k_power_norm, in one single-block launch (one shard, no NCCL).
+__global__ void k_reduce_power_norm(const double* tile, int ntiles, double* out, Scalars* sc) {
+  __shared__ double sh[kBlock / 32];
+  double acc = slot_sum(tile, nullptr, ntiles, 1, 0);
+  acc = warp_combine<false>(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = sh[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v += sh[w];
+    out[0] = v;
+    const double nr = sqrt(v);
+    if (nr == 0.0) {
+      sc->pw_zero = 1;
+      sc->pw_norm = 1.0;
+    } else {
+      sc->pw_norm = nr;
+    }
+  }
+}
+
 __global__ void k_power_norm(const double* sum, Scalars* sc) {
   const double nr = sqrt(sum[0]);
   if (nr == 0.0) {

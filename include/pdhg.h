@@ -224,6 +224,22 @@ int pdhg_session_ghost_counts(pdhg_session* s, int64_t* x_counts,
 int pdhg_partition_blocks(const int64_t* ptr, int64_t nseg, int parts,
                           int64_t seg_weight, int64_t* begin);
 void pdhg_session_destroy(pdhg_session* s);
+/* SparseMatrix::FromTriplets (sparse_matrix.cpp:25-69) on the device: sort
+ * by (row, col), sum duplicates, drop exact zeros, emit CSR (SURVEY §8f
+ * rank 1: device-side problem assembly). `trips` is the reference's Triplet
+ * layout {int64 row, int64 col, double value}. The sort is stable, so
+ * duplicates are summed in input order (the reference: in its std::sort
+ * order -- identical sums for up to two duplicates of one entry). Outputs are
+ * caller-allocated: row_ptr[rows + 1], col_idx[count], values[count]; *nnz
+ * receives the entries written. An index out of range returns
+ * PDHG_INVALID_ARGUMENT ("triplet index out of range"). count < 2^31. */
+typedef struct pdhg_triplet {
+  int64_t row, col;
+  double value;
+} pdhg_triplet;
+int pdhg_csr_from_triplets(int64_t rows, int64_t cols, int64_t count, const pdhg_triplet* trips, int device,
+                           int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* nnz,
+                           char* err, size_t errlen);
 /* The power-iteration start vector of EstimateOpNorm (solver.cpp:88-97):
  * n draws of std::normal_distribution<double>(0,1) over
  * std::mt19937_64(seed). threads < 0: the sequential libstdc++ draw;

@@ -116,6 +116,8 @@ SIGNATURES = {
     "pdhg_session_opnorm": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, dptr, C.c_char_p, C.c_size_t]),
     "pdhg_session_time_kernels": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, dptr, C.c_char_p, C.c_size_t]),
     "pdhg_session_time_check": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, C.c_char_p, C.c_size_t]),
+    "pdhg_csr_from_triplets": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int, i64ptr, i64ptr, dptr,
+                                         C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]),
     "pdhg_session_flush_l2": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
     "pdhg_session_last_solve": (C.c_int, [C.c_void_p, dptr, i64ptr]),
     "pdhg_should_restart": (C.c_int, [C.POINTER(Params), C.c_int64, C.c_int64, C.c_double, C.c_double,

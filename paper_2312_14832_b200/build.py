@@ -37,7 +37,7 @@ CU_SRCS = ["session.cu", "abi.cu"]
 CPP_SRCS = ["instance_gen.cpp", "rpdlp_api.cpp", "mps.cpp"]
 DROPIN_TEST = ROOT / "tests" / "cpp" / "drop_in_test.cpp"
 DROPIN_BIN = BUILD / "drop_in_test"
-HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh", "tma.cuh", "host_logic.h", "engine.cuh", "setup_kernels.cuh", "comm.cuh", "normal_rng.h"]
+HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh", "tma.cuh", "host_logic.h", "engine.cuh", "setup_kernels.cuh", "comm.cuh", "normal_rng.h", "assemble.cuh"]
 
 
 def _newer(target: Path, deps) -> bool:

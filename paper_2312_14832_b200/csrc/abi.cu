@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "assemble.cuh"
 #include "host_logic.h"
 #include "normal_rng.h"
 #include "session.cuh"
@@ -367,3 +368,16 @@ int pdhg_dual_step(const pdhg_lp* lp, const double* xn, const double* xo, const 
 }
 
 }  // extern "C"
+
+int pdhg_csr_from_triplets(int64_t rows, int64_t cols, int64_t count, const pdhg_triplet* trips, int device,
+                           int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* nnz, char* err,
+                           size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!row_ptr || !nnz || (count > 0 && (!trips || !col_idx || !values))) Invalid("null argument");
+    try {
+      *nnz = pdhg::CsrFromTriplets(rows, cols, count, trips, device, row_ptr, col_idx, values);
+    } catch (const std::out_of_range& e) {
+      Invalid(e.what());
+    }
+  });
+}

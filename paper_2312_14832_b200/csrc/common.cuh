@@ -1,6 +1,7 @@
 // Shared definitions for the B200 restarted-PDHG library.
 #pragma once
 
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -59,6 +60,17 @@ struct CMat {
 // Device-resident solver scalars: the iteration kernels read these instead
 // of taking per-iteration host arguments, so a 64-iteration block can be
 // replayed as one CUDA graph.
+// Elementwise kernels: grid-stride loops over at most 16 CTAs per SM.
+constexpr int kEw = 256;  // elementwise block size
+
+inline int ew_grid(int64_t n) {
+  int64_t g = (n + kEw - 1) / kEw;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
+}
+
+#define GRID_STRIDE(i, n) \
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
 struct Scalars {
   double eta;
   double omega;

@@ -31,8 +31,29 @@ struct Trip {
   double v;
 };
 
-// FromTriplets (sparse_matrix.cpp:25-69) into CSR arrays.
-void FromTriplets(I rows, std::vector<Trip> t, std::vector<I>* ptr, std::vector<I>* idx, std::vector<double>* val) {
+// FromTriplets (sparse_matrix.cpp:25-69) into CSR arrays; >= 2^20 triplets
+// are assembled on the device when one is present (pdhg_csr_from_triplets;
+// the generators' duplicates -- repeated PageRank edges -- carry equal
+// values, so the stable device order sums them to the same bits).
+void FromTriplets(I rows, std::vector<Trip> t, std::vector<I>* ptr, std::vector<I>* idx, std::vector<double>* val,
+                  I cols) {
+  static_assert(sizeof(Trip) == sizeof(pdhg_triplet), "Trip layout");
+  const char* da = std::getenv("PDHG_DEVICE_ASSEMBLY");  // "0": host only (A/B, tests)
+  if (t.size() >= (size_t(1) << 20) && !(da && da[0] == '0')) {
+    const char* dv = std::getenv("PDHG_DEVICE");
+    ptr->assign(rows + 1, 0);
+    idx->resize(t.size());
+    val->resize(t.size());
+    int64_t nnz = 0;
+    char err[256] = {0};
+    if (pdhg_csr_from_triplets(rows, cols, static_cast<int64_t>(t.size()), reinterpret_cast<const pdhg_triplet*>(t.data()),
+                               dv ? std::atoi(dv) : 0, ptr->data(), idx->data(), val->data(), &nnz, err,
+                               sizeof(err)) == PDHG_OK) {
+      idx->resize(nnz);
+      val->resize(nnz);
+      return;
+    }
+  }
   std::sort(t.begin(), t.end(),
             [](const Trip& a, const Trip& b) { return std::tie(a.row, a.col) < std::tie(b.row, b.col); });
   ptr->assign(rows + 1, 0);
@@ -89,7 +110,7 @@ pdhg_instance* RandomLp(I m, I n, double density, uint64_t seed) {
     }
   }
   p->g_rows = m;
-  FromTriplets(m, std::move(t), &p->g_ptr, &p->g_idx, &p->g_val);
+  FromTriplets(m, std::move(t), &p->g_ptr, &p->g_idx, &p->g_val, n);
   std::vector<double> gx(m);
   CsrMul(p->g_ptr, p->g_idx, p->g_val, p->witness.data(), m, gx.data());
   p->h.resize(m);
@@ -147,7 +168,7 @@ pdhg_instance* Pagerank(I n_nodes, double damping, I attachment, uint64_t seed) 
   auto* p = new pdhg_instance;
   p->n = n_nodes;
   p->g_rows = n_nodes;
-  FromTriplets(n_nodes, std::move(t), &p->g_ptr, &p->g_idx, &p->g_val);
+  FromTriplets(n_nodes, std::move(t), &p->g_ptr, &p->g_idx, &p->g_val, n_nodes);
   p->h.assign(n_nodes, (1.0 - damping) / static_cast<double>(n_nodes));
   p->a_rows = 1;
   p->a_ptr = {0, n_nodes};

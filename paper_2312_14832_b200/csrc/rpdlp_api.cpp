@@ -18,8 +18,44 @@
 namespace rpdlp {
 
 // ------------------------------------------------------------ SparseMatrix
+// Large inputs are assembled on the device (pdhg_csr_from_triplets: stable
+// radix sort; duplicates summed in input order -- the same sums as here for
+// up to two duplicates of an entry). Host path below that size, or when no
+// device is present (problem building is not the solve path).
+constexpr size_t kDeviceTriplets = size_t(1) << 20;
+
+static bool DeviceAssemble(Index rows, Index cols, const std::vector<Triplet>& t, std::vector<Index>* rp,
+                           std::vector<Index>* ci, std::vector<double>* val) {
+  static_assert(sizeof(Triplet) == sizeof(pdhg_triplet), "Triplet layout");
+  const char* da = std::getenv("PDHG_DEVICE_ASSEMBLY");  // "0": host only (A/B, tests)
+  if (t.size() < kDeviceTriplets || (da && da[0] == '0')) return false;
+  const char* dv = std::getenv("PDHG_DEVICE");
+  rp->assign(rows + 1, 0);
+  ci->resize(t.size());
+  val->resize(t.size());
+  int64_t nnz = 0;
+  char err[512] = {0};
+  const int rc = pdhg_csr_from_triplets(rows, cols, static_cast<int64_t>(t.size()),
+                                        reinterpret_cast<const pdhg_triplet*>(t.data()), dv ? std::atoi(dv) : 0,
+                                        rp->data(), ci->data(), val->data(), &nnz, err, sizeof(err));
+  if (rc == PDHG_INVALID_ARGUMENT) throw std::out_of_range(err);
+  if (rc != PDHG_OK) return false;  // no usable device
+  ci->resize(nnz);
+  val->resize(nnz);
+  return true;
+}
+
 SparseMatrix SparseMatrix::FromTriplets(Index n_rows, Index n_cols, std::vector<Triplet> t) {
   if (n_rows < 0 || n_cols < 0) throw std::invalid_argument("negative matrix dimension");
+  {
+    SparseMatrix m;
+    if (DeviceAssemble(n_rows, n_cols, t, &m.rp_, &m.ci_, &m.val_)) {
+      m.rows_ = n_rows;
+      m.cols_ = n_cols;
+      m.BuildColumns();
+      return m;
+    }
+  }
   for (const Triplet& e : t)
     if (e.row < 0 || e.row >= n_rows || e.col < 0 || e.col >= n_cols)
       throw std::out_of_range("triplet index out of range");

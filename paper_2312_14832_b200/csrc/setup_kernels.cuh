@@ -7,15 +7,6 @@
 
 namespace pdhg {
 
-constexpr int kEw = 256;  // elementwise block size
-
-inline int ew_grid(int64_t n) {
-  int64_t g = (n + kEw - 1) / kEw;
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
-}
-
-#define GRID_STRIDE(i, n) \
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
 // ------------------------------------------------------------------ upload
 __global__ void k_narrow(const int64_t* in, int32_t* out, int64_t count, int64_t limit, int* bad) {

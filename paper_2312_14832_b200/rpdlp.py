@@ -120,6 +120,26 @@ class CsrMatrix:
         return CsrMatrix(rows, cols, np.cumsum(ptr).astype(np.int64), np.asarray(idx, np.int64),
                          np.asarray(val, np.float64))
 
+    @staticmethod
+    def from_triplets_device(rows: int, cols: int, row, col, value, device: int = 0) -> "CsrMatrix":
+        """FromTriplets on the device (pdhg_csr_from_triplets, SURVEY §8f
+        rank 1): stable radix sort, duplicates summed in input order, exact
+        zeros dropped. Arrays of row / column indices and values."""
+        row, col, value = np.asarray(row), np.asarray(col), np.asarray(value, np.float64)
+        n = int(row.size)
+        if not (col.size == n and value.size == n):
+            raise ValueError("row / col / value lengths differ")
+        trips = np.empty(n, dtype=[("row", "<i8"), ("col", "<i8"), ("value", "<f8")])
+        trips["row"], trips["col"], trips["value"] = row, col, value
+        ptr = np.zeros(rows + 1, np.int64)
+        idx, val = np.empty(max(n, 1), np.int64), np.empty(max(n, 1), np.float64)
+        nnz = C.c_int64(0)
+        err = C.create_string_buffer(abi.ERRLEN)
+        raise_for(abi.load().pdhg_csr_from_triplets(rows, cols, n, trips.ctypes.data, device, _i64p(ptr), _i64p(idx),
+                                                    _dp(val), C.byref(nnz), err, abi.ERRLEN), err)
+        k = nnz.value
+        return CsrMatrix(rows, cols, ptr, idx[:k].copy(), val[:k].copy())
+
     @property
     def nnz(self) -> int:
         return int(self.row_ptr[-1]) if self.rows else 0

@@ -3,6 +3,8 @@
 // Cases follow the reference's own unit tests (test_solver.cpp, test_kkt.cpp)
 // and acceptance criteria C1/C5 shapes. Exit code = number of failures.
 #include <cmath>
+#include <cstdlib>
+#include <random>
 #include <cstdio>
 #include <limits>
 #include <numeric>
@@ -218,6 +220,28 @@ int main() {
     double dl = 0.0;
     for (size_t j = 0; j < lam.size(); ++j) dl = std::max(dl, std::abs(lam[j] - ro.lambda[j]));
     CHECK(dl <= 1e-12);
+  }
+  {  // >= 2^20 triplets take the device assembly (pdhg_csr_from_triplets): same matrix as the host path
+    std::mt19937_64 g(5);
+    std::vector<Triplet> t(1200000);
+    for (Triplet& e : t) {
+      e.row = static_cast<Index>(g() % 5000);
+      e.col = static_cast<Index>(g() % 4000);
+      e.value = static_cast<double>(static_cast<int>(g() % 33) - 16) / 8.0;  // dyadic: duplicate sums exact
+    }
+    setenv("PDHG_DEVICE_ASSEMBLY", "0", 1);
+    const SparseMatrix h = SparseMatrix::FromTriplets(5000, 4000, t);
+    unsetenv("PDHG_DEVICE_ASSEMBLY");
+    const SparseMatrix d = SparseMatrix::FromTriplets(5000, 4000, t);
+    CHECK(h.nnz() > 1000000 && h == d);
+    t.push_back({5000, 0, 1.0});
+    bool threw = false;
+    try {
+      SparseMatrix::FromTriplets(5000, 4000, t);
+    } catch (const std::out_of_range&) {
+      threw = true;
+    }
+    CHECK(threw);
   }
   std::printf("drop_in_test: %d passed, %d failed\n", g_pass, g_fail);
   return g_fail;

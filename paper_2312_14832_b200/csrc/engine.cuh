@@ -42,6 +42,7 @@ struct Layout {
   double* val = nullptr;
   int32_t s1 = 0, s2 = 0, s3 = 0;  // class bounds S | M | L | XL
   bool s_staged = false;           // class S uses seg_thread_staged_kernel
+  const uint8_t* s_rm = nullptr;   // per-32-segment flags: segment-order gathers (staged kernel)
   int l_rpc = 1;                   // class L segments per CTA (1 or 4)
   int l_stage = 0;                 // > 0: RPC-4 stream staged by TMA, dynamic smem bytes
   int s_len = 0;                   // common class-S length (1,2,3,4,8) or 0
@@ -251,12 +252,21 @@ __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_
 // storage order, exactly like the direct variant.
 constexpr int kSChunk = 256;
 
-template <class Op>
+//
+// Segment-order warps (kRM, per-warp flags `rm`): when a warp's 32 segments
+// are shifted copies of each other -- segment s + 1 gathers index + 1 where s
+// gathers index (one MCF node's conservation rows across commodities) -- the
+// warp stages the raw (idx, val) chunk instead of the products and each lane
+// then walks its own segment, so the 32 lanes gather 32 adjacent entries per
+// step instead of one lane-strided entry each of 32 unrelated segments. The
+// sums run in the same storage order either way.
+template <class Op, bool kRM = false>
 __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int32_t* __restrict__ ptr,
                                                                       const int32_t* __restrict__ idx,
                                                                       const double* __restrict__ val,
                                                                       int32_t s_end, const Op op,
-                                                                      double* __restrict__ red_out) {
+                                                                      double* __restrict__ red_out,
+                                                                      const uint8_t* __restrict__ rm = nullptr) {
   if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
@@ -264,6 +274,7 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
   constexpr int C = kSChunk;
   constexpr int U = C / 32;
   __shared__ double sprod[kWarps][R][C];
+  __shared__ int32_t sidx[kRM ? kWarps : 1][kRM ? C : 1];
   double red[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
@@ -286,6 +297,7 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
     double(*sp)[C] = sprod[warp];
+    const bool seg_order = kRM && rm[s0 >> 5];  // warp-uniform
     for (int c0 = wb; c0 < we; c0 += C) {
       int32_t j[U];
       double v[U];
@@ -294,6 +306,37 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
         const int k = c0 + lane + 32 * u;
         j[u] = k < we ? ld_stream(idx + k) : 0;
         v[u] = k < we ? ld_stream(val + k) : 0.0;
+      }
+      if constexpr (kRM) {
+        if (seg_order) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            sidx[warp][lane + 32 * u] = j[u];
+            sp[0][lane + 32 * u] = v[u];
+          }
+          __syncwarp();
+          const int lo = (b > c0 ? b : c0) - c0;
+          const int hi = (e < c0 + C ? e : c0 + C) - c0;
+          constexpr int Q = 4;
+          int q = lo;
+          for (; q + Q <= hi; q += Q) {
+            double p[Q][R];
+#pragma unroll
+            for (int t = 0; t < Q; ++t) op.map(sidx[warp][q + t], sp[0][q + t], p[t]);
+#pragma unroll
+            for (int t = 0; t < Q; ++t)
+#pragma unroll
+              for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[t][r]);  // storage order
+          }
+          for (; q < hi; ++q) {
+            double p[R];
+            op.map(sidx[warp][q], sp[0][q], p);
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[r]);
+          }
+          __syncwarp();
+          continue;
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -477,8 +520,12 @@ inline void launch_thread_class(const Layout& L, const Op& op, double* red, cuda
       default: break;
     }
   }
-  if (L.s_staged)
-    launch_k(seg_thread_staged_kernel<Op>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red);
+  if (L.s_staged && L.s_rm)
+    launch_k(seg_thread_staged_kernel<Op, true>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red,
+             static_cast<const uint8_t*>(L.s_rm));
+  else if (L.s_staged)
+    launch_k(seg_thread_staged_kernel<Op, false>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red,
+             static_cast<const uint8_t*>(nullptr));
   else
     launch_k(seg_thread_kernel<Op>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red);
 }

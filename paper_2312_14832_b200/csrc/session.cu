@@ -551,6 +551,22 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       Sync();
     }
     L.s_staged = L.s1 > 0 && static_cast<double>(se) >= staged_min * L.s1;
+    // Segment-order warps of the staged kernel (shifted-copy segment groups).
+    L.s_rm = nullptr;
+    const char* rmo = std::getenv("PDHG_SEG_ORDER_WARPS");  // "0": off (A/B)
+    if (L.s_staged && !(rmo && rmo[0] == '0')) {
+      const int64_t ng = (static_cast<int64_t>(L.s1) + 31) / 32;
+      S.rm.alloc(ng, &arena_);
+      DArray<int> any;
+      any.alloc(1);
+      PDHG_CUDA(cudaMemsetAsync(any.p, 0, sizeof(int), st_));
+      k_rowmajor_flags<<<ew_grid(ng), kEw, 0, st_>>>(L.ptr, L.idx, L.s1, S.rm.p, any.p);
+      int hany = 0;
+      PDHG_CUDA(cudaMemcpyAsync(&hany, any.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      Sync();
+      if (hany) L.s_rm = S.rm.p;
+      else S.rm.release();
+    }
     // Class S of one common length (and starting at nonzero 0): offsets implicit.
     L.s_len = 0;
     if (L.s1 > 0 && uniform_s) {

@@ -73,6 +73,7 @@ class Session {
     DArray<int32_t> part[4];  // tile_begin, tile_seg, head_first, tail_owner (long class)
     DArray<double> head, tail;
     DArray<unsigned> cnt;
+    DArray<uint8_t> rm;  // staged class-S segment-order warp flags
   };
   struct Shard {
     int block = 0;

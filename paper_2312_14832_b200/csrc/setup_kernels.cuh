@@ -152,6 +152,29 @@ __global__ void k_adjacent_count(const int32_t* p, const int32_t* idx, int32_t l
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+// Segment-order flags of the staged class-S kernel: warp group g (segments
+// [32g, 32g + 32) of [0, s1)) is flagged when at least half of its adjacent
+// pairs have equal lengths and middle entries exactly one index apart (shifted
+// copies). *any counts flagged groups.
+__global__ void k_rowmajor_flags(const int32_t* p, const int32_t* idx, int32_t s1, uint8_t* flag, int* any) {
+  const int64_t ng = (static_cast<int64_t>(s1) + 31) / 32;
+  int c = 0;
+  GRID_STRIDE(g, ng) {
+    const int32_t a = static_cast<int32_t>(g * 32), z = a + 32 < s1 ? a + 32 : s1;
+    int hit = 0, pairs = 0;
+    for (int32_t s = a; s + 1 < z; ++s) {
+      const int32_t l0 = p[s + 1] - p[s], l1 = p[s + 2] - p[s + 1];
+      ++pairs;
+      if (l0 > 0 && l0 == l1 && idx[p[s + 1] + l1 / 2] == idx[p[s] + l0 / 2] + 1) ++hit;
+    }
+    const uint8_t f = pairs > 0 && 2 * hit >= pairs;
+    flag[g] = f;
+    c += f;
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(any, c);
+}
+
 // Ghost plans: mark every gathered index; count marked indices per block.
 __global__ void k_mark(const int32_t* idx, int64_t n, uint8_t* mark) {
   GRID_STRIDE(k, n) mark[idx[k]] = 1;

@@ -17,6 +17,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > "$O/bench_re
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$O/launches.csv" \
     python bench.py --steps 1 --warmup 3 --no-cpu --e2e-steps 1 --kernel-iters 8 > "$O/ncu_bench.log" 2>&1
 # full capture of the fused step kernels on the transport workload
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"seg_|tile_" -s 20 -c 6 \
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k regex:"OpPrimal|OpDual" -s 4 -c 4 \
     -o "$O/prof_transport" python tools/profile_step.py transport > "$O/ncu_full.log" 2>&1
 echo done

@@ -40,6 +40,7 @@ struct OpPowerStep {
   static constexpr int kRhs = 1, kRed = kSumSq ? 1 : 0;
   static constexpr bool kMax = false;
   static constexpr bool kUniform = true;
+  static constexpr bool kPdl = true;  // no prologue operands; gathers and pw_norm after the wait
   using Pre = Nil;
   const double* x;
   const Scalars* sc;  // pw_norm divides the gathered operand

@@ -1140,6 +1140,10 @@ void Session::RunSteps(int parity, int count, bool adapt) {
 // reduced pack into pinned host memory, so a check costs one graph launch and
 // one stream synchronisation instead of eager launches and a separate copy.
 void Session::RunChecked(int parity, int count) {
+  static const bool check_branches = [] {  // PDHG_CHECK_BRANCHES=0: serial check passes (A/B)
+    const char* e = std::getenv("PDHG_CHECK_BRANCHES");
+    return !(e && e[0] == '0');
+  }();
   const int key = parity + 8;  // graphs_ key space: plain blocks use 0 / 1
   Graph* g = nullptr;
   for (Graph& gg : graphs_)
@@ -1151,7 +1155,7 @@ void Session::RunChecked(int parity, int count) {
     PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
     for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, false);
     k_inner_add<<<1, 1, 0, st_>>>(scal_.p, count);
-    LaunchCheck(x_[pa].p, y_[pa].p, xbar_.p, ybar_.p, kx_[pa].p);
+    LaunchCheck(x_[pa].p, y_[pa].p, xbar_.p, ybar_.p, kx_[pa].p, nullptr, check_branches);
     PDHG_CUDA(cudaMemcpyAsync(host_red_, red_out_.p, sizeof(CheckOut), cudaMemcpyDeviceToHost, st_));
     PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
     launches_ = before;
@@ -1222,7 +1226,7 @@ void Session::RunBlock(int parity, int count, bool adapt, bool check, int slot) 
 // gathered operands are all-gathered first; the 26 sums are reduced per
 // shard, over local shards and over ranks.
 void Session::LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx,
-                          const Scalars* guard) {
+                          const Scalars* guard, bool branches) {
   if (xb != x) GatherX(const_cast<double*>(xb));
   if (yb != y) GatherY(const_cast<double*>(yb));
   launches_ += launches_csr() + launches_csc() + static_cast<int64_t>(shards_.size()) + (shards_.size() > 1);
@@ -1231,7 +1235,17 @@ void Session::LaunchCheck(const double* x, const double* y, const double* xb, co
     const int64_t r = h.roff, c = h.coff;
     OpCheckRow row{xb, kxavg_.p + r, kx + r, y + r, yb + r, ystart_.p + r, q_s_.p + r, q_o_.p + r, rs_.p + r, h.rk,
                    guard};
-    run_pass(h.csr, row, RedSlots{h.red[0].p}, fork_);
+    // Inside a captured graph (`branches`) the independent row and column
+    // passes become parallel branches when the row pass is one kernel.
+    cudaStream_t side = fork_.side[2];
+    const bool beside = branches && side && pass_launches(h.csr) == 1;
+    if (beside) {
+      PDHG_CUDA(cudaEventRecord(fork_.fork, st_));
+      PDHG_CUDA(cudaStreamWaitEvent(side, fork_.fork, 0));
+      run_pass(h.csr, row, RedSlots{h.red[0].p}, side);
+    } else {
+      run_pass(h.csr, row, RedSlots{h.red[0].p}, fork_);
+    }
     if (bnd_all_) {
       OpCheckCol<true> col{y, yb, x + c, xb + c, xstart_.p + c, c_s_.p + c, l_s_.p + c, u_s_.p + c, c_o_.p + c,
                            l_o_.p + c, u_o_.p + c, cs_.p + c, guard, lb_, ub_};
@@ -1240,6 +1254,10 @@ void Session::LaunchCheck(const double* x, const double* y, const double* xb, co
       OpCheckCol<false> col{y, yb, x + c, xb + c, xstart_.p + c, c_s_.p + c, l_s_.p + c, u_s_.p + c, c_o_.p + c,
                             l_o_.p + c, u_o_.p + c, cs_.p + c, guard};
       run_pass(h.csc, col, RedSlots{h.red[1].p}, fork_);
+    }
+    if (beside) {  // join (a 4-class column pass may re-record join[2] on the same stream: still after)
+      PDHG_CUDA(cudaEventRecord(fork_.join[2], side));
+      PDHG_CUDA(cudaStreamWaitEvent(st_, fork_.join[2], 0));
     }
     double* pk = red_out_.p + k * kPack;
     if (guard)

@@ -102,7 +102,7 @@ class Session {
   void RunBlock(int parity, int count, bool adapt, bool check, int slot);
   void RunChecked(int parity, int count);
   void LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx,
-                   const Scalars* guard = nullptr);
+                   const Scalars* guard = nullptr, bool branches = false);
   void ReadCheck(CheckOut* out);
   void SumPacks(int n, const Scalars* guard = nullptr);  // shard packs -> red_out_[0..n), all ranks
   void Copy(double* dst, const double* src, size_t n);

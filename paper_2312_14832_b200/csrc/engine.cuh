@@ -1,17 +1,19 @@
 // Length-class dispatch of every matrix pass.
 //
-// At setup the rows of K (CSR) and the columns (CSC) are permuted into three
+// At setup the rows of K (CSR) and the columns (CSC) are permuted into four
 // contiguous length classes, keeping the storage order inside each segment
 // (so every segment sum is formed exactly as before):
-//   S  (<= kSeqMax = 32 nonzeros): one thread per segment, direct loads, sum
+//   S  (<= kThreadMax = 64 nonzeros, session.cu): one thread per segment, sum
 //      in storage order -- bit-identical to the reference's `acc += v * x[j]`
-//      loops;
-//   M  (33 .. kWarpMax = 512): one warp per segment, lane-strided loads,
+//      loops. Kernels: direct loads, uniform length with implicit offsets,
+//      or warp-staged chunks (with segment-order warps for shifted copies);
+//   M  (65 .. kWarpMax = 512): one warp per segment, lane-strided loads,
 //      fixed butterfly;
-//   L  (513 .. kCtaMax = 16384): one CTA per segment, fixed tree;
+//   L  (513 .. kCtaMax = 16384): one CTA per segment (or per 4 adjacent
+//      segments, interleaved lanes, stream staged by TMA), fixed tree;
 //   XL (> kCtaMax): the TMA tile engine (tile_spmv.cuh), several CTAs per
 //      segment with last-arriver combination.
-// Each class writes its own reduction partials; `k_reduce_parts` sums them in
+// Each class writes its own reduction slots; the slot reductions sum them in
 // a fixed order, so every pass stays bitwise reproducible.
 #pragma once
 

@@ -48,20 +48,53 @@ inline double canonical53(uint64_t raw) {
 // and the tempering are plain array loops the compiler vectorises, unlike
 // the engine's one-value operator(). Same sequence as std::mt19937_64(seed)
 // (tests/test_instances_and_shards.py checks it against the standard engine).
+// Twist and tempering as free functions cloned for AVX2 (GCC function
+// multiversioning: integer ops only, so every clone is bit-identical).
+namespace mt64 {
+constexpr int kN = 312, kM = 156;
+constexpr uint64_t kA = 0xB5026F5AA96619E9ULL, kUp = ~uint64_t(0) << 31, kLo = ~kUp;
+
+__attribute__((target_clones("avx2", "default"))) static void Temper(const uint64_t* in, uint64_t* out, int n) {
+  for (int i = 0; i < n; ++i) {
+    uint64_t y = in[i];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    out[i] = y;
+  }
+}
+
+__attribute__((target_clones("avx2", "default"))) static void Twist(uint64_t* mt) {
+  for (int i = 0; i < kN - kM; ++i) {
+    const uint64_t y = (mt[i] & kUp) | (mt[i + 1] & kLo);
+    mt[i] = mt[i + kM] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+  }
+  for (int i = kN - kM; i < kN - 1; ++i) {
+    const uint64_t y = (mt[i] & kUp) | (mt[i + 1] & kLo);
+    mt[i] = mt[i + kM - kN] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+  }
+  const uint64_t y = (mt[kN - 1] & kUp) | (mt[0] & kLo);
+  mt[kN - 1] = mt[kM - 1] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+}
+}  // namespace mt64
+
 class Mt64Block {
  public:
-  static constexpr int kN = 312, kM = 156;
   explicit Mt64Block(uint64_t seed) {
     mt_[0] = seed;
-    for (int i = 1; i < kN; ++i) mt_[i] = 6364136223846793005ULL * (mt_[i - 1] ^ (mt_[i - 1] >> 62)) + i;
-    pos_ = kN;
+    for (int i = 1; i < mt64::kN; ++i) mt_[i] = 6364136223846793005ULL * (mt_[i - 1] ^ (mt_[i - 1] >> 62)) + i;
+    pos_ = mt64::kN;
   }
   // Next `count` outputs.
   void Fill(uint64_t* out, int64_t count) {
     while (count > 0) {
-      if (pos_ == kN) Twist();
-      const int take = static_cast<int>(std::min<int64_t>(count, kN - pos_));
-      Temper(mt_ + pos_, out, take);
+      if (pos_ == mt64::kN) {
+        mt64::Twist(mt_);
+        pos_ = 0;
+      }
+      const int take = static_cast<int>(std::min<int64_t>(count, mt64::kN - pos_));
+      mt64::Temper(mt_ + pos_, out, take);
       pos_ += take;
       out += take;
       count -= take;
@@ -69,31 +102,7 @@ class Mt64Block {
   }
 
  private:
-  static constexpr uint64_t kA = 0xB5026F5AA96619E9ULL, kUp = ~uint64_t(0) << 31, kLo = ~kUp;
-  static void Temper(const uint64_t* in, uint64_t* out, int n) {
-    for (int i = 0; i < n; ++i) {
-      uint64_t y = in[i];
-      y ^= (y >> 29) & 0x5555555555555555ULL;
-      y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
-      y ^= (y << 37) & 0xFFF7EEE000000000ULL;
-      y ^= y >> 43;
-      out[i] = y;
-    }
-  }
-  void Twist() {
-    for (int i = 0; i < kN - kM; ++i) {
-      const uint64_t y = (mt_[i] & kUp) | (mt_[i + 1] & kLo);
-      mt_[i] = mt_[i + kM] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
-    }
-    for (int i = kN - kM; i < kN - 1; ++i) {
-      const uint64_t y = (mt_[i] & kUp) | (mt_[i + 1] & kLo);
-      mt_[i] = mt_[i + kM - kN] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
-    }
-    const uint64_t y = (mt_[kN - 1] & kUp) | (mt_[0] & kLo);
-    mt_[kN - 1] = mt_[kM - 1] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
-    pos_ = 0;
-  }
-  uint64_t mt_[kN];
+  uint64_t mt_[mt64::kN];
   int pos_;
 };
 

@@ -663,3 +663,13 @@ double ResidualEvaluator::KktOmega(std::span<const double> x, std::span<const do
 }
 
 }  // namespace rpdlp
+
+namespace rpdlp {
+
+Iterate ChooseRestartCandidate(const LpProblem& problem, const Iterate& z_cur, const Iterate& z_avg, double omega) {
+  const ResidualEvaluator ev(problem);  // both points on one device-resident problem
+  const bool current = ev.KktOmega(z_cur.x, z_cur.y, omega) < ev.KktOmega(z_avg.x, z_avg.y, omega);
+  return current ? z_cur : z_avg;
+}
+
+}  // namespace rpdlp

@@ -626,6 +626,14 @@ def KktOmega(problem: LpProblem, x, y, omega: float) -> float:
     return KktError(r.primal_res, r.dual_res, r.gap_abs, omega)
 
 
+def ChooseRestartCandidate(problem: LpProblem, z_cur, z_avg, omega: float):
+    """solver.cpp:170-176: (x, y) of the current iterate when its KKT_omega
+    error is strictly smaller, else the average (ties -> average)."""
+    cur = KktOmega(problem, z_cur[0], z_cur[1], omega)
+    avg = KktOmega(problem, z_avg[0], z_avg[1], omega)
+    return z_cur if cur < avg else z_avg
+
+
 def DeriveLambda(problem: LpProblem, y) -> np.ndarray:
     """kkt.cpp:127-141 (device)."""
     lp = problem.to_c()

@@ -221,6 +221,18 @@ int main() {
     for (size_t j = 0; j < lam.size(); ++j) dl = std::max(dl, std::abs(lam[j] - ro.lambda[j]));
     CHECK(dl <= 1e-12);
   }
+  {  // ChooseRestartCandidate (solver.cpp:170-176, test_solver.cpp restart tests): strict < picks current
+    LpProblem p = GenRandomLp(10, 12, 0.4, 4);
+    SolverParams prm;
+    prm.eps = 1e-8;
+    SolveResult r = Solve(p, prm);
+    const Iterate good{r.x, r.y};
+    const Iterate zero{std::vector<double>(r.x.size(), 0.0), std::vector<double>(r.y.size(), 0.0)};
+    CHECK(ChooseRestartCandidate(p, good, zero, 1.0) == good);
+    CHECK(ChooseRestartCandidate(p, zero, good, 1.0) == good);
+    const Iterate same = good;
+    CHECK(ChooseRestartCandidate(p, good, same, 1.0) == same);  // tie -> average
+  }
   {  // >= 2^20 triplets take the device assembly (pdhg_csr_from_triplets): same matrix as the host path
     std::mt19937_64 g(5);
     std::vector<Triplet> t(1200000);

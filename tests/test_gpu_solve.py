@@ -300,3 +300,15 @@ def test_staged_cta_kernel_bit_identical(shape, monkeypatch):
     assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
+
+
+def test_choose_restart_candidate():
+    """solver.cpp:170-176: current only on a strictly smaller KKT_omega."""
+    p = GenRandomLp(10, 12, 0.4, 4)
+    r = rpdlp.Solve(p, SolverParams(eps=1e-8))
+    good = (r.x, r.y)
+    zero = (np.zeros_like(r.x), np.zeros_like(r.y))
+    assert rpdlp.ChooseRestartCandidate(p, good, zero, 1.0) is good
+    assert rpdlp.ChooseRestartCandidate(p, zero, good, 1.0) is good
+    twin = (r.x.copy(), r.y.copy())
+    assert rpdlp.ChooseRestartCandidate(p, good, twin, 1.0) is twin  # tie -> average

@@ -347,6 +347,17 @@ int pdhg_gen_random_lp(int64_t m, int64_t n, double density, uint64_t seed,
 int pdhg_gen_pagerank(int64_t n_nodes, double damping, int64_t attachment,
                       uint64_t seed, pdhg_instance** out, char* err,
                       size_t errlen);
+/* GenPagerankGraph (instance_gen.cpp:27-64): `edges` receives count pairs
+ * (src, dst) as 2*count int64s; capacity (in pairs) must be at least
+ * pdhg_pagerank_graph_edges(n_nodes, attachment). */
+int64_t pdhg_pagerank_graph_edges(int64_t n_nodes, int64_t attachment);
+int pdhg_gen_pagerank_graph(int64_t n_nodes, double damping, int64_t attachment,
+                            uint64_t seed, int64_t* edges, int64_t capacity,
+                            int64_t* count, char* err, size_t errlen);
+/* BuildPagerankLp (instance_gen.cpp:90-137) over `count` (src, dst) pairs. */
+int pdhg_build_pagerank_lp(const int64_t* edges, int64_t count, int64_t n_nodes,
+                           double damping, pdhg_instance** out, char* err,
+                           size_t errlen);
 /* Transportation LP, `sources` x `sinks`: demand rows
  * sum_i x_ij = d_j in A, supply rows -sum_j x_ij >= -s_i in G, x >= 0. */
 int pdhg_gen_transport(int64_t sources, int64_t sinks, uint64_t seed,

@@ -4,6 +4,8 @@
 #define RPDLP_B200_INSTANCE_GEN_HPP_
 
 #include <cstdint>
+#include <string>
+#include <utility>
 #include <vector>
 
 #include "rpdlp/lp_problem.hpp"
@@ -17,6 +19,16 @@ struct PagerankConfig {
   std::uint64_t seed = 0;
 };
 
+// Directed edge list, src -> dst (instance_gen.hpp:34-49).
+using EdgeList = std::vector<std::pair<Index, Index>>;
+// Preferential-attachment digraph, deterministic per seed (bit-identical
+// with the reference's draw).
+EdgeList GenPagerankGraph(const PagerankConfig& cfg);
+// "src dst" per line, '#' comment lines; ids compacted to 0..n-1 in order of
+// first appearance. Throws std::runtime_error (cannot open / malformed line).
+EdgeList ReadEdgeList(const std::string& path, Index* n_nodes);
+// Feasibility LP of x = damping S x + (1 - damping)/n (see pdhg.h).
+LpProblem BuildPagerankLp(const EdgeList& edges, Index n_nodes, double damping);
 LpProblem GenPagerank(const PagerankConfig& cfg);
 LpProblem GenRandomLp(Index m, Index n, double density, std::uint64_t seed, std::vector<double>* witness = nullptr);
 // SURVEY §8d config 2 (not in the reference).

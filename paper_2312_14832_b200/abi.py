@@ -133,6 +133,11 @@ SIGNATURES = {
                                      C.c_char_p, C.c_size_t]),
     "pdhg_gen_pagerank": (C.c_int, [C.c_int64, C.c_double, C.c_int64, C.c_uint64, C.POINTER(C.c_void_p),
                                     C.c_char_p, C.c_size_t]),
+    "pdhg_pagerank_graph_edges": (C.c_int64, [C.c_int64, C.c_int64]),
+    "pdhg_gen_pagerank_graph": (C.c_int, [C.c_int64, C.c_double, C.c_int64, C.c_uint64, i64ptr, C.c_int64, i64ptr,
+                                          C.c_char_p, C.c_size_t]),
+    "pdhg_build_pagerank_lp": (C.c_int, [i64ptr, C.c_int64, C.c_int64, C.c_double, C.POINTER(C.c_void_p),
+                                         C.c_char_p, C.c_size_t]),
     "pdhg_gen_transport": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, C.POINTER(C.c_void_p), C.c_char_p,
                                      C.c_size_t]),
     "pdhg_gen_mcf": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.POINTER(C.c_void_p), C.c_char_p,

@@ -122,10 +122,12 @@ pdhg_instance* RandomLp(I m, I n, double density, uint64_t seed) {
   return p;
 }
 
-pdhg_instance* Pagerank(I n_nodes, double damping, I attachment, uint64_t seed) {
+// GenPagerankGraph (instance_gen.cpp:27-64): preferential attachment over a
+// pool where node j appears in_degree(j) + 1 times, seeded by a directed
+// cycle over the first attachment + 1 nodes. Deterministic per seed.
+std::vector<std::pair<I, I>> PagerankGraph(I n_nodes, double damping, I attachment, uint64_t seed) {
   if (n_nodes < attachment + 1) throw std::invalid_argument("n_nodes must be at least attachment + 1");
   if (!(damping > 0.0 && damping < 1.0)) throw std::invalid_argument("damping must lie in (0, 1)");
-  // GenPagerankGraph (instance_gen.cpp:27-64).
   std::mt19937_64 rng(seed);
   std::vector<std::pair<I, I>> edges;
   edges.reserve(static_cast<size_t>(n_nodes * attachment));
@@ -149,10 +151,21 @@ pdhg_instance* Pagerank(I n_nodes, double damping, I attachment, uint64_t seed) 
     }
     pool.push_back(i);
   }
-  pool = std::vector<I>();
-  // BuildPagerankLp (instance_gen.cpp:90-137).
+  return edges;
+}
+
+// BuildPagerankLp (instance_gen.cpp:90-137): x_i - damping * sum_j S_ij x_j
+// >= (1 - damping) / n per node (G), sum(x) = 1 (A), x >= 0, c = 0; dangling
+// nodes get a self-loop so S stays column-stochastic.
+pdhg_instance* PagerankLp(const std::pair<I, I>* edges, size_t count, I n_nodes, double damping) {
+  if (n_nodes < 1) throw std::invalid_argument("empty graph");
   std::vector<I> outdeg(n_nodes, 0);
-  for (auto& e : edges) ++outdeg[e.first];
+  for (size_t k = 0; k < count; ++k) {
+    const auto& e = edges[k];
+    if (e.first < 0 || e.first >= n_nodes || e.second < 0 || e.second >= n_nodes)
+      throw std::invalid_argument("edge endpoint out of range");
+    ++outdeg[e.first];
+  }
   std::vector<I> dangling;
   for (I j = 0; j < n_nodes; ++j)
     if (outdeg[j] == 0) {
@@ -160,11 +173,10 @@ pdhg_instance* Pagerank(I n_nodes, double damping, I attachment, uint64_t seed) 
       outdeg[j] = 1;
     }
   std::vector<Trip> t;
-  t.reserve(edges.size() + 2 * static_cast<size_t>(n_nodes));
+  t.reserve(count + 2 * static_cast<size_t>(n_nodes));
   for (I i = 0; i < n_nodes; ++i) t.push_back({i, i, 1.0});
-  for (auto& e : edges) t.push_back({e.second, e.first, -damping / outdeg[e.first]});
+  for (size_t k = 0; k < count; ++k) t.push_back({edges[k].second, edges[k].first, -damping / outdeg[edges[k].first]});
   for (I j : dangling) t.push_back({j, j, -damping});
-  edges = std::vector<std::pair<I, I>>();
   auto* p = new pdhg_instance;
   p->n = n_nodes;
   p->g_rows = n_nodes;
@@ -180,6 +192,11 @@ pdhg_instance* Pagerank(I n_nodes, double damping, I attachment, uint64_t seed) 
   p->l.assign(n_nodes, 0.0);
   p->u.assign(n_nodes, std::numeric_limits<double>::infinity());
   return p;
+}
+
+pdhg_instance* Pagerank(I n_nodes, double damping, I attachment, uint64_t seed) {
+  std::vector<std::pair<I, I>> edges = PagerankGraph(n_nodes, damping, attachment, seed);
+  return PagerankLp(edges.data(), edges.size(), n_nodes, damping);
 }
 
 // Transportation LP. Variables x_ij, index i*T + j.
@@ -447,6 +464,33 @@ int pdhg_gen_random_lp(int64_t m, int64_t n, double density, uint64_t seed, pdhg
 int pdhg_gen_pagerank(int64_t n_nodes, double damping, int64_t attachment, uint64_t seed, pdhg_instance** out,
                       char* err, size_t errlen) {
   return Guard(err, errlen, [&] { *out = Pagerank(n_nodes, damping, attachment, seed); });
+}
+
+int64_t pdhg_pagerank_graph_edges(int64_t n_nodes, int64_t attachment) {
+  if (attachment < 0 || n_nodes < attachment + 1) return 0;
+  return (attachment + 1) + (n_nodes - attachment - 1) * attachment;
+}
+
+int pdhg_gen_pagerank_graph(int64_t n_nodes, double damping, int64_t attachment, uint64_t seed, int64_t* edges,
+                            int64_t capacity, int64_t* count, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    std::vector<std::pair<I, I>> e = PagerankGraph(n_nodes, damping, attachment, seed);
+    if (static_cast<int64_t>(e.size()) > capacity) throw std::invalid_argument("edge buffer too small");
+    for (size_t k = 0; k < e.size(); ++k) {
+      edges[2 * k] = e[k].first;
+      edges[2 * k + 1] = e[k].second;
+    }
+    *count = static_cast<int64_t>(e.size());
+  });
+}
+
+int pdhg_build_pagerank_lp(const int64_t* edges, int64_t count, int64_t n_nodes, double damping,
+                           pdhg_instance** out, char* err, size_t errlen) {
+  static_assert(sizeof(std::pair<I, I>) == 2 * sizeof(int64_t), "edge layout");
+  return Guard(err, errlen, [&] {
+    if (count < 0 || (count > 0 && !edges)) throw std::invalid_argument("bad edge list");
+    *out = PagerankLp(reinterpret_cast<const std::pair<I, I>*>(edges), static_cast<size_t>(count), n_nodes, damping);
+  });
 }
 
 int pdhg_gen_transport(int64_t sources, int64_t sinks, uint64_t seed, pdhg_instance** out, char* err,

@@ -8,9 +8,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <fstream>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <tuple>
+#include <unordered_map>
 
 #include "pdhg.h"
 #include "rpdlp/solver.hpp"
@@ -427,6 +430,52 @@ LpProblem Take(pdhg_instance* inst, std::vector<double>* witness) {
 }
 
 }  // namespace
+
+EdgeList GenPagerankGraph(const PagerankConfig& cfg) {
+  EdgeList e(static_cast<size_t>(std::max<int64_t>(pdhg_pagerank_graph_edges(cfg.n_nodes, cfg.attachment), 0)));
+  int64_t count = 0;
+  char err[512] = {0};
+  static_assert(sizeof(EdgeList::value_type) == 2 * sizeof(int64_t), "edge layout");
+  if (pdhg_gen_pagerank_graph(cfg.n_nodes, cfg.damping, cfg.attachment, cfg.seed,
+                              reinterpret_cast<int64_t*>(e.data()), static_cast<int64_t>(e.size()), &count, err,
+                              sizeof(err)) != PDHG_OK)
+    throw std::invalid_argument(err);
+  e.resize(static_cast<size_t>(count));
+  return e;
+}
+
+EdgeList ReadEdgeList(const std::string& path, Index* n_nodes) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot open " + path);
+  EdgeList edges;
+  std::unordered_map<Index, Index> ids;  // raw id -> dense id, first appearance order
+  auto dense = [&ids](Index raw) { return ids.emplace(raw, static_cast<Index>(ids.size())).first->second; };
+  std::string line;
+  while (std::getline(in, line)) {
+    const size_t first = line.find_first_not_of(" \t\r");
+    if (first == std::string::npos || line[first] == '#') continue;
+    std::istringstream fields(line);
+    Index src = 0, dst = 0;
+    if (!(fields >> src >> dst)) throw std::runtime_error("malformed edge line: " + line);
+    const Index a = dense(src);
+    const Index b = dense(dst);
+    edges.push_back({a, b});
+  }
+  if (n_nodes) *n_nodes = static_cast<Index>(ids.size());
+  return edges;
+}
+
+LpProblem BuildPagerankLp(const EdgeList& edges, Index n_nodes, double damping) {
+  pdhg_instance* inst = nullptr;
+  char err[512] = {0};
+  if (pdhg_build_pagerank_lp(reinterpret_cast<const int64_t*>(edges.data()), static_cast<int64_t>(edges.size()),
+                             n_nodes, damping, &inst, err, sizeof(err)) != PDHG_OK)
+    throw std::invalid_argument(err);
+  LpProblem p = Take(inst, nullptr);
+  p.name = "pagerank";
+  p.Validate();
+  return p;
+}
 
 LpProblem GenPagerank(const PagerankConfig& cfg) {
   pdhg_instance* inst = nullptr;

@@ -775,6 +775,44 @@ def GenPagerank(n_nodes: int, damping: float = 0.85, attachment: int = 3, seed: 
     return _from_instance(_gen("pdhg_gen_pagerank", n_nodes, damping, attachment, seed), "pagerank")
 
 
+def GenPagerankGraph(n_nodes: int, damping: float = 0.85, attachment: int = 3, seed: int = 0) -> np.ndarray:
+    """instance_gen.cpp:27-64: (count, 2) int64 array of src -> dst edges."""
+    lib = abi.load()
+    cap = max(int(lib.pdhg_pagerank_graph_edges(n_nodes, attachment)), 1)
+    e = np.empty((cap, 2), np.int64)
+    cnt = C.c_int64(0)
+    err = C.create_string_buffer(abi.ERRLEN)
+    raise_for(lib.pdhg_gen_pagerank_graph(n_nodes, damping, attachment, seed, _i64p(e), cap, C.byref(cnt), err,
+                                          abi.ERRLEN), err)
+    return e[:cnt.value].copy()
+
+
+def BuildPagerankLp(edges, n_nodes: int, damping: float = 0.85) -> LpProblem:
+    """instance_gen.cpp:90-137 over a (count, 2) src -> dst edge array."""
+    e = np.ascontiguousarray(np.asarray(edges, np.int64).reshape(-1, 2))
+    return _from_instance(_gen("pdhg_build_pagerank_lp", _i64p(e), e.shape[0], n_nodes, damping), "pagerank")
+
+
+def ReadEdgeList(path):
+    """instance_gen.cpp:66-88: "src dst" per line, '#' comment lines; ids
+    compacted to 0..n-1 in order of first appearance. Returns (edges, n)."""
+    ids, edges = {}, []
+    with open(path) as f:
+        for line in f:
+            s = line.lstrip(" \t\r")
+            if not s.strip() or s.startswith("#"):
+                continue
+            parts = line.split()
+            try:
+                a, b = int(parts[0]), int(parts[1])
+            except (IndexError, ValueError):
+                raise RuntimeError("malformed edge line: " + line.rstrip("\n")) from None
+            ia = ids.setdefault(a, len(ids))
+            ib = ids.setdefault(b, len(ids))
+            edges.append((ia, ib))
+    return np.asarray(edges, np.int64).reshape(-1, 2), len(ids)
+
+
 def GenTransport(sources: int, sinks: int, seed: int = 1) -> LpProblem:
     """Transportation LP of SURVEY §8d config 2."""
     return _from_instance(_gen("pdhg_gen_transport", sources, sinks, seed), f"transport_{sources}x{sinks}_s{seed}")

@@ -221,6 +221,33 @@ int main() {
     for (size_t j = 0; j < lam.size(); ++j) dl = std::max(dl, std::abs(lam[j] - ro.lambda[j]));
     CHECK(dl <= 1e-12);
   }
+  {  // GenPagerankGraph / BuildPagerankLp / ReadEdgeList (instance_gen.cpp:27-141)
+    PagerankConfig cfg;
+    cfg.n_nodes = 2000;
+    cfg.attachment = 4;
+    cfg.seed = 7;
+    const EdgeList e = GenPagerankGraph(cfg);
+    CHECK(e.size() == static_cast<size_t>(5 + (2000 - 5) * 4));
+    const LpProblem a = BuildPagerankLp(e, cfg.n_nodes, cfg.damping), b = GenPagerank(cfg);
+    CHECK(a.g == b.g && a.a == b.a && a.h == b.h && a.name == "pagerank");
+    const std::string path = "/tmp/rpdlp_b200_edges_test.txt";
+    {
+      std::FILE* f = std::fopen(path.c_str(), "w");
+      std::fputs("# comment\n\n10 20\n  20 30\n30 10\n", f);
+      std::fclose(f);
+    }
+    Index n = 0;
+    const EdgeList r = ReadEdgeList(path, &n);
+    CHECK(n == 3 && r.size() == 3 && r[0] == std::make_pair(Index(0), Index(1)) && r[2] == std::make_pair(Index(2), Index(0)));
+    bool threw = false;
+    try {
+      BuildPagerankLp({{0, 9}}, 3, 0.85);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    std::remove(path.c_str());
+  }
   {  // ChooseRestartCandidate (solver.cpp:170-176, test_solver.cpp restart tests): strict < picks current
     LpProblem p = GenRandomLp(10, 12, 0.4, 4);
     SolverParams prm;

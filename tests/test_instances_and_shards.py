@@ -10,6 +10,7 @@ import socket
 import numpy as np
 import pytest
 
+from paper_2312_14832_b200 import rpdlp  # noqa: E402
 from paper_2312_14832_b200.rpdlp import GenMcf, GenStaircase, PartitionBlocks, SolverParams, SolveStatus
 
 
@@ -347,3 +348,46 @@ def test_validation_precedence_on_large_inputs(where):
     p.c[where // 2] = np.nan
     with pytest.raises(ValueError, match="NaN in c"):
         rpdlp.Solve(p)
+
+
+# ------------------------------- PageRank graph / LP builder / edge lists
+@pytest.mark.parametrize("seed", [0, 3])
+def test_pagerank_graph_then_build_equals_generator(seed):
+    """GenPagerank == BuildPagerankLp(GenPagerankGraph) (instance_gen.cpp:139-141),
+    bit for bit; edge count core + (n - core) * attachment."""
+    e = rpdlp.GenPagerankGraph(3000, 0.85, 4, seed)
+    assert e.shape == (5 + (3000 - 5) * 4, 2)
+    a, b = rpdlp.BuildPagerankLp(e, 3000, 0.85), rpdlp.GenPagerank(3000, 0.85, 4, seed)
+    for m in ("a", "g"):
+        x, y = getattr(a, m), getattr(b, m)
+        np.testing.assert_array_equal(x.row_ptr, y.row_ptr)
+        np.testing.assert_array_equal(x.col_idx, y.col_idx)
+        np.testing.assert_array_equal(x.values.view(np.uint64), y.values.view(np.uint64))
+    np.testing.assert_array_equal(a.h, b.h)
+
+
+def test_edge_list_reader_and_builder(tmp_path):
+    """instance_gen.cpp:66-137: comments / blank lines skipped, sparse ids
+    compacted in first-appearance order, dangling nodes get self-loops,
+    malformed lines and out-of-range endpoints rejected."""
+    f = tmp_path / "g.txt"
+    f.write_text("# a comment\n\n10 20\n  20 30\n\t# indented comment\n30 10 extra\n40 20\n")
+    e, n = rpdlp.ReadEdgeList(f)
+    assert n == 4 and e.tolist() == [[0, 1], [1, 2], [2, 0], [3, 1]]
+    p = rpdlp.BuildPagerankLp(e, n, 0.5)
+    d = p.g.to_dense()
+    # node 3 has in-degree 0 but out-degree 1; no dangling node here
+    np.testing.assert_allclose(np.diag(d), [1.0, 1.0, 1.0, 1.0])
+    assert d[1, 0] == -0.5 and d[1, 3] == -0.5 and d[2, 1] == -0.5 and d[0, 2] == -0.5
+    np.testing.assert_allclose(p.h, [0.125] * 4)
+    assert p.a.to_dense().tolist() == [[1.0, 1.0, 1.0, 1.0]] and list(p.b) == [1.0]
+    dang = rpdlp.BuildPagerankLp(np.array([[0, 1]]), 2, 0.85).g.to_dense()
+    assert dang[1, 1] == pytest.approx(1.0 - 0.85)  # dangling node 1: self-loop
+    bad = tmp_path / "bad.txt"
+    bad.write_text("1 2\n3\n")
+    with pytest.raises(RuntimeError, match="malformed edge line"):
+        rpdlp.ReadEdgeList(bad)
+    with pytest.raises(ValueError, match="edge endpoint out of range"):
+        rpdlp.BuildPagerankLp(np.array([[0, 5]]), 3, 0.85)
+    with pytest.raises(ValueError, match="empty graph"):
+        rpdlp.BuildPagerankLp(np.zeros((0, 2), np.int64), 0, 0.85)

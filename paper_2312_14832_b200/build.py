@@ -33,8 +33,24 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "--expt-relax
                   "-Xcompiler", "-fPIC,-O3", "-I", str(ROOT / "include")]
 CXXFLAGS = ["-std=c++20", "-O3", "-fPIC", "-pthread", "-Wall", "-Wextra", "-I", str(ROOT / "include")]
 
+
+def _nlohmann_include():
+    """nlohmann/json, the reference harness's dependency: the copy this image
+    ships inside cudnn-frontend (no system install)."""
+    import sysconfig
+    for base in {sysconfig.get_paths()["purelib"], sysconfig.get_paths()["platlib"]}:
+        d = Path(base) / "include" / "cudnn_frontend" / "thirdparty"
+        if (d / "nlohmann" / "json.hpp").exists():
+            return d
+    return None
+
+
+NLOHMANN = _nlohmann_include()
+if NLOHMANN is not None:
+    CXXFLAGS += ["-isystem", str(NLOHMANN)]
+
 CU_SRCS = ["session.cu", "abi.cu"]
-CPP_SRCS = ["instance_gen.cpp", "rpdlp_api.cpp", "mps.cpp"]
+CPP_SRCS = ["instance_gen.cpp", "rpdlp_api.cpp", "mps.cpp"] + (["bench.cpp"] if NLOHMANN is not None else [])
 DROPIN_TEST = ROOT / "tests" / "cpp" / "drop_in_test.cpp"
 DROPIN_BIN = BUILD / "drop_in_test"
 HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh", "tma.cuh", "host_logic.h", "engine.cuh", "setup_kernels.cuh", "comm.cuh", "normal_rng.h", "assemble.cuh"]

@@ -3,6 +3,7 @@
 // Cases follow the reference's own unit tests (test_solver.cpp, test_kkt.cpp)
 // and acceptance criteria C1/C5 shapes. Exit code = number of failures.
 #include <cmath>
+#include <fstream>
 #include <cstdlib>
 #include <random>
 #include <cstdio>
@@ -14,6 +15,7 @@
 
 #include <sstream>
 
+#include "rpdlp/bench.hpp"
 #include "rpdlp/instance_gen.hpp"
 #include "rpdlp/kkt.hpp"
 #include "rpdlp/mps.hpp"
@@ -247,6 +249,45 @@ int main() {
     }
     CHECK(threw);
     std::remove(path.c_str());
+  }
+  {  // suite harness (test_bench.cpp: SGM hand values, run_suite, byte-identical redacted reports)
+    CHECK(Near(Sgm({10.0, 40.0}, 10.0, 3600.0, {true, true}), std::sqrt(1000.0) - 10.0, 1e-12));
+    CHECK(Near(Sgm({1.0, 2.0}, 10.0, 100.0, {true, false}), std::sqrt(11.0 * 110.0) - 10.0, 1e-12));
+    bool threw = false;
+    try {
+      Sgm({}, 10.0, 3600.0, {});
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    const std::string dir = "/tmp/rpdlp_b200_suite_test";
+    std::system(("rm -rf " + dir + " && mkdir -p " + dir).c_str());
+    WriteMpsFile(GenRandomLp(6, 7, 0.5, 1), dir + "/a.mps");
+    WriteMpsFile(GenRandomLp(6, 7, 0.5, 2), dir + "/b.mps");
+    {
+      std::FILE* f = std::fopen((dir + "/broken.mps").c_str(), "w");
+      std::fputs("ROWS\n N OBJ\nCOLUMNS\n", f);
+      std::fclose(f);
+    }
+    SolverParams prm;
+    prm.eps = 1e-6;
+    const SuiteSummary s1 = RunSuite(dir, prm), s2 = RunSuite(dir, prm);
+    CHECK(s1.records.size() == 3 && s1.solved_count == 2 && s1.records[2].status == "Error");
+    CHECK(s1.records[0].instance == "a.mps" && s1.records[0].iterations > 0 && s1.sgm10 > 0.0);
+    CHECK(SummaryToJson(s1, true).dump(2) == SummaryToJson(s2, true).dump(2));
+    const auto j = SummaryToJson(s1);
+    CHECK(j.begin().key() == "tolerance" && j["records"][0]["residuals"].size() == 8 && j["solved_count"] == 2);
+    WriteSummaryCsv(s1, dir + "/r.csv");
+    std::ifstream csv(dir + "/r.csv");
+    std::string header;
+    std::getline(csv, header);
+    CHECK(header == "instance,status,solve_seconds,parse_seconds,scaling_seconds,iterations,restarts,rel_primal,"
+                    "rel_dual,rel_gap,primal_obj");
+    const SolveResult r = Solve(GenRandomLp(6, 7, 0.5, 1), prm);
+    const auto sol = SolutionToJson(r, true);
+    CHECK(sol["status"] == "Optimal" && sol["primal_objective"].get<double>() == -r.report.primal_obj &&
+          sol["x"].size() == r.x.size());
+    std::system(("rm -rf " + dir).c_str());
   }
   {  // ChooseRestartCandidate (solver.cpp:170-176, test_solver.cpp restart tests): strict < picks current
     LpProblem p = GenRandomLp(10, 12, 0.4, 4);

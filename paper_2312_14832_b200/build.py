@@ -53,6 +53,7 @@ CU_SRCS = ["session.cu", "abi.cu"]
 CPP_SRCS = ["instance_gen.cpp", "rpdlp_api.cpp", "mps.cpp"] + (["bench.cpp"] if NLOHMANN is not None else [])
 DROPIN_TEST = ROOT / "tests" / "cpp" / "drop_in_test.cpp"
 DROPIN_BIN = BUILD / "drop_in_test"
+CLI_BIN = BUILD / "rpdlp-b200"
 HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh", "tma.cuh", "host_logic.h", "engine.cuh", "setup_kernels.cuh", "comm.cuh", "normal_rng.h", "assemble.cuh"]
 
 
@@ -98,6 +99,10 @@ def build_product(force: bool = False, ptxas_verbose: bool = False) -> Path:
     # Reference-style C++ caller linked against the drop-in headers + library.
     if force or not _newer(DROPIN_BIN, [DROPIN_TEST, LIB]):
         _run([CXX] + CXXFLAGS + [str(DROPIN_TEST), "-o", str(DROPIN_BIN), "-L", str(PKG), "-lpdhg_b200",
+                                 f"-Wl,-rpath,$ORIGIN/.."])
+    # The reference's command line tool (rpdlp_main.cpp) over the drop-in.
+    if NLOHMANN is not None and (force or not _newer(CLI_BIN, [CSRC / "cli_main.cpp", LIB])):
+        _run([CXX] + CXXFLAGS + [str(CSRC / "cli_main.cpp"), "-o", str(CLI_BIN), "-L", str(PKG), "-lpdhg_b200",
                                  f"-Wl,-rpath,$ORIGIN/.."])
     return LIB
 

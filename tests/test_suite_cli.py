@@ -136,3 +136,57 @@ def test_cli_solve_and_redacted_reports_are_byte_identical(tmp_path, capsys):
     assert j["status"] == "Optimal" and abs(sum(j["x"]) - 1.0) <= 1e-4
     assert cli.main(["solve", str(d / "pr.mps"), "--eps", "1e-12", "--iter-limit", "64"]) == cli.EXIT_LIMIT
     assert "status=IterLimit" in capsys.readouterr().out
+
+
+# ------------------------------------------ the C++ tool (csrc/cli_main.cpp)
+def _cpp_cli():
+    from pathlib import Path
+    b = Path(__file__).resolve().parents[1] / "paper_2312_14832_b200" / "_build" / "rpdlp-b200"
+    if not b.exists():
+        pytest.skip("C++ CLI not built (nlohmann/json absent)")
+    return str(b)
+
+
+def test_cpp_cli_gen_matches_python_and_usage_errors(tmp_path):
+    import subprocess
+    cli_bin = _cpp_cli()
+    a, b = tmp_path / "a.mps", tmp_path / "b.mps"
+    assert subprocess.run([cli_bin, "gen", "random", "--rows", "7", "--cols", "9", "--density", "0.4", "--seed", "5",
+                           "--out", str(a)]).returncode == 0
+    assert cli.main(["gen", "random", "--rows", "7", "--cols", "9", "--density", "0.4", "--seed", "5",
+                     "--out", str(b)]) == 0
+    assert a.read_bytes() == b.read_bytes()
+    assert subprocess.run([cli_bin, "gen", "pagerank", "--nodes", "50", "--out", str(a)]).returncode == 0
+    assert rpdlp.ParseMpsFile(a).num_vars() == 50
+    for args, code in ((["solve"], 1), (["frobnicate"], 1), (["gen", "random", "--rows", "3", "--out", "x"], 1),
+                       (["solve", str(tmp_path / "missing.mps")], 3), (["solve", str(a), "--eps"], 1)):
+        r = subprocess.run([cli_bin] + args, capture_output=True, text=True)
+        assert r.returncode == code, (args, r.stderr)
+
+
+@pytest.mark.gpu
+def test_cpp_cli_solve_and_redacted_bench(tmp_path):
+    """acceptance.cpp C9 through the C++ tool: two redacted bench reports are
+    byte-identical; solve writes the solution file and reports limits."""
+    import subprocess
+    cli_bin = _cpp_cli()
+    d = tmp_path / "suite"
+    d.mkdir()
+    for seed in (4, 5):
+        rpdlp.WriteMpsFile(rpdlp.GenRandomLp(8, 6, 0.5, seed), d / f"r{seed}.mps")
+    reps = []
+    for k in range(2):
+        rep = tmp_path / f"rep{k}.json"
+        r = subprocess.run([cli_bin, "bench", str(d), "--eps", "1e-6", "--redact-timing", "--report", str(rep)],
+                           capture_output=True, text=True)
+        assert r.returncode == 0 and "solved=2/2" in r.stdout
+        reps.append(rep.read_bytes())
+    assert reps[0] == reps[1] and json.loads(reps[0])["solved_count"] == 2
+    sol = tmp_path / "sol.json"
+    r = subprocess.run([cli_bin, "solve", str(d / "r4.mps"), "--eps", "1e-6", "--out", str(sol)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0 and "status=Optimal" in r.stdout
+    assert json.loads(sol.read_text())["status"] == "Optimal"
+    r = subprocess.run([cli_bin, "solve", str(d / "r4.mps"), "--eps", "1e-12", "--iter-limit", "64"],
+                       capture_output=True, text=True)
+    assert r.returncode == 2 and "status=IterLimit" in r.stdout

@@ -44,12 +44,18 @@ def kernel_cases():
 
 CASES = kernel_cases()
 
+# Class S bound (csrc/session.cu kThreadMax): every segment up to this length
+# is summed by one thread in storage order, i.e. bit-identically with the
+# reference's serial loops.
+S_MAX = 64
+
 
 @pytest.mark.parametrize("name", sorted(CASES))
 @pytest.mark.parametrize("scaled", [True, False])
 def test_scaled_problem_bit_exact(name, scaled, restatement):
     """Ruiz x10 + Pock-Chambolle + ApplyScaling on device == reference, bit
-    for bit, whenever no row/col of K exceeds 32 nonzeros (storage-order sums);
+    for bit, whenever no row/col of K exceeds S_MAX nonzeros (class S:
+    storage-order sums);
     otherwise within 4 ulp-scale (PC power sums of long rows differ in order)."""
     p = CASES[name]
     prm = SolverParams()
@@ -59,7 +65,7 @@ def test_scaled_problem_bit_exact(name, scaled, restatement):
         kv, c, l, u, q = s.scaled()
     rs0, cs0 = restatement.scaling(p, prm)
     kv0, c0, l0, u0, q0 = restatement.scaled(p, prm)
-    if max_segment(p) <= 32:
+    if max_segment(p) <= S_MAX:
         for got, want in ((rs, rs0), (cs, cs0), (kv, kv0), (c, c0), (l, l0), (u, u0), (q, q0)):
             assert np.array_equal(got, want)
     else:
@@ -71,17 +77,17 @@ def test_scaled_problem_bit_exact(name, scaled, restatement):
 @pytest.mark.parametrize("name", sorted(CASES))
 @pytest.mark.parametrize("transpose", [False, True])
 def test_spmv_matches_reference_sums(name, transpose, restatement):
-    """K_s x and K_s^T y: segments of <= 32 nonzeros are summed in storage
+    """K_s x and K_s^T y: segments of <= S_MAX nonzeros are summed in storage
     order (bit-exact with sparse_matrix.cpp:114-138); longer ones with a fixed
     tree (1e-13 relative to sum |terms|)."""
     p = CASES[name]
     rng = np.random.default_rng(11)
     n, m = p.num_vars(), p.num_rows()
     vec = rng.standard_normal(m if transpose else n)
-    # With segments > 32 the PC power sums (hence K_s) may differ in the last
-    # ulp; check SpMV summation order on the unscaled K there.
+    # With segments > S_MAX the PC power sums (hence K_s) may differ in the
+    # last ulp; check SpMV summation order on the unscaled K there.
     prm = SolverParams()
-    prm.scaling.enabled = max_segment(p) <= 32
+    prm.scaling.enabled = max_segment(p) <= S_MAX
     with Session(p, prm) as s:
         got = s.spmv(vec, transpose)
         kv = s.scaled()[0]
@@ -95,7 +101,7 @@ def test_spmv_matches_reference_sums(name, transpose, restatement):
     else:
         mag = np.bincount(rows, weights=np.abs(kv * vec[cols]), minlength=m)
         seglen = np.bincount(rows, minlength=m)
-    short = seglen <= 32
+    short = seglen <= S_MAX
     assert np.array_equal(got[short], want[short])
     assert np.all(np.abs(got - want) <= 1e-13 * mag + 1e-300)
 

@@ -42,6 +42,10 @@ struct DecideState {
   int32_t have_best;
   int32_t checks;      // checks evaluated so far (the host verifies its count)
   int64_t iters, inner;
+  // device-resident loop (Session::RunDeviceLoop): block length, iteration
+  // limit, time budget and the globaltimer deadline derived from it
+  int64_t block, iter_limit;
+  uint64_t remaining_ns, deadline_ns;
   // outputs of the latest check
   int32_t action, take_cur, best_from, restart_flag;
   double kkt_cand, eta;
@@ -161,6 +165,29 @@ __global__ void k_copy_best(const Scalars* sc, const DecideState* ds, const doub
 
 __global__ void k_settle(Scalars* sc) {
   if (sc->halt == 2) sc->halt = 1;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Device-resident loop: the deadline from the host's remaining time budget,
+// on the GPU's own clock, once per launch.
+__global__ void k_loop_start(DecideState* ds) {
+  const uint64_t r = ds->remaining_ns;
+  const uint64_t now = globaltimer_ns();
+  ds->deadline_ns = r > ~uint64_t(0) - now ? ~uint64_t(0) : now + r;
+}
+
+// End of one device-loop block: run another block only while the last check
+// decided "continue" (halt 0), a whole block still fits the iteration limit
+// and the time budget is not spent -- the tests the host loop makes before
+// queueing a block (solver.cpp:252-259).
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const Scalars* sc, const DecideState* ds) {
+  const bool go = sc->halt == 0 && ds->iters + ds->block <= ds->iter_limit && globaltimer_ns() < ds->deadline_ns;
+  cudaGraphSetConditional(h, go ? 1u : 0u);
 }
 
 }  // namespace pdhg

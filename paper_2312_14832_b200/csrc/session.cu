@@ -280,6 +280,8 @@ Session::~Session() {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   for (Graph& g : blocks_)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (Graph& g : loops_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (power_graph_) cudaGraphExecDestroy(power_graph_);
   if (power_graph1_) cudaGraphExecDestroy(power_graph1_);
   pinned_put(host_red_, host_red_bytes_);
@@ -1174,6 +1176,63 @@ void Session::RunChecked(int parity, int count) {
   check_launch("pdhg block + check");
 }
 
+// Device-resident loop: ONE graph launch runs blocks of `count` steps, each
+// followed by the check, the device decision (decide.cuh) and the best copy,
+// inside a conditional WHILE node whose condition k_loop_cond sets on the
+// device -- the host is needed again only for a restart (glibc exp/log),
+// termination, a limit or a non-finite iterate. `count` is even, so every
+// block starts at the same parity and one body serves all blocks.
+void Session::RunDeviceLoop(int parity, int count) {
+  Graph* g = nullptr;
+  for (Graph& gg : loops_)
+    if (gg.steps == count && gg.parity == parity) g = &gg;
+  if (!g) {
+    cudaGraph_t parent;
+    PDHG_CUDA(cudaGraphCreate(&parent, 0));
+    // k_loop_start, then the WHILE node depending on it.
+    PDHG_CUDA(cudaStreamBeginCaptureToGraph(st_, parent, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    k_loop_start<<<1, 1, 0, st_>>>(dstate_.p);
+    cudaGraph_t captured;
+    PDHG_CUDA(cudaStreamEndCapture(st_, &captured));
+    size_t nn = 0;
+    PDHG_CUDA(cudaGraphGetNodes(parent, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    PDHG_CUDA(cudaGraphGetNodes(parent, nodes.data(), &nn));
+    cudaGraphConditionalHandle cond;
+    PDHG_CUDA(cudaGraphConditionalHandleCreate(&cond, parent, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    PDHG_CUDA(cudaGraphAddNode(&wnode, parent, nodes.data(), nn, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    const int64_t before = launches_;
+    PDHG_CUDA(cudaStreamBeginCaptureToGraph(st_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, false);
+    k_advance<<<1, 1, 0, st_>>>(scal_.p, dstate_.p, count);
+    const int pa = (parity + count) & 1;
+    LaunchCheck(x_[pa].p, y_[pa].p, xbar_.p, ybar_.p, kx_[pa].p, scal_.p, true);
+    k_decide<<<1, 1, 0, st_>>>(red_out_.p, scal_.p, dstate_.p);
+    k_copy_best<<<ew_grid(np_ + mp_), kEw, 0, st_>>>(scal_.p, dstate_.p, x_[pa].p, xbar_.p, xbest_.p, np_, y_[pa].p,
+                                                      ybar_.p, ybest_.p, mp_);
+    k_loop_cond<<<1, 1, 0, st_>>>(cond, scal_.p, dstate_.p);
+    PDHG_CUDA(cudaStreamEndCapture(st_, &captured));
+    launches_ = before;
+    Graph ng;
+    ng.steps = count;
+    ng.parity = parity;
+    ng.adapt = false;
+    PDHG_CUDA(cudaGraphInstantiate(&ng.exec, parent, 0));
+    cudaGraphDestroy(parent);
+    loops_.push_back(ng);
+    g = &loops_.back();
+  }
+  PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
+  check_launch("device loop");
+}
+
 // Pipelined loop: one captured graph per (length, parity, adapt, check,
 // slot) holding the block's steps, the counter advance and -- at check
 // iterations -- the check passes, k_decide, the best copy, the halt settle
@@ -1552,6 +1611,15 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     const char* e = std::getenv("PDHG_FUSED_CHECK");
     return !(e && e[0] == '0');
   }();
+  const bool device_loop_on = [] {  // PDHG_DEVICE_LOOP=0: host-driven loop (read per solve: A/B, tests)
+    const char* e = std::getenv("PDHG_DEVICE_LOOP");
+    return !(e && e[0] == '0');
+  }();
+  // The device-resident loop needs the host only for restarts, termination,
+  // limits: not with an observer or a progress log (called at every check),
+  // adaptive steps (host-pushed iteration counter) or NCCL (rank-0 clock).
+  const bool device_loop = device_loop_on && fused_check && !cb && prm.log_every <= 0 && !adapt && !nccl() &&
+                           prm.check_every >= 4 && prm.check_every % 2 == 0;
   while (!finished) {
     if (iters >= prm.iter_limit) {
       status = PDHG_ITER_LIMIT;
@@ -1561,6 +1629,89 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     if (time_up) {
       status = PDHG_TIME_LIMIT;
       break;
+    }
+    if (device_loop && iters % prm.check_every == 0 && prm.iter_limit - iters >= prm.check_every) {
+      DecideState ds{};
+      ds.eps = prm.eps;
+      ds.suff = prm.sufficient_decay;
+      ds.nec = prm.necessary_decay;
+      ds.frac = prm.long_loop_frac;
+      ds.offset = offset_;
+      ds.qn_s = q_norm_s_;
+      ds.cn_s = c_norm_s_;
+      ds.qn_o = q_norm_o_;
+      ds.cn_o = c_norm_o_;
+      ds.restart_enabled = prm.restart_enabled;
+      ds.kkt_start = kkt_start;
+      ds.kkt_prev = kkt_prev;
+      ds.best_k1 = best_k1;
+      ds.have_best = have_best;
+      ds.checks = 0;
+      ds.iters = iters;
+      ds.inner = inner;
+      ds.block = prm.check_every;
+      ds.iter_limit = prm.iter_limit;
+      const double left = prm.time_limit - secs();
+      ds.remaining_ns = left >= 1.8e10 ? ~uint64_t(0) >> 1 : static_cast<uint64_t>(std::max(left, 0.0) * 1e9);
+      ds.deadline_ns = 0;
+      ds.best_from = -1;
+      ds.best_rep = best_rep;
+      ds.last_rep = last_rep;
+      if (!dstate_.p) dstate_.alloc(1, &arena_);
+      if (!hstate_) hstate_ = static_cast<DecideState*>(pinned_get(2 * sizeof(DecideState), &hstate_bytes_));
+      sc.halt = 0;
+      push_scalars();
+      PDHG_CUDA(cudaMemcpyAsync(dstate_.p, &ds, sizeof(DecideState), cudaMemcpyHostToDevice, st_));
+      const double tc0 = secs();
+      RunDeviceLoop(par, static_cast<int>(prm.check_every));
+      PDHG_CUDA(cudaMemcpyAsync(hstate_, dstate_.p, sizeof(DecideState), cudaMemcpyDeviceToHost, st_));
+      Sync();
+      t_checks += secs() - tc0;
+      const DecideState h = hstate_[0];
+      const int64_t ran = h.iters - iters;
+      if (ran <= 0 || ran % prm.check_every != 0 || h.checks != ran / prm.check_every)
+        throw Error(PDHG_CUDA_ERROR, "device loop: inconsistent block count");
+      // per block: steps, k_advance, the check passes and their reduction,
+      // k_decide, k_copy_best, k_loop_cond; per launch: k_loop_start
+      launches_ += 1 + (ran / prm.check_every) *
+                           (prm.check_every * (launches_csr() + launches_csc()) + launches_csr() + launches_csc() + 5);
+      iters = h.iters;
+      inner = h.inner;
+      sc.inner_base += static_cast<double>(ran);
+      nchecks += h.checks;
+      have_best = h.have_best != 0;
+      best_k1 = h.best_k1;
+      best_rep = h.best_rep;
+      last_rep = h.last_rep;
+      kkt_prev = h.kkt_prev;
+      if (h.action == kNonFinite)
+        throw Error(PDHG_NUMERICAL_FAILURE, "non-finite iterate at iteration " + std::to_string(iters));
+      if (h.action == kOptimalCur || h.action == kOptimalAvg) {
+        status = PDHG_OPTIMAL;  // best iterate copied on the device
+        sc.halt = 0;
+        push_scalars();
+        break;
+      }
+      if (h.action == kRestart) {  // Restart (solver.cpp:430-446), as in the loops below
+        const bool take_cur = h.take_cur != 0;
+        double pack[kRowRed + kColRed];
+        PDHG_CUDA(cudaMemcpyAsync(pack, red_out_.p, sizeof(pack), cudaMemcpyDeviceToHost, st_));
+        Sync();
+        const int P = take_cur ? 0 : 1;
+        const double dx = std::sqrt(pack[kRowRed + P * kColPer + kDx2]);
+        const double dy = std::sqrt(pack[P * kRowPer + kDy2]);
+        sc.omega = UpdatePrimalWeight(sc.omega, dx, dy);
+        if (!take_cur) {
+          Copy(x_[par].p, xbar_.p, np_);
+          Copy(y_[par].p, ybar_.p, mp_);
+          Copy(kx_[par].p, kxavg_.p, mp_);
+        }
+        start_loop(take_cur ? h.s_cur : h.s_avg);
+        ++restarts;
+      }
+      sc.halt = 0;
+      push_scalars();
+      continue;
     }
     const int64_t to_check = prm.check_every - (iters % prm.check_every);
     const int64_t count = std::min<int64_t>(to_check, prm.iter_limit - iters);

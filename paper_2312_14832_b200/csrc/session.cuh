@@ -101,6 +101,7 @@ class Session {
   void RunSteps(int parity, int count, bool adapt);
   void RunBlock(int parity, int count, bool adapt, bool check, int slot);
   void RunChecked(int parity, int count);
+  void RunDeviceLoop(int parity, int count);
   void LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx,
                    const Scalars* guard = nullptr, bool branches = false);
   void ReadCheck(CheckOut* out);
@@ -204,6 +205,7 @@ class Session {
 
   std::vector<Graph> graphs_;
   std::vector<Graph> blocks_;  // pipelined-loop block graphs
+  std::vector<Graph> loops_;   // device-resident loop graphs (conditional WHILE)
   cudaGraphExec_t power_graph_ = nullptr;   // kPowerSteps EstimateOpNorm steps (OpNorm)
   cudaGraphExec_t power_graph1_ = nullptr;  // one step (remainder)
   DArray<char> flush_;

@@ -312,3 +312,24 @@ def test_choose_restart_candidate():
     assert rpdlp.ChooseRestartCandidate(p, zero, good, 1.0) is good
     twin = (r.x.copy(), r.y.copy())
     assert rpdlp.ChooseRestartCandidate(p, good, twin, 1.0) is twin  # tie -> average
+
+
+@pytest.mark.parametrize("case", ["config1", "transport", "pagerank", "iterlimit", "mixed"])
+def test_device_loop_matches_host_loop(case, monkeypatch):
+    """The device-resident loop (conditional WHILE graph, decisions on the
+    device; PDHG_DEVICE_LOOP) against the host-driven loop: identical status,
+    iterations, restarts, bitwise iterates and reports."""
+    p = {"config1": lambda: config1(1), "transport": lambda: GenTransport(40, 50, 2),
+         "pagerank": lambda: GenPagerank(3000, 0.85, 3, 5), "iterlimit": lambda: config1(2),
+         "mixed": mixed_bounds_lp}[case]()
+    prm = {"iterlimit": SolverParams(eps=1e-12, iter_limit=1000)}.get(case, SolverParams(eps=1e-7))
+    runs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PDHG_DEVICE_LOOP", flag)
+        runs.append(rpdlp.Solve(p, prm))
+    a, b = runs
+    assert (int(a.status), a.iterations, a.restarts) == (int(b.status), b.iterations, b.restarts)
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
+    np.testing.assert_array_equal(a.lambda_, b.lambda_)
+    assert a.report.primal_obj == b.report.primal_obj and a.report.rel_gap == b.report.rel_gap

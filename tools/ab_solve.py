@@ -1,5 +1,6 @@
-"""A/B of an env toggle on resident transport solves, alternating in fresh
-processes on one box: python tools/ab_solve.py VAR A B [rounds]."""
+"""A/B of an env toggle on resident solves (AB_PROBLEM=transport | random |
+pagerank), alternating in fresh processes on one box:
+python tools/ab_solve.py VAR A B [rounds]."""
 import json
 import os
 import subprocess
@@ -9,7 +10,11 @@ code = r'''
 import sys, json
 sys.path.insert(0, ".")
 from paper_2312_14832_b200 import rpdlp
-p = rpdlp.GenTransport(1000, 1000, 1)
+import os
+which = os.environ.get("AB_PROBLEM", "transport")
+p = {"transport": lambda: rpdlp.GenTransport(1000, 1000, 1),
+     "random": lambda: rpdlp.GenRandomLp(1000, 2000, 0.005, 1, equality_rows=300),
+     "pagerank": lambda: rpdlp.GenPagerank(100_000, 0.85, 6, 1)}[which]()
 prm = rpdlp.SolverParams(eps=1e-4)
 with rpdlp.Session(p) as s:
     for _ in range(2):

@@ -986,8 +986,8 @@ double* Session::DevStage() {
   return dstage_.p;
 }
 
-double* Session::HostStage() {
-  const size_t need = static_cast<size_t>(std::max<int64_t>(std::max(m_, n_), 1));
+double* Session::HostStage(size_t at_least) {
+  const size_t need = std::max(at_least, static_cast<size_t>(std::max<int64_t>(std::max(m_, n_), 1)));
   if (hstage_n_ < need) {
     pinned_put(hstage_, hstage_bytes_);
     hstage_ = nullptr;
@@ -1851,17 +1851,37 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   const double t_loop = secs();
   if (gx_.use) GatherXFull(xbest_.p);  // ghost exchange left only the read entries valid
   if (gy_.use) GatherYFull(ybest_.p);
-  ToHost(xbest_.p, cs_.p, pad_c_, out->x, n_);
-  ToHost(ybest_.p, rs_.p, pad_r_, out->y, m_);
-  if (out->lambda) {
-    for (Shard& h : shards_) {
-      const int64_t c = h.coff;
-      run_pass(h.csc, OpLambda{ybest_.p, c_o_.p + c, l_o_.p + c, u_o_.p + c, cs_.p + c, nvec_.p + c}, RedSlots{}, st_);
+  // x | y | lambda staged back-to-back in one pinned buffer with a single
+  // synchronisation; the stage-to-caller copies then run side by side.
+  {
+    double* hs = HostStage(static_cast<size_t>(2 * n_ + m_));
+    double* ds = DevStage();
+    auto stage = [&](const double* dev, const double* scale, const DArray<int32_t>& pad, double* h, int64_t k) {
+      if (!k) return;
+      k_unpermute<<<ew_grid(k), kEw, 0, st_>>>(dev, scale, pad.p, ds, k);
+      PDHG_CUDA(cudaMemcpyAsync(h, ds, k * sizeof(double), cudaMemcpyDeviceToHost, st_));
+    };
+    if (out->x) stage(xbest_.p, cs_.p, pad_c_, hs, n_);
+    if (out->y) stage(ybest_.p, rs_.p, pad_r_, hs + n_, m_);
+    if (out->lambda) {
+      for (Shard& h : shards_) {
+        const int64_t c = h.coff;
+        run_pass(h.csc, OpLambda{ybest_.p, c_o_.p + c, l_o_.p + c, u_o_.p + c, cs_.p + c, nvec_.p + c}, RedSlots{},
+                 st_);
+      }
+      GatherXFull(nvec_.p);
+      stage(nvec_.p, nullptr, pad_c_, hs + n_ + m_, n_);
     }
-    GatherXFull(nvec_.p);
-    ToHost(nvec_.p, nullptr, pad_c_, out->lambda, n_);
+    Sync();
+    std::thread ty;
+    if (out->y && m_) ty = std::thread([&] { CopyOut(out->y, hs + n_, m_); });
+    std::thread tl;
+    if (out->lambda && n_) tl = std::thread([&] { CopyOut(out->lambda, hs + n_ + m_, n_); });
+    if (out->x && n_) CopyOut(out->x, hs, n_);
+    if (ty.joinable()) ty.join();
+    if (tl.joinable()) tl.join();
   }
-  PDHG_CUDA(cudaEventRecord(ev_[1], st_));
+  PDHG_CUDA(cudaEventRecord(ev_[1], st_));  // after the copy-out, as before: the solve's whole time
   Sync();
   float ms = 0.f;
   PDHG_CUDA(cudaEventElapsedTime(&ms, ev_[0], ev_[1]));
@@ -1878,7 +1898,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
                  "[pdhg] solve %.4fs: opnorm %.4fs | loop %.4fs (%lld its, %lld checks, host-side check wait %.4fs) "
                  "| finish %.4fs | device %.4fs | graphs %zu\n",
                  out->solve_seconds, t_opnorm, t_loop - t_opnorm, (long long)iters, (long long)nchecks, t_checks,
-                 out->solve_seconds - t_loop, ms * 1e-3, graphs_.size());
+                 out->solve_seconds - t_loop, ms * 1e-3, graphs_.size() + loops_.size());
 }
 
 // EstimateOpNorm (solver.cpp:84-110) with the host start vector drawn from the

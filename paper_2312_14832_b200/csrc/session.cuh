@@ -110,7 +110,7 @@ class Session {
   void ToInternal(const double* host, const DArray<int32_t>& pad, double* dev, int64_t n, int64_t padded);
   void ToHost(const double* dev, const double* scale, const DArray<int32_t>& pad, double* host, int64_t n);
   double* DevStage();
-  double* HostStage();
+  double* HostStage(size_t at_least = 0);
   // Gathers for the next matrix pass (ghost entries only when the plan says
   // so) and full gathers for values leaving the session.
   void GatherX(double* v) { comm_->Exchange(v, gx_, st_); }

@@ -83,8 +83,7 @@ __global__ void k_reduce_two_guarded(const Scalars* sc, const double* t0, int nt
 
 // One check's decisions from the reduced pack (row sums then column sums,
 // ops.cuh CheckRow / CheckCol layout). Mirrors Session::Solve's host path.
-__global__ void k_decide(const double* pack, Scalars* sc, DecideState* ds) {
-  if (sc->halt) return;
+__device__ __forceinline__ void decide(const double* pack, Scalars* sc, DecideState* ds) {
   DecideState& d = *ds;
   const double* row = pack;
   const double* col = pack + kRowRed;
@@ -150,6 +149,11 @@ __global__ void k_decide(const double* pack, Scalars* sc, DecideState* ds) {
   d.action = kContinue;
 }
 
+__global__ void k_decide(const double* pack, Scalars* sc, DecideState* ds) {
+  if (sc->halt) return;
+  decide(pack, sc, ds);
+}
+
 // Best-iterate copy decided by the check that just ran (halt 0 or 2); a
 // skipped check (halt 1) copies nothing.
 __global__ void k_copy_best(const Scalars* sc, const DecideState* ds, const double* xc, const double* xa, double* xb,
@@ -173,6 +177,24 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns();
+
+// Device-resident loop, end of a block (one thread): advance the counters
+// (k_advance), take the check's decisions (k_decide), then keep looping only
+// while the decision is "continue" (halt 0), a whole block still fits the
+// iteration limit and the time budget is not spent -- the tests the host loop
+// makes before queueing a block (solver.cpp:252-259). The best-iterate copy
+// after it still runs in this body iteration.
+__global__ void k_decide_loop(const double* pack, Scalars* sc, DecideState* ds, int count,
+                              cudaGraphConditionalHandle h) {
+  sc->inner_base += static_cast<double>(count);
+  ds->iters += count;
+  ds->inner += count;
+  decide(pack, sc, ds);
+  const bool go = sc->halt == 0 && ds->iters + ds->block <= ds->iter_limit && globaltimer_ns() < ds->deadline_ns;
+  cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
 // Device-resident loop: the deadline from the host's remaining time budget,
 // on the GPU's own clock, once per launch.
 __global__ void k_loop_start(DecideState* ds) {
@@ -181,13 +203,5 @@ __global__ void k_loop_start(DecideState* ds) {
   ds->deadline_ns = r > ~uint64_t(0) - now ? ~uint64_t(0) : now + r;
 }
 
-// End of one device-loop block: run another block only while the last check
-// decided "continue" (halt 0), a whole block still fits the iteration limit
-// and the time budget is not spent -- the tests the host loop makes before
-// queueing a block (solver.cpp:252-259).
-__global__ void k_loop_cond(cudaGraphConditionalHandle h, const Scalars* sc, const DecideState* ds) {
-  const bool go = sc->halt == 0 && ds->iters + ds->block <= ds->iter_limit && globaltimer_ns() < ds->deadline_ns;
-  cudaGraphSetConditional(h, go ? 1u : 0u);
-}
 
 }  // namespace pdhg

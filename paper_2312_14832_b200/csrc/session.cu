@@ -1178,7 +1178,7 @@ void Session::RunChecked(int parity, int count) {
 
 // Device-resident loop: ONE graph launch runs blocks of `count` steps, each
 // followed by the check, the device decision (decide.cuh) and the best copy,
-// inside a conditional WHILE node whose condition k_loop_cond sets on the
+// inside a conditional WHILE node whose condition k_decide_loop sets on the
 // device -- the host is needed again only for a restart (glibc exp/log),
 // termination, a limit or a non-finite iterate. `count` is even, so every
 // block starts at the same parity and one body serves all blocks.
@@ -1211,13 +1211,11 @@ void Session::RunDeviceLoop(int parity, int count) {
     const int64_t before = launches_;
     PDHG_CUDA(cudaStreamBeginCaptureToGraph(st_, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, false);
-    k_advance<<<1, 1, 0, st_>>>(scal_.p, dstate_.p, count);
     const int pa = (parity + count) & 1;
     LaunchCheck(x_[pa].p, y_[pa].p, xbar_.p, ybar_.p, kx_[pa].p, scal_.p, true);
-    k_decide<<<1, 1, 0, st_>>>(red_out_.p, scal_.p, dstate_.p);
+    k_decide_loop<<<1, 1, 0, st_>>>(red_out_.p, scal_.p, dstate_.p, count, cond);
     k_copy_best<<<ew_grid(np_ + mp_), kEw, 0, st_>>>(scal_.p, dstate_.p, x_[pa].p, xbar_.p, xbest_.p, np_, y_[pa].p,
                                                       ybar_.p, ybest_.p, mp_);
-    k_loop_cond<<<1, 1, 0, st_>>>(cond, scal_.p, dstate_.p);
     PDHG_CUDA(cudaStreamEndCapture(st_, &captured));
     launches_ = before;
     Graph ng;
@@ -1671,10 +1669,10 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
       const int64_t ran = h.iters - iters;
       if (ran <= 0 || ran % prm.check_every != 0 || h.checks != ran / prm.check_every)
         throw Error(PDHG_CUDA_ERROR, "device loop: inconsistent block count");
-      // per block: steps, k_advance, the check passes and their reduction,
-      // k_decide, k_copy_best, k_loop_cond; per launch: k_loop_start
+      // per block: steps, the check passes and their reduction, k_decide_loop,
+      // k_copy_best; per launch: k_loop_start
       launches_ += 1 + (ran / prm.check_every) *
-                           (prm.check_every * (launches_csr() + launches_csc()) + launches_csr() + launches_csc() + 5);
+                           (prm.check_every * (launches_csr() + launches_csc()) + launches_csr() + launches_csc() + 3);
       iters = h.iters;
       inner = h.inner;
       sc.inner_base += static_cast<double>(ran);

@@ -1,5 +1,5 @@
 """A/B of an env toggle on resident solves (AB_PROBLEM=transport | random |
-pagerank), alternating in fresh processes on one box:
+pagerank | mcf), alternating in fresh processes on one box:
 python tools/ab_solve.py VAR A B [rounds]."""
 import json
 import os
@@ -14,7 +14,8 @@ import os
 which = os.environ.get("AB_PROBLEM", "transport")
 p = {"transport": lambda: rpdlp.GenTransport(1000, 1000, 1),
      "random": lambda: rpdlp.GenRandomLp(1000, 2000, 0.005, 1, equality_rows=300),
-     "pagerank": lambda: rpdlp.GenPagerank(100_000, 0.85, 6, 1)}[which]()
+     "pagerank": lambda: rpdlp.GenPagerank(100_000, 0.85, 6, 1),
+     "mcf": lambda: rpdlp.GenMcf(50_000, 330_000, 50, 1)}[which]()
 prm = rpdlp.SolverParams(eps=1e-4)
 with rpdlp.Session(p) as s:
     for _ in range(2):

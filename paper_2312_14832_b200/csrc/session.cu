@@ -1609,9 +1609,13 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     const char* e = std::getenv("PDHG_FUSED_CHECK");
     return !(e && e[0] == '0');
   }();
-  const bool device_loop_on = [] {  // PDHG_DEVICE_LOOP=0: host-driven loop (read per solve: A/B, tests)
+  // PDHG_DEVICE_LOOP=1: device-resident loop (read per solve: A/B, tests).
+  // Opt-in: 0.3 % faster on transport, but kernels inside conditional-graph
+  // bodies are invisible to kernel-replay profilers (ncu), so the default
+  // keeps every launch observable.
+  const bool device_loop_on = [] {
     const char* e = std::getenv("PDHG_DEVICE_LOOP");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   // The device-resident loop needs the host only for restarts, termination,
   // limits: not with an observer or a progress log (called at every check),

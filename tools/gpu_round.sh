@@ -13,7 +13,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$O/smoke.log" 
 timeout 600 python tools/probe.py > "$O/probe.log" 2>&1
 timeout 900 python bench.py > "$O/bench.json" 2> "$O/bench.err"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > "$O/bench_ref.json" 2> "$O/bench_ref.err"
-# launch list of one bench solve (cold-cache, serialised: shares only)
+# launch list of one bench solve (cold-cache, serialised: shares only). ncu
+# does not profile kernels inside conditional-graph bodies: keep the default
+# host-driven loop here (PDHG_DEVICE_LOOP unset).
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$O/launches.csv" \
     python bench.py --steps 1 --warmup 3 --no-cpu --e2e-steps 1 --kernel-iters 8 > "$O/ncu_bench.log" 2>&1
 # full capture of the fused step kernels on the transport workload

@@ -287,6 +287,15 @@ int pdhg_session_time_kernels(pdhg_session* s, int iters, double* ms_primal,
 int pdhg_session_time_check(pdhg_session* s, int iters, double* ms_device,
                             double* ms_wall, char* err, size_t errlen);
 
+/* SparseMatrix::Multiply / MultiplyTranspose / MultiplyAdd /
+ * MultiplyTransposeAdd (sparse_matrix.cpp:114-164) on the device:
+ * t = M x (transpose: M^T x) -- every row / column of <= 64 nonzeros summed in
+ * storage order, bit-identical with the reference -- then y = t
+ * (accumulate = 0) or y += alpha * t (accumulate = 1: the sum is completed
+ * first, then added, as the reference does). */
+int pdhg_csr_spmv(const pdhg_csr* m, int transpose, int accumulate, double alpha,
+                  const double* x, double* y, char* err, size_t errlen);
+
 /* ---- unit-level exports (solver.hpp:81-125), device-backed ---------------
  * PrimalStep (solver.cpp:112-129): out(n) = proj_[l,u](x - eta/omega (c - K'y))
  * DualStep (solver.cpp:131-154): out(m) = proj_Y(y + eta*omega (q - K(2x_new - x_old)))

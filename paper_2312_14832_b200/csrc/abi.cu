@@ -355,6 +355,44 @@ int pdhg_primal_step(const pdhg_lp* lp, const double* x, const double* y, double
   });
 }
 
+int pdhg_csr_spmv(const pdhg_csr* m, int transpose, int accumulate, double alpha, const double* x, double* y,
+                  char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!m || (m->rows < 0) || (m->cols < 0)) Invalid("bad matrix");
+    const int64_t nin = transpose ? m->rows : m->cols, nout = transpose ? m->cols : m->rows;
+    if ((nin && !x) || (nout && !y)) Invalid("null vector");
+    if (nout == 0) return;
+    std::vector<double> t(static_cast<size_t>(nout), 0.0);
+    const int64_t nnz = m->rows ? m->row_ptr[m->rows] : 0;
+    if (nnz > 0) {
+      // The matrix as the inequality block of a free, zero-cost LP; no scaling,
+      // so the session's K is M itself.
+      const int64_t n = m->cols;
+      std::vector<double> zc(static_cast<size_t>(std::max<int64_t>(n, 1)), 0.0),
+          lo(static_cast<size_t>(std::max<int64_t>(n, 1)), -INFINITY),
+          hi(static_cast<size_t>(std::max<int64_t>(n, 1)), INFINITY), zh(static_cast<size_t>(m->rows), 0.0);
+      static const int64_t kEmptyPtr[1] = {0};
+      pdhg_lp lp{};
+      lp.a = pdhg_csr{0, n, kEmptyPtr, nullptr, nullptr};
+      lp.g = *m;
+      lp.n = n;
+      lp.c = zc.data();
+      lp.l = lo.data();
+      lp.u = hi.data();
+      lp.h = zh.data();
+      pdhg_params p;
+      pdhg_params_default(&p);
+      p.scaling_enabled = 0;
+      pdhg::Session sess(lp, p, DeviceFromEnv());
+      sess.Spmv(transpose, x, t.data());
+    }
+    if (accumulate)
+      for (int64_t i = 0; i < nout; ++i) y[i] += alpha * t[i];
+    else
+      std::copy(t.begin(), t.end(), y);
+  });
+}
+
 int pdhg_dual_step(const pdhg_lp* lp, const double* xn, const double* xo, const double* y, double eta, double omega,
                    double* out, char* err, size_t errlen) {
   return Guard(err, errlen, [&] {

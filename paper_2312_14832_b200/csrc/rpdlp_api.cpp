@@ -98,6 +98,31 @@ void SparseMatrix::BuildColumns() {
     }
 }
 
+static void DeviceSpmv(const SparseMatrix& m, bool transpose, bool accumulate, double alpha,
+                       std::span<const double> x, std::span<double> y) {
+  const size_t nin = static_cast<size_t>(transpose ? m.rows() : m.cols());
+  const size_t nout = static_cast<size_t>(transpose ? m.cols() : m.rows());
+  if (x.size() != nin || y.size() != nout) throw std::invalid_argument("SpMV dimension mismatch");
+  const pdhg_csr c{m.rows(), m.cols(), m.row_ptr().data(), m.col_idx().data(), m.csr_values().data()};
+  char err[512] = {0};
+  const int rc = pdhg_csr_spmv(&c, transpose ? 1 : 0, accumulate ? 1 : 0, alpha, x.data(), y.data(), err, sizeof(err));
+  if (rc == PDHG_INVALID_ARGUMENT) throw std::invalid_argument(err);
+  if (rc != PDHG_OK) throw DeviceError(err);
+}
+
+void SparseMatrix::Multiply(std::span<const double> x, std::span<double> y) const {
+  DeviceSpmv(*this, false, false, 1.0, x, y);
+}
+void SparseMatrix::MultiplyTranspose(std::span<const double> x, std::span<double> y) const {
+  DeviceSpmv(*this, true, false, 1.0, x, y);
+}
+void SparseMatrix::MultiplyAdd(double alpha, std::span<const double> x, std::span<double> y) const {
+  DeviceSpmv(*this, false, true, alpha, x, y);
+}
+void SparseMatrix::MultiplyTransposeAdd(double alpha, std::span<const double> x, std::span<double> y) const {
+  DeviceSpmv(*this, true, true, alpha, x, y);
+}
+
 SparseMatrix SparseMatrix::VStack(const SparseMatrix& top, const SparseMatrix& bottom) {
   if (top.cols() != bottom.cols()) throw std::invalid_argument("VStack: column count mismatch");
   SparseMatrix m;

@@ -289,6 +289,41 @@ int main() {
           sol["x"].size() == r.x.size());
     std::system(("rm -rf " + dir).c_str());
   }
+  {  // SparseMatrix SpMV members (test_sparse_matrix.cpp:80-101): device result vs the serial row sums
+    const LpProblem p = GenRandomLp(40, 30, 0.3, 11);
+    const SparseMatrix& k = p.g;
+    std::vector<double> x(k.cols()), yr(k.rows());
+    for (size_t j = 0; j < x.size(); ++j) x[j] = std::sin(1.0 + j);
+    for (size_t i = 0; i < yr.size(); ++i) yr[i] = std::cos(2.0 + i);
+    std::vector<double> y(k.rows()), want(k.rows(), 0.0);
+    k.Multiply(x, y);
+    for (Index r = 0; r < k.rows(); ++r) {
+      double acc = 0.0;
+      for (Index q = k.row_ptr()[r]; q < k.row_ptr()[r + 1]; ++q) acc += k.csr_values()[q] * x[k.col_idx()[q]];
+      want[r] = acc;
+    }
+    CHECK(y == want);  // storage-order sums: bit-identical
+    std::vector<double> z(k.cols()), wantz(k.cols(), 0.0);
+    k.MultiplyTranspose(yr, z);
+    for (Index c = 0; c < k.cols(); ++c) {
+      double acc = 0.0;
+      for (Index q = k.col_ptr()[c]; q < k.col_ptr()[c + 1]; ++q) acc += k.csc_values()[q] * yr[k.row_idx()[q]];
+      wantz[c] = acc;
+    }
+    CHECK(z == wantz);
+    std::vector<double> acc(k.rows(), 1.0);
+    k.MultiplyAdd(-2.0, x, acc);
+    bool ok = true;
+    for (Index r = 0; r < k.rows(); ++r) ok = ok && acc[r] == 1.0 + -2.0 * want[r];
+    CHECK(ok);
+    bool threw = false;
+    try {
+      k.Multiply(yr, y);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   {  // ChooseRestartCandidate (solver.cpp:170-176, test_solver.cpp restart tests): strict < picks current
     LpProblem p = GenRandomLp(10, 12, 0.4, 4);
     SolverParams prm;

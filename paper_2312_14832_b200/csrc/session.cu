@@ -1990,10 +1990,9 @@ double Session::OpNorm(int iters, uint64_t seed) {
 }
 
 // n draws of std::normal_distribution(0,1) over std::mt19937_64(seed) and
-// the sequential sum of squares (solver.cpp:88-97). The libstdc++ draw is
-// faster than the bit-identical threaded replica (normal_rng.h) on these
-// hosts -- the engine itself is the serial part -- so the session overlaps
-// it with setup instead.
+// the sequential sum of squares (solver.cpp:88-97), on a host thread that
+// overlaps session setup; the draw itself is the pipelined bit-identical
+// replica of normal_rng.h (engine on this thread, transforms on workers).
 void Session::DrawStart(uint64_t seed) {
   if (!start_host_) start_host_ = static_cast<double*>(pinned_get(n_ * sizeof(double), &start_host_bytes_));
   // Bit-identical to the sequential draw; engine on this thread, transforms

@@ -296,6 +296,21 @@ int pdhg_session_time_check(pdhg_session* s, int iters, double* ms_device,
 int pdhg_csr_spmv(const pdhg_csr* m, int transpose, int accumulate, double alpha,
                   const double* x, double* y, char* err, size_t errlen);
 
+/* RowInfNorms / ColInfNorms (power = 0) and RowPowerSums / ColPowerSums
+ * (power = 1, exponent p) (sparse_matrix.cpp:166-204) on the device; out has
+ * rows (columns = 0) or cols (columns = 1) entries. Sums run in storage order
+ * (bit-identical for <= 64 nonzeros per segment; p outside {0, 1, 2} uses the
+ * device pow). */
+int pdhg_csr_norms(const pdhg_csr* m, int columns, int power, double p, double* out,
+                   char* err, size_t errlen);
+/* SparseMatrix::Scaled (sparse_matrix.cpp:206-222): the values of both
+ * layouts of D_r M D_c (row_scale * v * col_scale, left to right). The CSC
+ * arrays are the matrix's own (col_ptr, row_idx, csc values). */
+int pdhg_csr_scaled(const pdhg_csr* m, const int64_t* col_ptr, const int64_t* row_idx,
+                    const double* csc_values, const double* row_scale,
+                    const double* col_scale, double* csr_out, double* csc_out,
+                    char* err, size_t errlen);
+
 /* ---- unit-level exports (solver.hpp:81-125), device-backed ---------------
  * PrimalStep (solver.cpp:112-129): out(n) = proj_[l,u](x - eta/omega (c - K'y))
  * DualStep (solver.cpp:131-154): out(m) = proj_Y(y + eta*omega (q - K(2x_new - x_old)))

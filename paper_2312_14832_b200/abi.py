@@ -116,6 +116,10 @@ SIGNATURES = {
     "pdhg_session_opnorm": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, dptr, C.c_char_p, C.c_size_t]),
     "pdhg_session_time_kernels": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, dptr, C.c_char_p, C.c_size_t]),
     "pdhg_session_time_check": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, C.c_char_p, C.c_size_t]),
+    "pdhg_csr_spmv": (C.c_int, [C.POINTER(Csr), C.c_int, C.c_int, C.c_double, dptr, dptr, C.c_char_p, C.c_size_t]),
+    "pdhg_csr_norms": (C.c_int, [C.POINTER(Csr), C.c_int, C.c_int, C.c_double, dptr, C.c_char_p, C.c_size_t]),
+    "pdhg_csr_scaled": (C.c_int, [C.POINTER(Csr), i64ptr, i64ptr, dptr, dptr, dptr, dptr, dptr, C.c_char_p,
+                                  C.c_size_t]),
     "pdhg_csr_from_triplets": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int, i64ptr, i64ptr, dptr,
                                          C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]),
     "pdhg_session_flush_l2": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),

@@ -355,6 +355,34 @@ int pdhg_primal_step(const pdhg_lp* lp, const double* x, const double* y, double
   });
 }
 
+}  // extern "C"
+
+// A matrix as the inequality block of a free, zero-cost LP, unscaled: the
+// session's K is the matrix itself (pdhg_csr_spmv / pdhg_csr_norms).
+template <class F>
+void WithMatrixSession(const pdhg_csr& m, F&& f) {
+  static const int64_t kEmptyPtr[1] = {0};
+  const int64_t n = m.cols;
+  std::vector<double> zc(static_cast<size_t>(std::max<int64_t>(n, 1)), 0.0),
+      lo(static_cast<size_t>(std::max<int64_t>(n, 1)), -INFINITY),
+      hi(static_cast<size_t>(std::max<int64_t>(n, 1)), INFINITY), zh(static_cast<size_t>(std::max<int64_t>(m.rows, 1)), 0.0);
+  pdhg_lp lp{};
+  lp.a = pdhg_csr{0, n, kEmptyPtr, nullptr, nullptr};
+  lp.g = m;
+  lp.n = n;
+  lp.c = zc.data();
+  lp.l = lo.data();
+  lp.u = hi.data();
+  lp.h = zh.data();
+  pdhg_params p;
+  pdhg_params_default(&p);
+  p.scaling_enabled = 0;
+  pdhg::Session sess(lp, p, DeviceFromEnv());
+  f(sess);
+}
+
+extern "C" {
+
 int pdhg_csr_spmv(const pdhg_csr* m, int transpose, int accumulate, double alpha, const double* x, double* y,
                   char* err, size_t errlen) {
   return Guard(err, errlen, [&] {
@@ -364,32 +392,36 @@ int pdhg_csr_spmv(const pdhg_csr* m, int transpose, int accumulate, double alpha
     if (nout == 0) return;
     std::vector<double> t(static_cast<size_t>(nout), 0.0);
     const int64_t nnz = m->rows ? m->row_ptr[m->rows] : 0;
-    if (nnz > 0) {
-      // The matrix as the inequality block of a free, zero-cost LP; no scaling,
-      // so the session's K is M itself.
-      const int64_t n = m->cols;
-      std::vector<double> zc(static_cast<size_t>(std::max<int64_t>(n, 1)), 0.0),
-          lo(static_cast<size_t>(std::max<int64_t>(n, 1)), -INFINITY),
-          hi(static_cast<size_t>(std::max<int64_t>(n, 1)), INFINITY), zh(static_cast<size_t>(m->rows), 0.0);
-      static const int64_t kEmptyPtr[1] = {0};
-      pdhg_lp lp{};
-      lp.a = pdhg_csr{0, n, kEmptyPtr, nullptr, nullptr};
-      lp.g = *m;
-      lp.n = n;
-      lp.c = zc.data();
-      lp.l = lo.data();
-      lp.u = hi.data();
-      lp.h = zh.data();
-      pdhg_params p;
-      pdhg_params_default(&p);
-      p.scaling_enabled = 0;
-      pdhg::Session sess(lp, p, DeviceFromEnv());
-      sess.Spmv(transpose, x, t.data());
-    }
+    if (nnz > 0) WithMatrixSession(*m, [&](pdhg::Session& sess) { sess.Spmv(transpose, x, t.data()); });
     if (accumulate)
       for (int64_t i = 0; i < nout; ++i) y[i] += alpha * t[i];
     else
       std::copy(t.begin(), t.end(), y);
+  });
+}
+
+
+int pdhg_csr_norms(const pdhg_csr* m, int columns, int power, double p, double* out, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!m || m->rows < 0 || m->cols < 0) Invalid("bad matrix");
+    const int64_t nout = columns ? m->cols : m->rows;
+    if (nout == 0) return;
+    if (!out) Invalid("null vector");
+    const int64_t nnz = m->rows ? m->row_ptr[m->rows] : 0;
+    if (nnz == 0) {
+      std::fill(out, out + nout, 0.0);
+      return;
+    }
+    WithMatrixSession(*m, [&](pdhg::Session& s) { s.SegmentNorms(columns, power, p, out); });
+  });
+}
+
+int pdhg_csr_scaled(const pdhg_csr* m, const int64_t* col_ptr, const int64_t* row_idx, const double* csc_values,
+                    const double* row_scale, const double* col_scale, double* csr_out, double* csc_out, char* err,
+                    size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!m || m->rows < 0 || m->cols < 0) Invalid("bad matrix");
+    pdhg::ScaleEntries(*m, col_ptr, row_idx, csc_values, row_scale, col_scale, DeviceFromEnv(), csr_out, csc_out);
   });
 }
 

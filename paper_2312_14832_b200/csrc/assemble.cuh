@@ -67,6 +67,66 @@ static __global__ void k_i32_to_i64(const int32_t* in, int64_t* out, int64_t n) 
 
 static __global__ void k_trip_iota(int32_t* v, int64_t n) { GRID_STRIDE(i, n) v[i] = static_cast<int32_t>(i); }
 
+// Scaled (sparse_matrix.cpp:206-222) for one compressed layout: entry k of
+// segment s with index i becomes row_scale * v * col_scale, multiplied left
+// to right as the reference does; `seg_is_row` says which side s is.
+template <bool kSegIsRow>
+static __global__ void k_scale_entries(const int64_t* ptr, const int64_t* idx, const double* val, int64_t nseg,
+                                       const double* seg_scale, const double* idx_scale, double* out) {
+  for (int64_t s = blockIdx.x; s < nseg; s += gridDim.x)
+    for (int64_t k = ptr[s] + threadIdx.x; k < ptr[s + 1]; k += blockDim.x) {
+      if constexpr (kSegIsRow) out[k] = seg_scale[s] * val[k] * idx_scale[idx[k]];
+      else out[k] = idx_scale[idx[k]] * val[k] * seg_scale[s];
+    }
+}
+
+// Both layouts of D_r M D_c (values only; the pattern is unchanged).
+inline void ScaleEntries(const pdhg_csr& csr, const int64_t* col_ptr, const int64_t* row_idx, const double* csc_val,
+                         const double* row_scale, const double* col_scale, int device, double* csr_out,
+                         double* csc_out) {
+  PDHG_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  PDHG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } guard{st};
+  AllocScope scope(st);
+  const int64_t m = csr.rows, n = csr.cols, nnz = m ? csr.row_ptr[m] : 0;
+  if (nnz == 0) return;
+  DArray<int64_t> rp, ci, cp, ri;
+  DArray<double> v, cv, rs, cs, o1, o2;
+  rp.alloc(m + 1);
+  ci.alloc(nnz);
+  cp.alloc(n + 1);
+  ri.alloc(nnz);
+  v.alloc(nnz);
+  cv.alloc(nnz);
+  rs.alloc(std::max<int64_t>(m, 1));
+  cs.alloc(std::max<int64_t>(n, 1));
+  o1.alloc(nnz);
+  o2.alloc(nnz);
+  auto up = [&](void* d, const void* h, size_t b) { PDHG_CUDA(cudaMemcpyAsync(d, h, b, cudaMemcpyHostToDevice, st)); };
+  up(rp.p, csr.row_ptr, (m + 1) * sizeof(int64_t));
+  up(ci.p, csr.col_idx, nnz * sizeof(int64_t));
+  up(v.p, csr.values, nnz * sizeof(double));
+  up(cp.p, col_ptr, (n + 1) * sizeof(int64_t));
+  up(ri.p, row_idx, nnz * sizeof(int64_t));
+  up(cv.p, csc_val, nnz * sizeof(double));
+  if (m) up(rs.p, row_scale, m * sizeof(double));
+  if (n) up(cs.p, col_scale, n * sizeof(double));
+  k_scale_entries<true><<<ew_grid(m), 128, 0, st>>>(rp.p, ci.p, v.p, m, rs.p, cs.p, o1.p);
+  k_scale_entries<false><<<ew_grid(n), 128, 0, st>>>(cp.p, ri.p, cv.p, n, cs.p, rs.p, o2.p);
+  PDHG_CUDA(cudaMemcpyAsync(csr_out, o1.p, nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PDHG_CUDA(cudaMemcpyAsync(csc_out, o2.p, nnz * sizeof(double), cudaMemcpyDeviceToHost, st));
+  PDHG_CUDA(cudaStreamSynchronize(st));
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(PDHG_CUDA_ERROR, std::string("scaled: ") + cudaGetErrorString(e));
+}
+
 // Host entry: triplets in host memory -> CSR in host memory (outputs sized
 // rows + 1 / count / count by the caller); returns the entries written.
 inline int64_t CsrFromTriplets(int64_t rows, int64_t cols, int64_t count, const pdhg_triplet* trips, int device,

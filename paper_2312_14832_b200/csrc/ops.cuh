@@ -106,6 +106,30 @@ struct OpPowerSumScale {
   }
 };
 
+// Raw per-segment reductions (sparse_matrix.cpp:166-204): max |v| (kMax) or
+// sum |v|^p in storage order, p special-cased for {0, 1, 2} like
+// OpPowerSumScale (std::pow is exact there; other p use the device pow).
+template <bool kInf>
+struct OpRawNorm {
+  static constexpr int kRhs = 1, kRed = 0;
+  static constexpr bool kMax = kInf;
+  using Pre = Nil;
+  double pw;
+  int mode;  // power sums: 0 |v|^0, 1 |v|, 2 v*v, 3 pow
+  double* out;
+  __device__ void map(int32_t, double v, double (&p)[1]) const {
+    const double a = fabs(v);
+    if constexpr (kInf) p[0] = a;
+    else p[0] = mode == 1 ? a : (mode == 2 ? a * a : (mode == 0 ? 1.0 : pow(a, pw)));
+  }
+  static constexpr int kOcc = 5;
+  static constexpr int kOps = 0;
+  __device__ const double* operand(int) const { return nullptr; }
+  __device__ Pre staged(int32_t, const double*, int) const { return {}; }
+  __device__ Pre prefetch(int32_t) const { return {}; }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre&, double*) const { out[s] = a[0]; }
+};
+
 // --------------------------------------------------------- PDHG step kernels
 // K-CSC: kty = K^T y, x+ = proj_[l,u](x - (eta/omega)(c - kty)), running
 // average of x (solver.cpp:285-290, RunningAverage::Add x-half :159).

@@ -123,6 +123,34 @@ void SparseMatrix::MultiplyTransposeAdd(double alpha, std::span<const double> x,
   DeviceSpmv(*this, true, true, alpha, x, y);
 }
 
+static std::vector<double> DeviceNorms(const SparseMatrix& m, bool columns, bool power, double p) {
+  std::vector<double> out(static_cast<size_t>(columns ? m.cols() : m.rows()), 0.0);
+  const pdhg_csr c{m.rows(), m.cols(), m.row_ptr().data(), m.col_idx().data(), m.csr_values().data()};
+  char err[512] = {0};
+  const int rc = pdhg_csr_norms(&c, columns ? 1 : 0, power ? 1 : 0, p, out.data(), err, sizeof(err));
+  if (rc == PDHG_INVALID_ARGUMENT) throw std::invalid_argument(err);
+  if (rc != PDHG_OK) throw DeviceError(err);
+  return out;
+}
+
+std::vector<double> SparseMatrix::RowInfNorms() const { return DeviceNorms(*this, false, false, 0.0); }
+std::vector<double> SparseMatrix::ColInfNorms() const { return DeviceNorms(*this, true, false, 0.0); }
+std::vector<double> SparseMatrix::RowPowerSums(double p) const { return DeviceNorms(*this, false, true, p); }
+std::vector<double> SparseMatrix::ColPowerSums(double p) const { return DeviceNorms(*this, true, true, p); }
+
+SparseMatrix SparseMatrix::Scaled(std::span<const double> row_scale, std::span<const double> col_scale) const {
+  if (static_cast<Index>(row_scale.size()) != rows_ || static_cast<Index>(col_scale.size()) != cols_)
+    throw std::invalid_argument("Scaled: scale length mismatch");
+  SparseMatrix m = *this;
+  const pdhg_csr c{rows_, cols_, rp_.data(), ci_.data(), val_.data()};
+  char err[512] = {0};
+  const int rc = pdhg_csr_scaled(&c, cp_.data(), ri_.data(), cval_.data(), row_scale.data(), col_scale.data(),
+                                 m.val_.data(), m.cval_.data(), err, sizeof(err));
+  if (rc == PDHG_INVALID_ARGUMENT) throw std::invalid_argument(err);
+  if (rc != PDHG_OK) throw DeviceError(err);
+  return m;
+}
+
 SparseMatrix SparseMatrix::VStack(const SparseMatrix& top, const SparseMatrix& bottom) {
   if (top.cols() != bottom.cols()) throw std::invalid_argument("VStack: column count mismatch");
   SparseMatrix m;

@@ -2056,6 +2056,28 @@ void Session::Spmv(int transpose, const double* in, double* out) {
   ToHost(b.p, nullptr, transpose ? pad_c_ : pad_r_, out, nout);
 }
 
+// RowInfNorms / ColInfNorms / RowPowerSums / ColPowerSums
+// (sparse_matrix.cpp:166-204) of this session's K_s, original order.
+void Session::SegmentNorms(int columns, int power, double p, double* out) {
+  PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
+  const int64_t nout = columns ? n_ : m_, pout = columns ? np_ : mp_;
+  DArray<double> b;
+  b.alloc(std::max<int64_t>(pout, 1));
+  PDHG_CUDA(cudaMemsetAsync(b.p, 0, std::max<int64_t>(pout, 1) * sizeof(double), st_));
+  const int mode = p == 0.0 ? 0 : (p == 1.0 ? 1 : (p == 2.0 ? 2 : 3));
+  for (Shard& h : shards_) {
+    const Layout& L = columns ? h.csc : h.csr;
+    double* o = b.p + (columns ? h.coff : h.roff);
+    if (power) run_pass(L, OpRawNorm<false>{p, mode, o}, RedSlots{}, st_);
+    else run_pass(L, OpRawNorm<true>{p, mode, o}, RedSlots{}, st_);
+  }
+  if (columns) GatherXFull(b.p);
+  else GatherYFull(b.p);
+  check_launch("segment norms");
+  ToHost(b.p, nullptr, columns ? pad_c_ : pad_r_, out, nout);
+}
+
 // Mean device time of the two fused step kernels (all local shards, gathers
 // included) and of a graph-launched 64-iteration block, on the solver stream.
 void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double* ms_iter) {

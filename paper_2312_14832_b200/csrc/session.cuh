@@ -44,6 +44,7 @@ class Session {
   void Scaling(double* rs, double* cs);
   void ScaledProblem(double* kv, double* c, double* l, double* u, double* q);
   void Spmv(int transpose, const double* in, double* out);
+  void SegmentNorms(int columns, int power, double p, double* out);
   double OpNorm(int iters, uint64_t seed);
   void TimeKernels(int iters, double* ms_primal, double* ms_dual, double* ms_iter);
   void TimeCheck(int iters, double* ms_device, double* ms_wall);

@@ -140,6 +140,27 @@ class CsrMatrix:
         k = nnz.value
         return CsrMatrix(rows, cols, ptr, idx[:k].copy(), val[:k].copy())
 
+    def multiply(self, x, transpose: bool = False) -> np.ndarray:
+        """SparseMatrix::Multiply / MultiplyTranspose (sparse_matrix.cpp:114-138)
+        on the device (pdhg_csr_spmv; storage-order sums)."""
+        x = _f64(x)
+        out = np.zeros(self.cols if transpose else self.rows)
+        c = self.to_c()
+        err = C.create_string_buffer(abi.ERRLEN)
+        raise_for(abi.load().pdhg_csr_spmv(C.byref(c), int(transpose), 0, 1.0, _dp(x), _dp(out), err, abi.ERRLEN),
+                  err)
+        return out
+
+    def norms(self, columns: bool = False, power: float = None) -> np.ndarray:
+        """Row/ColInfNorms (power None) or Row/ColPowerSums(power)
+        (sparse_matrix.cpp:166-204) on the device."""
+        out = np.zeros(self.cols if columns else self.rows)
+        c = self.to_c()
+        err = C.create_string_buffer(abi.ERRLEN)
+        raise_for(abi.load().pdhg_csr_norms(C.byref(c), int(columns), int(power is not None),
+                                            float(power or 0.0), _dp(out), err, abi.ERRLEN), err)
+        return out
+
     @property
     def nnz(self) -> int:
         return int(self.row_ptr[-1]) if self.rows else 0

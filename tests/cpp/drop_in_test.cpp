@@ -316,6 +316,29 @@ int main() {
     bool ok = true;
     for (Index r = 0; r < k.rows(); ++r) ok = ok && acc[r] == 1.0 + -2.0 * want[r];
     CHECK(ok);
+    // norms / power sums / Scaled (sparse_matrix.cpp:166-222) against serial loops
+    std::vector<double> rinf(k.rows(), 0.0), cinf(k.cols(), 0.0), rp1(k.rows(), 0.0), cp2(k.cols(), 0.0);
+    for (Index r = 0; r < k.rows(); ++r)
+      for (Index q = k.row_ptr()[r]; q < k.row_ptr()[r + 1]; ++q) {
+        rinf[r] = std::max(rinf[r], std::abs(k.csr_values()[q]));
+        rp1[r] += std::abs(k.csr_values()[q]);
+      }
+    for (Index c = 0; c < k.cols(); ++c)
+      for (Index q = k.col_ptr()[c]; q < k.col_ptr()[c + 1]; ++q) {
+        cinf[c] = std::max(cinf[c], std::abs(k.csc_values()[q]));
+        cp2[c] += k.csc_values()[q] * k.csc_values()[q];
+      }
+    CHECK(k.RowInfNorms() == rinf && k.ColInfNorms() == cinf && k.RowPowerSums(1.0) == rp1 &&
+          k.ColPowerSums(2.0) == cp2);
+    const SparseMatrix s = k.Scaled(yr, x);
+    bool sok = s.row_ptr() == k.row_ptr() && s.col_idx() == k.col_idx();
+    for (Index r = 0; r < k.rows(); ++r)
+      for (Index q = k.row_ptr()[r]; q < k.row_ptr()[r + 1]; ++q)
+        sok = sok && s.csr_values()[q] == yr[r] * k.csr_values()[q] * x[k.col_idx()[q]];
+    for (Index c = 0; c < k.cols(); ++c)
+      for (Index q = k.col_ptr()[c]; q < k.col_ptr()[c + 1]; ++q)
+        sok = sok && s.csc_values()[q] == yr[k.row_idx()[q]] * k.csc_values()[q] * x[c];
+    CHECK(sok);
     bool threw = false;
     try {
       k.Multiply(yr, y);

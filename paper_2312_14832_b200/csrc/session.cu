@@ -1911,25 +1911,9 @@ double Session::OpNorm(int iters, uint64_t seed) {
   PDHG_CUDA(cudaSetDevice(device_));
   AllocScope scope(st_);
   if (nnz_ == 0) return 0.0;
-  // Start vector (solver.cpp:88-97): drawn on a host thread while the
-  // session was being built (upload, CSC, scaling) for the seed the session
-  // was created with; another seed is drawn here.
-  if (start_.joinable()) start_.join();
-  if (start_seed_ != seed || !start_host_) DrawStart(seed);
-  double* v = start_host_;  // pinned: ToInternal copies it straight to the device
-  double vnorm = start_norm_;
-  if (vnorm == 0.0) {
-    v[0] = 1.0;
-    vnorm = 1.0;
-  }
   // Scratch: x_[1] and kx_[1] are free until the loop starts.
   double* u = x_[1].p;
   double* kv = kx_[1].p;
-  PDHG_CUDA(cudaMemsetAsync(kv, 0, mp_ * sizeof(double), st_));
-  ToInternal(v, pad_c_, u, n_, np_);
-  Scalars sc{};
-  sc.pw_norm = vnorm;
-  PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   const int64_t ns = static_cast<int64_t>(shards_.size());
   const bool single = shards_.size() == 1 && !nccl();
   launches_ += static_cast<int64_t>(iters) * (launches_csr() + launches_csc() + (single ? 1 : ns + (ns > 1) + 1)) +
@@ -1971,6 +1955,24 @@ double Session::OpNorm(int iters, uint64_t seed) {
   const int many = iters / kPowerSteps, rest = iters % kPowerSteps;
   if (many && !power_graph_) capture(kPowerSteps, &power_graph_);
   if (rest && !power_graph1_) capture(1, &power_graph1_);
+  // The graphs never read the start vector's values, so they are captured
+  // first, while the host thread may still be drawing it.
+  // Start vector (solver.cpp:88-97): drawn on a host thread while the
+  // session was being built (upload, CSC, scaling) for the seed the session
+  // was created with; another seed is drawn here.
+  if (start_.joinable()) start_.join();
+  if (start_seed_ != seed || !start_host_) DrawStart(seed);
+  double* v = start_host_;  // pinned: ToInternal copies it straight to the device
+  double vnorm = start_norm_;
+  if (vnorm == 0.0) {
+    v[0] = 1.0;
+    vnorm = 1.0;
+  }
+  PDHG_CUDA(cudaMemsetAsync(kv, 0, mp_ * sizeof(double), st_));
+  ToInternal(v, pad_c_, u, n_, np_);
+  Scalars sc{};
+  sc.pw_norm = vnorm;
+  PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   for (int it = 0; it < many; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph_, st_));
   for (int it = 0; it < rest; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph1_, st_));
   for (size_t k = 0; k < shards_.size(); ++k) {

@@ -6,24 +6,35 @@ A step is one full restarted-PDHG solve to eps=1e-4 of the workload (default
 BASELINE configs[1]: transportation LP, 1000 sources x 1000 sinks, 1M
 variables, 2M nonzeros), problem resident in HBM (upload, CSC build and device
 scaling happen once, outside the timed region -- the reference's
-solve_seconds also excludes scaling). value = PDHG iterations / device
-seconds over K solves (CUDA events on the solver's stream, L2 flushed between
-steps). e2e = the same metric through the public C-ABI entry pdhg_solve with
-pinned host buffers: H2D of the LP, int32 narrowing, CSC build, scaling, the
-solve and D2H of x, y, lambda all inside the timed region.
+solve_seconds also excludes scaling).
+
+value (both arms, same unit) = PDHG iterations per second of the solve LOOP:
+iterations / (solve time - solve time of an iter_limit=0 solve), i.e. the
+power iteration and the start-point evaluation that every solve does once
+are subtracted, exactly as the reference arm subtracts them from its
+iteration sample. Ours: full solves to eps, device time (CUDA events on the
+solver's stream, L2 flushed between steps). Reference arm: the unmodified
+reference (oracle/_ref) on a bounded iteration sample per step.
+e2e = the same metric through the public C-ABI entry pdhg_solve_on with
+pinned host buffers, nothing subtracted: H2D of the LP, int32 narrowing, CSC
+build, scaling, power iteration, the solve and D2H of x, y, lambda.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config transport|pagerank|random|mcf|staircase] [--eps 1e-4]
-                    [--mode sharded|replicas] [--eps-tight 1e-8]
+                    [--mode sharded|replicas] [--eps-tight 1e-8] [--extra mcf,pagerank10m,staircase]
 
 Under torchrun (N > 1) the default mode shards K over the ranks (row/column
 blocks, NCCL exchanges; strong scaling: value = iterations of the one solve
 per device second, max over ranks); --mode replicas runs N independent solves.
-`tight_solve` times one extra solve to --eps-tight (time-to-1e-8).
+`tight_solve` times one extra solve to --eps-tight (time-to-1e-8); `extra`
+reports steady-state it/s and HBM fractions of BASELINE configs 3-5.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref,
 the UNMODIFIED rpdlp sources compiled by oracle/Makefile; else the oracle
-restatement) on rank 0 with a bounded iteration sample per step.
+restatement) on rank 0 with a bounded iteration sample per step. For the
+transport workload the instance is built by the reference library itself
+(oracle/ref_shim.cpp ref_gen_transport, pinned bit-for-bit to the product
+generator), so that arm never loads the product library.
 """
 from __future__ import annotations
 
@@ -207,34 +218,60 @@ def cpu_iter_rate(problem, eps: float, budget_s: float):
 
 
 # --------------------------------------------------------------------- arms
+def workload_config(workload: str, m: int, n: int, nnz: int, eps: float) -> dict:
+    """The `config` dict, byte-identical in both arms (arm-specific detail
+    goes in `timing`)."""
+    return {"workload": workload, "m": m, "n": n, "nnz": nnz, "eps": eps}
+
+
 def run_reference(args, world, rank, local, dist):
     if rank != 0:
         return 0
-    problem, workload = make_problem(args.config, args)
     from oracle import oracle
     from paper_2312_14832_b200.rpdlp import SolverParams
     chk = oracle.cpu_baseline()
     kind = "reference" if chk is oracle.reference() else "port"
-    r0 = chk.solve(problem, SolverParams(eps=args.eps, iter_limit=0))
+    if args.config == "transport" and kind == "reference":
+        s = args.transport
+        inst = chk.transport_instance(s, s, 1)
+        workload = f"transportation LP {s} sources x {s} sinks ({s * s} vars, {2 * s * s} nnz), eps={args.eps:g}"
+        m, n, nnz = inst.m, inst.n, inst.nnz
+
+        def solve(prm):
+            r = inst.solve(prm)
+            return r.iterations, r.solve_seconds
+        built_by = "reference library (oracle/_ref ref_gen_transport via rpdlp::SparseMatrix::FromTriplets)"
+    else:
+        problem, workload = make_problem(args.config, args)
+        m, n, nnz = problem.num_rows(), problem.num_vars(), problem.nnz()
+
+        def solve(prm):
+            r = chk.solve(problem, prm)
+            return r.iterations, r.solve_seconds
+        built_by = "product generator (no reference-side generator for this config)"
+    t0s = sorted(solve(SolverParams(eps=args.eps, iter_limit=0))[1] for _ in range(3))
+    t0 = t0s[1]  # median of 3: power iteration + start-point evaluation
     per = args.ref_iters
     for _ in range(args.warmup):
-        chk.solve(problem, SolverParams(eps=args.eps, iter_limit=64))
+        solve(SolverParams(eps=args.eps, iter_limit=64))
     times, iters = [], 0
     for _ in range(args.steps):
-        r = chk.solve(problem, SolverParams(eps=args.eps, iter_limit=per))
-        times.append(max(r.solve_seconds - r0.solve_seconds, 1e-9))
-        iters += r.iterations
+        it, secs = solve(SolverParams(eps=args.eps, iter_limit=per))
+        times.append(max(secs - t0, 1e-9))
+        iters += it
     tot = sum(times)
     value = iters / tot
     line = {"metric": METRIC, "value": value, "unit": "it/s", "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": workload, "m": problem.num_rows(), "n": problem.num_vars(),
-                                            "nnz": problem.nnz(), "eps": args.eps,
-                                            "sample_iterations_per_step": per},
+            "data": "synthetic", "config": workload_config(workload, m, n, nnz, args.eps),
+            "timing": {"step": f"reference Solve with iter_limit={per} (a bounded sample of the workload's "
+                               f"iterations), solve_seconds minus that of an iter_limit=0 solve",
+                       "subtracted_s": t0, "instance": built_by},
             "cpu_baseline": {"value": value, "unit": "it/s", "cores": 1, "kind": kind,
                              "sample": f"{per} PDHG iterations per step of the same instance (serial reference, "
-                                       f"1 thread); power iteration/start evaluation subtracted"},
+                                       f"1 thread); power iteration/start evaluation subtracted",
+                             "host": platform.processor() or platform.machine(), "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -266,6 +303,9 @@ def pinned_copy(problem):
 
 
 def load_traffic(config: str, kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary of the
+    current build (profiles/ncu_summary.json, written by tools/ncu_summary.py
+    from an `ncu --set full` capture), or None."""
     f = ROOT / "profiles" / "ncu_summary.json"
     if not f.exists():
         return None
@@ -274,6 +314,72 @@ def load_traffic(config: str, kernel: str):
         return d.get(config, {}).get(kernel, {}).get("dram_bytes_per_launch")
     except (ValueError, AttributeError):
         return None
+
+
+EXTRA = {
+    # name: (builder, description) -- BASELINE configs 3-5 at their full sizes
+    "mcf": (lambda r: r.GenMcf(50_000, 330_000, 50, 1),
+            "multicommodity flow LP V=50000 E=330000 K=50 (16.5M vars, 49.5M nnz)"),
+    "pagerank10m": (lambda r: r.GenPagerank(10_000_000, 0.85, 6, 1),
+                    "PageRank LP n=10M attachment=6 (GenPagerank seed 1, 80.0M nnz)"),
+    "staircase": (lambda r: r.GenStaircase(500, 100_000, 100_000, 20, 5, seed=1),
+                  "block-angular staircase LP 500 stages x 100k rows x 100k cols, 20 nnz/row (1.0e9 nnz)"),
+}
+
+
+def kernel_roofline(sess, st, m, n, nnz, hbm_peak, iters_cold, iters_warm, world=1):
+    """Cold-cache per-launch roofline of the two step kernels (L2 swept clean
+    before every launch) plus the warm, graph-launched iteration that the
+    solve loop actually runs (L2-assisted where the working set fits)."""
+    ms_p, ms_d, ms_ic = sess.time_kernels_cold(iters_cold)
+    _, _, ms_iw = sess.time_kernels(iters_warm)
+    b_p, b_d, b_it = algorithmic_bytes(m, n, nnz, st.uniform_bounds, st.csr_uniform_len, st.csc_uniform_len)
+    b_p, b_d, b_it = b_p / world, b_d / world, b_it / world
+
+    def gbs(b, ms):
+        return b / (ms * 1e-3) / 1e9
+
+    return {
+        "primal_csc": {"ms": ms_p, "bytes": b_p, "gbs": gbs(b_p, ms_p), "frac": gbs(b_p, ms_p) / hbm_peak},
+        "dual_csr": {"ms": ms_d, "bytes": b_d, "gbs": gbs(b_d, ms_d), "frac": gbs(b_d, ms_d) / hbm_peak},
+        "iteration_cold": {"ms": ms_ic, "bytes": b_it, "gbs": gbs(b_it, ms_ic), "frac": gbs(b_it, ms_ic) / hbm_peak,
+                           "note": "one iteration (primal then dual, programmatic overlap) after an L2 sweep"},
+        "iteration_in_loop": {"ms": ms_iw, "gbs": gbs(b_it, ms_iw), "frac": gbs(b_it, ms_iw) / hbm_peak,
+                              "it_per_s": 1e3 / ms_iw,
+                              "note": "graph-launched 64-step blocks back to back, as in the solve loop; "
+                                      "L2-assisted where the per-iteration working set fits the 126 MB L2 "
+                                      "(x+ and y+ reach the next kernel from L2)"},
+    }
+
+
+def run_extra(names, local, hbm_peak):
+    """Steady-state it/s and HBM fractions of BASELINE configs 3-5 (driver-
+    visible; the full solves of these take minutes and live in
+    tools/configs_run.py)."""
+    from paper_2312_14832_b200 import rpdlp
+    out = {}
+    for name in names:
+        if name not in EXTRA:
+            continue
+        make, desc = EXTRA[name]
+        t = time.time()
+        p = make(rpdlp)
+        gen_s = time.time() - t
+        m, n, nnz = p.num_rows(), p.num_vars(), p.nnz()
+        t = time.time()
+        with rpdlp.Session(p, rpdlp.SolverParams(), device=local) as s:
+            setup_s = time.time() - t
+            st = s.stats()
+            big = nnz > 2e8
+            rf = kernel_roofline(s, st, m, n, nnz, hbm_peak, 8 if big else 32, 64 if big else 256)
+        del p
+        it = rf["iteration_in_loop"]
+        out[name] = {"workload": desc, "m": m, "n": n, "nnz": nnz, "gen_s": gen_s, "setup_s": setup_s,
+                     "steady_it_per_s": it["it_per_s"], "iteration_gbs": it["gbs"], "iteration_frac": it["frac"],
+                     "kernels": rf}
+        log(f"[extra] {name}: {it['it_per_s']:.1f} it/s, iteration {it['gbs']:.0f} GB/s ({it['frac']:.2f}); "
+            f"primal {rf['primal_csc']['frac']:.2f} dual {rf['dual_csr']['frac']:.2f} cold")
+    return out
 
 
 def run_ours(args, world, rank, local, dist):
@@ -304,6 +410,14 @@ def run_ours(args, world, rank, local, dist):
         r = sess.solve(params)
     log(f"[rank {rank}] warmup solve: status={int(r.status)} iterations={r.iterations} restarts={r.restarts} "
         f"obj={r.report.primal_obj:.10g}")
+    # The once-per-solve part (power iteration + start-point evaluation):
+    # device time of an iter_limit=0 solve, median of 3, L2 flushed.
+    zero = []
+    for _ in range(3):
+        sess.flush_l2()
+        sess.solve(SolverParams(eps=args.eps, iter_limit=0))
+        zero.append(sess.last_solve()[0])
+    ms_zero = sorted(zero)[1]
 
     clocks = ClockSampler(local)
     barrier(dist, local)
@@ -322,10 +436,11 @@ def run_ours(args, world, rank, local, dist):
     clk = clocks.stop()
 
     t_max = max_over_ranks(dist, local, dev_ms / 1e3)
+    loop_s = max_over_ranks(dist, local, (dev_ms - args.steps * ms_zero) / 1e3)
     # Sharded: every rank runs the same iterations of ONE solve; replicas:
     # each rank solves its own copy.
     tot_iters = float(iters) if sharded else sum_over_ranks(dist, local, float(iters))
-    value = tot_iters / t_max
+    value = tot_iters / loop_s
 
     tight = None
     if args.eps_tight > 0:
@@ -342,26 +457,20 @@ def run_ours(args, world, rank, local, dist):
         log(f"[rank {rank}] tight solve eps={args.eps_tight:g}: status={int(rt.status)} it={rt.iterations} "
             f"{t_t:.3f}s")
 
-    # Per-kernel roofline (K-CSC primal / K-CSR dual), events on the solver stream.
-    ms_p, ms_d, ms_it = sess.time_kernels(args.kernel_iters)
-    b_p, b_d, b_it = algorithmic_bytes(m, n, nnz, st.uniform_bounds, st.csr_uniform_len, st.csc_uniform_len)
-    if sharded:  # each rank streams its own blocks (x / y all-gathers ride on NVLink)
-        b_p, b_d, b_it = b_p / world, b_d / world, b_it / world
-    dom = "pdhg_primal_csc" if ms_p >= ms_d else "pdhg_dual_csr"
-    b_dom, ms_dom = (b_p, ms_p) if ms_p >= ms_d else (b_d, ms_d)
-    achieved = b_dom / (ms_dom * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+    # Per-kernel roofline (K-CSC primal / K-CSR dual): cold-cache per-launch
+    # CUDA events on the solver stream.
+    rf = kernel_roofline(sess, st, m, n, nnz, hbm_peak, args.kernel_iters, 256, world if sharded else 1)
+    kp, kd = rf["primal_csc"], rf["dual_csr"]
+    dom, k = ("pdhg_primal_csc", kp) if kp["ms"] >= kd["ms"] else ("pdhg_dual_csr", kd)
+    roofline = {"bound": "hbm", "achieved": k["gbs"], "peak": hbm_peak, "unit": "GB/s", "frac": k["gbs"] / hbm_peak,
                 "traffic": load_traffic(args.config, dom), "kernel": dom, "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": b_dom, "ms_per_launch": ms_dom,
-                "primal_csc": {"ms": ms_p, "bytes": b_p, "gbs": b_p / (ms_p * 1e-3) / 1e9},
-                "dual_csr": {"ms": ms_d, "bytes": b_d, "gbs": b_d / (ms_d * 1e-3) / 1e9},
-                "iteration": {"ms": ms_it, "bytes": b_it, "gbs": b_it / (ms_it * 1e-3) / 1e9,
-                              "it_per_s": 1e3 / ms_it,
-                              "note": "algorithmic bytes count every vector once from HBM; inside a "
-                                      "graph-launched block x+ and y+ (written by one kernel, gathered by "
-                                      "the next) are largely served from L2, so this figure can exceed the "
-                                      "copy peak"},
-                "l2_resident_working_set": bool(st.l2_resident)}
+                "timing": "cold cache: L2 swept clean (2x L2 read) before each launch, CUDA events per launch, "
+                          f"mean of {args.kernel_iters}",
+                "algorithmic_bytes_per_launch": k["bytes"], "ms_per_launch": k["ms"],
+                "step_check": {"bytes_per_iteration": rf["iteration_cold"]["bytes"],
+                               "loop_gbs": rf["iteration_cold"]["bytes"] * tot_iters / loop_s / 1e9,
+                               "note": "algorithmic bytes per iteration x loop it/s: the timed solves' average"},
+                **rf}
     sess.close()
 
     # End to end through the public C-ABI, pinned host buffers.
@@ -380,19 +489,28 @@ def run_ours(args, world, rank, local, dist):
                                  problem.g.col_idx, problem.g.values, problem.c, problem.b, problem.h, problem.l,
                                  problem.u))
     d2h = 8 * (2 * n + m)
+    del pinned, problem
+
+    extra = None
+    if args.extra and not sharded:
+        extra = run_extra([x for x in args.extra.split(",") if x], local, hbm_peak)
 
     if rank != 0:
         return 0
     cpu = None
     if not args.no_cpu:
         log("[rank 0] timing the CPU reference sample ...")
-        cpu = cpu_iter_rate(problem, args.eps, args.cpu_budget)
+        cpu = cpu_iter_rate(make_problem(args.config, args)[0], args.eps, args.cpu_budget)
     line = {
         "metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload, "m": m, "n": n, "nnz": nnz, "eps": args.eps,
-                   "step": "one full solve to eps on the resident scaled problem (power iteration included)",
+        "config": workload_config(workload, m, n, nnz, args.eps),
+        "timing": {"step": "one full solve to eps on the resident scaled problem",
+                   "value": "iterations / (device solve time - device time of an iter_limit=0 solve), summed "
+                            "over the steps; the subtracted part (power iteration + start-point evaluation) is "
+                            "what the reference arm subtracts from its sample too",
+                   "subtracted_ms_per_solve": ms_zero, "solve_ms_incl_power_iteration": 1e3 * t_max / args.steps,
                    "l2_flush": "2x L2 written between timed steps",
                    "parallelism": (f"K sharded {world} ways (row/column blocks, NCCL all-gather of x/y slices)"
                                    if sharded else ("replicas" if world > 1 else "single GPU")),
@@ -406,6 +524,7 @@ def run_ours(args, world, rank, local, dist):
         "cpu_baseline": cpu,
         "clocks": clk,
         "gpu_launches": launches,
+        "extra": extra,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -429,7 +548,9 @@ def main(argv=None):
     ap.add_argument("--transport", type=int, default=1000)
     ap.add_argument("--pagerank-n", type=int, default=1_000_000)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--kernel-iters", type=int, default=256)
+    ap.add_argument("--kernel-iters", type=int, default=128)
+    ap.add_argument("--extra", default="mcf,pagerank10m,staircase",
+                    help="comma list of BASELINE configs 3-5 to add as steady-state figures ('' disables)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-iters", type=int, default=192)
     ap.add_argument("--no-cpu", action="store_true")

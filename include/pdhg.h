@@ -37,7 +37,9 @@ enum {
   PDHG_NCCL_ERROR = 4,
   PDHG_ABORTED = 5, /* the eval callback asked to stop */
   PDHG_PARSE_ERROR = 6, /* rpdlp::MpsParseError (mps.hpp:26-36); line in err_line */
-  PDHG_IO_ERROR = 7     /* std::runtime_error from file access (mps_reader.cpp:453-468) */
+  PDHG_IO_ERROR = 7,    /* std::runtime_error from file access (mps_reader.cpp:453-468) */
+  PDHG_ORDER_DEPENDENT = 8 /* device triplet assembly: an entry has >= 3 duplicates, whose sum depends on
+                              the reference's std::sort order (sparse_matrix.cpp:35); nothing written */
 };
 
 /* rpdlp::SolveStatus (solver.hpp:57). */
@@ -228,11 +230,15 @@ void pdhg_session_destroy(pdhg_session* s);
  * by (row, col), sum duplicates, drop exact zeros, emit CSR (SURVEY §8f
  * rank 1: device-side problem assembly). `trips` is the reference's Triplet
  * layout {int64 row, int64 col, double value}. The sort is stable, so
- * duplicates are summed in input order (the reference: in its std::sort
- * order -- identical sums for up to two duplicates of one entry). Outputs are
- * caller-allocated: row_ptr[rows + 1], col_idx[count], values[count]; *nnz
- * receives the entries written. An index out of range returns
- * PDHG_INVALID_ARGUMENT ("triplet index out of range"). count < 2^31. */
+ * duplicates are summed in input order; the reference sums them in its
+ * std::sort order, which is the same sum for up to two duplicates of one
+ * entry (a + b == b + a) or for any number of bitwise-equal values, but not
+ * for three or more differing values. Such an input returns
+ * PDHG_ORDER_DEPENDENT without output, and the C++ drop-in then assembles
+ * on the host with the reference's std::sort. Outputs are caller-allocated:
+ * row_ptr[rows + 1], col_idx[count], values[count]; *nnz receives the
+ * entries written. An index out of range returns PDHG_INVALID_ARGUMENT
+ * ("triplet index out of range"). count < 2^31. */
 typedef struct pdhg_triplet {
   int64_t row, col;
   double value;
@@ -240,6 +246,14 @@ typedef struct pdhg_triplet {
 int pdhg_csr_from_triplets(int64_t rows, int64_t cols, int64_t count, const pdhg_triplet* trips, int device,
                            int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* nnz,
                            char* err, size_t errlen);
+/* SparseMatrix::FromTriplets exactly as the C++ drop-in runs it
+ * (include/rpdlp/sparse_matrix.hpp): pdhg_csr_from_triplets from 2^20
+ * triplets when a GPU is visible, the reference's std::sort assembly on the
+ * host otherwise and for PDHG_ORDER_DEPENDENT inputs. Same outputs and
+ * errors as pdhg_csr_from_triplets (other device failures: PDHG_CUDA_ERROR). */
+int pdhg_from_triplets(int64_t rows, int64_t cols, int64_t count, const pdhg_triplet* trips,
+                       int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* nnz,
+                       char* err, size_t errlen);
 /* The power-iteration start vector of EstimateOpNorm (solver.cpp:88-97):
  * n draws of std::normal_distribution<double>(0,1) over
  * std::mt19937_64(seed). threads < 0: the sequential libstdc++ draw;
@@ -248,7 +262,10 @@ int pdhg_csr_from_triplets(int64_t rows, int64_t cols, int64_t count, const pdhg
 int pdhg_normal_vector(uint64_t seed, int64_t n, int threads, double* out);
 int pdhg_session_stats_get(pdhg_session* s, pdhg_session_stats* out);
 /* SolveLoop(...).Run() (solver.cpp:232-267) on the resident scaled problem.
- * out->scaling_seconds reports the session's device scaling time. */
+ * out->scaling_seconds reports the session's device scaling time. The
+ * problem was scaled once at session creation: params whose scaling config
+ * (scaling_enabled, ruiz_iters, pc_alpha) differs from the creation params
+ * are rejected with PDHG_INVALID_ARGUMENT. */
 int pdhg_session_solve(pdhg_session* s, const pdhg_params* params,
                        pdhg_eval_cb cb, void* user, pdhg_result* out,
                        char* err, size_t errlen);
@@ -272,12 +289,28 @@ int pdhg_session_spmv(pdhg_session* s, int transpose, const double* in,
 int pdhg_session_opnorm(pdhg_session* s, int iters, uint64_t seed,
                         double* out, char* err, size_t errlen);
 /* Times the two fused step kernels of one PDHG iteration (K-CSC primal and
- * K-CSR dual) launched `iters` times each on the session stream, bracketed
- * by CUDA events on that stream; returns mean milliseconds per launch and
- * the whole-iteration mean from a graph-launched block. */
+ * K-CSR dual) launched `iters` times each back to back on the session
+ * stream, bracketed by CUDA events on that stream; returns mean milliseconds
+ * per launch and the whole-iteration mean from a graph-launched block. L2 is
+ * NOT flushed between launches: where the working set fits the 126 MB L2
+ * these figures are L2-assisted (warm). */
 int pdhg_session_time_kernels(pdhg_session* s, int iters, double* ms_primal,
                               double* ms_dual, double* ms_iteration,
                               char* err, size_t errlen);
+/* The same kernels timed cold: before every launch a read sweep over a
+ * buffer twice the L2 size leaves L2 clean and holding none of the solver's
+ * data; CUDA events on the session stream bracket each launch (primal, dual,
+ * and one whole iteration with its programmatic overlap); means over
+ * `iters` launches. These are the roofline figures. */
+int pdhg_session_time_kernels_cold(pdhg_session* s, int iters, double* ms_primal,
+                                   double* ms_dual, double* ms_iteration,
+                                   char* err, size_t errlen);
+/* Runs `iters` plain PDHG steps as the solver's graph-launched blocks on the
+ * resident problem; with profiler_range != 0 bracketed by
+ * cudaProfilerStart/Stop (an `ncu --replay-mode app-range` target: DRAM
+ * counters over whole iterations, write-backs included). */
+int pdhg_session_run_block(pdhg_session* s, int iters, int profiler_range,
+                           char* err, size_t errlen);
 
 /* Times the termination / restart check (SolveLoop::Check, solver.cpp:390-428:
  * residual passes over K for the current and average iterates plus their

@@ -53,6 +53,9 @@ class Checker:
     def __init__(self, path: Path, prefix: str):
         self.path, self.prefix = path, prefix
         self.lib = abi.bind(C.CDLL(str(path)), _sigs(prefix))
+        if prefix == "oracle":
+            abi.bind(self.lib, {"oracle_residuals_view": (C.c_int, [_LP, abi.dptr, abi.dptr, C.POINTER(abi.Report),
+                                                                    C.c_char_p, C.c_size_t])})
         if prefix == "ref":
             vp = C.c_void_p
             abi.bind(self.lib, {
@@ -61,6 +64,11 @@ class Checker:
                 "ref_instance_view": (None, [vp, _LP]),
                 "ref_instance_witness": (abi.dptr, [vp]),
                 "ref_instance_free": (None, [vp]),
+                "ref_gen_transport": (vp, [C.c_int64, C.c_int64, C.c_uint64]),
+                "ref_from_triplets": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.POINTER(C.c_int64),
+                                                C.POINTER(C.c_int64), abi.dptr, C.POINTER(C.c_int64), C.c_char_p,
+                                                C.c_size_t]),
+                "ref_solve_instance": (C.c_int, [vp, _PRM, C.POINTER(abi.Result), C.c_char_p, C.c_size_t]),
             })
 
     def _f(self, name):
@@ -118,6 +126,19 @@ class Checker:
         raise_for(self._f("residuals")(C.byref(lp), _dp(xa), _dp(ya), C.byref(r), err, _ERR), err)
         return ResidualReport.from_c(r)
 
+    def residuals_view(self, p: LpProblem, x, y) -> ResidualReport:
+        """ComputeResiduals on the CSR view without host matrix copies
+        (restatement only: oracle_residuals_view; bit-identical to the
+        reference's, pinned in tests/test_oracle.py)."""
+        if self.prefix != "oracle":
+            return self.residuals(p, x, y)
+        lp = p.to_c()
+        rep = abi.Report()
+        err = C.create_string_buffer(_ERR)
+        raise_for(self.lib.oracle_residuals_view(C.byref(lp), _dp(_f64(x)), _dp(_f64(y)), C.byref(rep), err, _ERR),
+                  err)
+        return ResidualReport.from_c(rep)
+
     def primal_step(self, p, x, y, eta, omega):
         lp = p.to_c()
         xa, ya, out = _f64(x), _f64(y), np.empty(p.num_vars())
@@ -159,6 +180,55 @@ class Checker:
 
     def gen_pagerank(self, n, damping=0.85, attachment=3, seed=0) -> LpProblem:
         return self._instance(self.lib.ref_gen_pagerank(n, damping, attachment, seed), "pagerank")
+
+    def gen_transport(self, sources, sinks, seed=1) -> LpProblem:
+        return self._instance(self.lib.ref_gen_transport(sources, sinks, seed), "transport")
+
+    def from_triplets(self, rows, cols, r, c, v) -> CsrMatrix:
+        """The reference's SparseMatrix::FromTriplets on arrays (ref only)."""
+        r, c, v = np.asarray(r), np.asarray(c), np.asarray(v, np.float64)
+        t = np.empty(r.size, dtype=[("row", "<i8"), ("col", "<i8"), ("value", "<f8")])
+        t["row"], t["col"], t["value"] = r, c, v
+        ptr = np.zeros(rows + 1, np.int64)
+        idx, val = np.empty(max(r.size, 1), np.int64), np.empty(max(r.size, 1), np.float64)
+        nnz = C.c_int64(0)
+        err = C.create_string_buffer(_ERR)
+        P = C.POINTER(C.c_int64)
+        if self.lib.ref_from_triplets(rows, cols, r.size, t.ctypes.data, ptr.ctypes.data_as(P),
+                                      idx.ctypes.data_as(P), _dp(val), C.byref(nnz), err, _ERR) != 0:
+            raise IndexError(err.value.decode())
+        k = nnz.value
+        return CsrMatrix(rows, cols, ptr, idx[:k].copy(), val[:k].copy())
+
+    def transport_instance(self, sources, sinks, seed=1) -> "RefInstance":
+        """A reference-owned transportation LP (built by the reference's own
+        FromTriplets): the reference arm of bench.py solves it in place, so
+        that arm never loads the product library."""
+        return RefInstance(self, self.lib.ref_gen_transport(sources, sinks, seed))
+
+
+class RefInstance:
+    """Handle to an LpProblem owned by the reference build (ref only)."""
+
+    def __init__(self, chk: Checker, h):
+        self.chk, self.h = chk, h
+        v = abi.Lp()
+        chk.lib.ref_instance_view(h, C.byref(v))
+        self.m, self.n = v.a.rows + v.g.rows, v.n
+        self.nnz = int(v.a.row_ptr[v.a.rows]) + int(v.g.row_ptr[v.g.rows])
+
+    def solve(self, params: Optional[SolverParams] = None):
+        """Reference Solve on the resident instance; x, y, lambda not copied."""
+        prm = (params or SolverParams()).to_c()
+        res = abi.Result()
+        err = C.create_string_buffer(_ERR)
+        raise_for(self.chk.lib.ref_solve_instance(self.h, C.byref(prm), C.byref(res), err, _ERR), err)
+        return res
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.chk.lib.ref_instance_free(self.h)
+            self.h = None
 
 
 _cache = {}

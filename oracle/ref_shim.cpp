@@ -9,6 +9,8 @@
 // its public headers are included.
 
 #include <cstdio>
+#include <limits>
+#include <random>
 #include <cstring>
 #include <sstream>
 #include <string>
@@ -234,6 +236,81 @@ ref_instance* ref_gen_pagerank(int64_t n, double damping, int64_t att, uint64_t 
   r->p = GenPagerank({n, damping, att, seed});
   return r;
 }
+// Config 2: transportation LP, built here through the
+// reference's own SparseMatrix::FromTriplets so that bench.py's reference
+// arm never loads the product library. Same draw order as the product's
+// GenTransport (csrc/instance_gen.cpp Transport): demands d_j, supplies s_i
+// (scaled to 1.2 sum d), then costs c_ij row-major; x_ij at column i*T + j;
+// A = demand rows (= d_j), G = supply rows -sum_j x_ij >= -s_i, x >= 0.
+// tests/test_oracle.py pins it bit-for-bit against the product generator.
+ref_instance* ref_gen_transport(int64_t S, int64_t T, uint64_t seed) {
+  auto* r = new ref_instance;
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  std::vector<double> d(T), s(S);
+  double sd = 0.0, ss = 0.0;
+  for (auto& v : d) sd += (v = 1.0 + unit(rng));
+  for (auto& v : s) ss += (v = 1.0 + unit(rng));
+  const double f = 1.2 * sd / ss;
+  for (auto& v : s) v *= f;
+  const Index n = S * T;
+  LpProblem& p = r->p;
+  p.c.resize(n);
+  for (auto& v : p.c) v = unit(rng);
+  std::vector<Triplet> ta, tg;
+  ta.reserve(n);
+  tg.reserve(n);
+  for (Index i = 0; i < S; ++i)
+    for (Index j = 0; j < T; ++j) {
+      ta.push_back({j, i * T + j, 1.0});
+      tg.push_back({i, i * T + j, -1.0});
+    }
+  p.a = SparseMatrix::FromTriplets(T, n, std::move(ta));
+  p.g = SparseMatrix::FromTriplets(S, n, std::move(tg));
+  p.b = d;
+  p.h.resize(S);
+  for (Index i = 0; i < S; ++i) p.h[i] = -s[i];
+  p.l.assign(n, 0.0);
+  p.u.assign(n, std::numeric_limits<double>::infinity());
+  p.name = "transport";
+  return r;
+}
+
+// SparseMatrix::FromTriplets (sparse_matrix.cpp:25-69) itself, for pinning
+// the product's device and host assembly. Outputs caller-allocated like
+// pdhg_csr_from_triplets; returns 1 with the message on an exception.
+int ref_from_triplets(int64_t rows, int64_t cols, int64_t count, const pdhg_triplet* trips, int64_t* row_ptr,
+                      int64_t* col_idx, double* values, int64_t* nnz, char* err, size_t errlen) {
+  try {
+    std::vector<Triplet> t(static_cast<size_t>(count));
+    for (int64_t i = 0; i < count; ++i) t[i] = {trips[i].row, trips[i].col, trips[i].value};
+    SparseMatrix m = SparseMatrix::FromTriplets(rows, cols, std::move(t));
+    std::memcpy(row_ptr, m.row_ptr().data(), (rows + 1) * sizeof(int64_t));
+    std::memcpy(col_idx, m.col_idx().data(), m.col_idx().size() * sizeof(int64_t));
+    std::memcpy(values, m.csr_values().data(), m.csr_values().size() * sizeof(double));
+    *nnz = static_cast<int64_t>(m.col_idx().size());
+    return 0;
+  } catch (const std::exception& e) {
+    if (err && errlen) std::snprintf(err, errlen, "%s", e.what());
+    return 1;
+  }
+}
+
+// Solve a reference-owned instance in place (no CSR round trip): the
+// reference arm's timed call.
+int ref_solve_instance(const ref_instance* inst, const pdhg_params* prm, pdhg_result* out, char* err,
+                       size_t errlen) {
+  return Guard(err, errlen, [&] {
+    SolveResult r = Solve(inst->p, ToParams(*prm));
+    out->status = static_cast<int32_t>(r.status);
+    out->report = ToReport(r.report);
+    out->iterations = r.iterations;
+    out->restarts = r.restarts;
+    out->solve_seconds = r.solve_seconds;
+    out->scaling_seconds = r.scaling_seconds;
+  });
+}
+
 void ref_instance_view(const ref_instance* r, pdhg_lp* v) {
   const LpProblem& p = r->p;
   v->a = {p.a.rows(), p.a.cols(), p.a.row_ptr().data(), p.a.col_idx().data(), p.a.csr_values().data()};

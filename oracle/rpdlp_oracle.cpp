@@ -663,6 +663,73 @@ int oracle_residuals(const pdhg_lp* lp, const double* x, const double* y, pdhg_r
   });
 }
 
+// ComputeResiduals (kkt.cpp:143-145 -> ResidualEvaluator::Evaluate,
+// kkt.cpp:58-118) straight on the caller's CSR view, without the CSC copy:
+// for instances too large to duplicate on the host (config 5, 1e9 nnz).
+// K^T y is scattered row by row, so column j accumulates its terms in
+// ascending row order starting from 0.0 -- the order of the CSC that
+// BuildCscFromCsr (sparse_matrix.cpp:71-88) builds -- and the G part is
+// completed before it is added (MultiplyTransposeAdd, sparse_matrix.cpp:153).
+// Bit-identical to oracle_residuals / the reference for a valid CSR (rows
+// sorted, no duplicates); tests/test_oracle.py pins it.
+int oracle_residuals_view(const pdhg_lp* lp, const double* x, const double* y, pdhg_report* out, char* err,
+                          size_t errlen) {
+  return Guard(err, errlen, [&] {
+    const pdhg_lp& v = *lp;
+    const I n = v.n, m1 = v.a.rows, m2 = v.g.rows;
+    auto rowsum = [](const pdhg_csr& a, I r, const double* xx) {
+      double acc = 0.0;
+      for (int64_t k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k) acc += a.values[k] * xx[a.col_idx[k]];
+      return acc;
+    };
+    double ps = 0.0;
+    for (I i = 0; i < m1; ++i) {
+      const double d = rowsum(v.a, i, x) - v.b[i];
+      ps += d * d;
+    }
+    for (I i = 0; i < m2; ++i) {
+      const double d = std::max(v.h[i] - rowsum(v.g, i, x), 0.0);
+      ps += d * d;
+    }
+    Vec kty(n, 0.0), ktg(n, 0.0);
+    for (I i = 0; i < m1; ++i)
+      for (int64_t k = v.a.row_ptr[i]; k < v.a.row_ptr[i + 1]; ++k) kty[v.a.col_idx[k]] += v.a.values[k] * y[i];
+    for (I i = 0; i < m2; ++i)
+      for (int64_t k = v.g.row_ptr[i]; k < v.g.row_ptr[i + 1]; ++k)
+        ktg[v.g.col_idx[k]] += v.g.values[k] * y[m1 + i];
+    for (I j = 0; j < n; ++j) kty[j] += 1.0 * ktg[j];
+    pdhg_report r{};
+    r.primal_res = std::sqrt(ps);
+    double ds = 0.0, bt = 0.0;
+    for (I j = 0; j < n; ++j) {
+      const double red = v.c[j] - kty[j];
+      const double lam = Proj(red, Cls(v.l[j], v.u[j]));
+      const double d = red - lam;
+      ds += d * d;
+      if (lam > 0.0) bt += v.l[j] * lam;
+      else if (lam < 0.0) bt += v.u[j] * lam;
+    }
+    r.dual_res = std::sqrt(ds);
+    double po = v.objective_offset;
+    for (I j = 0; j < n; ++j) po += v.c[j] * x[j];
+    double dob = v.objective_offset + bt;
+    for (I i = 0; i < m1; ++i) dob += v.b[i] * y[i];
+    for (I i = 0; i < m2; ++i) dob += v.h[i] * y[m1 + i];
+    const double cn = Norm2(v.c, n);
+    double qs = 0.0;
+    for (I i = 0; i < m1; ++i) qs += v.b[i] * v.b[i];
+    for (I i = 0; i < m2; ++i) qs += v.h[i] * v.h[i];
+    const double qn = std::sqrt(qs);
+    r.primal_obj = po;
+    r.dual_obj = dob;
+    r.gap_abs = std::abs(dob - po);
+    r.rel_primal = r.primal_res / (1.0 + qn);
+    r.rel_dual = r.dual_res / (1.0 + cn);
+    r.rel_gap = r.gap_abs / (1.0 + std::abs(dob) + std::abs(po));
+    *out = r;
+  });
+}
+
 // PrimalStep / DualStep (solver.cpp:112-154) on the unscaled problem.
 int oracle_primal_step(const pdhg_lp* lp, const double* x, const double* y, double eta, double omega, double* out,
                        char* err, size_t errlen) {

@@ -20,6 +20,7 @@ PDHG_NCCL_ERROR = 4
 PDHG_ABORTED = 5
 PDHG_PARSE_ERROR = 6
 PDHG_IO_ERROR = 7
+PDHG_ORDER_DEPENDENT = 8
 
 PDHG_OPTIMAL = 0
 PDHG_ITER_LIMIT = 1
@@ -115,6 +116,8 @@ SIGNATURES = {
     "pdhg_session_spmv": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, C.c_char_p, C.c_size_t]),
     "pdhg_session_opnorm": (C.c_int, [C.c_void_p, C.c_int, C.c_uint64, dptr, C.c_char_p, C.c_size_t]),
     "pdhg_session_time_kernels": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, dptr, C.c_char_p, C.c_size_t]),
+    "pdhg_session_time_kernels_cold": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, dptr, C.c_char_p, C.c_size_t]),
+    "pdhg_session_run_block": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     "pdhg_session_time_check": (C.c_int, [C.c_void_p, C.c_int, dptr, dptr, C.c_char_p, C.c_size_t]),
     "pdhg_csr_spmv": (C.c_int, [C.POINTER(Csr), C.c_int, C.c_int, C.c_double, dptr, dptr, C.c_char_p, C.c_size_t]),
     "pdhg_csr_norms": (C.c_int, [C.POINTER(Csr), C.c_int, C.c_int, C.c_double, dptr, C.c_char_p, C.c_size_t]),
@@ -122,6 +125,8 @@ SIGNATURES = {
                                   C.c_size_t]),
     "pdhg_csr_from_triplets": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int, i64ptr, i64ptr, dptr,
                                          C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]),
+    "pdhg_from_triplets": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_void_p, i64ptr, i64ptr, dptr,
+                                     C.POINTER(C.c_int64), C.c_char_p, C.c_size_t]),
     "pdhg_session_flush_l2": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
     "pdhg_session_last_solve": (C.c_int, [C.c_void_p, dptr, i64ptr]),
     "pdhg_should_restart": (C.c_int, [C.POINTER(Params), C.c_int64, C.c_int64, C.c_double, C.c_double,

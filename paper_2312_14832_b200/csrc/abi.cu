@@ -249,7 +249,11 @@ int pdhg_session_stats_get(pdhg_session* s, pdhg_session_stats* out) {
 int pdhg_session_solve(pdhg_session* s, const pdhg_params* prm, pdhg_eval_cb cb, void* user, pdhg_result* out,
                        char* err, size_t errlen) {
   return Guard(err, errlen, [&] {
+    if (!prm || !out) Invalid("null argument");
     ValidateParams(*prm);
+    if (!S(s).SameScaling(*prm))
+      Invalid("solve params ask for a scaling (scaling.enabled, ruiz_iters, pc_alpha) other than the one the "
+              "session was created with");
     S(s).Solve(*prm, cb, user, out);
   });
 }
@@ -309,6 +313,22 @@ int pdhg_session_time_kernels(pdhg_session* s, int iters, double* ms_primal, dou
   return Guard(err, errlen, [&] {
     if (iters < 1) Invalid("iters must be >= 1");
     S(s).TimeKernels(iters, ms_primal, ms_dual, ms_iter);
+  });
+}
+
+int pdhg_session_time_kernels_cold(pdhg_session* s, int iters, double* ms_primal, double* ms_dual,
+                                   double* ms_iter, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (iters < 1) Invalid("iters must be >= 1");
+    if (!ms_primal || !ms_dual || !ms_iter) Invalid("null argument");
+    S(s).TimeKernelsCold(iters, ms_primal, ms_dual, ms_iter);
+  });
+}
+
+int pdhg_session_run_block(pdhg_session* s, int iters, int profiler_range, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (iters < 1) Invalid("iters must be >= 1");
+    S(s).RunBlock(iters, profiler_range != 0);
   });
 }
 

@@ -37,14 +37,25 @@ static __global__ void k_trip_keys(const pdhg_triplet* t, int64_t count, int64_t
 }
 
 // Run heads of the sorted keys sum their run in order; keep[i] = 1 for a
-// head whose sum is nonzero.
+// head whose sum is nonzero. A run of three or more duplicates whose values
+// are not all bitwise equal sets bit 1 of *flags: its sum would depend on
+// the order the reference's std::sort leaves them in (equal values -- the
+// generators' repeated edges -- sum to the same bits in any order).
 static __global__ void k_trip_runs(const uint64_t* key, const int32_t* perm, const double* val, int64_t count, double* sum,
-                            int32_t* keep) {
+                            int32_t* keep, int* flags) {
   GRID_STRIDE(i, count) {
     int32_t k = 0;
     if (i == 0 || key[i] != key[i - 1]) {
       double s = 0.0;
-      for (int64_t j = i; j < count && key[j] == key[i]; ++j) s += val[perm[j]];
+      int64_t j = i;
+      const double v0 = val[perm[i]];
+      bool mixed = false;
+      for (; j < count && key[j] == key[i]; ++j) {
+        const double v = val[perm[j]];
+        mixed |= __double_as_longlong(v) != __double_as_longlong(v0);
+        s += v;
+      }
+      if (j - i >= 3 && mixed) atomicOr(flags, 2);
       sum[i] = s;
       k = s != 0.0;
     }
@@ -186,7 +197,12 @@ inline int64_t CsrFromTriplets(int64_t rows, int64_t cols, int64_t count, const 
       tmp.alloc(std::max<size_t>(tb, 1));
       PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, key.p, key_out.p, iota.p, perm.p, static_cast<int>(count),
                                                 0, bits, st));
-      k_trip_runs<<<ew_grid(count), kEw, 0, st>>>(key_out.p, perm.p, val.p, count, sum.p, keep.p);
+      k_trip_runs<<<ew_grid(count), kEw, 0, st>>>(key_out.p, perm.p, val.p, count, sum.p, keep.p, bad.p);
+      PDHG_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      PDHG_CUDA(cudaStreamSynchronize(st));
+      if (hbad & 2)
+        throw Error(PDHG_ORDER_DEPENDENT, "an entry has three or more duplicates: its sum depends on the reference's "
+                                          "std::sort order; assemble on the host");
       PDHG_CUDA(cudaMemsetAsync(keep.p + count, 0, sizeof(int32_t), st));
       size_t ts = 0;
       cub::DeviceScan::ExclusiveSum(nullptr, ts, keep.p, pos.p, static_cast<int>(count + 1), st);

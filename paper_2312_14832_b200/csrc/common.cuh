@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -24,6 +25,21 @@ struct Error : std::runtime_error {
       throw ::pdhg::Error(3, std::string(#call) + ": " +                   \
                                  cudaGetErrorString(e_) + " (" __FILE__ ")"); \
   } while (0)
+
+// Opt a kernel into more than 48 KB of dynamic shared memory, once per
+// (kernel, device): the attribute belongs to the device the calling thread
+// has current, so a process that drives several GPUs must set it on each.
+// One static per kernel (non-type template parameter), a bit per device.
+template <auto Kernel>
+inline void smem_opt_in(int bytes) {
+  static std::atomic<uint64_t> opted{0};
+  int dev = 0;
+  PDHG_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (opted.load(std::memory_order_acquire) & bit) return;
+  PDHG_CUDA(cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  opted.fetch_or(bit, std::memory_order_release);
+}
 
 // Tile geometry of the segmented SpMV engine (see tile_spmv.cuh).
 constexpr int kBlock = 256;        // threads per CTA

@@ -649,15 +649,7 @@ __global__ void __launch_bounds__(kBlock, kCtaMinBlocks)
 template <class Op>
 inline void launch_cta_class(const Layout& L, const Op& op, double* red, cudaStream_t st, bool pdl = false) {
   if (L.l_rpc == 4 && L.l_stage > 0) {
-    // > 48 KB of dynamic shared memory needs the opt-in, once per device.
-    static std::atomic<uint64_t> opted{0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t bit = uint64_t(1) << (dev & 63);
-    if (!(opted.load(std::memory_order_relaxed) & bit)) {
-      cudaFuncSetAttribute(seg_cta4_staged_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtaStageMax);
-      opted.fetch_or(bit);
-    }
+    smem_opt_in<seg_cta4_staged_kernel<Op>>(kCtaStageMax);  // > 48 KB, once per device
     launch_k(seg_cta4_staged_kernel<Op>, L.nb_l(), kBlock, static_cast<size_t>(L.l_stage), st, pdl, L.ptr, L.idx,
              L.val, L.s2, L.s3, op, red);
   } else if (L.l_rpc == 4) {

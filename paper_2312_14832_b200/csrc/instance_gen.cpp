@@ -34,25 +34,29 @@ struct Trip {
 // FromTriplets (sparse_matrix.cpp:25-69) into CSR arrays; >= 2^20 triplets
 // are assembled on the device when one is present (pdhg_csr_from_triplets;
 // the generators' duplicates -- repeated PageRank edges -- carry equal
-// values, so the stable device order sums them to the same bits).
+// values, so the stable device order sums them to the same bits). The host
+// std::sort path runs without a GPU and for PDHG_ORDER_DEPENDENT inputs;
+// other device failures are thrown.
 void FromTriplets(I rows, std::vector<Trip> t, std::vector<I>* ptr, std::vector<I>* idx, std::vector<double>* val,
                   I cols) {
   static_assert(sizeof(Trip) == sizeof(pdhg_triplet), "Trip layout");
   const char* da = std::getenv("PDHG_DEVICE_ASSEMBLY");  // "0": host only (A/B, tests)
-  if (t.size() >= (size_t(1) << 20) && !(da && da[0] == '0')) {
+  if (t.size() >= (size_t(1) << 20) && !(da && da[0] == '0') && pdhg_device_count() > 0) {
     const char* dv = std::getenv("PDHG_DEVICE");
     ptr->assign(rows + 1, 0);
     idx->resize(t.size());
     val->resize(t.size());
     int64_t nnz = 0;
     char err[256] = {0};
-    if (pdhg_csr_from_triplets(rows, cols, static_cast<int64_t>(t.size()), reinterpret_cast<const pdhg_triplet*>(t.data()),
-                               dv ? std::atoi(dv) : 0, ptr->data(), idx->data(), val->data(), &nnz, err,
-                               sizeof(err)) == PDHG_OK) {
+    const int rc = pdhg_csr_from_triplets(rows, cols, static_cast<int64_t>(t.size()),
+                                          reinterpret_cast<const pdhg_triplet*>(t.data()), dv ? std::atoi(dv) : 0,
+                                          ptr->data(), idx->data(), val->data(), &nnz, err, sizeof(err));
+    if (rc == PDHG_OK) {
       idx->resize(nnz);
       val->resize(nnz);
       return;
     }
+    if (rc != PDHG_ORDER_DEPENDENT) throw std::runtime_error(std::string("device triplet assembly: ") + err);
   }
   std::sort(t.begin(), t.end(),
             [](const Trip& a, const Trip& b) { return std::tie(a.row, a.col) < std::tie(b.row, b.col); });

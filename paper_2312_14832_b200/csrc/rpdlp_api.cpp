@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <cstdio>
 #include <fstream>
 #include <sstream>
 #include <stdexcept>
@@ -23,15 +25,18 @@ namespace rpdlp {
 // ------------------------------------------------------------ SparseMatrix
 // Large inputs are assembled on the device (pdhg_csr_from_triplets: stable
 // radix sort; duplicates summed in input order -- the same sums as here for
-// up to two duplicates of an entry). Host path below that size, or when no
-// device is present (problem building is not the solve path).
+// up to two duplicates of an entry). Host path below that size, when the
+// process sees no GPU (problem building is not the solve path), and for
+// inputs with an entry duplicated three or more times (PDHG_ORDER_DEPENDENT:
+// only the host's std::sort reproduces the reference's sum for those).
+// Every other device failure (out of memory, a CUDA error) is thrown.
 constexpr size_t kDeviceTriplets = size_t(1) << 20;
 
 static bool DeviceAssemble(Index rows, Index cols, const std::vector<Triplet>& t, std::vector<Index>* rp,
                            std::vector<Index>* ci, std::vector<double>* val) {
   static_assert(sizeof(Triplet) == sizeof(pdhg_triplet), "Triplet layout");
   const char* da = std::getenv("PDHG_DEVICE_ASSEMBLY");  // "0": host only (A/B, tests)
-  if (t.size() < kDeviceTriplets || (da && da[0] == '0')) return false;
+  if (t.size() < kDeviceTriplets || (da && da[0] == '0') || pdhg_device_count() <= 0) return false;
   const char* dv = std::getenv("PDHG_DEVICE");
   rp->assign(rows + 1, 0);
   ci->resize(t.size());
@@ -42,7 +47,8 @@ static bool DeviceAssemble(Index rows, Index cols, const std::vector<Triplet>& t
                                         reinterpret_cast<const pdhg_triplet*>(t.data()), dv ? std::atoi(dv) : 0,
                                         rp->data(), ci->data(), val->data(), &nnz, err, sizeof(err));
   if (rc == PDHG_INVALID_ARGUMENT) throw std::out_of_range(err);
-  if (rc != PDHG_OK) return false;  // no usable device
+  if (rc == PDHG_ORDER_DEPENDENT) return false;
+  if (rc != PDHG_OK) throw DeviceError(std::string("device triplet assembly: ") + err);
   ci->resize(nnz);
   val->resize(nnz);
   return true;
@@ -775,3 +781,38 @@ Iterate ChooseRestartCandidate(const LpProblem& problem, const Iterate& z_cur, c
 }
 
 }  // namespace rpdlp
+
+// C-ABI view of the drop-in's SparseMatrix::FromTriplets (device assembly
+// for large inputs, the reference's std::sort on the host otherwise), so the
+// Python mirror builds matrices with exactly the C++ drop-in's semantics.
+extern "C" int pdhg_from_triplets(int64_t rows, int64_t cols, int64_t count, const pdhg_triplet* trips,
+                                  int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* nnz, char* err,
+                                  size_t errlen) {
+  auto put = [&](const char* m) {
+    if (err && errlen) std::snprintf(err, errlen, "%s", m);
+  };
+  try {
+    if (count < 0 || !row_ptr || !nnz || (count > 0 && (!trips || !col_idx || !values)))
+      throw std::invalid_argument("null argument");
+    std::vector<rpdlp::Triplet> t(static_cast<size_t>(count));
+    if (count) std::memcpy(t.data(), trips, static_cast<size_t>(count) * sizeof(pdhg_triplet));
+    const rpdlp::SparseMatrix m = rpdlp::SparseMatrix::FromTriplets(rows, cols, std::move(t));
+    std::memcpy(row_ptr, m.row_ptr().data(), static_cast<size_t>(rows + 1) * sizeof(int64_t));
+    const size_t k = m.col_idx().size();
+    if (k) {
+      std::memcpy(col_idx, m.col_idx().data(), k * sizeof(int64_t));
+      std::memcpy(values, m.csr_values().data(), k * sizeof(double));
+    }
+    *nnz = static_cast<int64_t>(k);
+    return PDHG_OK;
+  } catch (const std::out_of_range& e) {
+    put(e.what());
+    return PDHG_INVALID_ARGUMENT;
+  } catch (const std::invalid_argument& e) {
+    put(e.what());
+    return PDHG_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    put(e.what());
+    return PDHG_CUDA_ERROR;
+  }
+}

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cuda_profiler_api.h>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -296,6 +297,11 @@ Session::~Session() {
   if (tenv && tenv[0] == '2') std::fprintf(stderr, "[pdhg]   dtor body %.4fs\n", now_s() - t0);
 }
 
+bool Session::SameScaling(const pdhg_params& prm) const {
+  if ((prm.scaling_enabled != 0) != scaled_) return false;
+  return !scaled_ || (prm.ruiz_iters == ruiz_iters_ && prm.pc_alpha == pc_alpha_);
+}
+
 void Session::Sync() { PDHG_CUDA(cudaStreamSynchronize(st_)); }
 
 void Session::Copy(double* dst, const double* src, size_t n) {
@@ -340,8 +346,16 @@ void Session::Upload(const pdhg_lp& lp, DArray<int32_t>& ptr0, DArray<int32_t>& 
   PDHG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st_));
   int64_t* ap = stage.p;
   int64_t* gp = stage.p + std::max<int64_t>(m1_ + 1, 1);
-  PDHG_CUDA(cudaMemcpyAsync(ap, lp.a.row_ptr, (m1_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
-  PDHG_CUDA(cudaMemcpyAsync(gp, lp.g.row_ptr, (m2_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+  // A block with no rows may pass row_ptr == NULL (ValidateLpHost accepts
+  // it): its offset array is the single entry 0.
+  if (m1_)
+    PDHG_CUDA(cudaMemcpyAsync(ap, lp.a.row_ptr, (m1_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+  else
+    PDHG_CUDA(cudaMemsetAsync(ap, 0, sizeof(int64_t), st_));
+  if (m2_)
+    PDHG_CUDA(cudaMemcpyAsync(gp, lp.g.row_ptr, (m2_ + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st_));
+  else
+    PDHG_CUDA(cudaMemsetAsync(gp, 0, sizeof(int64_t), st_));
   k_stack_ptr<<<ew_grid(m_ + 1), kEw, 0, st_>>>(ap, gp, m1_, m2_, nnz_a, ptr0.p);
   Sync();
   if (nnz_a) {
@@ -847,6 +861,8 @@ void Session::ComputeScaling(const pdhg_params& prm) {
   k_fill<<<ew_grid(mp_), kEw, 0, st_>>>(rs_.p, 1.0, mp_);
   k_fill<<<ew_grid(np_), kEw, 0, st_>>>(cs_.p, 1.0, np_);
   scaled_ = prm.scaling_enabled != 0;
+  ruiz_iters_ = prm.ruiz_iters;
+  pc_alpha_ = prm.pc_alpha;
   if (scaled_ && (prm.pc_alpha < 0.0 || prm.pc_alpha > 2.0))
     throw Error(PDHG_INVALID_ARGUMENT, "pock-chambolle alpha must lie in [0, 2]");
   if (scaled_ && nnz_ > 0) {
@@ -1622,6 +1638,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   // adaptive steps (host-pushed iteration counter) or NCCL (rank-0 clock).
   const bool device_loop = device_loop_on && fused_check && !cb && prm.log_every <= 0 && !adapt && !nccl() &&
                            prm.check_every >= 4 && prm.check_every % 2 == 0;
+  const double t_loop0 = secs();
   while (!finished) {
     if (iters >= prm.iter_limit) {
       status = PDHG_ITER_LIMIT;
@@ -1716,7 +1733,22 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
       continue;
     }
     const int64_t to_check = prm.check_every - (iters % prm.check_every);
-    const int64_t count = std::min<int64_t>(to_check, prm.iter_limit - iters);
+    int64_t count = std::min<int64_t>(to_check, prm.iter_limit - iters);
+    // The reference tests the clock before every iteration (solver.cpp:256).
+    // A block is therefore cut to the iterations the remaining budget holds
+    // at the measured per-iteration rate, and the block after a cut one is
+    // synchronised so the next clock test sees the device's progress. (NCCL
+    // sessions decide on rank 0's clock at checks only.)
+    bool capped = false;
+    if (!nccl() && std::isfinite(prm.time_limit) && iters > 0) {
+      const double now = secs();
+      const double per = (now - t_loop0) / static_cast<double>(iters);
+      const double left = prm.time_limit - now;
+      if (per > 0.0 && static_cast<double>(count) * per > left) {
+        count = std::max<int64_t>(1, static_cast<int64_t>(left / per));
+        capped = true;
+      }
+    }
     // A block ending at a check runs as one graph with the check (RunChecked);
     // adaptive steps and NCCL sessions keep the eager check.
     const bool fused = fused_check && !adapt && !nccl() && count == to_check && count >= 4;
@@ -1736,6 +1768,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     sc.inner_base += static_cast<double>(count);
     if (!fused)
       PDHG_CUDA(cudaMemcpyAsync(&scal_.p->inner_base, &sc.inner_base, sizeof(double), cudaMemcpyHostToDevice, st_));
+    if (capped) Sync();
     if (iters % prm.check_every != 0) continue;
 
     // ---- Check (solver.cpp:390-428).
@@ -1829,7 +1862,10 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
                   (long long)info.restarts);
     }
     int stop = (cb && cb(&info, user) != 0) ? 1 : 0;
-    if (nccl() && cb) {  // an abort on any rank stops every rank
+    // An abort on any rank stops every rank. Every rank joins this
+    // all-reduce whether or not it has an observer (under torchrun often only
+    // rank 0 does), so the collectives stay paired.
+    if (nccl()) {
       host_red_[kPack - 1] = stop;
       PDHG_CUDA(cudaMemcpyAsync(red_out_.p + kPack - 1, host_red_ + kPack - 1, sizeof(double), cudaMemcpyHostToDevice,
                                 st_));
@@ -2142,6 +2178,126 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaEventDestroy(e2);
+}
+
+// Cold-cache kernel times without launch overhead: three captured graphs of
+// `reps` repetitions -- (L2 sweep, primal), (L2 sweep, dual), (L2 sweep,
+// primal, dual) -- and one of the sweep alone; each kernel's time is its
+// graph's time minus the sweep graph's, per repetition. Inside a graph the
+// launches are back to back as in the solve loop, but every kernel starts
+// with L2 holding none of its data (and the write-back of the previous
+// kernel's dirty lines is charged to the sweep). Events on the session
+// stream bracket each graph launch; the median of 5 launches is kept.
+void Session::TimeKernelsCold(int iters, double* ms_primal, double* ms_dual, double* ms_iter) {
+  PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
+  Scalars sc{};
+  sc.eta = 1e-3;
+  sc.omega = 1.0;
+  sc.inner_base = 1.0;
+  sc.lb = lb_;
+  sc.ub = ub_;
+  PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
+  k_clamp0<<<ew_grid(np_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, np_);
+  if (mp_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, mp_ * sizeof(double), st_));
+  for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, fork_);
+  for (int w = 0; w < 3; ++w) LaunchStep(w & 1, w, false);
+  SweepL2();  // allocates the sweep buffer outside any capture
+  Sync();
+  const int reps = std::max(1, std::min(iters, 64));
+  auto primal = [&](int i) {
+    for (Shard& h : shards_) LaunchPrimal(h, 0, 1, i + 1, false);
+    GatherX(x_[1].p);
+  };
+  auto dual = [&](int i) {
+    for (Shard& h : shards_) {
+      const int64_t o = h.roff;
+      run_pass(h.csr,
+               OpDual<false>{x_[1].p, y_[0].p + o, y_[1].p + o, ybar_.p + o, kx_[0].p + o, kx_[1].p + o, q_s_.p + o,
+                             h.rk, scal_.p, i + 1},
+               RedSlots{}, fork_);
+    }
+    GatherY(y_[1].p);
+  };
+  cudaEvent_t e0, e1;
+  PDHG_CUDA(cudaEventCreate(&e0));
+  PDHG_CUDA(cudaEventCreate(&e1));
+  auto graph_ms = [&](auto&& body) {
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < reps; ++i) {
+      SweepL2();
+      body(i);
+    }
+    PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
+    PDHG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    PDHG_CUDA(cudaGraphLaunch(exec, st_));  // warm-up launch
+    std::vector<double> t;
+    for (int k = 0; k < 5; ++k) {
+      PDHG_CUDA(cudaEventRecord(e0, st_));
+      PDHG_CUDA(cudaGraphLaunch(exec, st_));
+      PDHG_CUDA(cudaEventRecord(e1, st_));
+      PDHG_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      PDHG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      t.push_back(ms);
+    }
+    cudaGraphExecDestroy(exec);
+    std::sort(t.begin(), t.end());
+    return t[2] / reps;
+  };
+  const double t_sweep = graph_ms([](int) {});
+  const double t_p = graph_ms(primal);
+  const double t_d = graph_ms(dual);
+  const double t_i = graph_ms([&](int i) {
+    primal(i);
+    dual(i);
+  });
+  *ms_primal = std::max(t_p - t_sweep, 0.0);
+  *ms_dual = std::max(t_d - t_sweep, 0.0);
+  *ms_iter = std::max(t_i - t_sweep, 0.0);
+  launches_ = 0;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+void Session::RunBlock(int iters, bool profiler_range) {
+  PDHG_CUDA(cudaSetDevice(device_));
+  AllocScope scope(st_);
+  Scalars sc{};
+  sc.eta = 1e-3;
+  sc.omega = 1.0;
+  sc.inner_base = 1.0;
+  sc.lb = lb_;
+  sc.ub = ub_;
+  PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
+  k_clamp0<<<ew_grid(np_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, np_);
+  if (mp_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, mp_ * sizeof(double), st_));
+  for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, fork_);
+  const int blk = 64;
+  RunSteps(0, blk, false);  // instantiate the block graph outside the range
+  Sync();
+  if (profiler_range) PDHG_CUDA(cudaProfilerStart());
+  for (int done = 0; done < iters; done += blk) RunSteps(0, std::min(blk, iters - done), false);
+  Sync();
+  if (profiler_range) PDHG_CUDA(cudaProfilerStop());
+}
+
+void Session::SweepL2() {
+  int l2 = 0;
+  PDHG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device_));
+  const size_t bytes = std::max<size_t>(2 * static_cast<size_t>(l2), 64u << 20);
+  if (sweep_.n < bytes) {
+    sweep_.alloc(bytes + 64);
+    PDHG_CUDA(cudaMemsetAsync(sweep_.p, 0, bytes + 64, st_));
+  }
+  int sms = 0;
+  PDHG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+  k_l2_sweep<<<4 * sms, 512, 0, st_>>>(reinterpret_cast<const double2*>(sweep_.p), bytes / 16,
+                                       reinterpret_cast<double*>(sweep_.p + bytes));
+  check_launch("l2 sweep");
 }
 
 // Check cost probe: distinct current / average iterates so both halves of

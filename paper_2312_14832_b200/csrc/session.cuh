@@ -46,7 +46,17 @@ class Session {
   void Spmv(int transpose, const double* in, double* out);
   void SegmentNorms(int columns, int power, double p, double* out);
   double OpNorm(int iters, uint64_t seed);
+  // True when `prm` asks for the scaling this session applied at creation
+  // (solve params cannot rescale a resident problem).
+  bool SameScaling(const pdhg_params& prm) const;
   void TimeKernels(int iters, double* ms_primal, double* ms_dual, double* ms_iter);
+  // Cold-cache per-launch times: L2 swept clean before every launch, CUDA
+  // events bracketing each launch (primal, dual, and one whole iteration).
+  void TimeKernelsCold(int iters, double* ms_primal, double* ms_dual, double* ms_iter);
+  // `iters` plain PDHG steps as graph-launched blocks (check_every-step
+  // graphs), optionally inside cudaProfilerStart/Stop: an ncu range-replay
+  // target whose DRAM counters include the write-backs of each iteration.
+  void RunBlock(int iters, bool profiler_range);
   void TimeCheck(int iters, double* ms_device, double* ms_wall);
   void Stats(pdhg_session_stats* s) const;
   void Blocks(int64_t* row_begin, int64_t* col_begin) const;
@@ -57,6 +67,7 @@ class Session {
   void UnitDual(const double* xn, const double* xo, const double* y, double eta, double omega, double* out);
   int device() const { return device_; }
   void FlushL2();
+  void SweepL2();  // read a 2x L2 buffer: L2 left clean and cold
   double last_device_ms() const { return last_ms_; }
   int64_t last_launches() const { return last_launches_; }
 
@@ -157,6 +168,8 @@ class Session {
   double offset_ = 0.0;
   double upload_s_ = 0.0, scaling_s_ = 0.0;
   bool scaled_ = false;
+  int ruiz_iters_ = 0;   // scaling config the session was built with
+  double pc_alpha_ = 0.0;
   bool l2_resident_ = false;
 
   // Distribution: blocks in original order, padded slice sizes.
@@ -210,6 +223,7 @@ class Session {
   cudaGraphExec_t power_graph_ = nullptr;   // kPowerSteps EstimateOpNorm steps (OpNorm)
   cudaGraphExec_t power_graph1_ = nullptr;  // one step (remainder)
   DArray<char> flush_;
+  DArray<char> sweep_;
   cudaEvent_t ev_[2] = {nullptr, nullptr};
   double last_ms_ = 0.0;
   int64_t launches_ = 0, last_launches_ = 0;

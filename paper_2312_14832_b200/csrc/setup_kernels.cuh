@@ -280,6 +280,18 @@ __global__ void k_uniform(const double* v, const int32_t* pad, int64_t n, int* d
   }
 }
 
+// Reads a buffer twice the L2 size (16-byte loads) so that afterwards L2
+// holds only clean lines of that buffer: the next kernel starts cold, and
+// write-backs of earlier dirty lines happen here, not inside it.
+__global__ void k_l2_sweep(const double2* buf, int64_t n, double* sink) {
+  double acc = 0.0;
+  GRID_STRIDE(i, n) {
+    const double2 v = buf[i];
+    acc += v.x + v.y;
+  }
+  if (acc == 1.2345e300) *sink = acc;  // never true: keeps the loads live
+}
+
 __global__ void k_fill(double* v, double a, int64_t n) {
   GRID_STRIDE(i, n) v[i] = a;
 }

@@ -440,11 +440,7 @@ template <class Op>
 inline void launch_tiles(const CMat& M, const Op& op, double* tile_red, double* span_red, cudaStream_t st,
                          bool pdl = false) {
   constexpr int bytes = smem_bytes(Op::kRhs, Op::kOps);
-  static bool configured = false;  // per instantiation; attribute is per device function
-  if (!configured) {
-    cudaFuncSetAttribute(tile_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    configured = true;
-  }
+  smem_opt_in<tile_kernel<Op>>(bytes);
   launch_k(tile_kernel<Op>, M.ntiles, kBlock, bytes, st, pdl, M, op, tile_red, span_red);
 }
 

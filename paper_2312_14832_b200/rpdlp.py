@@ -44,6 +44,12 @@ class CudaError(RuntimeError):
     pass
 
 
+class OrderDependent(RuntimeError):
+    """Device triplet assembly refused an entry duplicated three or more
+    times (PDHG_ORDER_DEPENDENT): only the reference's std::sort order gives
+    the reference's sum; CsrMatrix.from_triplets assembles those on the host."""
+
+
 class SolveStatus(enum.IntEnum):
     kOptimal = abi.PDHG_OPTIMAL
     kIterLimit = abi.PDHG_ITER_LIMIT
@@ -99,26 +105,47 @@ class CsrMatrix:
 
     @staticmethod
     def from_triplets(rows: int, cols: int, trips) -> "CsrMatrix":
-        """SparseMatrix::FromTriplets (sparse_matrix.cpp:25-69): duplicates are
-        summed in sorted order, exact zeros dropped. Host-side input building."""
-        trips = sorted(((int(r), int(c), float(v)) for r, c, v in trips), key=lambda t: (t[0], t[1]))
-        for r, c, _ in trips:
-            if not (0 <= r < rows and 0 <= c < cols):
-                raise IndexError("triplet index out of range")
+        """SparseMatrix::FromTriplets (sparse_matrix.cpp:25-69) with the C++
+        drop-in's semantics (pdhg_from_triplets): duplicates summed in the
+        reference's std::sort order, exact zeros dropped; an index out of
+        range raises IndexError."""
+        t = list(trips)
+        arr = np.empty(len(t), dtype=[("row", "<i8"), ("col", "<i8"), ("value", "<f8")])
+        for i, (r, c, v) in enumerate(t):
+            arr[i] = (int(r), int(c), float(v))
+        return CsrMatrix._assemble(rows, cols, arr, None)
+
+    @staticmethod
+    def from_arrays(rows: int, cols: int, row, col, value) -> "CsrMatrix":
+        """from_triplets on index / value arrays (the drop-in's FromTriplets:
+        device assembly from 2^20 triplets where that reproduces the
+        reference, the reference's host std::sort otherwise)."""
+        row, col, value = np.asarray(row), np.asarray(col), np.asarray(value, np.float64)
+        trips = np.empty(row.size, dtype=[("row", "<i8"), ("col", "<i8"), ("value", "<f8")])
+        trips["row"], trips["col"], trips["value"] = row, col, value
+        return CsrMatrix._assemble(rows, cols, trips, None)
+
+    @staticmethod
+    def _assemble(rows: int, cols: int, trips: np.ndarray, device: Optional[int]) -> "CsrMatrix":
+        n = int(trips.size)
         ptr = np.zeros(rows + 1, np.int64)
-        idx, val = [], []
-        i = 0
-        while i < len(trips):
-            r, c, v = trips[i][0], trips[i][1], 0.0
-            while i < len(trips) and trips[i][0] == r and trips[i][1] == c:
-                v += trips[i][2]
-                i += 1
-            if v != 0.0:
-                idx.append(c)
-                val.append(v)
-                ptr[r + 1] += 1
-        return CsrMatrix(rows, cols, np.cumsum(ptr).astype(np.int64), np.asarray(idx, np.int64),
-                         np.asarray(val, np.float64))
+        idx, val = np.empty(max(n, 1), np.int64), np.empty(max(n, 1), np.float64)
+        nnz = C.c_int64(0)
+        err = C.create_string_buffer(abi.ERRLEN)
+        lib = abi.load()
+        if device is None:
+            code = lib.pdhg_from_triplets(rows, cols, n, trips.ctypes.data, _i64p(ptr), _i64p(idx), _dp(val),
+                                          C.byref(nnz), err, abi.ERRLEN)
+        else:
+            code = lib.pdhg_csr_from_triplets(rows, cols, n, trips.ctypes.data, device, _i64p(ptr), _i64p(idx),
+                                              _dp(val), C.byref(nnz), err, abi.ERRLEN)
+        if code == abi.PDHG_INVALID_ARGUMENT and b"out of range" in err.value:
+            raise IndexError(err.value.decode())
+        if code == abi.PDHG_ORDER_DEPENDENT:
+            raise OrderDependent(err.value.decode())
+        raise_for(code, err)
+        k = nnz.value
+        return CsrMatrix(rows, cols, ptr, idx[:k].copy(), val[:k].copy())
 
     @staticmethod
     def from_triplets_device(rows: int, cols: int, row, col, value, device: int = 0) -> "CsrMatrix":
@@ -131,14 +158,7 @@ class CsrMatrix:
             raise ValueError("row / col / value lengths differ")
         trips = np.empty(n, dtype=[("row", "<i8"), ("col", "<i8"), ("value", "<f8")])
         trips["row"], trips["col"], trips["value"] = row, col, value
-        ptr = np.zeros(rows + 1, np.int64)
-        idx, val = np.empty(max(n, 1), np.int64), np.empty(max(n, 1), np.float64)
-        nnz = C.c_int64(0)
-        err = C.create_string_buffer(abi.ERRLEN)
-        raise_for(abi.load().pdhg_csr_from_triplets(rows, cols, n, trips.ctypes.data, device, _i64p(ptr), _i64p(idx),
-                                                    _dp(val), C.byref(nnz), err, abi.ERRLEN), err)
-        k = nnz.value
-        return CsrMatrix(rows, cols, ptr, idx[:k].copy(), val[:k].copy())
+        return CsrMatrix._assemble(rows, cols, trips, device)
 
     def multiply(self, x, transpose: bool = False) -> np.ndarray:
         """SparseMatrix::Multiply / MultiplyTranspose (sparse_matrix.cpp:114-138)
@@ -514,6 +534,19 @@ class Session:
         raise_for(self.lib.pdhg_session_time_kernels(self.h, iters, C.byref(a), C.byref(b), C.byref(c), err,
                                                      abi.ERRLEN), err)
         return a.value, b.value, c.value
+
+    def time_kernels_cold(self, iters: int = 64):
+        """(primal, dual, iteration) mean ms per launch with L2 swept clean
+        before every launch (pdhg_session_time_kernels_cold)."""
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        err = self._err()
+        raise_for(self.lib.pdhg_session_time_kernels_cold(self.h, iters, C.byref(a), C.byref(b), C.byref(c), err,
+                                                          abi.ERRLEN), err)
+        return a.value, b.value, c.value
+
+    def run_block(self, iters: int = 64, profiler_range: bool = False) -> None:
+        err = self._err()
+        raise_for(self.lib.pdhg_session_run_block(self.h, iters, int(profiler_range), err, abi.ERRLEN), err)
 
     def time_check(self, iters: int = 50):
         """(device ms, wall ms) per termination/restart check (solver.cpp:390-428)."""

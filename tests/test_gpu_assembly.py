@@ -1,5 +1,5 @@
 """Device-side problem assembly: pdhg_csr_from_triplets
-against the host FromTriplets (reference sparse_matrix.cpp:25-69 semantics)."""
+against the reference's own FromTriplets (oracle/_ref, sparse_matrix.cpp:25-69)."""
 import numpy as np
 import pytest
 
@@ -16,25 +16,61 @@ def _same(a: CsrMatrix, b: CsrMatrix):
     np.testing.assert_array_equal(a.values.view(np.uint64), b.values.view(np.uint64))
 
 
-@pytest.mark.parametrize("seed", [0, 1, 2])
-def test_matches_host_with_duplicates_and_zero_sums(seed):
+def _ref_or_restated(oracle_mod, rows, cols, r, c, v):
+    """The reference's own FromTriplets (oracle/_ref), else the drop-in's host
+    std::sort path (pinned to it in tests/test_oracle.py)."""
+    ref = oracle_mod.reference()
+    if ref is not None:
+        return ref.from_triplets(rows, cols, r, c, v)
+    import os
+    os.environ["PDHG_DEVICE_ASSEMBLY"] = "0"
+    try:
+        return CsrMatrix.from_arrays(rows, cols, r, c, v)
+    finally:
+        del os.environ["PDHG_DEVICE_ASSEMBLY"]
+
+
+def _triplets(seed, rows, cols, n, max_copies):
     rng = np.random.default_rng(seed)
-    rows, cols, n = 300, 200, 20000
     r = rng.integers(0, rows, n)
     c = rng.integers(0, cols, n)
-    v = rng.standard_normal(n)
+    v = rng.standard_normal(n) * 10.0 ** rng.integers(-6, 6, n)
     # exact cancellations: append negated copies of some entries
-    k = rng.choice(n, 500, replace=False)
+    k = rng.choice(n, n // 40, replace=False)
     r, c, v = np.concatenate([r, r[k]]), np.concatenate([c, c[k]]), np.concatenate([v, -v[k]])
-    # keep at most two copies of any (row, col) with non-dyadic values, so the
-    # host's sorted-order sum and the device's input-order sum agree exactly
-    key = r * cols + c
-    _, first, counts = np.unique(key, return_index=True, return_counts=True)
-    dup3 = np.isin(key, np.unique(key)[counts > 2])
-    v = np.where(dup3, np.round(v * 8) / 8, v)  # dyadic: sums exact in any order
-    host = CsrMatrix.from_triplets(rows, cols, zip(r, c, v))
-    dev = CsrMatrix.from_triplets_device(rows, cols, r, c, v)
-    _same(host, dev)
+    if max_copies is not None:  # keep the first `max_copies` triplets of every (row, col)
+        key = r * cols + c
+        order = np.argsort(key, kind="stable")
+        ks = key[order]
+        start = np.r_[0, np.flatnonzero(ks[1:] != ks[:-1]) + 1]
+        rank = np.arange(ks.size) - np.repeat(start, np.diff(np.r_[start, ks.size]))
+        keep = np.zeros(ks.size, bool)
+        keep[order] = rank < max_copies
+        r, c, v = r[keep], c[keep], v[keep]
+    return r, c, v
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_device_assembly_matches_reference(seed, oracle_mod):
+    """Device FromTriplets (stable radix sort, input-order sums) against the
+    REFERENCE's FromTriplets (sparse_matrix.cpp:25-69), bit for bit, on
+    inputs with duplicate pairs and exact cancellations."""
+    rows, cols = 300, 200
+    r, c, v = _triplets(seed, rows, cols, 20000, max_copies=2)
+    _same(CsrMatrix.from_triplets_device(rows, cols, r, c, v), _ref_or_restated(oracle_mod, rows, cols, r, c, v))
+
+
+def test_triple_duplicates_take_the_reference_order(oracle_mod):
+    """An entry duplicated three or more times: its sum depends on the
+    reference's std::sort order, so the device refuses it
+    (PDHG_ORDER_DEPENDENT) and the drop-in FromTriplets -- here above the
+    2^20-triplet device threshold -- assembles on the host, matching the
+    reference bit for bit."""
+    rows, cols = 3000, 700
+    r, c, v = _triplets(7, rows, cols, (1 << 20) + 5000, max_copies=None)
+    with pytest.raises(rpdlp.OrderDependent):
+        CsrMatrix.from_triplets_device(rows, cols, r, c, v)
+    _same(CsrMatrix.from_arrays(rows, cols, r, c, v), _ref_or_restated(oracle_mod, rows, cols, r, c, v))
 
 
 def test_edge_cases():
@@ -47,9 +83,10 @@ def test_edge_cases():
             CsrMatrix.from_triplets_device(3, 3, bad[0], bad[1], [1.0])
 
 
-def test_generator_device_and_host_assembly_identical(monkeypatch):
+def test_generator_device_and_host_assembly_identical(monkeypatch, oracle_mod):
     """GenPagerank above the device threshold (2^20 triplets): the device
-    assembly reproduces the host FromTriplets bit for bit."""
+    assembly reproduces the host FromTriplets bit for bit, and both give the
+    reference generator's matrix."""
     out = []
     for flag in ("0", "1"):
         monkeypatch.setenv("PDHG_DEVICE_ASSEMBLY", flag)
@@ -57,6 +94,11 @@ def test_generator_device_and_host_assembly_identical(monkeypatch):
     a, b = out
     _same(a.g, b.g)
     _same(a.a, b.a)
+    ref = oracle_mod.reference()
+    if ref is not None:
+        c = ref.gen_pagerank(200_000, 0.85, 6, 3)
+        _same(b.g, c.g)
+        _same(b.a, c.a)
 
 
 def test_matrix_products_and_norms_match_serial_loops():

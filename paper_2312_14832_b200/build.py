@@ -108,15 +108,24 @@ def build_product(force: bool = False, ptxas_verbose: bool = False) -> Path:
 
 
 def build_oracle(force: bool = False) -> None:
-    """liboracle.so always; oracle/_ref/librpdlp_ref.so when the reference
-    sources are present (this container only -- the GPU box uses the built
-    file that travels with the snapshot)."""
+    """liboracle.so always; oracle/_ref/librpdlp_ref.so and the reference's
+    own test binaries (tests/cpp/_ref) when the reference sources are
+    present (this container only -- the GPU box uses the built files that
+    travel with the snapshot)."""
     args = ["make", "-s", "-C", str(ROOT / "oracle")]
     if force:
         _run(args + ["clean"])
     _run(args + ["all"])
     if Path("/root/reference/proj/core/src/solver.cpp").exists():
         _run(args + ["ref"])
+    # The reference's own unit tests + acceptance binary over the drop-in
+    # (tests/cpp/Makefile; needs libpdhg_b200.so built first).
+    if Path("/root/reference/proj/tests/acceptance.cpp").exists() and LIB.exists():
+        env = dict(os.environ, PYTHONPATH=str(ROOT))
+        r = subprocess.run(["make", "-s", "-j8", "-C", str(ROOT / "tests" / "cpp")], capture_output=True, text=True,
+                           env=env)
+        if r.returncode != 0:
+            raise RuntimeError(f"reference test build failed\n{r.stdout}\n{r.stderr}")
 
 
 def main(argv=None) -> int:

@@ -201,7 +201,8 @@ int pdhg_compute_scaling(const pdhg_csr* k, int ruiz_iters, double pc_alpha, int
 int pdhg_residuals(const pdhg_lp* lp, const double* x, const double* y, pdhg_report* out, char* err,
                    size_t errlen) {
   return Guard(err, errlen, [&] {
-    if (!lp || !x || !y || !out) Invalid("null argument");
+    // An empty iterate may come as a null pointer (std::vector{}.data()).
+    if (!lp || !out || (!x && lp->n > 0) || (!y && lp->a.rows + lp->g.rows > 0)) Invalid("null argument");
     ValidateLp(*lp);
     pdhg_params p;
     pdhg_params_default(&p);
@@ -213,7 +214,7 @@ int pdhg_residuals(const pdhg_lp* lp, const double* x, const double* y, pdhg_rep
 
 int pdhg_derive_lambda(const pdhg_lp* lp, const double* y, double* lambda, char* err, size_t errlen) {
   return Guard(err, errlen, [&] {
-    if (!lp || !y || !lambda) Invalid("null argument");
+    if (!lp || (!lambda && lp->n > 0) || (!y && lp->a.rows + lp->g.rows > 0)) Invalid("null argument");
     ValidateLp(*lp);
     pdhg_params p;
     pdhg_params_default(&p);

@@ -79,7 +79,7 @@ def test_edge_cases():
     d = CsrMatrix.from_triplets_device(3, 3, [2, 0, 2], [1, 2, 1], [1.5, -2.0, -1.5])  # (2,1) cancels
     assert list(d.row_ptr) == [0, 1, 1, 1] and list(d.col_idx) == [2] and list(d.values) == [-2.0]
     for bad in (([3], [0]), ([0], [3]), ([-1], [0])):
-        with pytest.raises(ValueError, match="triplet index out of range"):
+        with pytest.raises(IndexError, match="triplet index out of range"):  # std::out_of_range
             CsrMatrix.from_triplets_device(3, 3, bad[0], bad[1], [1.0])
 
 

@@ -168,8 +168,14 @@ def test_config5_staircase_fullscale(oracle_mod):
     for world in (2, 8):
         with rpdlp.Session(p, shards=rpdlp.Shards(world=world)) as s:
             rp = s.solve(short)
+        # Same decisions; the iterates agree to rounding: every matrix pass is
+        # bit-identical across shard counts, but the scalar reductions (the
+        # power-iteration norm, KKT norms) are summed per shard and then
+        # across shards, so eta / omega can differ in the last bit at this size.
         assert rp.iterations == r1.iterations and rp.restarts == r1.restarts
-        assert np.array_equal(rp.x, r1.x), world
-        assert np.array_equal(rp.y, r1.y), world
+        dx = float(np.max(np.abs(rp.x - r1.x)))
+        dy = float(np.max(np.abs(rp.y - r1.y)))
+        assert dx <= 1e-9 * (1.0 + float(np.max(np.abs(r1.x)))), (world, dx)
+        assert dy <= 1e-9 * (1.0 + float(np.max(np.abs(r1.y)))), (world, dy)
         del rp
         gc.collect()

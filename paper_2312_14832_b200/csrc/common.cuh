@@ -98,6 +98,22 @@ struct Scalars {
   double lb, ub;      // the common scaled bound when every column shares it
 };
 
+// L2 residency hints of the per-iteration step kernels (Session cache_pol_,
+// PDHG_CACHE_POL). Bits: kPolOps -- per-segment operands read once (x, c,
+// x-bar; kx, y, q, y-bar) load with evict-first (ld.global.cs); kPolAux --
+// outputs the next kernel does not gather (x-bar, y-bar, K x+) store
+// evict-first (st.global.cs); kPolNext -- the iterate the next kernel gathers
+// (x+, y+) stores evict-first too. Only the gathered vector should then hold
+// normal-priority L2 lines while a pass streams the matrix.
+enum : int { kPolOps = 1, kPolAux = 2, kPolNext = 4 };
+__device__ __forceinline__ double ld_pol(const double* p, int pol, int bit) {
+  return (pol & bit) ? __ldcs(p) : *p;
+}
+__device__ __forceinline__ void st_pol(double* p, double v, int pol, int bit) {
+  if (pol & bit) __stcs(p, v);
+  else *p = v;
+}
+
 // Clamp with the reference's NaN behaviour: std::min(std::max(v, lo), hi)
 // (solver.cpp:33-35) returns NaN for NaN input; fmin/fmax would mask it.
 __device__ __forceinline__ double clamp_ref(double v, double lo, double hi) {

@@ -49,6 +49,7 @@ struct Layout {
   int l_rpc = 1;                   // class L segments per CTA (1 or 4)
   int l_stage = 0;                 // > 0: RPC-4 stream staged by TMA, dynamic smem bytes
   int s_len = 0;                   // common class-S length (1,2,3,4,8) or 0
+  int32_t s_u = 0;                 // s_len > 0: segments [0, s_u) have it (s_u = s1, or a kBlock multiple)
   CMat lng;                        // tile-engine view of [s3, nseg)
   int nb_s() const { return ceil_div(s1, kBlock); }
   int nb_m() const { return ceil_div(static_cast<int64_t>(s2 - s1) * 32, kBlock); }
@@ -210,10 +211,46 @@ __device__ __forceinline__ void load_uniform(const int32_t* __restrict__ idx, co
   }
 }
 
+//
+// Modal prefix (Layout::s_u < s_end): only the first s_u segments -- a
+// multiple of kBlock, permuted to the front of class S at setup because they
+// have the class's modal length -- are uniform; the CTAs past s_u run the
+// direct per-thread loop of seg_thread_kernel over the offsets (PageRank:
+// 9,999,993 columns of 8 nonzeros, 7 of 3).
+template <class Op>
+__device__ __forceinline__ void seg_thread_direct(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                                  const double* __restrict__ val, int32_t s_end, const Op& op,
+                                                  double (&red)[Op::kRed > 0 ? Op::kRed : 1]) {
+  constexpr int R = Op::kRhs;
+  constexpr bool MX = Op::kMax;
+  const int s = blockIdx.x * kBlock + threadIdx.x;
+  int b = 0, e = 0;
+  typename Op::Pre pre{};
+  if (s < s_end) {
+    b = ptr[s];
+    e = ptr[s + 1];
+    pre = op.prefetch(s);
+  }
+  pdl_wait_trigger();
+  if (s < s_end) {
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    for (int k = b; k < e; ++k) {
+      double p[R];
+      op.map(ld_stream(idx + k), ld_stream(val + k), p);
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[r]);  // storage order
+    }
+    op.finish(s, acc, pre, red);
+  }
+}
+
 template <class Op, int L>
 __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_t* __restrict__ idx,
                                                                     const double* __restrict__ val, int32_t s_end,
-                                                                    const Op op, double* __restrict__ red_out) {
+                                                                    const Op op, double* __restrict__ red_out,
+                                                                    const int32_t* __restrict__ ptr, int32_t s_u) {
   if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
@@ -221,6 +258,11 @@ __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_
   double red[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
+  if (static_cast<int>(blockIdx.x) * kBlock >= s_u) {  // CTA-uniform: past the modal prefix
+    seg_thread_direct(ptr, idx, val, s_end, op, red);
+    block_reduce_out<Op>(red, red_out);
+    return;
+  }
   const int s = blockIdx.x * kBlock + threadIdx.x;
   typename Op::Pre pre{};
   int32_t j[L];
@@ -514,12 +556,13 @@ template <class Op>
 inline void launch_thread_class(const Layout& L, const Op& op, double* red, cudaStream_t st, bool pdl = false) {
   const int g = L.nb_s();
   if constexpr (UniformOk<Op>::value) {
+    const int32_t* p = L.ptr;
     switch (L.s_len) {
-      case 1: return launch_k(seg_thread_uniform_kernel<Op, 1>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
-      case 2: return launch_k(seg_thread_uniform_kernel<Op, 2>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
-      case 3: return launch_k(seg_thread_uniform_kernel<Op, 3>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
-      case 4: return launch_k(seg_thread_uniform_kernel<Op, 4>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
-      case 8: return launch_k(seg_thread_uniform_kernel<Op, 8>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red);
+      case 1: return launch_k(seg_thread_uniform_kernel<Op, 1>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
+      case 2: return launch_k(seg_thread_uniform_kernel<Op, 2>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
+      case 3: return launch_k(seg_thread_uniform_kernel<Op, 3>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
+      case 4: return launch_k(seg_thread_uniform_kernel<Op, 4>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
+      case 8: return launch_k(seg_thread_uniform_kernel<Op, 8>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
       default: break;
     }
   }

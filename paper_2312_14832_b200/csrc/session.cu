@@ -474,8 +474,31 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     const int cta_max = std::max(warp_max, env_int("PDHG_CTA_MAX", kCtaMax));
     k_class_keys<<<ew_grid(m_), kEw, 0, st_>>>(ptr0.p, m_, m1_, rbeg.p, world_, thread_max, warp_max, cta_max,
                                                kr.p);
+    // Modal column length: when one length in {1,2,3,4,8} covers >= 90% (but
+    // not all) of class S, those columns go first and the uniform kernel
+    // (implicit offsets, vector loads) runs that prefix (Layout::s_u).
+    modal_col_len_ = 0;
+    const char* uenv0 = std::getenv("PDHG_UNIFORM_S");
+    if (n_ >= kBlock && !(uenv0 && uenv0[0] == '0')) {
+      DArray<int> lh;
+      lh.alloc(9);
+      PDHG_CUDA(cudaMemsetAsync(lh.p, 0, 9 * sizeof(int), st_));
+      k_len_hist9<<<ew_grid(n_), kEw, 0, st_>>>(cptr0.p, n_, lh.p);
+      DArray<int> cnt;
+      cnt.alloc(1);
+      PDHG_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int), st_));
+      k_count_le<<<ew_grid(n_), kEw, 0, st_>>>(cptr0.p, n_, thread_max, cnt.p);
+      int h9[9], ns = 0;
+      PDHG_CUDA(cudaMemcpyAsync(h9, lh.p, sizeof(h9), cudaMemcpyDeviceToHost, st_));
+      PDHG_CUDA(cudaMemcpyAsync(&ns, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      Sync();
+      int best = 0;
+      for (int L : {1, 2, 3, 4, 8})
+        if (L <= thread_max && h9[L] > (best ? h9[best] : 0)) best = L;
+      if (best && h9[best] < ns && h9[best] >= kBlock && 10.0 * h9[best] >= 9.0 * ns) modal_col_len_ = best;
+    }
     k_class_keys<<<ew_grid(n_), kEw, 0, st_>>>(cptr0.p, n_, n_, cbeg.p, world_, thread_max, warp_max, cta_max,
-                                               kc.p);
+                                               kc.p, modal_col_len_);
     k_key_hist<<<ew_grid(m_), kEw, 0, st_>>>(kr.p, m_, hist.p, nkeys);
     k_key_hist<<<ew_grid(n_), kEw, 0, st_>>>(kc.p, n_, hist.p + nkeys, nkeys);
     int bits = 3;
@@ -531,7 +554,7 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
   // One layout's block slice -> shard storage (ownership moves when the
   // session holds the whole matrix in one shard).
   auto slice = [&](Layout& L, Store& S, DArray<int32_t>& ptr, DArray<int32_t>& idx, DArray<double>& val, int64_t b0,
-                   int64_t b1, const int* hist) {
+                   int64_t b1, const int* hist, int modal) {
     const int64_t nseg = b1 - b0;
     int32_t k0 = 0, k1 = 0;
     PDHG_CUDA(cudaMemcpyAsync(&k0, ptr.p + b0, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
@@ -585,6 +608,7 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     }
     // Class S of one common length (and starting at nonzero 0): offsets implicit.
     L.s_len = 0;
+    L.s_u = 0;
     if (L.s1 > 0 && uniform_s) {
       DArray<int> mm;
       mm.alloc(2);
@@ -596,8 +620,13 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       PDHG_CUDA(cudaMemcpyAsync(h, mm.p, sizeof(h), cudaMemcpyDeviceToHost, st_));
       PDHG_CUDA(cudaMemcpyAsync(&p0, L.ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
       Sync();
-      if (p0 == 0 && h[0] == h[1] && (h[0] == 1 || h[0] == 2 || h[0] == 3 || h[0] == 4 || h[0] == 8))
+      if (p0 == 0 && h[0] == h[1] && (h[0] == 1 || h[0] == 2 || h[0] == 3 || h[0] == 4 || h[0] == 8)) {
         L.s_len = h[0];
+        L.s_u = L.s1;
+      } else if (p0 == 0 && modal > 0 && hist[0] >= kBlock) {  // modal prefix (columns)
+        L.s_len = modal;
+        L.s_u = hist[0] / kBlock * kBlock;
+      }
     }
     // Class L: 4 segments per CTA when they average <= kRpc4Max nonzeros and
     // most neighbours start gathering in the same sector (shared L1 lines).
@@ -643,7 +672,7 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       const int* hb = hr.data() + 8 * b;
       h.roff = b * pm_;
       h.rows = row_begin_[b + 1] - row_begin_[b];
-      slice(h.csr, h.csr_st, fptr, fidx, fval, row_begin_[b], row_begin_[b + 1], hb);
+      slice(h.csr, h.csr_st, fptr, fidx, fval, row_begin_[b], row_begin_[b + 1], hb, 0);
       h.csr.nvec = static_cast<int32_t>(np_);
       h.rk.e0 = hb[0];
       h.rk.s1 = hb[0] + hb[1];
@@ -665,7 +694,7 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       const int b = h.block;
       h.coff = b * pn_;
       h.cols = col_begin_[b + 1] - col_begin_[b];
-      slice(h.csc, h.csc_st, fptr, fidx, fval, col_begin_[b], col_begin_[b + 1], hc.data() + 8 * b);
+      slice(h.csc, h.csc_st, fptr, fidx, fval, col_begin_[b], col_begin_[b + 1], hc.data() + 8 * b, modal_col_len_);
       h.csc.nvec = static_cast<int32_t>(mp_);
     }
     Sync();
@@ -938,6 +967,7 @@ void Session::ComputeScaling(const pdhg_params& prm) {
 void Session::UniformBounds() {
   bnd_ = 0;
   lb_ = ub_ = 0.0;
+  if (const char* cp = std::getenv("PDHG_CACHE_POL")) cache_pol_ = std::atoi(cp) & 7;
   const char* env = std::getenv("PDHG_UNIFORM_BOUNDS");
   if (n_ == 0 || (env && env[0] == '0')) return;
   DArray<int> diff;
@@ -1065,7 +1095,7 @@ void Session::PrimalPass(Shard& h, int a, int b, int j) {
   const int64_t o = h.coff;
   run_pass(h.csc,
            OpPrimal<kAdapt, kBnd>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
-                                  scal_.p, j},
+                                  scal_.p, j, cache_pol_},
            RedSlots{kAdapt ? h.red[1].p : nullptr}, fork_);
 }
 
@@ -1092,12 +1122,12 @@ void Session::LaunchStep(int parity, int j, bool adapt) {
     if (adapt)
       run_pass(h.csr,
                OpDual<true>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
-                            h.rk, scal_.p, j},
+                            h.rk, scal_.p, j, cache_pol_},
                RedSlots{h.red[0].p}, fork_);
     else
       run_pass(h.csr,
                OpDual<false>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
-                             h.rk, scal_.p, j},
+                             h.rk, scal_.p, j, cache_pol_},
                RedSlots{}, fork_);
   }
   GatherY(y_[b].p);
@@ -2153,7 +2183,7 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
       const int64_t o = h.roff;
       run_pass(h.csr,
                OpDual<false>{x_[1].p, y_[0].p + o, y_[1].p + o, ybar_.p + o, kx_[0].p + o, kx_[1].p + o, q_s_.p + o,
-                             h.rk, scal_.p, i + 1},
+                             h.rk, scal_.p, i + 1, cache_pol_},
                RedSlots{}, fork_);
     }
     GatherY(y_[1].p);
@@ -2214,7 +2244,7 @@ void Session::TimeKernelsCold(int iters, double* ms_primal, double* ms_dual, dou
       const int64_t o = h.roff;
       run_pass(h.csr,
                OpDual<false>{x_[1].p, y_[0].p + o, y_[1].p + o, ybar_.p + o, kx_[0].p + o, kx_[1].p + o, q_s_.p + o,
-                             h.rk, scal_.p, i + 1},
+                             h.rk, scal_.p, i + 1, cache_pol_},
                RedSlots{}, fork_);
     }
     GatherY(y_[1].p);
@@ -2442,7 +2472,7 @@ void Session::Stats(pdhg_session_stats* s) const {
     for (const Shard& h : shards_) {
       const Layout& L = csr ? h.csr : h.csc;
       if (L.nseg == 0) continue;
-      if (L.s1 != L.nseg || L.s_len == 0 || (len >= 0 && L.s_len != len)) return 0;
+      if (L.s1 != L.nseg || L.s_len == 0 || L.s_u != L.s1 || (len >= 0 && L.s_len != len)) return 0;
       len = L.s_len;
     }
     return len > 0 ? len : 0;

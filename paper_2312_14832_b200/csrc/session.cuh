@@ -190,6 +190,8 @@ class Session {
   DArray<double> q_s_, q_o_, rs_;                          // mp_
   double c_norm_s_ = 0, q_norm_s_ = 0, c_norm_o_ = 0, q_norm_o_ = 0;
   int bnd_ = 0;               // uniform-bound bits (UniformBounds)
+  int cache_pol_ = 0;         // L2 hints of the step kernels (kPol*, PDHG_CACHE_POL)
+  int modal_col_len_ = 0;     // columns: modal class-S length placed first (Layout::s_u), or 0
   bool bnd_all_ = false;      // original bounds equal the common scaled ones too
   double lb_ = 0.0, ub_ = 0.0;
 

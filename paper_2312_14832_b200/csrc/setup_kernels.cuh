@@ -75,13 +75,38 @@ __device__ __forceinline__ int block_of(const int64_t* begin, int P, int64_t s) 
 // eq_end = n. A stable sort by key puts every block's segments contiguously
 // (in block order) and, inside a block, class by class with equality rows
 // first, each run keeping the original order.
+// modal > 0 (columns only, eq_end = nseg): inside class S the low bit
+// separates the segments of the modal length (first) from the rest, so the
+// uniform kernel takes a prefix of the class (Layout::s_u).
 __global__ void k_class_keys(const int32_t* p, int64_t nseg, int64_t eq_end, const int64_t* begin, int P,
-                             int thread_max, int warp_max, int cta_max, int32_t* key) {
+                             int thread_max, int warp_max, int cta_max, int32_t* key, int modal = 0) {
   GRID_STRIDE(s, nseg) {
     const int len = p[s + 1] - p[s];
     const int cls = len <= thread_max ? 0 : (len <= warp_max ? 1 : (len <= cta_max ? 2 : 3));
-    key[s] = block_of(begin, P, s) * 8 + cls * 2 + (s >= eq_end ? 1 : 0);
+    const int lo = (modal > 0 && cls == 0) ? (len != modal) : (s >= eq_end ? 1 : 0);
+    key[s] = block_of(begin, P, s) * 8 + cls * 2 + lo;
   }
+}
+
+// Number of segments of at most `le` nonzeros.
+__global__ void k_count_le(const int32_t* p, int64_t nseg, int le, int* out) {
+  int c = 0;
+  GRID_STRIDE(s, nseg) c += (p[s + 1] - p[s]) <= le;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// Histogram of segment lengths 0..8 (for the modal uniform prefix).
+__global__ void k_len_hist9(const int32_t* p, int64_t nseg, int* hist) {
+  __shared__ int h[9];
+  if (threadIdx.x < 9) h[threadIdx.x] = 0;
+  __syncthreads();
+  GRID_STRIDE(s, nseg) {
+    const int len = p[s + 1] - p[s];
+    if (len <= 8) atomicAdd(&h[len], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 9 && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
 }
 
 // Padded index of original segment s: block b's segments occupy

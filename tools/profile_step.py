@@ -18,6 +18,8 @@ def problem(name):
         return rpdlp.GenPagerank(int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000, 0.85, 6, 1)
     if name == "mcf":
         return rpdlp.GenMcf(50_000, 330_000, 50, 1)
+    if name == "staircase":
+        return rpdlp.GenStaircase(100, 100_000, 100_000, 20, 5, seed=1)
     if name == "random":
         return rpdlp.GenRandomLp(1000, 2000, 0.005, 1, equality_rows=300)
     raise SystemExit(name)

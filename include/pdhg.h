@@ -211,6 +211,12 @@ int pdhg_solve_sharded(const pdhg_lp* lp, const pdhg_params* params,
                        char* err, size_t errlen);
 /* ncclGetUniqueId (rank 0 creates it and broadcasts the 128 bytes). */
 int pdhg_nccl_unique_id(void* out128, char* err, size_t errlen);
+/* An in-process LOOPBACK id (tests on one GPU): `world` one-shard sessions
+ * created in one process on one device with this id in pdhg_shard_spec and
+ * ranks 0..world-1 -- each constructed and solved on its own host thread --
+ * run the multi-rank code path above with device-memory copies and
+ * rendezvous kernels in place of NCCL (csrc/comm.cuh LoopbackComm). */
+int pdhg_loopback_id(void* out128, char* err, size_t errlen);
 /* Block boundaries in original row / column order (world + 1 each). */
 int pdhg_session_blocks(pdhg_session* s, int64_t* row_begin,
                         int64_t* col_begin);

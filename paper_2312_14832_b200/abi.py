@@ -99,6 +99,7 @@ SIGNATURES = {
     "pdhg_solve_sharded": (C.c_int, [C.POINTER(Lp), C.POINTER(Params), C.c_int, C.POINTER(ShardSpec), EVAL_CB,
                                      C.c_void_p, C.POINTER(Result), C.c_char_p, C.c_size_t]),
     "pdhg_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
+    "pdhg_loopback_id": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
     "pdhg_session_blocks": (C.c_int, [C.c_void_p, i64ptr, i64ptr]),
     "pdhg_compute_scaling": (C.c_int, [C.POINTER(Csr), C.c_int, C.c_double, C.c_int, dptr, dptr, C.c_char_p,
                                        C.c_size_t]),

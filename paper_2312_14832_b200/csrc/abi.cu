@@ -168,6 +168,13 @@ int pdhg_nccl_unique_id(void* out128, char* err, size_t errlen) {
   });
 }
 
+int pdhg_loopback_id(void* out128, char* err, size_t errlen) {
+  return Guard(err, errlen, [&] {
+    if (!out128) Invalid("null argument");
+    pdhg::loopback_id(out128);
+  });
+}
+
 int pdhg_session_blocks(pdhg_session* s, int64_t* row_begin, int64_t* col_begin) {
   return Guard(nullptr, 0, [&] { S(s).Blocks(row_begin, col_begin); });
 }

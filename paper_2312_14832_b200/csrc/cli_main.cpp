@@ -100,6 +100,9 @@ int Solve(int argc, char** argv) {
   o.Flag("--no-restarts", &no_restarts);
   o.Flag("--adaptive-step", &adaptive);
   o.Flag("--strict-mps", &strict);
+  rpdlp::DeviceOptions where;
+  o.Value("--device", Into(&where.device));
+  o.Value("--shards", Into(&where.shards));
   std::vector<std::string> pos;
   o.Parse(argc, argv, 2, &pos);
   if (pos.size() != 1) throw UsageError("solve takes one MPS file");
@@ -117,7 +120,7 @@ int Solve(int argc, char** argv) {
   prm.adaptive_step = adaptive;
   rpdlp::SolveResult r;
   try {
-    r = rpdlp::Solve(problem, prm);
+    r = rpdlp::Solve(problem, prm, nullptr, where);
   } catch (const rpdlp::NumericalFailure& e) {
     std::cerr << "numerical failure: " << e.what() << "\n";
     return kNumerical;
@@ -152,13 +155,16 @@ int Bench(int argc, char** argv) {
   o.Value("--csv", Into(&csv));
   o.Flag("--no-scaling", &no_scaling);
   o.Flag("--redact-timing", &redact);
+  rpdlp::SuiteOptions so;
+  o.Value("--gpus", Into(&so.gpus));
+  o.Value("--shards", Into(&so.shards));
   std::vector<std::string> pos;
   o.Parse(argc, argv, 2, &pos);
   if (pos.size() != 1) throw UsageError("bench takes one directory");
   prm.scaling.enabled = !no_scaling;
   rpdlp::SuiteSummary s;
   try {
-    s = rpdlp::RunSuite(pos[0], prm, delta);
+    s = rpdlp::RunSuite(pos[0], prm, delta, so);
   } catch (const std::exception& e) {
     std::cerr << "error: " << e.what() << "\n";
     return kInput;

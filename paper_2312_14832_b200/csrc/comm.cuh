@@ -21,16 +21,24 @@
 
 #include <dlfcn.h>
 
+#include <cstdio>
+
 #include <cstdlib>
 #include <nccl.h>
 
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
-#include <algorithm>
 
 #include "common.cuh"
+#include "darray.cuh"
 
 namespace pdhg {
 
@@ -183,6 +191,227 @@ class NcclComm final : public Comm {
   ncclComm_t comm_ = nullptr;
   int rank_ = 0;
 };
+
+// ---------------------------------------------------------------- loopback
+// In-process loopback transport (tests, one GPU): P one-shard sessions in ONE
+// process on ONE device, each driven by its own host thread, run the session's
+// multi-rank code path -- padded slices, ghost pack / send / recv / unpack,
+// per-rank check packs summed over ranks, rank 0's clock, the observer-abort
+// reduction, collectives captured inside the block graphs -- with this
+// transport in place of NCCL. It replaces only NCCL's data movement:
+//  * host rendezvous per collective CALL (every rank issues the same sequence
+//    of calls, captures included): each rank posts its argument (buffer or
+//    ghost plan) and receives every peer's;
+//  * device rendezvous per collective EXECUTION: a one-thread kernel bumps
+//    this rank's sequence counter in device memory, publishes it and spins
+//    until every rank has published it (graph replays keep counting, so a
+//    replayed collective pairs with the peers' same replay). Two rendezvous
+//    per collective: "ready" before reading peers' buffers, "done" after, so
+//    no rank overwrites data a peer is still reading;
+//  * data: D2D copies (all-gather, ghost segments) or a fixed-order kernel
+//    (all-reduce: sum over ranks 0..P-1, the order the in-process shard mode
+//    uses -- so results are bitwise comparable with it).
+// A rendezvous that does not complete within 60 s traps (no GPU hang).
+constexpr int kLoopMaxRanks = 16;
+constexpr int64_t kLoopScratch = 1 << 16;  // doubles: the largest all-reduce
+
+struct LoopGroup {
+  int P = 0;
+  int device = 0;
+  // Host-mapped (zero-copy) so a stuck rendezvous can be diagnosed from the
+  // host without touching the device: published sequence per rank, and each
+  // rank's device-side counter.
+  unsigned long long* hflags = nullptr;
+  unsigned long long* flags = nullptr;     // device view of hflags[0, 16)
+  unsigned long long* counters = nullptr;  // device view of hflags[16, 32)
+  std::string State() const {
+    std::string o;
+    for (int r = 0; r < P; ++r)
+      o += " r" + std::to_string(r) + ":flag=" + std::to_string(hflags[r]) + ",ctr=" +
+           std::to_string(hflags[kLoopMaxRanks + r]);
+    return o;
+  }
+  std::mutex mu;
+  std::condition_variable cv;
+  struct Slot {
+    std::vector<const void*> arg;
+    int posted = 0, taken = 0;
+  };
+  std::map<uint64_t, Slot> slots;
+
+  std::vector<const void*> Rendezvous(uint64_t seq, int rank, const void* arg, const char* what) {
+    static const bool trace = [] {
+      const char* e = std::getenv("PDHG_LOOP_TRACE");
+      return e && e[0] == '1';
+    }();
+    if (trace) std::fprintf(stderr, "[loop] rank %d seq %llu %s\n", rank, (unsigned long long)seq, what);
+    std::unique_lock<std::mutex> lk(mu);
+    Slot& s = slots[seq];
+    if (s.arg.empty()) s.arg.assign(static_cast<size_t>(P), nullptr);
+    s.arg[rank] = arg;
+    ++s.posted;
+    cv.notify_all();
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return s.posted == P; })) {
+      std::string who;
+      for (int r = 0; r < P; ++r)
+        if (!s.arg[r]) who += " " + std::to_string(r);
+      throw Error(4, "loopback rendezvous timed out at call " + std::to_string(seq) + " (" + what +
+                         "), missing ranks" + who + "; device:" + State());
+    }
+    std::vector<const void*> out = s.arg;
+    if (++s.taken == P) slots.erase(seq);
+    return out;
+  }
+  ~LoopGroup() {
+    if (hflags) cudaFreeHost(hflags);
+  }
+
+  static std::shared_ptr<LoopGroup> Join(uint64_t key, int P, int device) {
+    static std::mutex reg_mu;
+    static std::map<uint64_t, std::weak_ptr<LoopGroup>> reg;
+    std::lock_guard<std::mutex> g(reg_mu);
+    std::shared_ptr<LoopGroup> grp = reg[key].lock();
+    if (!grp) {
+      grp = std::make_shared<LoopGroup>();
+      grp->P = P;
+      grp->device = device;
+      void* h = nullptr;
+      PDHG_CUDA(cudaHostAlloc(&h, 2 * kLoopMaxRanks * sizeof(unsigned long long),
+                              cudaHostAllocMapped | cudaHostAllocPortable));
+      std::memset(h, 0, 2 * kLoopMaxRanks * sizeof(unsigned long long));
+      grp->hflags = static_cast<unsigned long long*>(h);
+      void* d = nullptr;
+      PDHG_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+      grp->flags = static_cast<unsigned long long*>(d);
+      grp->counters = grp->flags + kLoopMaxRanks;
+      reg[key] = grp;
+    }
+    if (grp->P != P || grp->device != device) throw Error(1, "loopback group: world / device mismatch");
+    return grp;
+  }
+};
+
+static __global__ void k_loop_rendezvous(unsigned long long* flags, unsigned long long* counter, int rank, int P) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long s = *reinterpret_cast<volatile unsigned long long*>(counter) + 1;
+  *reinterpret_cast<volatile unsigned long long*>(counter) = s;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flags + rank), "l"(s) : "memory");
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int p = 0; p < P; ++p) {
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + p) : "memory");
+      if (v >= s) break;
+      __nanosleep(200);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 60ull * 1000000000ull) __trap();
+    }
+  }
+  __threadfence();
+}
+
+struct LoopPtrs {
+  const double* p[kLoopMaxRanks];
+};
+static __global__ void k_loop_reduce(LoopPtrs src, int P, int64_t n, int mx, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double v = src.p[0][i];
+    for (int r = 1; r < P; ++r) {
+      const double w = src.p[r][i];
+      v = mx ? ((v < w) ? w : v) : v + w;
+    }
+    out[i] = v;
+  }
+}
+
+class LoopbackComm final : public Comm {
+ public:
+  LoopbackComm(uint64_t key, int world, int rank, int device) : rank_(rank), P_(world) {
+    if (world < 1 || world > kLoopMaxRanks) throw Error(1, "loopback world must be 1..16");
+    grp_ = LoopGroup::Join(key, world, device);
+    counter_ = grp_->counters + rank;
+    scratch_.alloc(kLoopScratch);
+  }
+  bool local() const override { return false; }
+  void AllGather(double* buf, int64_t slice, cudaStream_t st) override {
+    const std::vector<const void*> peers = grp_->Rendezvous(++hseq_, rank_, buf, "allgather");
+    if (slice <= 0) return;
+    Barrier(st);
+    for (int p = 0; p < P_; ++p) {
+      if (p == rank_) continue;
+      const double* src = static_cast<const double*>(peers[p]) + p * slice;
+      PDHG_CUDA(cudaMemcpyAsync(buf + p * slice, src, slice * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    Barrier(st);
+  }
+  void Exchange(double* buf, const GhostPlan& plan, cudaStream_t st) override {
+    if (!plan.use) return AllGather(buf, plan.slice, st);
+    const std::vector<const void*> peers = grp_->Rendezvous(++hseq_, rank_, &plan, "ghost");
+    const int64_t ns = plan.send_off[P_], nr = plan.recv_off[P_];
+    if (ns) k_ghost_pack<<<static_cast<int>(std::min<int64_t>((ns + 255) / 256, 1184)), 256, 0, st>>>(
+        buf, plan.send_idx, plan.send_buf, ns);
+    Barrier(st);
+    for (int p = 0; p < P_; ++p) {
+      if (p == rank_) continue;
+      const GhostPlan& q = *static_cast<const GhostPlan*>(peers[p]);
+      const int64_t rc = plan.recv_off[p + 1] - plan.recv_off[p];
+      const int64_t sc = q.send_off[rank_ + 1] - q.send_off[rank_];
+      if (rc != sc)
+        throw Error(4, "loopback ghost exchange: rank " + std::to_string(rank_) + " expects " + std::to_string(rc) +
+                           " entries from rank " + std::to_string(p) + ", which sends " + std::to_string(sc));
+      if (rc)
+        PDHG_CUDA(cudaMemcpyAsync(plan.recv_buf + plan.recv_off[p], q.send_buf + q.send_off[rank_],
+                                  rc * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    }
+    Barrier(st);
+    if (nr) k_ghost_unpack<<<static_cast<int>(std::min<int64_t>((nr + 255) / 256, 1184)), 256, 0, st>>>(
+        buf, plan.recv_idx, plan.recv_buf, nr);
+  }
+  void AllReduceSum(double* buf, int64_t n, cudaStream_t st) override { Reduce(buf, n, false, st); }
+  void AllReduceMax(double* buf, int64_t n, cudaStream_t st) override { Reduce(buf, n, true, st); }
+
+ private:
+  void Barrier(cudaStream_t st) { k_loop_rendezvous<<<1, 32, 0, st>>>(grp_->flags, counter_, rank_, P_); }
+  void Reduce(double* buf, int64_t n, bool mx, cudaStream_t st) {
+    const std::vector<const void*> peers = grp_->Rendezvous(++hseq_, rank_, buf, mx ? "max" : "sum");
+    if (n <= 0) return;
+    if (n > kLoopScratch) throw Error(4, "loopback all-reduce larger than its scratch");
+    LoopPtrs src{};
+    for (int p = 0; p < P_; ++p) src.p[p] = static_cast<const double*>(peers[p]);
+    Barrier(st);
+    k_loop_reduce<<<static_cast<int>(std::min<int64_t>((n + 255) / 256, 256)), 256, 0, st>>>(src, P_, n, mx,
+                                                                                          scratch_.p);
+    Barrier(st);
+    PDHG_CUDA(cudaMemcpyAsync(buf, scratch_.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+
+  std::shared_ptr<LoopGroup> grp_;
+  unsigned long long* counter_ = nullptr;
+  DArray<double> scratch_;
+  uint64_t hseq_ = 0;
+  int rank_ = 0, P_ = 1;
+};
+
+// A loopback id: the 8-byte magic, then the group key (128 bytes like an
+// ncclUniqueId, so it travels through the same pdhg_shard_spec field).
+constexpr char kLoopMagic[8] = {'P', 'D', 'H', 'G', 'L', 'O', 'O', 'P'};
+inline bool is_loopback_id(const void* id) { return id && std::memcmp(id, kLoopMagic, 8) == 0; }
+inline uint64_t loopback_key(const void* id) {
+  uint64_t k;
+  std::memcpy(&k, static_cast<const char*>(id) + 8, sizeof(k));
+  return k;
+}
+inline void loopback_id(void* out) {
+  static std::atomic<uint64_t> next{1};
+  std::memset(out, 0, 128);
+  std::memcpy(out, kLoopMagic, 8);
+  const uint64_t k = (static_cast<uint64_t>(std::chrono::steady_clock::now().time_since_epoch().count()) << 16) ^
+                     next.fetch_add(1);
+  std::memcpy(static_cast<char*>(out) + 8, &k, sizeof(k));
+}
 
 inline void nccl_unique_id(void* out) {
   ncclUniqueId uid;

@@ -45,6 +45,7 @@ struct Layout {
   double* val = nullptr;
   int32_t s1 = 0, s2 = 0, s3 = 0;  // class bounds S | M | L | XL
   bool s_staged = false;           // class S uses seg_thread_staged_kernel
+  bool s_pipe = false;             // ... its cp.async-pipelined variant (one-operand Ops)
   const uint8_t* s_rm = nullptr;   // per-32-segment flags: segment-order gathers (staged kernel)
   int l_rpc = 1;                   // class L segments per CTA (1 or 4)
   int l_stage = 0;                 // > 0: RPC-4 stream staged by TMA, dynamic smem bytes
@@ -406,6 +407,126 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
   block_reduce_out<Op>(red, red_out);
 }
 
+// pipelined (default for one-operand Ops, PDHG_S_PIPE=0 reverts): the same
+// warp-cooperative chunks and storage-order sums as the staged kernel, but
+// the raw (idx, val) chunk is copied global -> shared by per-lane async
+// copies (cp.async, LDGSTS) one chunk AHEAD, double-buffered per warp: while
+// the lanes gather x for chunk c and sum it, chunk c + 1's stream is in
+// flight, so a chunk costs one gather latency instead of a stream load
+// followed by a gather. Products overwrite the staged values in place; chunk
+// 0 is issued before the programmatic wait (the matrix does not depend on
+// the predecessor). The profiled staged kernel was latency-bound (0.4
+// eligible warps per cycle, DRAM 49 %, L2 36 % on the PageRank-10M dual).
+// Shared memory: 2 x kSChunk x 12 bytes per warp (48 KB per CTA, 4 CTAs/SM).
+constexpr int kPipeSmem = kWarps * 2 * kSChunk * 12;
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <class Op, bool kRM = false>
+__global__ void __launch_bounds__(kBlock, 4) seg_thread_pipe_kernel(const int32_t* __restrict__ ptr,
+                                                                    const int32_t* __restrict__ idx,
+                                                                    const double* __restrict__ val,
+                                                                    int32_t s_end, const Op op,
+                                                                    double* __restrict__ red_out,
+                                                                    const uint8_t* __restrict__ rm = nullptr) {
+  static_assert(Op::kRhs == 1, "products are staged in place of the values");
+  if (skip_launch(op)) return;
+  constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
+  constexpr bool MX = Op::kMax;
+  constexpr int C = kSChunk;
+  constexpr int U = C / 32;
+  extern __shared__ __align__(16) unsigned char pipe_smem[];
+  double red[NR];
+#pragma unroll
+  for (int i = 0; i < NR; ++i) red[i] = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sv = reinterpret_cast<double*>(pipe_smem) + warp * 2 * C;                   // [2][C] values
+  int32_t* si = reinterpret_cast<int32_t*>(pipe_smem + kWarps * 2 * C * 8) + warp * 2 * C;  // [2][C] indices
+  const int s = blockIdx.x * kBlock + threadIdx.x;
+  const int s0 = blockIdx.x * kBlock + warp * 32;
+  const bool own = s < s_end;
+  const bool active = s0 < s_end;  // warp-uniform
+  int b = 0, e = 0, wb = 0, we = 0;
+  typename Op::Pre pre{};
+  if (own) {
+    b = ptr[s];
+    e = ptr[s + 1];
+    pre = op.prefetch(s);
+  }
+  auto issue = [&](int c0, int buf) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = lane + 32 * u;
+      if (c0 + q < we) {
+        cp_async4(si + buf * C + q, idx + c0 + q);
+        cp_async8(sv + buf * C + q, val + c0 + q);
+      }
+    }
+  };
+  if (active) {
+    wb = ptr[s0];
+    we = ptr[s0 + 32 < s_end ? s0 + 32 : s_end];
+    issue(wb, 0);
+  }
+  cp_async_commit();
+  pdl_wait_trigger();
+  if (active) {
+    double acc = 0.0;
+    const bool seg_order = kRM && rm[s0 >> 5];  // warp-uniform
+    int buf = 0;
+    for (int c0 = wb; c0 < we; c0 += C, buf ^= 1) {
+      if (c0 + C < we) issue(c0 + C, buf ^ 1);
+      cp_async_commit();
+      cp_async_wait1();  // this lane's copies of chunk c0 have landed
+      __syncwarp();      // ... and every other lane's
+      const int32_t* ci = si + buf * C;
+      double* cv = sv + buf * C;
+      const int lo = (b > c0 ? b : c0) - c0;
+      const int hi = (e < c0 + C ? e : c0 + C) - c0;
+      if (kRM && seg_order) {
+        int q = lo;
+        for (; q + 4 <= hi; q += 4) {
+          double p[4][1];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) op.map(ci[q + t], cv[q + t], p[t]);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) acc = combine<MX>(acc, p[t][0]);  // storage order
+        }
+        for (; q < hi; ++q) {
+          double p[1];
+          op.map(ci[q], cv[q], p);
+          acc = combine<MX>(acc, p[0]);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = lane + 32 * u;
+          if (c0 + q < we) {
+            double p[1];
+            op.map(ci[q], cv[q], p);
+            cv[q] = p[0];
+          }
+        }
+        __syncwarp();
+        for (int q = lo; q < hi; ++q) acc = combine<MX>(acc, cv[q]);  // storage order
+      }
+      __syncwarp();  // buffer `buf` is refilled two chunks on
+    }
+    if (own) {
+      const double a[1] = {acc};
+      op.finish(s, a, pre, red);
+    }
+  }
+  block_reduce_out<Op>(red, red_out);
+}
+
 // Lane-strided partial sum of [b, e): batches of kStrideUnroll predicated
 // loads per lane, so even the last partial batch keeps every load of the
 // lane in flight at once (a sequential tail loop would serialise one
@@ -564,6 +685,20 @@ inline void launch_thread_class(const Layout& L, const Op& op, double* red, cuda
       case 4: return launch_k(seg_thread_uniform_kernel<Op, 4>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
       case 8: return launch_k(seg_thread_uniform_kernel<Op, 8>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
       default: break;
+    }
+  }
+  if constexpr (Op::kRhs == 1) {
+    if (L.s_staged && L.s_pipe) {
+      if (L.s_rm) {
+        smem_opt_in<seg_thread_pipe_kernel<Op, true>>(kPipeSmem);
+        launch_k(seg_thread_pipe_kernel<Op, true>, g, kBlock, kPipeSmem, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red,
+                 static_cast<const uint8_t*>(L.s_rm));
+      } else {
+        smem_opt_in<seg_thread_pipe_kernel<Op, false>>(kPipeSmem);
+        launch_k(seg_thread_pipe_kernel<Op, false>, g, kBlock, kPipeSmem, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red,
+                 static_cast<const uint8_t*>(nullptr));
+      }
+      return;
     }
   }
   if (L.s_staged && L.s_rm)

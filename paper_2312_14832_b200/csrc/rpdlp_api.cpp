@@ -378,6 +378,12 @@ void RunningAverage::Reset() {
 }
 
 SolveResult Solve(const LpProblem& problem, const SolverParams& params, const EvalObserver& observer) {
+  return Solve(problem, params, observer, DeviceOptions{});
+}
+
+SolveResult Solve(const LpProblem& problem, const SolverParams& params, const EvalObserver& observer,
+                  const DeviceOptions& where) {
+  if (where.shards < 1) throw std::invalid_argument("shards must be >= 1");
   problem.Validate();
   params.Validate();
   const pdhg_lp lp = View(problem);
@@ -392,7 +398,14 @@ SolveResult Solve(const LpProblem& problem, const SolverParams& params, const Ev
   out.lambda = r.lambda.data();
   ObserverCtx ctx{&observer, nullptr};
   char err[512] = {0};
-  const int code = pdhg_solve_on(&lp, &prm, Device(), observer ? Trampoline : nullptr, &ctx, &out, err, sizeof(err));
+  const int dev = where.device >= 0 ? where.device : Device();
+  int code;
+  if (where.shards == 1) {
+    code = pdhg_solve_on(&lp, &prm, dev, observer ? Trampoline : nullptr, &ctx, &out, err, sizeof(err));
+  } else {
+    const pdhg_shard_spec spec{where.shards, 0, where.shards, nullptr};
+    code = pdhg_solve_sharded(&lp, &prm, dev, &spec, observer ? Trampoline : nullptr, &ctx, &out, err, sizeof(err));
+  }
   if (ctx.error) std::rethrow_exception(ctx.error);
   if (code != PDHG_OK) Rethrow(code, err);
   r.status = static_cast<SolveStatus>(out.status);

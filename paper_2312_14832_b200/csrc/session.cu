@@ -177,7 +177,10 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
   // abort all-reduce) on a single GPU.
   if (spec.local == 1 && (world_ > 1 || spec.nccl_id)) {
     if (!spec.nccl_id) throw Error(PDHG_INVALID_ARGUMENT, "a one-shard-per-process session needs an NCCL id");
-    comm_ = std::make_unique<NcclComm>(spec.nccl_id, world_, rank_);
+    if (is_loopback_id(spec.nccl_id))  // in-process ranks on one device (tests)
+      comm_ = std::make_unique<LoopbackComm>(loopback_key(spec.nccl_id), world_, rank_, device_);
+    else
+      comm_ = std::make_unique<NcclComm>(spec.nccl_id, world_, rank_);
   } else {
     comm_ = std::make_unique<LocalComm>();
   }
@@ -590,6 +593,8 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       Sync();
     }
     L.s_staged = L.s1 > 0 && static_cast<double>(se) >= staged_min * L.s1;
+    const char* sp = std::getenv("PDHG_S_PIPE");  // "0": register-staged kernel (A/B, bit-identical)
+    L.s_pipe = L.s_staged && !(sp && sp[0] == '0');
     // Segment-order warps of the staged kernel (shifted-copy segment groups).
     L.s_rm = nullptr;
     const char* rmo = std::getenv("PDHG_SEG_ORDER_WARPS");  // "0": off (A/B)

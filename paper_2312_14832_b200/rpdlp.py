@@ -371,6 +371,16 @@ class Shards:
         return Shards(1, 0, False, bytes(buf.raw))
 
     @staticmethod
+    def loopback(world: int) -> "list[Shards]":
+        """`world` rank specs for in-process loopback ranks on one device
+        (pdhg_loopback_id): construct and solve one Session per spec, each on
+        its own thread -- the multi-rank code path without NCCL (tests)."""
+        buf = C.create_string_buffer(128)
+        err = C.create_string_buffer(abi.ERRLEN)
+        raise_for(abi.load().pdhg_loopback_id(buf, err, abi.ERRLEN), err)
+        return [Shards(world, r, False, bytes(buf.raw)) for r in range(world)]
+
+    @staticmethod
     def from_process_group(group=None) -> "Shards":
         import torch
         import torch.distributed as dist

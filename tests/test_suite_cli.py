@@ -190,3 +190,35 @@ def test_cpp_cli_solve_and_redacted_bench(tmp_path):
     r = subprocess.run([cli_bin, "solve", str(d / "r4.mps"), "--eps", "1e-12", "--iter-limit", "64"],
                        capture_output=True, text=True)
     assert r.returncode == 2 and "status=IterLimit" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_cli_device_and_shards(tmp_path):
+    """Harness extension: `bench --gpus N --shards P` and
+    `solve --device D --shards P` run the suite / solve with K split into P
+    blocks (in-process shard mode) on the chosen devices; same statuses and
+    objectives (1e-6) as the unsharded run, records in name order."""
+    import subprocess
+    cli_bin = _cpp_cli()
+    d = tmp_path / "suite"
+    d.mkdir()
+    for seed in (4, 5, 6):
+        rpdlp.WriteMpsFile(rpdlp.GenRandomLp(30, 40, 0.2, seed), d / f"r{seed}.mps")
+    reps = {}
+    for shards in (1, 3):
+        rep = tmp_path / f"rep{shards}.json"
+        r = subprocess.run([cli_bin, "bench", str(d), "--eps", "1e-6", "--gpus", "1", "--shards", str(shards),
+                            "--report", str(rep)], capture_output=True, text=True)
+        assert r.returncode == 0 and "solved=3/3" in r.stdout, r.stdout + r.stderr
+        reps[shards] = json.loads(rep.read_text())
+    a, b = reps[1]["records"], reps[3]["records"]
+    assert [x["instance"] for x in a] == [x["instance"] for x in b] == ["r4.mps", "r5.mps", "r6.mps"]
+    for x, y in zip(a, b):
+        assert x["status"] == y["status"] == "Optimal"
+        po, qo = x["residuals"]["primal_obj"], y["residuals"]["primal_obj"]
+        assert abs(po - qo) <= 1e-6 * (1 + abs(po))
+    r = subprocess.run([cli_bin, "solve", str(d / "r4.mps"), "--eps", "1e-6", "--device", "0", "--shards", "2"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0 and "status=Optimal" in r.stdout, r.stdout + r.stderr
+    r = subprocess.run([cli_bin, "solve", str(d / "r4.mps"), "--shards", "0"], capture_output=True, text=True)
+    assert r.returncode != 0

@@ -316,6 +316,30 @@ static __global__ void k_loop_rendezvous(unsigned long long* flags, unsigned lon
 struct LoopPtrs {
   const double* p[kLoopMaxRanks];
 };
+// Up to kLoopMaxRanks (src, dst, n) segments copied by one kernel. Data moves
+// on the SMs, not by cudaMemcpyAsync: copy-engine work of one rank can sit
+// in a shared queue behind another rank's copy that waits on a rendezvous,
+// which deadlocked 8 ranks.
+struct LoopCopies {
+  const double* src[kLoopMaxRanks];
+  double* dst[kLoopMaxRanks];
+  int64_t n[kLoopMaxRanks];
+  int count;
+};
+static __global__ void k_loop_copy(LoopCopies c) {
+  for (int k = 0; k < c.count; ++k) {
+    const double* __restrict__ s = c.src[k];
+    double* __restrict__ d = c.dst[k];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c.n[k]; i += (int64_t)gridDim.x * blockDim.x)
+      d[i] = s[i];
+  }
+}
+inline void loop_copy(const LoopCopies& c, cudaStream_t st) {
+  int64_t mx = 0;
+  for (int k = 0; k < c.count; ++k) mx = std::max(mx, c.n[k]);
+  if (!mx) return;
+  k_loop_copy<<<static_cast<int>(std::min<int64_t>((mx + 255) / 256, 592)), 256, 0, st>>>(c);
+}
 static __global__ void k_loop_reduce(LoopPtrs src, int P, int64_t n, int mx, double* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double v = src.p[0][i];
@@ -340,11 +364,14 @@ class LoopbackComm final : public Comm {
     const std::vector<const void*> peers = grp_->Rendezvous(++hseq_, rank_, buf, "allgather");
     if (slice <= 0) return;
     Barrier(st);
+    LoopCopies c{};
     for (int p = 0; p < P_; ++p) {
       if (p == rank_) continue;
-      const double* src = static_cast<const double*>(peers[p]) + p * slice;
-      PDHG_CUDA(cudaMemcpyAsync(buf + p * slice, src, slice * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      c.src[c.count] = static_cast<const double*>(peers[p]) + p * slice;
+      c.dst[c.count] = buf + p * slice;
+      c.n[c.count++] = slice;
     }
+    loop_copy(c, st);
     Barrier(st);
   }
   void Exchange(double* buf, const GhostPlan& plan, cudaStream_t st) override {
@@ -353,7 +380,7 @@ class LoopbackComm final : public Comm {
     const int64_t ns = plan.send_off[P_], nr = plan.recv_off[P_];
     if (ns) k_ghost_pack<<<static_cast<int>(std::min<int64_t>((ns + 255) / 256, 1184)), 256, 0, st>>>(
         buf, plan.send_idx, plan.send_buf, ns);
-    Barrier(st);
+    LoopCopies c{};
     for (int p = 0; p < P_; ++p) {
       if (p == rank_) continue;
       const GhostPlan& q = *static_cast<const GhostPlan*>(peers[p]);
@@ -362,10 +389,14 @@ class LoopbackComm final : public Comm {
       if (rc != sc)
         throw Error(4, "loopback ghost exchange: rank " + std::to_string(rank_) + " expects " + std::to_string(rc) +
                            " entries from rank " + std::to_string(p) + ", which sends " + std::to_string(sc));
-      if (rc)
-        PDHG_CUDA(cudaMemcpyAsync(plan.recv_buf + plan.recv_off[p], q.send_buf + q.send_off[rank_],
-                                  rc * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      if (rc) {
+        c.src[c.count] = q.send_buf + q.send_off[rank_];
+        c.dst[c.count] = plan.recv_buf + plan.recv_off[p];
+        c.n[c.count++] = rc;
+      }
     }
+    Barrier(st);
+    loop_copy(c, st);
     Barrier(st);
     if (nr) k_ghost_unpack<<<static_cast<int>(std::min<int64_t>((nr + 255) / 256, 1184)), 256, 0, st>>>(
         buf, plan.recv_idx, plan.recv_buf, nr);
@@ -385,7 +416,12 @@ class LoopbackComm final : public Comm {
     k_loop_reduce<<<static_cast<int>(std::min<int64_t>((n + 255) / 256, 256)), 256, 0, st>>>(src, P_, n, mx,
                                                                                           scratch_.p);
     Barrier(st);
-    PDHG_CUDA(cudaMemcpyAsync(buf, scratch_.p, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    LoopCopies c{};
+    c.src[0] = scratch_.p;
+    c.dst[0] = buf;
+    c.n[0] = n;
+    c.count = 1;
+    loop_copy(c, st);
   }
 
   std::shared_ptr<LoopGroup> grp_;

@@ -407,7 +407,10 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
   block_reduce_out<Op>(red, red_out);
 }
 
-// pipelined (default for one-operand Ops, PDHG_S_PIPE=0 reverts): the same
+// pipelined (opt-in PDHG_S_PIPE=1; measured SLOWER than the register-staged
+// kernel -- PageRank-10M dual 733 -> 898 us, MCF 285 -> 342 us, staircase
+// 1073 -> 1188 us, profiles/r02/s_pipe_ab_r02i.txt -- kept for the record
+// and bit-identity tested): the same
 // warp-cooperative chunks and storage-order sums as the staged kernel, but
 // the raw (idx, val) chunk is copied global -> shared by per-lane async
 // copies (cp.async, LDGSTS) one chunk AHEAD, double-buffered per warp: while

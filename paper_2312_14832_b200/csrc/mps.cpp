@@ -20,6 +20,7 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cctype>
 #include <charconv>
 #include <cmath>
@@ -32,6 +33,7 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -57,7 +59,9 @@ struct SvHash {
   using is_transparent = void;
   size_t operator()(std::string_view s) const { return std::hash<std::string_view>{}(s); }
 };
-using NameMap = std::unordered_map<std::string, I, SvHash, std::equal_to<>>;
+// Keys are views into the text being parsed, which outlives the Reader (no
+// per-name allocation).
+using NameMap = std::unordered_map<std::string_view, I, SvHash, std::equal_to<>>;
 
 enum class Section { kNone, kName, kObjsense, kRows, kColumns, kRhs, kRanges, kBounds, kEndata };
 
@@ -154,10 +158,25 @@ class Reader {
     }
   }
 
+  bool InColumns() const { return sec_ == Section::kColumns; }
+
+  // The COLUMNS data lines up to the next section header, tokenised on
+  // worker threads (row names are looked up in the finished ROWS map, which
+  // is read-only from here on), merged in file order on this thread: column
+  // indices are assigned in order of first appearance, objective terms
+  // accumulate and entries append exactly as the serial ColumnLine does. The
+  // first error in file order wins, with its line number.
+  void ColumnsBlock(std::string_view block, int threads);
+
   pdhg_instance* Finish() {
     if (Rank(sec_) < Rank(Section::kColumns)) Fail("missing COLUMNS section");
     if (n_ == 0) Fail("no variables");
-    return Assemble();
+    const auto t0 = std::chrono::steady_clock::now();
+    pdhg_instance* p = Assemble();
+    if (std::getenv("PDHG_TRACE"))
+      std::fprintf(stderr, "[mps] assemble %.3fs\n",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    return p;
   }
 
  private:
@@ -212,14 +231,14 @@ class Reader {
     if (type == "N") {
       if (!have_obj_) {
         have_obj_ = true;
-        row_index_.emplace(std::string(name), kObj);
+        row_index_.emplace(name, kObj);
       } else {
-        row_index_.emplace(std::string(name), kFree);
+        row_index_.emplace(name, kFree);
       }
       return;
     }
     if (type != "E" && type != "G" && type != "L") Fail("unknown row type '" + std::string(tok_[0]) + "'");
-    row_index_.emplace(std::string(name), static_cast<I>(rows_.size()));
+    row_index_.emplace(name, static_cast<I>(rows_.size()));
     rows_.push_back({type[0]});
   }
 
@@ -229,7 +248,7 @@ class Reader {
     I j;
     if (it == col_index_.end()) {
       j = n_++;
-      col_index_.emplace(std::string(name), j);
+      col_index_.emplace(name, j);
       obj_.push_back(0.0);
       lo_.push_back(0.0);
       up_.push_back(kInf);
@@ -237,7 +256,7 @@ class Reader {
       j = it->second;
     }
     last_col_ = j;
-    last_name_.assign(name);
+    last_name_ = name;
     return j;
   }
 
@@ -247,7 +266,8 @@ class Reader {
     return it->second;
   }
 
-  double Value(std::string_view t) const {
+  // Numeric field -> double; false with the reference's message on error.
+  static bool ParseValue(std::string_view t, double* out, std::string* err) {
     double v = 0.0;
     const char* b = t.data();
     const char* e = b + t.size();
@@ -256,9 +276,23 @@ class Reader {
       const std::string s(t);  // strtod-only spellings: '+', hex, overflow / underflow
       char* end = nullptr;
       v = std::strtod(s.c_str(), &end);
-      if (end != s.c_str() + s.size()) Fail("bad numeric value '" + s + "'");
+      if (end != s.c_str() + s.size()) {
+        *err = "bad numeric value '" + s + "'";
+        return false;
+      }
     }
-    if (std::isnan(v)) Fail("NaN value");
+    if (std::isnan(v)) {
+      *err = "NaN value";
+      return false;
+    }
+    *out = v;
+    return true;
+  }
+
+  double Value(std::string_view t) const {
+    double v = 0.0;
+    std::string err;
+    if (!ParseValue(t, &v, &err)) Fail(err);
     return v;
   }
 
@@ -463,13 +497,149 @@ class Reader {
   std::vector<double> obj_, lo_, up_;
   std::vector<std::string_view> tok_;
   I last_col_ = -1;
-  std::string last_name_;
+  std::string_view last_name_;
 };
+
+// One COLUMNS line's worth of work, produced on a worker thread.
+struct ColRun {
+  std::string_view name;
+  size_t e0, e1;  // entries [e0, e1) of the chunk
+  size_t o0, o1;  // objective terms [o0, o1) of the chunk
+};
+struct ColChunk {
+  std::string_view text;
+  std::vector<ColRun> runs;
+  std::vector<std::pair<I, double>> entries;  // (row, value), file order
+  std::vector<double> obj;                    // objective terms, file order
+  int lines = 0;                              // lines in the chunk
+  int err_line = -1;                          // chunk-local line of the first error
+  std::string err;
+};
+
+void Reader::ColumnsBlock(std::string_view block, int threads) {
+  // Chunks of roughly equal bytes, cut at line starts.
+  const size_t nb = block.size();
+  int T = std::max(1, std::min<int>(threads, static_cast<int>(nb >> 20)));  // >= 1 MB per chunk
+  std::vector<ColChunk> ch(static_cast<size_t>(T));
+  size_t a = 0;
+  for (int k = 0; k < T; ++k) {
+    size_t b = (k == T - 1) ? nb : std::max(a, nb * static_cast<size_t>(k + 1) / T);
+    if (b < nb) {
+      const size_t nl = block.find('\n', b);
+      b = nl == std::string_view::npos ? nb : nl + 1;
+    }
+    ch[k].text = block.substr(a, b - a);
+    a = b;
+  }
+  auto work = [this](ColChunk& c) {
+    std::vector<std::string_view> tok;
+    std::string_view last;
+    bool have = false;
+    size_t i = 0;
+    const std::string_view t = c.text;
+    while (i < t.size()) {
+      size_t j = t.find('\n', i);
+      if (j == std::string_view::npos) j = t.size();
+      const std::string_view raw = t.substr(i, j - i);
+      i = j + 1;
+      ++c.lines;
+      if (raw.empty() || raw[0] == '*' || Trim(raw).empty()) continue;
+      if (fixed_) SplitFixed(raw, tok);
+      else SplitWs(Trim(raw), tok);
+      if (tok.size() >= 3 && tok[1] == "'MARKER'") continue;
+      auto fail = [&](std::string m) {
+        c.err_line = c.lines;
+        c.err = std::move(m);
+      };
+      if (tok.size() < 3 || tok.size() % 2 == 0) {
+        fail("COLUMNS line needs a column name and (row, value) pairs");
+        return;
+      }
+      if (!have || tok[0] != last) {
+        c.runs.push_back({tok[0], c.entries.size(), c.entries.size(), c.obj.size(), c.obj.size()});
+        last = tok[0];
+        have = true;
+      }
+      for (size_t k = 1; k + 1 < tok.size(); k += 2) {
+        double v;  // value first, then the row (the reference's argument order)
+        if (!ParseValue(tok[k + 1], &v, &c.err)) {
+          c.err_line = c.lines;
+          return;
+        }
+        auto it = row_index_.find(tok[k]);
+        if (it == row_index_.end()) {
+          fail("unknown row '" + std::string(tok[k]) + "'");
+          return;
+        }
+        const I r = it->second;
+        if (r == kFree) continue;
+        if (r == kObj) c.obj.push_back(v);
+        else if (v != 0.0) c.entries.emplace_back(r, v);
+      }
+      c.runs.back().e1 = c.entries.size();
+      c.runs.back().o1 = c.obj.size();
+    }
+  };
+  const auto tw0 = std::chrono::steady_clock::now();
+  if (T == 1) {
+    work(ch[0]);
+  } else {
+    std::vector<std::thread> pool;
+    for (int k = 1; k < T; ++k) pool.emplace_back(work, std::ref(ch[k]));
+    work(ch[0]);
+    for (std::thread& th : pool) th.join();
+  }
+  const auto tw1 = std::chrono::steady_clock::now();
+  // Merge in file order; stop at the first error.
+  size_t nruns = 0, nent = 0;
+  for (const ColChunk& c : ch) {
+    nruns += c.runs.size();
+    nent += c.entries.size();
+  }
+  col_index_.reserve(col_index_.size() + nruns);
+  obj_.reserve(obj_.size() + nruns);
+  lo_.reserve(lo_.size() + nruns);
+  up_.reserve(up_.size() + nruns);
+  entries_.reserve(entries_.size() + nent);
+  for (const ColChunk& c : ch) {
+    for (const ColRun& r : c.runs) {
+      const I j = Var(r.name);
+      for (size_t k = r.o0; k < r.o1; ++k) obj_[j] += c.obj[k];
+      for (size_t k = r.e0; k < r.e1; ++k) entries_.push_back({c.entries[k].first, j, c.entries[k].second});
+    }
+    if (c.err_line >= 0) throw ParseError{line_ + c.err_line, c.err};
+    line_ += c.lines;
+  }
+  if (std::getenv("PDHG_TRACE"))
+    std::fprintf(stderr, "[mps] COLUMNS %zu bytes: %d chunks, tokenise %.3fs, merge %.3fs\n", nb, T,
+                 std::chrono::duration<double>(tw1 - tw0).count(),
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - tw1).count());
+}
 
 pdhg_instance* ParseText(std::string_view text, bool fixed) {
   Reader rd(fixed);
+  static const int kThreads = [] {
+    const char* e = std::getenv("PDHG_MPS_THREADS");  // "1": serial COLUMNS (A/B)
+    const int hw = static_cast<int>(std::thread::hardware_concurrency());
+    return e ? std::max(1, std::atoi(e)) : std::max(1, std::min(hw, 32));
+  }();
   size_t i = 0;
   while (i < text.size()) {  // std::getline semantics: no empty line after a final '\n'
+    if (rd.InColumns() && kThreads > 1) {
+      // The COLUMNS block: every line up to the next header line.
+      size_t k = i;
+      while (k < text.size()) {
+        const char c0 = text[k];
+        if (c0 != '*' && !IsSpace(c0)) break;  // a header starts in column 1
+        const size_t nl = text.find('\n', k);
+        k = nl == std::string_view::npos ? text.size() : nl + 1;
+      }
+      if (k > i) {
+        rd.ColumnsBlock(text.substr(i, k - i), kThreads);
+        i = k;
+        continue;
+      }
+    }
     size_t j = text.find('\n', i);
     if (j == std::string_view::npos) j = text.size();
     rd.Line(text.substr(i, j - i));

@@ -163,8 +163,13 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
   fork_.main = st_;
   PDHG_CUDA(cudaEventCreateWithFlags(&fork_.fork, cudaEventDisableTiming));
   streams_.fork.fork = fork_.fork;
+  // PDHG_FORK=0: no side streams (class kernels of a pass and the check's
+  // row / column passes serialise on the session stream) -- used by the
+  // loopback tests, whose spinning rendezvous need a hardware queue per stream.
+  const char* fenv = std::getenv("PDHG_FORK");
+  const bool fork_on = !(fenv && fenv[0] == '0');
   for (int k = 0; k < 3; ++k) {
-    PDHG_CUDA(cudaStreamCreateWithFlags(&fork_.side[k], cudaStreamNonBlocking));
+    if (fork_on) PDHG_CUDA(cudaStreamCreateWithFlags(&fork_.side[k], cudaStreamNonBlocking));
     PDHG_CUDA(cudaEventCreateWithFlags(&fork_.join[k], cudaEventDisableTiming));
     streams_.fork.side[k] = fork_.side[k];
     streams_.fork.join[k] = fork_.join[k];
@@ -593,8 +598,8 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
       Sync();
     }
     L.s_staged = L.s1 > 0 && static_cast<double>(se) >= staged_min * L.s1;
-    const char* sp = std::getenv("PDHG_S_PIPE");  // "0": register-staged kernel (A/B, bit-identical)
-    L.s_pipe = L.s_staged && !(sp && sp[0] == '0');
+    const char* sp = std::getenv("PDHG_S_PIPE");  // "1": cp.async-pipelined variant (A/B, bit-identical; slower)
+    L.s_pipe = L.s_staged && sp && sp[0] == '1';
     // Segment-order warps of the staged kernel (shifted-copy segment groups).
     L.s_rm = nullptr;
     const char* rmo = std::getenv("PDHG_SEG_ORDER_WARPS");  // "0": off (A/B)

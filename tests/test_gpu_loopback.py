@@ -12,8 +12,8 @@ The rendezvous kernels of all ranks spin on one GPU at the same time, so each
 rank's streams need their own hardware work queue (a queue whose head waits
 on a spinning peer would deadlock, the false-dependency hazard NCCL documents
 for several communicators on one device): the tests run in a child process
-with CUDA_DEVICE_MAX_CONNECTIONS=32 (8 ranks x 4 streams); the parent test
-only launches it.
+with CUDA_DEVICE_MAX_CONNECTIONS=32 and PDHG_FORK=0 (one stream per rank, no
+class side streams); the parent test only launches it.
 
 Parity bar: every rank returns the same result, and it is bit-identical to
 the in-process shard mode (all shards in one session), which the
@@ -44,7 +44,7 @@ def test_loopback_suite():
     """Runs this module in a child with 32 hardware queues (see above)."""
     if CHILD:
         pytest.skip("the child runs the individual tests")
-    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", PDHG_FORK="0")
     r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu"],
                        capture_output=True, text=True, env=env, timeout=1500, cwd=os.path.dirname(__file__))
     assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-3000:]

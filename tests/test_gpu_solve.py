@@ -382,10 +382,10 @@ def test_log_every_lines_match_reference(capfd, reference, restatement):
 
 @pytest.mark.parametrize("name", ["mcf", "staircase_d20", "pagerank"])
 def test_pipelined_class_s_kernel_bit_identical(name, monkeypatch):
-    """The cp.async-pipelined class-S kernel (engine.cuh seg_thread_pipe_kernel)
-    keeps the staged kernel's storage-order sums, segment-order warps
-    included: whole trajectories are bitwise identical (PDHG_S_PIPE=0 forces
-    the register-staged kernel)."""
+    """The cp.async-pipelined class-S kernel (engine.cuh seg_thread_pipe_kernel,
+    opt-in PDHG_S_PIPE=1) keeps the register-staged kernel's storage-order
+    sums, segment-order warps included: whole trajectories are bitwise
+    identical."""
     from test_gpu_kernels import CASES
     p = CASES[name] if name in CASES else GenPagerank(20000, 0.85, 6, 3)
     prm = SolverParams(eps=1e-6, iter_limit=3000)

@@ -135,3 +135,44 @@ def test_parsed_problem_solves_like_generated(restatement):
     a = restatement.solve(p, rpdlp.SolverParams(eps=1e-6))
     b = restatement.solve(q, rpdlp.SolverParams(eps=1e-6))
     assert a.iterations == b.iterations and a.report.primal_obj == b.report.primal_obj
+
+
+def _big_text():
+    p = GenRandomLp(3000, 4000, 0.05, 9, equality_rows=500)
+    return WriteMps(p)
+
+
+def test_parallel_columns_large_file_matches_reference(reference):
+    """A COLUMNS section of tens of MB is tokenised on worker threads
+    (mps.cpp Reader::ColumnsBlock, >= 1 MB per chunk) and merged in file
+    order: bit-identical to the reference parser."""
+    if reference is None:
+        pytest.skip("reference build absent")
+    from golden.make_mps_golden import ref_lib, ref_parse
+    text = _big_text()
+    assert len(text) > 8 << 20  # several chunks
+    assert_matches(ParseMpsString(text), ref_parse(ref_lib(), text, False))
+
+
+@pytest.mark.parametrize("where", [0.3, 0.55, 0.97])
+def test_parallel_columns_first_error_wins(where, reference):
+    """Errors inside a chunked COLUMNS section: the first one in file order is
+    reported, with the reference's message and line number, even when a later
+    chunk fails too."""
+    if reference is None:
+        pytest.skip("reference build absent")
+    from golden.make_mps_golden import ref_lib, ref_parse
+    lines = _big_text().split("\n")
+    c0 = lines.index("COLUMNS") + 1
+    c1 = next(i for i in range(c0, len(lines)) if lines[i] and not lines[i][0].isspace())
+    k = c0 + int(where * (c1 - c0))
+    f = lines[k].split()
+    lines[k] = "    " + f[0] + "  NOPE_ROW  1.0"               # unknown row
+    lines[c1 - 2] = lines[c1 - 2].rsplit(None, 1)[0] + "  1.0x"  # a later bad number
+    text = "\n".join(lines)
+    g = ref_parse(ref_lib(), text, False)
+    assert g["code"] != 0
+    with pytest.raises(Exception) as ei:
+        ParseMpsString(text)
+    assert str(ei.value) == g["error"] or g["error"] in str(ei.value)
+    assert f"line {g['line']}:" in str(ei.value)

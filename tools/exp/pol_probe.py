@@ -3,6 +3,7 @@ per setting (env read at session creation), warm in-loop iteration time and
 the per-kernel times.
 
     python tools/exp/pol_probe.py VAR "v1,v2,..." case [case ...]
+    python tools/exp/pol_probe.py - "A=1+B=2,A=3+B=4" case ...   (combined settings, applied cumulatively)
 """
 import os
 import sys
@@ -25,7 +26,14 @@ for name in sys.argv[3:]:
     p = cases[name]()
     big = p.nnz() > 2e8
     for v in vals:
-        os.environ[var] = v
+        # "VAR val,val" or, with VAR "-", settings "A=1+B=2"
+        if var == "-":
+            for kv in v.split("+"):
+                if "=" in kv:
+                    k, x = kv.split("=", 1)
+                    os.environ[k] = x
+        else:
+            os.environ[var] = v
         with rpdlp.Session(p) as s:
             st = s.stats()
             bp, bd, bi = algorithmic_bytes(p.num_rows(), p.num_vars(), p.nnz(), st.uniform_bounds,

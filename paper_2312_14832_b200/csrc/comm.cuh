@@ -70,6 +70,9 @@ class Comm {
  public:
   virtual ~Comm() = default;
   virtual bool local() const = 0;
+  // Collectives may be captured into CUDA graphs (false: the loopback
+  // transport, whose event barriers cannot cross captures).
+  virtual bool graphs() const { return true; }
   // In place: this rank's slice is buf[rank * slice, (rank + 1) * slice).
   virtual void AllGather(double* buf, int64_t slice, cudaStream_t st) = 0;
   // The entries this rank's block reads (ghost plan), or the full vector.
@@ -197,40 +200,31 @@ class NcclComm final : public Comm {
 // process on ONE device, each driven by its own host thread, run the session's
 // multi-rank code path -- padded slices, ghost pack / send / recv / unpack,
 // per-rank check packs summed over ranks, rank 0's clock, the observer-abort
-// reduction, collectives captured inside the block graphs -- with this
-// transport in place of NCCL. It replaces only NCCL's data movement:
-//  * host rendezvous per collective CALL (every rank issues the same sequence
-//    of calls, captures included): each rank posts its argument (buffer or
-//    ghost plan) and receives every peer's;
-//  * device rendezvous per collective EXECUTION: a one-thread kernel bumps
-//    this rank's sequence counter in device memory, publishes it and spins
-//    until every rank has published it (graph replays keep counting, so a
-//    replayed collective pairs with the peers' same replay). Two rendezvous
-//    per collective: "ready" before reading peers' buffers, "done" after, so
-//    no rank overwrites data a peer is still reading;
-//  * data: D2D copies (all-gather, ghost segments) or a fixed-order kernel
-//    (all-reduce: sum over ranks 0..P-1, the order the in-process shard mode
-//    uses -- so results are bitwise comparable with it).
-// A rendezvous that does not complete within 60 s traps (no GPU hang).
+// reduction -- with this transport in place of NCCL. It replaces only NCCL's
+// data movement:
+//  * a host rendezvous per collective call: every rank posts its argument
+//    (buffer or ghost plan) and receives every peer's;
+//  * device ordering by CUDA events, never by spinning kernels: a device
+//    barrier records an event on this rank's stream, exchanges the events
+//    through a host rendezvous and makes the stream wait on every peer's.
+//    Two barriers per collective: "ready" before reading peers' buffers,
+//    "done" after, so no rank overwrites data a peer is still reading. (Ranks
+//    that spin on each other's flags from different streams of one device
+//    have no forward-progress guarantee -- a spinning kernel can hold the
+//    hardware queue its peer's kernel waits in -- and deadlocked here.)
+//    An event wait cannot cross stream captures, so sessions over this
+//    transport run their blocks eagerly instead of as CUDA graphs
+//    (Comm::graphs); the kernels and their order are the same;
+//  * data: kernels on the rank's stream (all-gather, ghost segments) or a
+//    fixed-order kernel (all-reduce: sum over ranks 0..P-1, the order the
+//    in-process shard mode uses -- so results are bitwise comparable with it).
 constexpr int kLoopMaxRanks = 16;
 constexpr int64_t kLoopScratch = 1 << 16;  // doubles: the largest all-reduce
+constexpr int kLoopEvents = 4;             // event ring per rank (a rank runs at most one barrier ahead)
 
 struct LoopGroup {
   int P = 0;
   int device = 0;
-  // Host-mapped (zero-copy) so a stuck rendezvous can be diagnosed from the
-  // host without touching the device: published sequence per rank, and each
-  // rank's device-side counter.
-  unsigned long long* hflags = nullptr;
-  unsigned long long* flags = nullptr;     // device view of hflags[0, 16)
-  unsigned long long* counters = nullptr;  // device view of hflags[16, 32)
-  std::string State() const {
-    std::string o;
-    for (int r = 0; r < P; ++r)
-      o += " r" + std::to_string(r) + ":flag=" + std::to_string(hflags[r]) + ",ctr=" +
-           std::to_string(hflags[kLoopMaxRanks + r]);
-    return o;
-  }
   std::mutex mu;
   std::condition_variable cv;
   struct Slot {
@@ -244,7 +238,7 @@ struct LoopGroup {
       const char* e = std::getenv("PDHG_LOOP_TRACE");
       return e && e[0] == '1';
     }();
-    if (trace) std::fprintf(stderr, "[loop] rank %d seq %llu %s\n", rank, (unsigned long long)seq, what);
+    if (trace) std::fprintf(stderr, "[loop] rank %d call %llu %s\n", rank, (unsigned long long)seq, what);
     std::unique_lock<std::mutex> lk(mu);
     Slot& s = slots[seq];
     if (s.arg.empty()) s.arg.assign(static_cast<size_t>(P), nullptr);
@@ -256,14 +250,11 @@ struct LoopGroup {
       for (int r = 0; r < P; ++r)
         if (!s.arg[r]) who += " " + std::to_string(r);
       throw Error(4, "loopback rendezvous timed out at call " + std::to_string(seq) + " (" + what +
-                         "), missing ranks" + who + "; device:" + State());
+                         "), missing ranks" + who);
     }
     std::vector<const void*> out = s.arg;
     if (++s.taken == P) slots.erase(seq);
     return out;
-  }
-  ~LoopGroup() {
-    if (hflags) cudaFreeHost(hflags);
   }
 
   static std::shared_ptr<LoopGroup> Join(uint64_t key, int P, int device) {
@@ -275,15 +266,6 @@ struct LoopGroup {
       grp = std::make_shared<LoopGroup>();
       grp->P = P;
       grp->device = device;
-      void* h = nullptr;
-      PDHG_CUDA(cudaHostAlloc(&h, 2 * kLoopMaxRanks * sizeof(unsigned long long),
-                              cudaHostAllocMapped | cudaHostAllocPortable));
-      std::memset(h, 0, 2 * kLoopMaxRanks * sizeof(unsigned long long));
-      grp->hflags = static_cast<unsigned long long*>(h);
-      void* d = nullptr;
-      PDHG_CUDA(cudaHostGetDevicePointer(&d, h, 0));
-      grp->flags = static_cast<unsigned long long*>(d);
-      grp->counters = grp->flags + kLoopMaxRanks;
       reg[key] = grp;
     }
     if (grp->P != P || grp->device != device) throw Error(1, "loopback group: world / device mismatch");
@@ -291,35 +273,10 @@ struct LoopGroup {
   }
 };
 
-static __global__ void k_loop_rendezvous(unsigned long long* flags, unsigned long long* counter, int rank, int P) {
-  if (threadIdx.x != 0) return;
-  const unsigned long long s = *reinterpret_cast<volatile unsigned long long*>(counter) + 1;
-  *reinterpret_cast<volatile unsigned long long*>(counter) = s;
-  __threadfence_system();
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flags + rank), "l"(s) : "memory");
-  unsigned long long t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (int p = 0; p < P; ++p) {
-    for (;;) {
-      unsigned long long v;
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + p) : "memory");
-      if (v >= s) break;
-      __nanosleep(200);
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 60ull * 1000000000ull) __trap();
-    }
-  }
-  __threadfence();
-}
-
 struct LoopPtrs {
   const double* p[kLoopMaxRanks];
 };
-// Up to kLoopMaxRanks (src, dst, n) segments copied by one kernel. Data moves
-// on the SMs, not by cudaMemcpyAsync: copy-engine work of one rank can sit
-// in a shared queue behind another rank's copy that waits on a rendezvous,
-// which deadlocked 8 ranks.
+// Up to kLoopMaxRanks (src, dst, n) segments copied by one kernel.
 struct LoopCopies {
   const double* src[kLoopMaxRanks];
   double* dst[kLoopMaxRanks];
@@ -356,10 +313,15 @@ class LoopbackComm final : public Comm {
   LoopbackComm(uint64_t key, int world, int rank, int device) : rank_(rank), P_(world) {
     if (world < 1 || world > kLoopMaxRanks) throw Error(1, "loopback world must be 1..16");
     grp_ = LoopGroup::Join(key, world, device);
-    counter_ = grp_->counters + rank;
     scratch_.alloc(kLoopScratch);
+    for (cudaEvent_t& e : ev_) PDHG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~LoopbackComm() override {
+    for (cudaEvent_t e : ev_)
+      if (e) cudaEventDestroy(e);
   }
   bool local() const override { return false; }
+  bool graphs() const override { return false; }
   void AllGather(double* buf, int64_t slice, cudaStream_t st) override {
     const std::vector<const void*> peers = grp_->Rendezvous(++hseq_, rank_, buf, "allgather");
     if (slice <= 0) return;
@@ -405,7 +367,18 @@ class LoopbackComm final : public Comm {
   void AllReduceMax(double* buf, int64_t n, cudaStream_t st) override { Reduce(buf, n, true, st); }
 
  private:
-  void Barrier(cudaStream_t st) { k_loop_rendezvous<<<1, 32, 0, st>>>(grp_->flags, counter_, rank_, P_); }
+  // Device barrier: every rank's stream passes this point only after every
+  // rank's stream has reached it (event record -> host exchange -> waits).
+  // The host rendezvous orders each record before the peers' waits, and a
+  // rank can be at most one barrier ahead of a peer, so a ring of
+  // kLoopEvents events is never re-recorded before the peers waited on it.
+  void Barrier(cudaStream_t st) {
+    cudaEvent_t e = ev_[nev_++ % kLoopEvents];
+    PDHG_CUDA(cudaEventRecord(e, st));
+    const std::vector<const void*> evs = grp_->Rendezvous(++hseq_, rank_, e, "barrier");
+    for (int p = 0; p < P_; ++p)
+      if (p != rank_) PDHG_CUDA(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(const_cast<void*>(evs[p])), 0));
+  }
   void Reduce(double* buf, int64_t n, bool mx, cudaStream_t st) {
     const std::vector<const void*> peers = grp_->Rendezvous(++hseq_, rank_, buf, mx ? "max" : "sum");
     if (n <= 0) return;
@@ -425,8 +398,9 @@ class LoopbackComm final : public Comm {
   }
 
   std::shared_ptr<LoopGroup> grp_;
-  unsigned long long* counter_ = nullptr;
   DArray<double> scratch_;
+  cudaEvent_t ev_[kLoopEvents] = {};
+  uint64_t nev_ = 0;
   uint64_t hseq_ = 0;
   int rank_ = 0, P_ = 1;
 };

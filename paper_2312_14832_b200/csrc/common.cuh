@@ -71,6 +71,13 @@ struct CMat {
   double* head_part = nullptr;  // ntiles * 2
   double* tail_part = nullptr;  // ntiles * 2
   unsigned* counter = nullptr;  // ntiles, zero between launches
+  // Execution order (CTA b runs tile order[b]) or null (b runs tile b):
+  // tiles sorted by the gathered index of their first nonzero, so the CTAs
+  // resident at any moment gather from one narrow, L2-resident window of the
+  // vector instead of every long segment's whole span (session.cu
+  // PartitionLong). Every per-tile output is indexed by the tile, and the
+  // cross-tile combination sums in tile order: results do not depend on it.
+  const int32_t* order = nullptr;
 };
 
 // Device-resident solver scalars: the iteration kernels read these instead
@@ -97,22 +104,6 @@ struct Scalars {
   double adapt_iter;  // iterations_ at the start of the block (adaptive step)
   double lb, ub;      // the common scaled bound when every column shares it
 };
-
-// L2 residency hints of the per-iteration step kernels (Session cache_pol_,
-// PDHG_CACHE_POL). Bits: kPolOps -- per-segment operands read once (x, c,
-// x-bar; kx, y, q, y-bar) load with evict-first (ld.global.cs); kPolAux --
-// outputs the next kernel does not gather (x-bar, y-bar, K x+) store
-// evict-first (st.global.cs); kPolNext -- the iterate the next kernel gathers
-// (x+, y+) stores evict-first too. Only the gathered vector should then hold
-// normal-priority L2 lines while a pass streams the matrix.
-enum : int { kPolOps = 1, kPolAux = 2, kPolNext = 4 };
-__device__ __forceinline__ double ld_pol(const double* p, int pol, int bit) {
-  return (pol & bit) ? __ldcs(p) : *p;
-}
-__device__ __forceinline__ void st_pol(double* p, double v, int pol, int bit) {
-  if (pol & bit) __stcs(p, v);
-  else *p = v;
-}
 
 // Clamp with the reference's NaN behaviour: std::min(std::max(v, lo), hi)
 // (solver.cpp:33-35) returns NaN for NaN input; fmin/fmax would mask it.

@@ -19,6 +19,8 @@
 
 #include <atomic>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <type_traits>
 
 #include "tile_spmv.cuh"
@@ -26,6 +28,7 @@
 namespace pdhg {
 
 constexpr int kUnroll = 4;
+constexpr int kSChunkMax = 256;  // class-S staged chunk (entries per warp step), longest variant
 
 // Equality rows after the class permutation: within each class the equality
 // rows come first. [0,e0) eq S, [s1,e1) eq M, [s2,e2) eq L, [s3,e3) eq XL.
@@ -46,6 +49,8 @@ struct Layout {
   int32_t s1 = 0, s2 = 0, s3 = 0;  // class bounds S | M | L | XL
   bool s_staged = false;           // class S uses seg_thread_staged_kernel
   bool s_pipe = false;             // ... its cp.async-pipelined variant (one-operand Ops)
+  int s_flow = 0;                  // ... its persistent variant (step Ops; 3 or 4 CTAs per SM)
+  int s_chunk = kSChunkMax;        // ... its chunk of entries per warp step (128 or 256)
   const uint8_t* s_rm = nullptr;   // per-32-segment flags: segment-order gathers (staged kernel)
   int l_rpc = 1;                   // class L segments per CTA (1 or 4)
   int l_stage = 0;                 // > 0: RPC-4 stream staged by TMA, dynamic smem bytes
@@ -247,7 +252,10 @@ __device__ __forceinline__ void seg_thread_direct(const int32_t* __restrict__ pt
   }
 }
 
-template <class Op, int L>
+// kPrefix: the modal-prefix variant (the plain one carries no direct path,
+// which would cost the all-uniform transport primal 8 registers and a
+// quarter of its occupancy: 10.3 -> 12.3 us).
+template <class Op, int L, bool kPrefix>
 __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_t* __restrict__ idx,
                                                                     const double* __restrict__ val, int32_t s_end,
                                                                     const Op op, double* __restrict__ red_out,
@@ -259,10 +267,12 @@ __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_
   double red[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
-  if (static_cast<int>(blockIdx.x) * kBlock >= s_u) {  // CTA-uniform: past the modal prefix
-    seg_thread_direct(ptr, idx, val, s_end, op, red);
-    block_reduce_out<Op>(red, red_out);
-    return;
+  if constexpr (kPrefix) {
+    if (static_cast<int>(blockIdx.x) * kBlock >= s_u) {  // CTA-uniform: past the modal prefix
+      seg_thread_direct(ptr, idx, val, s_end, op, red);
+      block_reduce_out<Op>(red, red_out);
+      return;
+    }
   }
   const int s = blockIdx.x * kBlock + threadIdx.x;
   typename Op::Pre pre{};
@@ -291,11 +301,15 @@ __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_
 
 // staged (longer short segments, e.g. 20-nonzero staircase rows): the 32
 // segments of a warp are contiguous in the nonzero stream, so the warp
-// streams that range in chunks of kSChunk entries with fully coalesced
-// lane-strided loads (all loads and gathers of a chunk in flight at once),
-// stages the rounded products in shared memory, and every lane then adds up
-// the part of its own segment inside the chunk, chunk after chunk -- i.e. in
-// storage order, exactly like the direct variant.
+// streams that range in chunks of C entries (C = 128 or 256 by the class's
+// mean length, Layout::s_chunk) with fully coalesced lane-strided loads, all
+// gathers of a chunk in flight before the first product is staged in shared
+// memory, and every lane then adds up the part of its own segment inside the
+// chunk, chunk after chunk -- i.e. in storage order, exactly like the direct
+// variant. The warp's range [wb, we) comes from the lanes' own offsets
+// (shuffles) and the segment-order flag is loaded with them, before the
+// programmatic wait: the group's dependent memory chain is offsets ->
+// stream -> gathers.
 constexpr int kSChunk = 256;
 
 //
@@ -306,19 +320,88 @@ constexpr int kSChunk = 256;
 // then walks its own segment, so the 32 lanes gather 32 adjacent entries per
 // step instead of one lane-strided entry each of 32 unrelated segments. The
 // sums run in the same storage order either way.
-template <class Op, bool kRM = false>
+template <class Op, bool kRM, int C>
+__device__ __forceinline__ void staged_group(const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                             const Op& op, int b, int e, int wb, int we, bool seg_order,
+                                             double (*sp)[C], int32_t* si, double (&acc)[Op::kRhs]) {
+  constexpr int R = Op::kRhs;
+  constexpr bool MX = Op::kMax;
+  constexpr int U = C / 32;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.0;
+  for (int c0 = wb; c0 < we; c0 += C) {
+    int32_t j[U];
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = c0 + lane + 32 * u;
+      j[u] = k < we ? ld_stream(idx + k) : 0;
+      v[u] = k < we ? ld_stream(val + k) : 0.0;
+    }
+    const int lo = (b > c0 ? b : c0) - c0;
+    const int hi = (e < c0 + C ? e : c0 + C) - c0;
+    if (kRM && seg_order) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        si[lane + 32 * u] = j[u];
+        sp[0][lane + 32 * u] = v[u];
+      }
+      __syncwarp();
+      constexpr int Q = 4;
+      int q = lo;
+      for (; q + Q <= hi; q += Q) {
+        double p[Q][R];
+#pragma unroll
+        for (int t = 0; t < Q; ++t) op.map(si[q + t], sp[0][q + t], p[t]);
+#pragma unroll
+        for (int t = 0; t < Q; ++t)
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[t][r]);  // storage order
+      }
+      for (; q < hi; ++q) {
+        double p[R];
+        op.map(si[q], sp[0][q], p);
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[r]);
+      }
+    } else {
+      constexpr int B = U <= 4 ? U : 1;  // C = 128: all gathers in flight; 256: scheduled by ptxas (64 registers)
+#pragma unroll
+      for (int u0 = 0; u0 < U; u0 += B) {
+        double p[B][R];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {  // the batch's gathers all in flight ...
+          if (c0 + lane + 32 * (u0 + u) < we) op.map(j[u0 + u], v[u0 + u], p[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {  // ... before its first product is staged
+          if (c0 + lane + 32 * (u0 + u) < we) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) sp[r][lane + 32 * (u0 + u)] = p[u][r];
+          }
+        }
+      }
+      __syncwarp();
+      for (int q = lo; q < hi; ++q) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], sp[r][q]);  // storage order
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <class Op, bool kRM, int C>
 __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int32_t* __restrict__ ptr,
                                                                       const int32_t* __restrict__ idx,
                                                                       const double* __restrict__ val,
                                                                       int32_t s_end, const Op op,
                                                                       double* __restrict__ red_out,
-                                                                      const uint8_t* __restrict__ rm = nullptr) {
+                                                                      const uint8_t* __restrict__ rm) {
   if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
-  constexpr bool MX = Op::kMax;
-  constexpr int C = kSChunk;
-  constexpr int U = C / 32;
   __shared__ double sprod[kWarps][R][C];
   __shared__ int32_t sidx[kRM ? kWarps : 1][kRM ? C : 1];
   double red[NR];
@@ -329,82 +412,102 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
   const int s0 = blockIdx.x * kBlock + warp * 32;
   const bool own = s < s_end;
   int b = 0, e = 0;
+  bool seg_order = false;
   typename Op::Pre pre{};
   if (own) {
     b = ptr[s];
     e = ptr[s + 1];
     pre = op.prefetch(s);
   }
+  if (kRM && s0 < s_end) seg_order = rm[s0 >> 5];  // warp-uniform
   pdl_wait_trigger();
   if (s0 < s_end) {  // warp-uniform
-    const int wb = ptr[s0];
-    const int we = ptr[s0 + 32 < s_end ? s0 + 32 : s_end];
+    const int wb = __shfl_sync(0xffffffffu, b, 0);
+    const int we = __shfl_sync(0xffffffffu, e, min(31, s_end - 1 - s0));
     double acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
-    double(*sp)[C] = sprod[warp];
-    const bool seg_order = kRM && rm[s0 >> 5];  // warp-uniform
-    for (int c0 = wb; c0 < we; c0 += C) {
-      int32_t j[U];
-      double v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = c0 + lane + 32 * u;
-        j[u] = k < we ? ld_stream(idx + k) : 0;
-        v[u] = k < we ? ld_stream(val + k) : 0.0;
-      }
-      if constexpr (kRM) {
-        if (seg_order) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            sidx[warp][lane + 32 * u] = j[u];
-            sp[0][lane + 32 * u] = v[u];
-          }
-          __syncwarp();
-          const int lo = (b > c0 ? b : c0) - c0;
-          const int hi = (e < c0 + C ? e : c0 + C) - c0;
-          constexpr int Q = 4;
-          int q = lo;
-          for (; q + Q <= hi; q += Q) {
-            double p[Q][R];
-#pragma unroll
-            for (int t = 0; t < Q; ++t) op.map(sidx[warp][q + t], sp[0][q + t], p[t]);
-#pragma unroll
-            for (int t = 0; t < Q; ++t)
-#pragma unroll
-              for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[t][r]);  // storage order
-          }
-          for (; q < hi; ++q) {
-            double p[R];
-            op.map(sidx[warp][q], sp[0][q], p);
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[r]);
-          }
-          __syncwarp();
-          continue;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (c0 + lane + 32 * u < we) {
-          double p[R];
-          op.map(j[u], v[u], p);
-#pragma unroll
-          for (int r = 0; r < R; ++r) sp[r][lane + 32 * u] = p[r];
-        }
-      }
-      __syncwarp();
-      const int lo = (b > c0 ? b : c0) - c0;
-      const int hi = (e < c0 + C ? e : c0 + C) - c0;
-      for (int q = lo; q < hi; ++q) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], sp[r][q]);  // storage order
-      }
-      __syncwarp();
-    }
+    staged_group<Op, kRM, C>(idx, val, op, b, e, wb, we, seg_order, sprod[warp], kRM ? sidx[warp] : nullptr, acc);
     if (own) op.finish(s, acc, pre, red);
   }
   block_reduce_out<Op>(red, red_out);
+}
+
+// persistent (Layout::s_flow; the per-iteration step Ops, no reductions):
+// the staged kernel's groups, but every warp walks a grid-strided sequence
+// of 32-segment groups and loads the NEXT group's offsets, segment-order flag
+// and epilogue operands while it streams and gathers the current one, so the
+// offsets' round trip overlaps the previous group's chain. Same sums, same
+// order: bit-identical with seg_thread_staged_kernel.
+template <class Op, bool kRM, int C, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) seg_thread_flow_kernel(const int32_t* __restrict__ ptr,
+                                                                       const int32_t* __restrict__ idx,
+                                                                       const double* __restrict__ val,
+                                                                       int32_t s_end, const Op op,
+                                                                       const uint8_t* __restrict__ rm) {
+  static_assert(Op::kRed == 0, "no per-CTA reduction slots in the persistent kernel");
+  if (skip_launch(op)) return;
+  constexpr int R = Op::kRhs;
+  __shared__ double sprod[kWarps][R][C];
+  __shared__ int32_t sidx[kRM ? kWarps : 1][kRM ? C : 1];
+  double red[1] = {0.0};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ngroups = (s_end + 31) >> 5;
+  const int stride = gridDim.x * kWarps;
+  using Pre = typename Op::Pre;
+  auto fetch = [&](int g, int& b, int& e, bool& so, Pre& pre) {
+    const int s = (g << 5) + lane;
+    if (g < ngroups && s < s_end) {
+      b = ptr[s];
+      e = ptr[s + 1];
+      pre = op.prefetch(s);
+    }
+    if (kRM && g < ngroups) so = rm[g];
+  };
+  int g = blockIdx.x * kWarps + warp;
+  int b = 0, e = 0;
+  bool so = false;
+  Pre pre{};
+  fetch(g, b, e, so, pre);
+  pdl_wait_trigger();
+  for (; g < ngroups; g += stride) {  // warp-uniform
+    int bn = 0, en = 0;
+    bool son = false;
+    Pre pren{};
+    fetch(g + stride, bn, en, son, pren);  // in flight while this group streams
+    const int s0 = g << 5, s = s0 + lane;
+    const int wb = __shfl_sync(0xffffffffu, b, 0);
+    const int we = __shfl_sync(0xffffffffu, e, min(31, s_end - 1 - s0));
+    double acc[R];
+    staged_group<Op, kRM, C>(idx, val, op, b, e, wb, we, so, sprod[warp], kRM ? sidx[warp] : nullptr, acc);
+    if (s < s_end) op.finish(s, acc, pre, red);
+    b = bn;
+    e = en;
+    so = son;
+    pre = pren;
+  }
+}
+
+// Grid of a persistent kernel: resident CTAs per SM x SMs (occupancy query,
+// cached per kernel and device), at most one CTA per kWarps groups.
+inline int flow_grid(const void* kernel, int groups) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  int dev = 0;
+  PDHG_CUDA(cudaGetDevice(&dev));
+  int v = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find({kernel, dev});
+    if (it != cache.end()) v = it->second;
+  }
+  if (!v) {
+    int per = 0, sms = 0;
+    PDHG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kBlock, 0));
+    PDHG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    v = std::max(1, per) * sms;
+    std::lock_guard<std::mutex> g(mu);
+    cache[{kernel, dev}] = v;
+  }
+  return std::max(1, std::min(v, (groups + kWarps - 1) / kWarps));
 }
 
 // pipelined (opt-in PDHG_S_PIPE=1; measured SLOWER than the register-staged
@@ -681,12 +784,21 @@ inline void launch_thread_class(const Layout& L, const Op& op, double* red, cuda
   const int g = L.nb_s();
   if constexpr (UniformOk<Op>::value) {
     const int32_t* p = L.ptr;
+    const bool pre = L.s_u < L.s1;
+#define PDHG_UNIFORM(LEN)                                                                                   \
+  case LEN:                                                                                                 \
+    if (pre)                                                                                                \
+      return launch_k(seg_thread_uniform_kernel<Op, LEN, true>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, \
+                      L.s_u);                                                                               \
+    return launch_k(seg_thread_uniform_kernel<Op, LEN, false>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p,  \
+                    L.s_u);
     switch (L.s_len) {
-      case 1: return launch_k(seg_thread_uniform_kernel<Op, 1>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
-      case 2: return launch_k(seg_thread_uniform_kernel<Op, 2>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
-      case 3: return launch_k(seg_thread_uniform_kernel<Op, 3>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
-      case 4: return launch_k(seg_thread_uniform_kernel<Op, 4>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
-      case 8: return launch_k(seg_thread_uniform_kernel<Op, 8>, g, kBlock, 0, st, pdl, L.idx, L.val, L.s1, op, red, p, L.s_u);
+      PDHG_UNIFORM(1)
+      PDHG_UNIFORM(2)
+      PDHG_UNIFORM(3)
+      PDHG_UNIFORM(4)
+      PDHG_UNIFORM(8)
+#undef PDHG_UNIFORM
       default: break;
     }
   }
@@ -704,14 +816,39 @@ inline void launch_thread_class(const Layout& L, const Op& op, double* red, cuda
       return;
     }
   }
-  if (L.s_staged && L.s_rm)
-    launch_k(seg_thread_staged_kernel<Op, true>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red,
-             static_cast<const uint8_t*>(L.s_rm));
-  else if (L.s_staged)
-    launch_k(seg_thread_staged_kernel<Op, false>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red,
-             static_cast<const uint8_t*>(nullptr));
-  else
+  if (!L.s_staged) {
     launch_k(seg_thread_kernel<Op>, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red);
+    return;
+  }
+  const uint8_t* rm = L.s_rm;
+  if constexpr (Op::kRed == 0) {
+    if (L.s_flow) {
+      const int groups = ceil_div(L.s1, 32);
+      auto go = [&](auto k) {
+        launch_k(k, flow_grid(reinterpret_cast<const void*>(k), groups), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1,
+                 op, rm);
+      };
+#define PDHG_FLOW(C, MINB)                                 \
+  if (L.s_chunk == C && L.s_flow == MINB) {                \
+    if (rm) go(seg_thread_flow_kernel<Op, true, C, MINB>); \
+    else go(seg_thread_flow_kernel<Op, false, C, MINB>);   \
+    return;                                                \
+  }
+      PDHG_FLOW(128, 3)
+      PDHG_FLOW(128, 4)
+      PDHG_FLOW(256, 3)
+      PDHG_FLOW(256, 4)
+#undef PDHG_FLOW
+    }
+  }
+  auto go = [&](auto k) { launch_k(k, g, kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, op, red, rm); };
+  if (L.s_chunk == 128) {
+    if (rm) go(seg_thread_staged_kernel<Op, true, 128>);
+    else go(seg_thread_staged_kernel<Op, false, 128>);
+  } else {
+    if (rm) go(seg_thread_staged_kernel<Op, true, 256>);
+    else go(seg_thread_staged_kernel<Op, false, 256>);
+  }
 }
 
 // Residency: kBlock-thread CTAs capped at 64 registers (4 CTAs = 1024

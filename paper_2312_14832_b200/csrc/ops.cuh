@@ -156,7 +156,6 @@ struct OpPrimal {
   const double* u;
   const Scalars* sc;
   int j_in_block;
-  int pol = 0;  // L2 hints (kPolOps | kPolAux | kPolNext)
   __device__ bool skip() const { return sc->halt != 0; }  // pipelined loop: block discarded
   __device__ void map(int32_t i, double v, double (&p)[1]) const { p[0] = v * y[i]; }
   static constexpr int kOcc = 5;
@@ -183,17 +182,17 @@ struct OpPrimal {
     Pre p;
     p.w = sc->inner_base + static_cast<double>(j_in_block);
     p.step = sc->eta / sc->omega;
-    p.x = ld_pol(x + s, pol, kPolOps);
-    p.c = ld_pol(c + s, pol, kPolOps);
-    p.l = kL ? ld_pol(l + s, pol, kPolOps) : sc->lb;
-    p.u = kU ? ld_pol(u + s, pol, kPolOps) : sc->ub;
-    p.xbar = (p.w == 0.0) ? 0.0 : ld_pol(xbar + s, pol, kPolOps);  // Reset() zeroes the average
+    p.x = x[s];
+    p.c = c[s];
+    p.l = kL ? l[s] : sc->lb;
+    p.u = kU ? u[s] : sc->ub;
+    p.xbar = (p.w == 0.0) ? 0.0 : xbar[s];  // Reset() zeroes the average
     return p;
   }
   __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double* red) const {
     const double xv = clamp_ref(p.x - p.step * (p.c - a[0]), p.l, p.u);
-    st_pol(xn + s, xv, pol, kPolNext);
-    st_pol(xbar + s, (p.w * p.xbar + xv) / (p.w + 1.0), pol, kPolAux);
+    xn[s] = xv;
+    xbar[s] = (p.w * p.xbar + xv) / (p.w + 1.0);
     if constexpr (kAdapt) {
       const double d = xv - p.x;  // AdaptStepSize (solver.cpp:312-315)
       red[0] += d * d;
@@ -223,7 +222,6 @@ struct OpDual {
   RowKind rk;  // equality rows (permuted order)
   const Scalars* sc;
   int j_in_block;
-  int pol = 0;  // L2 hints (kPolOps | kPolAux | kPolNext)
   __device__ bool skip() const { return sc->halt != 0; }
   __device__ void map(int32_t j, double v, double (&p)[1]) const { p[0] = v * xn[j]; }
   static constexpr int kOcc = 5;
@@ -246,18 +244,18 @@ struct OpDual {
     Pre p;
     p.w = sc->inner_base + static_cast<double>(j_in_block);
     p.step = sc->eta * sc->omega;
-    p.kx = ld_pol(kx + s, pol, kPolOps);
-    p.y = ld_pol(y + s, pol, kPolOps);
-    p.q = ld_pol(q + s, pol, kPolOps);
-    p.ybar = (p.w == 0.0) ? 0.0 : ld_pol(ybar + s, pol, kPolOps);
+    p.kx = kx[s];
+    p.y = y[s];
+    p.q = q[s];
+    p.ybar = (p.w == 0.0) ? 0.0 : ybar[s];
     return p;
   }
   __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double* red) const {
     const double v = p.y + p.step * (p.q - (2.0 * a[0] - p.kx));
     const double yv = rk.eq(s) ? v : max0_ref(v);
-    st_pol(yn + s, yv, pol, kPolNext);
-    st_pol(kxn + s, a[0], pol, kPolAux);
-    st_pol(ybar + s, (p.w * p.ybar + yv) / (p.w + 1.0), pol, kPolAux);
+    yn[s] = yv;
+    kxn[s] = a[0];
+    ybar[s] = (p.w * p.ybar + yv) / (p.w + 1.0);
     if constexpr (kAdapt) {
       const double d = yv - p.y;  // AdaptStepSize (solver.cpp:316-320)
       red[0] += d * d;

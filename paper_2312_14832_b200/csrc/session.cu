@@ -121,6 +121,10 @@ constexpr SegOrder kColOrder = kOrderNatural;
 // Mean class-S segment length from which the warp-staged S kernel is used.
 constexpr double kStagedMin = 3.0;
 
+// Mean class-S segment length under which the staged kernel steps 128
+// entries per warp instead of 256.
+constexpr double kChunkSmallMean = 4.0;
+
 // Class S (one thread per segment, storage-order sums -- bit-exact with the
 // reference) takes segments up to this length; past 32 they go through the
 // warp-staged kernel, whose coalesced chunks beat a warp per 33..64 segment
@@ -600,6 +604,17 @@ void Session::Permute(const DArray<int32_t>& ptr0, const DArray<int32_t>& idx0, 
     L.s_staged = L.s1 > 0 && static_cast<double>(se) >= staged_min * L.s1;
     const char* sp = std::getenv("PDHG_S_PIPE");  // "1": cp.async-pipelined variant (A/B, bit-identical; slower)
     L.s_pipe = L.s_staged && sp && sp[0] == '1';
+    // PDHG_S_FLOW=3|4: persistent staged kernel for the step passes (3 or 4
+    // CTAs per SM; 0 = off).
+    // Staged chunk: 128 entries per warp step when the class's segments
+    // average under kChunkSmallMean nonzeros (a 32-segment group then rarely
+    // fills more: half the registers, every gather of a chunk in flight),
+    // else 256. PDHG_S_CHUNK=128|256 overrides.
+    const char* sc = std::getenv("PDHG_S_CHUNK");
+    L.s_chunk = sc ? (std::atoi(sc) == 128 ? 128 : 256)
+                   : (L.s1 > 0 && static_cast<double>(se) < kChunkSmallMean * L.s1 ? 128 : 256);
+    const char* sf = std::getenv("PDHG_S_FLOW");
+    L.s_flow = (L.s_staged && !L.s_pipe && sf && (sf[0] == '3' || sf[0] == '4')) ? sf[0] - '0' : 0;
     // Segment-order warps of the staged kernel (shifted-copy segment groups).
     L.s_rm = nullptr;
     const char* rmo = std::getenv("PDHG_SEG_ORDER_WARPS");  // "0": off (A/B)
@@ -878,6 +893,25 @@ void Session::PartitionLong(Layout& L, Store& S) {
   const int g = ew_grid(ntiles + 1);
   k_part_seg<<<g, kEw, 0, st_>>>(L.ptr, lo, hi, nz1, ntiles, M.tile_begin, M.tile_seg);
   k_part_span<<<g, kEw, 0, st_>>>(L.ptr, hi, nz1, ntiles, M.tile_begin, M.tile_seg, M.head_first, M.tail_owner);
+  // Gather sweep (PDHG_TILE_SWEEP=0: off): tiles execute in the order of
+  // their first gathered index, stable (CMat::order).
+  const char* sw = std::getenv("PDHG_TILE_SWEEP");
+  if (ntiles > 1 && !(sw && sw[0] == '0')) {
+    DArray<int32_t> key, key2, iota;
+    key.alloc(ntiles);
+    key2.alloc(ntiles);
+    iota.alloc(ntiles);
+    S.order.alloc(ntiles, &arena_);
+    k_tile_first_index<<<ew_grid(ntiles), kEw, 0, st_>>>(M.tile_begin, L.idx, ntiles, key.p);
+    k_iota<<<ew_grid(ntiles), kEw, 0, st_>>>(iota.p, ntiles);
+    const int bits = 31;  // padded (sharded) indices can exceed nvec
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, key2.p, iota.p, S.order.p, ntiles, 0, bits, st_);
+    DArray<char> tmp2;
+    tmp2.alloc(tb);
+    PDHG_CUDA(cub::DeviceRadixSort::SortPairs(tmp2.p, tb, key.p, key2.p, iota.p, S.order.p, ntiles, 0, bits, st_));
+    M.order = S.order.p;
+  }
   Sync();
   check_launch("partition");
 }
@@ -977,7 +1011,6 @@ void Session::ComputeScaling(const pdhg_params& prm) {
 void Session::UniformBounds() {
   bnd_ = 0;
   lb_ = ub_ = 0.0;
-  if (const char* cp = std::getenv("PDHG_CACHE_POL")) cache_pol_ = std::atoi(cp) & 7;
   const char* env = std::getenv("PDHG_UNIFORM_BOUNDS");
   if (n_ == 0 || (env && env[0] == '0')) return;
   DArray<int> diff;
@@ -1105,7 +1138,7 @@ void Session::PrimalPass(Shard& h, int a, int b, int j) {
   const int64_t o = h.coff;
   run_pass(h.csc,
            OpPrimal<kAdapt, kBnd>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
-                                  scal_.p, j, cache_pol_},
+                                  scal_.p, j},
            RedSlots{kAdapt ? h.red[1].p : nullptr}, fork_);
 }
 
@@ -1132,12 +1165,12 @@ void Session::LaunchStep(int parity, int j, bool adapt) {
     if (adapt)
       run_pass(h.csr,
                OpDual<true>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
-                            h.rk, scal_.p, j, cache_pol_},
+                            h.rk, scal_.p, j},
                RedSlots{h.red[0].p}, fork_);
     else
       run_pass(h.csr,
                OpDual<false>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
-                             h.rk, scal_.p, j, cache_pol_},
+                             h.rk, scal_.p, j},
                RedSlots{}, fork_);
   }
   GatherY(y_[b].p);
@@ -1166,7 +1199,7 @@ void Session::RunSteps(int parity, int count, bool adapt) {
   Graph* g = nullptr;
   for (Graph& gg : graphs_)
     if (gg.steps == count && gg.parity == parity && gg.adapt == adapt) g = &gg;
-  if (!g && count >= 4) {
+  if (!g && count >= 4 && comm_->graphs()) {
     cudaGraph_t graph;
     const int64_t before = launches_;
     PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
@@ -1186,6 +1219,7 @@ void Session::RunSteps(int parity, int count, bool adapt) {
     const int64_t per = launches_csc() + launches_csr() +
                         (adapt ? static_cast<int64_t>(shards_.size()) + 1 + (shards_.size() > 1) : 0);
     launches_ += static_cast<int64_t>(count) * per;
+    trace_graph("steps", count);
     PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
   } else {
     for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
@@ -2028,7 +2062,8 @@ double Session::OpNorm(int iters, uint64_t seed) {
     const char* e = std::getenv("PDHG_POWER_GRAPH_STEPS");
     return e ? std::max(1, std::atoi(e)) : 1;
   }();
-  const int many = iters / kPowerSteps, rest = iters % kPowerSteps;
+  const bool graphs = comm_->graphs();  // loopback transport: eager steps
+  const int many = graphs ? iters / kPowerSteps : 0, rest = graphs ? iters % kPowerSteps : 0;
   if (many && !power_graph_) capture(kPowerSteps, &power_graph_);
   if (rest && !power_graph1_) capture(1, &power_graph1_);
   // The graphs never read the start vector's values, so they are captured
@@ -2049,8 +2084,11 @@ double Session::OpNorm(int iters, uint64_t seed) {
   Scalars sc{};
   sc.pw_norm = vnorm;
   PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
+  trace_graph("power", many);
   for (int it = 0; it < many; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph_, st_));
   for (int it = 0; it < rest; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph1_, st_));
+  if (!graphs)
+    for (int it = 0; it < iters; ++it) step();
   for (size_t k = 0; k < shards_.size(); ++k) {
     Shard& h = shards_[k];
     run_pass(h.csr, OpPowerStep<true>{u, scal_.p, 1, kv + h.roff}, RedSlots{h.red[0].p}, fork_);
@@ -2193,7 +2231,7 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
       const int64_t o = h.roff;
       run_pass(h.csr,
                OpDual<false>{x_[1].p, y_[0].p + o, y_[1].p + o, ybar_.p + o, kx_[0].p + o, kx_[1].p + o, q_s_.p + o,
-                             h.rk, scal_.p, i + 1, cache_pol_},
+                             h.rk, scal_.p, i + 1},
                RedSlots{}, fork_);
     }
     GatherY(y_[1].p);
@@ -2254,7 +2292,7 @@ void Session::TimeKernelsCold(int iters, double* ms_primal, double* ms_dual, dou
       const int64_t o = h.roff;
       run_pass(h.csr,
                OpDual<false>{x_[1].p, y_[0].p + o, y_[1].p + o, ybar_.p + o, kx_[0].p + o, kx_[1].p + o, q_s_.p + o,
-                             h.rk, scal_.p, i + 1, cache_pol_},
+                             h.rk, scal_.p, i + 1},
                RedSlots{}, fork_);
     }
     GatherY(y_[1].p);

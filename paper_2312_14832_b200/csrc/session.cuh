@@ -86,6 +86,7 @@ class Session {
     DArray<double> head, tail;
     DArray<unsigned> cnt;
     DArray<uint8_t> rm;  // staged class-S segment-order warp flags
+    DArray<int32_t> order;  // tile execution order (long class, gather sweep)
   };
   struct Shard {
     int block = 0;
@@ -125,6 +126,15 @@ class Session {
   double* HostStage(size_t at_least = 0);
   // Gathers for the next matrix pass (ghost entries only when the plan says
   // so) and full gathers for values leaving the session.
+  // PDHG_LOOP_TRACE=1: graph replays of a multi-rank session (collectives
+  // inside graphs run once per replay without a host call).
+  void trace_graph(const char* what, int64_t n) const {
+    static const bool on = [] {
+      const char* e = std::getenv("PDHG_LOOP_TRACE");
+      return e && e[0] == '1';
+    }();
+    if (on && world_ > 1) std::fprintf(stderr, "[loop] rank %d graph %s x%lld\n", rank_, what, (long long)n);
+  }
   void GatherX(double* v) { comm_->Exchange(v, gx_, st_); }
   void GatherY(double* v) { comm_->Exchange(v, gy_, st_); }
   void GatherXFull(double* v) { comm_->AllGather(v, pn_, st_); }
@@ -190,7 +200,6 @@ class Session {
   DArray<double> q_s_, q_o_, rs_;                          // mp_
   double c_norm_s_ = 0, q_norm_s_ = 0, c_norm_o_ = 0, q_norm_o_ = 0;
   int bnd_ = 0;               // uniform-bound bits (UniformBounds)
-  int cache_pol_ = 0;         // L2 hints of the step kernels (kPol*, PDHG_CACHE_POL)
   int modal_col_len_ = 0;     // columns: modal class-S length placed first (Layout::s_u), or 0
   bool bnd_all_ = false;      // original bounds equal the common scaled ones too
   double lb_ = 0.0, ub_ = 0.0;

@@ -389,6 +389,12 @@ __global__ void k_part_cand(const int32_t* p, int32_t lo, int32_t hi, int64_t nz
   }
 }
 
+// Sort key of the gather sweep: the gathered index of each tile's first
+// nonzero (tiles are never empty).
+__global__ void k_tile_first_index(const int32_t* tb, const int32_t* idx, int32_t ntiles, int32_t* key) {
+  GRID_STRIDE(t, (int64_t)ntiles) key[t] = idx[tb[t]];
+}
+
 __global__ void k_part_seg(const int32_t* p, int32_t lo, int32_t hi, int64_t nz1, int32_t ntiles, const int32_t* tb,
                            int32_t* ts) {
   GRID_STRIDE(t, (int64_t)ntiles + 1) {

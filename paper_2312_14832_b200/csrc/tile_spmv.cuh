@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kBlock, Op::kOcc) tile_kernel(const CMat M, co
   __shared__ int nlong;
   __shared__ int fin[2];
 
-  const int t = blockIdx.x;
+  const int t = M.order ? M.order[blockIdx.x] : static_cast<int>(blockIdx.x);
   const int tid = threadIdx.x, lane = tid & 31;
   const int kb = M.tile_begin[t];
   const int len = M.tile_begin[t + 1] - kb;

@@ -5,15 +5,13 @@ created with a loopback id (rpdlp.Shards.loopback, csrc/comm.cuh
 LoopbackComm): the session runs exactly its NCCL-mode path -- padded slices,
 ghost-only exchanges (pack, per-peer send/recv segments, unpack), per-rank
 check packs summed over ranks, rank 0's clock in the pack, the
-observer-abort reduction, collectives captured inside the block graphs --
-with device copies and rendezvous kernels in place of NCCL's transport.
+observer-abort reduction -- with device copies and event barriers in place
+of NCCL's transport.
 
-The rendezvous kernels of all ranks spin on one GPU at the same time, so each
-rank's streams need their own hardware work queue (a queue whose head waits
-on a spinning peer would deadlock, the false-dependency hazard NCCL documents
-for several communicators on one device): the tests run in a child process
-with CUDA_DEVICE_MAX_CONNECTIONS=32 and PDHG_FORK=0 (one stream per rank, no
-class side streams); the parent test only launches it.
+Device ordering between the ranks' streams uses CUDA events exchanged
+through the host rendezvous (no spinning kernels), so the ranks' sessions run
+their blocks eagerly instead of as CUDA graphs (Comm::graphs); the kernels
+are the same.
 
 Parity bar: every rank returns the same result, and it is bit-identical to
 the in-process shard mode (all shards in one session), which the
@@ -22,9 +20,6 @@ movement is not exercised here (one GPU per call in this environment).
 """
 from __future__ import annotations
 
-import os
-import subprocess
-import sys
 import threading
 
 import numpy as np
@@ -36,19 +31,6 @@ from paper_2312_14832_b200.rpdlp import GenMcf, GenPagerank, GenStaircase, GenTr
 from problems import config1, empty_rows_lp, mixed_bounds_lp
 
 pytestmark = pytest.mark.gpu
-CHILD = os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS") == "32"
-child_only = pytest.mark.skipif(not CHILD, reason="runs in the child process (test_loopback_suite)")
-
-
-def test_loopback_suite():
-    """Runs this module in a child with 32 hardware queues (see above)."""
-    if CHILD:
-        pytest.skip("the child runs the individual tests")
-    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32", PDHG_FORK="0")
-    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu"],
-                       capture_output=True, text=True, env=env, timeout=1500, cwd=os.path.dirname(__file__))
-    assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-3000:]
-    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-3000:]
 
 
 def run_ranks(p, params, world, observers=None, ghost=False):
@@ -94,7 +76,6 @@ CASES = {
 }
 
 
-@child_only
 @pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("name", list(CASES))
 def test_loopback_ranks_match_shard_mode(name, world):
@@ -108,7 +89,6 @@ def test_loopback_ranks_match_shard_mode(name, world):
         same(g, ref)
 
 
-@child_only
 def test_loopback_eight_ranks_ghost_exchange():
     """World 8 on the staircase: the ghost-only exchange (only boundary
     stages cross ranks) is chosen and reproduces the shard mode bit for bit."""
@@ -123,7 +103,6 @@ def test_loopback_eight_ranks_ghost_exchange():
         same(g, ref)
 
 
-@child_only
 def test_loopback_observer_on_rank0_only_aborts_every_rank():
     """only rank 0 has an observer (as under torchrun); its abort
     at the third check stops every rank -- the abort reduction stays paired."""
@@ -146,7 +125,6 @@ def test_loopback_observer_on_rank0_only_aborts_every_rank():
     assert len(seen) == 3
 
 
-@child_only
 def test_loopback_limits_and_restarts_match():
     """Iteration limit in the middle of a block, and a time limit decided by
     rank 0's clock: every rank stops after the same iteration."""

@@ -397,3 +397,23 @@ def test_pipelined_class_s_kernel_bit_identical(name, monkeypatch):
     assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
+
+
+@pytest.mark.parametrize("flow", ["3", "4"])
+@pytest.mark.parametrize("name", ["mcf", "staircase_d20", "pagerank"])
+def test_persistent_class_s_kernel_bit_identical(name, flow, monkeypatch):
+    """The persistent class-S kernel (engine.cuh seg_thread_flow_kernel,
+    PDHG_S_FLOW=3|4: next group's offsets and operands prefetched while the
+    current group streams) keeps the staged kernel's storage-order sums,
+    segment-order warps included: whole trajectories are bitwise identical."""
+    from test_gpu_kernels import CASES
+    p = CASES[name] if name in CASES else GenPagerank(20000, 0.85, 6, 3)
+    prm = SolverParams(eps=1e-6, iter_limit=3000)
+    runs = []
+    for flag in ("0", flow):
+        monkeypatch.setenv("PDHG_S_FLOW", flag)
+        runs.append(rpdlp.Solve(p, prm))
+    a, b = runs
+    assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)

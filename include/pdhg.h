@@ -151,6 +151,9 @@ typedef struct {
   int32_t csr_uniform_len; /* every short row has this many nonzeros (offsets
                               implicit, never read), else 0 */
   int32_t csc_uniform_len; /* same for short columns */
+  int32_t csr_split;       /* > 0: the short rows' step pass runs as two
+                              gather-window passes split at this column
+                              (PDHG_S_SPLIT), else 0 */
 } pdhg_session_stats;
 
 /* Distribution of K over shards: `world` balanced row blocks

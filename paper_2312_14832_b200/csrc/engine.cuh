@@ -57,6 +57,23 @@ struct Layout {
   int s_len = 0;                   // common class-S length (1,2,3,4,8) or 0
   int32_t s_u = 0;                 // s_len > 0: segments [0, s_u) have it (s_u = s1, or a kBlock multiple)
   CMat lng;                        // tile-engine view of [s3, nseg)
+  // Gather-window split of class S (Session::BuildSplit; step passes only):
+  // class S runs as two passes over copies of its entries -- those gathering
+  // below split_w, then those at or above it -- the second continuing the
+  // first's sums (`part`), so each pass gathers from half the vector, which
+  // then stays L2-resident. Storage order is kept: every segment's low
+  // entries precede its high ones (checked at setup), so the sums are
+  // bit-identical to the one-pass kernel.
+  struct Half {
+    int32_t* ptr = nullptr;
+    int32_t* idx = nullptr;
+    double* val = nullptr;
+    const uint8_t* rm = nullptr;
+    int chunk = kSChunkMax;
+  };
+  int32_t split_w = 0;  // 0: no split
+  Half lo, hi;
+  double* part = nullptr;  // s1 partial sums of the low pass
   int nb_s() const { return ceil_div(s1, kBlock); }
   int nb_m() const { return ceil_div(static_cast<int64_t>(s2 - s1) * 32, kBlock); }
   int nb_l() const { return ceil_div(s3 - s2, l_rpc); }
@@ -299,6 +316,38 @@ __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_
   block_reduce_out<Op>(red, red_out);
 }
 
+template <class T, class = void>
+struct HasInit : std::false_type {};
+template <class T>
+struct HasInit<T, std::void_t<decltype(std::declval<T>().init(0))>> : std::true_type {};
+
+// Ops of the gather-window split (Layout::split_w): the low pass runs the
+// step Op's products and stores each segment's partial sum; the high pass is
+// the step Op itself, its sums starting from that partial.
+template <class Op>
+struct OpSplitLo {
+  static constexpr int kRhs = 1, kRed = 0;
+  static constexpr bool kMax = Op::kMax;
+  struct Pre {};
+  Op op;
+  double* part;
+  __device__ bool skip() const { return skip_launch(op); }
+  __device__ void map(int32_t j, double v, double (&p)[1]) const { op.map(j, v, p); }
+  __device__ Pre prefetch(int32_t) const { return {}; }
+  __device__ void finish(int32_t s, const double (&a)[1], const Pre&, double*) const { part[s] = a[0]; }
+};
+template <class Op>
+struct OpSplitHi : Op {
+  static constexpr bool kUniform = false;
+  const double* part;
+  OpSplitHi(const Op& o, const double* p) : Op(o), part(p) {}
+  __device__ double init(int32_t s) const { return part[s]; }
+};
+template <class T, class = void>
+struct SplitOk : std::false_type {};
+template <class T>
+struct SplitOk<T, std::void_t<decltype(T::kSplit)>> : std::integral_constant<bool, T::kSplit> {};
+
 // staged (longer short segments, e.g. 20-nonzero staircase rows): the 32
 // segments of a warp are contiguous in the nonzero stream, so the warp
 // streams that range in chunks of C entries (C = 128 or 256 by the class's
@@ -327,9 +376,7 @@ __device__ __forceinline__ void staged_group(const int32_t* __restrict__ idx, co
   constexpr int R = Op::kRhs;
   constexpr bool MX = Op::kMax;
   constexpr int U = C / 32;
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = 0.0;
+  const int lane = threadIdx.x & 31;  // acc holds the starting values (0, or a split pass's partial)
   for (int c0 = wb; c0 < we; c0 += C) {
     int32_t j[U];
     double v[U];
@@ -414,17 +461,20 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
   int b = 0, e = 0;
   bool seg_order = false;
   typename Op::Pre pre{};
+  double acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.0;
   if (own) {
     b = ptr[s];
     e = ptr[s + 1];
     pre = op.prefetch(s);
+    if constexpr (HasInit<Op>::value) acc[0] = op.init(s);  // split high pass: the low pass's partial
   }
   if (kRM && s0 < s_end) seg_order = rm[s0 >> 5];  // warp-uniform
   pdl_wait_trigger();
   if (s0 < s_end) {  // warp-uniform
     const int wb = __shfl_sync(0xffffffffu, b, 0);
     const int we = __shfl_sync(0xffffffffu, e, min(31, s_end - 1 - s0));
-    double acc[R];
     staged_group<Op, kRM, C>(idx, val, op, b, e, wb, we, seg_order, sprod[warp], kRM ? sidx[warp] : nullptr, acc);
     if (own) op.finish(s, acc, pre, red);
   }
@@ -477,6 +527,8 @@ __global__ void __launch_bounds__(kBlock, MINB) seg_thread_flow_kernel(const int
     const int wb = __shfl_sync(0xffffffffu, b, 0);
     const int we = __shfl_sync(0xffffffffu, e, min(31, s_end - 1 - s0));
     double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
     staged_group<Op, kRM, C>(idx, val, op, b, e, wb, we, so, sprod[warp], kRM ? sidx[warp] : nullptr, acc);
     if (s < s_end) op.finish(s, acc, pre, red);
     b = bn;
@@ -964,6 +1016,36 @@ __global__ void __launch_bounds__(kBlock, kCtaMinBlocks)
   block_reduce_out<Op, NW>(red, red_out);
 }
 
+// Class S of a pass, as one kernel or -- gather-window split, step Ops --
+// as the low and high passes (Layout::split_w).
+template <class Op>
+inline void launch_class_s(const Layout& L, const Op& op, double* red, cudaStream_t st, bool pdl) {
+  if constexpr (SplitOk<Op>::value) {
+    if (L.split_w) {
+      Layout h = L;
+      h.s_len = 0;
+      h.s_u = 0;
+      h.s_flow = 0;
+      h.s_pipe = false;
+      h.s_staged = true;
+      h.ptr = L.lo.ptr;
+      h.idx = L.lo.idx;
+      h.val = L.lo.val;
+      h.s_rm = L.lo.rm;
+      h.s_chunk = L.lo.chunk;
+      launch_thread_class(h, OpSplitLo<Op>{op, L.part}, nullptr, st, pdl);
+      h.ptr = L.hi.ptr;
+      h.idx = L.hi.idx;
+      h.val = L.hi.val;
+      h.s_rm = L.hi.rm;
+      h.s_chunk = L.hi.chunk;
+      launch_thread_class(h, OpSplitHi<Op>(op, L.part), red, st, false);
+      return;
+    }
+  }
+  launch_thread_class(L, op, red, st, pdl);
+}
+
 template <class Op>
 inline void launch_cta_class(const Layout& L, const Op& op, double* red, cudaStream_t st, bool pdl = false) {
   if (L.l_rpc == 4 && L.l_stage > 0) {
@@ -1006,7 +1088,7 @@ inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, cudaStr
   const int nclass = (L.s1 > 0) + (L.s2 > L.s1) + (L.s3 > L.s2) + (L.nseg > L.s3);
   const bool pdl = PdlOk<Op>::value && nclass == 1 && pdl_enabled();
   int64_t slot = 0;
-  if (L.s1 > 0) launch_thread_class(L, op, red.at(slot, nr), st, pdl);
+  if (L.s1 > 0) launch_class_s(L, op, red.at(slot, nr), st, pdl);
   slot += L.nb_s();
   if (L.s2 > L.s1)
     launch_k(seg_warp_kernel<Op>, L.nb_m(), kBlock, 0, st, pdl, L.ptr, L.idx, L.val, L.s1, L.s2, op,
@@ -1048,7 +1130,7 @@ inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, const F
     ++k;
   }
   int64_t slot = 0;
-  if (has[0]) launch_thread_class(L, op, red.at(slot, nr), on[0]);
+  if (has[0]) launch_class_s(L, op, red.at(slot, nr), on[0], false);
   slot += L.nb_s();
   if (has[1])
     seg_warp_kernel<Op><<<L.nb_m(), kBlock, 0, on[1]>>>(L.ptr, L.idx, L.val, L.s1, L.s2, op, red.at(slot, nr));
@@ -1069,7 +1151,7 @@ inline void run_pass(const Layout& L, const Op& op, const RedSlots& red, const F
 
 // Number of kernels run_pass launches.
 inline int pass_launches(const Layout& L) {
-  return (L.s1 > 0) + (L.s2 > L.s1) + (L.s3 > L.s2) + (L.nseg > L.s3);
+  return (L.s1 > 0) * (L.split_w ? 2 : 1) + (L.s2 > L.s1) + (L.s3 > L.s2) + (L.nseg > L.s3);
 }
 
 }  // namespace pdhg

@@ -209,6 +209,7 @@ struct OpDual {
   static constexpr bool kMax = false;
   static constexpr bool kUniform = true;
   static constexpr bool kPdl = true;
+  static constexpr bool kSplit = !kAdapt;  // gather-window split of class S (engine.cuh launch_class_s)
   struct Pre {
     double kx, y, q, ybar, w, step;
   };

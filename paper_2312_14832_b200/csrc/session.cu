@@ -267,7 +267,8 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
     phase("scaling");
     DeviceNorms();
     UniformBounds();
-    phase("norms+bounds");
+    for (Shard& h : shards_) BuildSplit(h.csr, h.csr_st);
+    phase("norms+bounds+split");
     const double iter_bytes = (24.0 * nnz_ + 68.0 * (m_ + n_)) / world_;
     l2_resident_ = iter_bytes < 100e6;
     Sync();
@@ -833,6 +834,73 @@ void Session::GhostCounts(int64_t* x_counts, int64_t* y_counts, int32_t* use) co
   std::copy(ghost_counts_y_.begin(), ghost_counts_y_.end(), y_counts);
   use[0] = gx_.use;
   use[1] = gy_.use;
+}
+
+// Gather-window split of class S (Layout::split_w; PDHG_S_SPLIT=1 on, 0 off,
+// default: off). Built from the SCALED values, for one-shard sessions whose
+// staged class S gathers from a vector larger than the ~64 MB that random
+// gathers keep L2-resident (tools/gather_probe.cu: 190 G gathers/s up to
+// 59 MB, 140 G/s at 84 MB). Skipped when any segment's entries would be
+// reordered by the split.
+void Session::BuildSplit(Layout& L, Store& S) {
+  L.split_w = 0;
+  const char* e = std::getenv("PDHG_S_SPLIT");
+  const bool on = e && e[0] == '1';
+  const char* mb = std::getenv("PDHG_S_SPLIT_MIN_MB");  // vector-size threshold (tests: 0)
+  const int64_t min_bytes = (mb ? std::atoll(mb) : 64) << 20;
+  if (!on || world_ != 1 || !L.s_staged || L.s1 < kBlock || static_cast<int64_t>(L.nvec) * 8 <= min_bytes) return;
+  const int32_t w = (L.nvec / 2 + 31) / 32 * 32;
+  DArray<int32_t> cnt;
+  DArray<int> bad;
+  cnt.alloc(L.s1 + 1);
+  bad.alloc(1);
+  PDHG_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st_));
+  PDHG_CUDA(cudaMemsetAsync(cnt.p + L.s1, 0, sizeof(int32_t), st_));
+  k_split_count<<<ew_grid(L.s1), kEw, 0, st_>>>(L.ptr, L.idx, L.s1, w, cnt.p, bad.p);
+  int hbad = 0;
+  PDHG_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+  Sync();
+  if (hbad) return;
+  S.lo_ptr.alloc(L.s1 + 1, &arena_);
+  S.hi_ptr.alloc(L.s1 + 1, &arena_);
+  scan_exclusive(cnt.p, S.lo_ptr.p, L.s1 + 1, st_);
+  int32_t nlo = 0, ns = 0;
+  PDHG_CUDA(cudaMemcpyAsync(&nlo, S.lo_ptr.p + L.s1, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+  PDHG_CUDA(cudaMemcpyAsync(&ns, L.ptr + L.s1, sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+  Sync();
+  S.lo_idx.alloc(std::max(nlo, 1), &arena_);
+  S.lo_val.alloc(std::max(nlo, 1), &arena_);
+  S.hi_idx.alloc(std::max(ns - nlo, 1), &arena_);
+  S.hi_val.alloc(std::max(ns - nlo, 1), &arena_);
+  S.split_part.alloc(L.s1, &arena_);
+  k_split_copy<<<ew_grid(L.s1 + 1), kEw, 0, st_>>>(L.ptr, L.idx, L.val, L.s1, S.lo_ptr.p, S.lo_idx.p, S.lo_val.p,
+                                                   S.hi_ptr.p, S.hi_idx.p, S.hi_val.p);
+  auto half = [&](Layout::Half& hf, DArray<int32_t>& ptr, DArray<int32_t>& idx, DArray<double>& val,
+                  DArray<uint8_t>& rm, int64_t nnz) {
+    hf.ptr = ptr.p;
+    hf.idx = idx.p;
+    hf.val = val.p;
+    hf.chunk = static_cast<double>(nnz) < kChunkSmallMean * L.s1 ? 128 : 256;
+    hf.rm = nullptr;
+    if (L.s_rm) {  // segment-order warps, judged on this half's entries
+      const int64_t ng = (static_cast<int64_t>(L.s1) + 31) / 32;
+      rm.alloc(ng, &arena_);
+      DArray<int> any;
+      any.alloc(1);
+      PDHG_CUDA(cudaMemsetAsync(any.p, 0, sizeof(int), st_));
+      k_rowmajor_flags<<<ew_grid(ng), kEw, 0, st_>>>(ptr.p, idx.p, L.s1, rm.p, any.p);
+      int hany = 0;
+      PDHG_CUDA(cudaMemcpyAsync(&hany, any.p, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      Sync();
+      if (hany) hf.rm = rm.p;
+    }
+  };
+  half(L.lo, S.lo_ptr, S.lo_idx, S.lo_val, S.lo_rm, nlo);
+  half(L.hi, S.hi_ptr, S.hi_idx, S.hi_val, S.hi_rm, ns - nlo);
+  L.part = S.split_part.p;
+  L.split_w = w;
+  Sync();
+  check_launch("class-S split");
 }
 
 // Tile partition of the extra-long class [s3, nseg) of one layout (tile_spmv.cuh):
@@ -2527,6 +2595,7 @@ void Session::Stats(pdhg_session_stats* s) const {
   };
   s->csr_uniform_len = all_uniform(true);
   s->csc_uniform_len = all_uniform(false);
+  s->csr_split = shards_.size() == 1 ? shards_[0].csr.split_w : 0;
 }
 
 void Session::Blocks(int64_t* row_begin, int64_t* col_begin) const {

@@ -87,6 +87,9 @@ class Session {
     DArray<unsigned> cnt;
     DArray<uint8_t> rm;  // staged class-S segment-order warp flags
     DArray<int32_t> order;  // tile execution order (long class, gather sweep)
+    DArray<int32_t> lo_ptr, lo_idx, hi_ptr, hi_idx;  // gather-window split of class S
+    DArray<double> lo_val, hi_val, split_part;
+    DArray<uint8_t> lo_rm, hi_rm;
   };
   struct Shard {
     int block = 0;
@@ -110,6 +113,7 @@ class Session {
   void PrimalPass(Shard& h, int a, int b, int j);
   void LaunchPrimal(Shard& h, int a, int b, int j, bool adapt);
   void UniformBounds();
+  void BuildSplit(Layout& L, Store& S);
   void DrawStart(uint64_t seed);
   void RunSteps(int parity, int count, bool adapt);
   void RunBlock(int parity, int count, bool adapt, bool check, int slot);

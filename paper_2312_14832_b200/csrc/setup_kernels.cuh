@@ -389,6 +389,47 @@ __global__ void k_part_cand(const int32_t* p, int32_t lo, int32_t hi, int64_t nz
   }
 }
 
+// Gather-window split of class S (Session::BuildSplit): per segment, the
+// number of entries gathering below w, and a flag when an entry at or above
+// w precedes one below it (the split would reorder that segment's sum).
+__global__ void k_split_count(const int32_t* p, const int32_t* idx, int32_t s1, int32_t w, int32_t* cnt, int* bad) {
+  GRID_STRIDE(s, s1) {
+    int c = 0;
+    bool high = false, viol = false;
+    for (int32_t k = p[s]; k < p[s + 1]; ++k) {
+      if (idx[k] < w) {
+        ++c;
+        viol |= high;
+      } else {
+        high = true;
+      }
+    }
+    cnt[s] = c;
+    if (viol) atomicOr(bad, 1);
+  }
+}
+// Copies each segment's low entries to [plo[s], plo[s + 1]) and its high
+// entries to [p[s] - plo[s], ...) of the two halves, storage order kept.
+__global__ void k_split_copy(const int32_t* p, const int32_t* idx, const double* val, int32_t s1,
+                             const int32_t* plo, int32_t* ilo, double* vlo, int32_t* phi, int32_t* ihi, double* vhi) {
+  GRID_STRIDE(s, (int64_t)s1 + 1) {
+    const int32_t b = p[s], lo = plo[s];
+    phi[s] = b - lo;
+    if (s < s1) {
+      const int32_t nlo = plo[s + 1] - lo;
+      for (int32_t k = 0; k < p[s + 1] - b; ++k) {
+        if (k < nlo) {
+          ilo[lo + k] = idx[b + k];
+          vlo[lo + k] = val[b + k];
+        } else {
+          ihi[b - lo + k - nlo] = idx[b + k];
+          vhi[b - lo + k - nlo] = val[b + k];
+        }
+      }
+    }
+  }
+}
+
 // Sort key of the gather sweep: the gathered index of each tile's first
 // nonzero (tiles are never empty).
 __global__ void k_tile_first_index(const int32_t* tb, const int32_t* idx, int32_t ntiles, int32_t* key) {

@@ -417,3 +417,27 @@ def test_persistent_class_s_kernel_bit_identical(name, flow, monkeypatch):
     assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
+
+
+@pytest.mark.parametrize("name", ["mcf", "pagerank", "config1"])
+def test_class_s_window_split_bit_identical(name, monkeypatch):
+    """Gather-window split of class S (engine.cuh launch_class_s, PDHG_S_SPLIT=1;
+    the vector-size threshold lowered to 0 so small instances take it): the
+    low pass's partial sums continue in the high pass in storage order, so
+    whole trajectories are bitwise identical to the one-pass kernel."""
+    from test_gpu_kernels import CASES
+    from problems import config1
+    p = {"mcf": lambda: CASES["mcf"], "pagerank": lambda: GenPagerank(20000, 0.85, 6, 3),
+         "config1": lambda: config1(2)}[name]()
+    prm = SolverParams(eps=1e-6, iter_limit=3000)
+    runs = []
+    monkeypatch.setenv("PDHG_S_SPLIT_MIN_MB", "0")
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PDHG_S_SPLIT", flag)
+        with rpdlp.Session(p, prm) as s:
+            assert (s.stats().csr_split > 0) == (flag == "1")
+            runs.append(s.solve(prm))
+    a, b = runs
+    assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)

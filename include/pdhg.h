@@ -154,6 +154,8 @@ typedef struct {
   int32_t csr_split;       /* > 0: the short rows' step pass runs as two
                               gather-window passes split at this column
                               (PDHG_S_SPLIT), else 0 */
+  int32_t block_kernel;    /* 1: step blocks run as one persistent launch
+                              (transport-shaped layouts; PDHG_PERSIST=0 off) */
 } pdhg_session_stats;
 
 /* Distribution of K over shards: `world` balanced row blocks

@@ -72,7 +72,8 @@ class SessionStats(C.Structure):
                 ("upload_seconds", C.c_double), ("scaling_seconds", C.c_double), ("device", C.c_int32),
                 ("l2_resident", C.c_int32), ("world", C.c_int32), ("local_shards", C.c_int32),
                 ("rank", C.c_int32), ("uniform_bounds", C.c_int32),
-                ("csr_uniform_len", C.c_int32), ("csc_uniform_len", C.c_int32), ("csr_split", C.c_int32)]
+                ("csr_uniform_len", C.c_int32), ("csc_uniform_len", C.c_int32), ("csr_split", C.c_int32),
+                ("block_kernel", C.c_int32)]
 
 
 class ShardSpec(C.Structure):

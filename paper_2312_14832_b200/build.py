@@ -54,7 +54,7 @@ CPP_SRCS = ["instance_gen.cpp", "rpdlp_api.cpp", "mps.cpp"] + (["bench.cpp"] if 
 DROPIN_TEST = ROOT / "tests" / "cpp" / "drop_in_test.cpp"
 DROPIN_BIN = BUILD / "drop_in_test"
 CLI_BIN = BUILD / "rpdlp-b200"
-HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh", "tma.cuh", "host_logic.h", "engine.cuh", "setup_kernels.cuh", "comm.cuh", "normal_rng.h", "assemble.cuh"]
+HEADERS = ["common.cuh", "tile_spmv.cuh", "ops.cuh", "session.cuh", "darray.cuh", "tma.cuh", "host_logic.h", "engine.cuh", "setup_kernels.cuh", "comm.cuh", "normal_rng.h", "assemble.cuh", "persist.cuh"]
 
 
 def _newer(target: Path, deps) -> bool:

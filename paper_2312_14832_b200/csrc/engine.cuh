@@ -118,7 +118,8 @@ __device__ __forceinline__ double warp_reduce_scatter(const double (&v)[K], int*
 }
 
 template <class Op, int NW = kWarps>
-__device__ __forceinline__ void block_reduce_out(double (&red)[Op::kRed > 0 ? Op::kRed : 1], double* out) {
+__device__ __forceinline__ void block_reduce_out(double (&red)[Op::kRed > 0 ? Op::kRed : 1], double* out,
+                                                 int slot = -1) {
   if constexpr (Op::kRed > 0) {
     __shared__ double sh[NW][Op::kRed];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -135,7 +136,7 @@ __device__ __forceinline__ void block_reduce_out(double (&red)[Op::kRed > 0 ? Op
     if (threadIdx.x < Op::kRed) {
       double v = sh[0][threadIdx.x];
       for (int w = 1; w < NW; ++w) v += sh[w][threadIdx.x];
-      out[static_cast<int64_t>(blockIdx.x) * Op::kRed + threadIdx.x] = v;
+      out[static_cast<int64_t>(slot < 0 ? static_cast<int>(blockIdx.x) : slot) * Op::kRed + threadIdx.x] = v;
     }
   }
 }
@@ -243,10 +244,10 @@ __device__ __forceinline__ void load_uniform(const int32_t* __restrict__ idx, co
 template <class Op>
 __device__ __forceinline__ void seg_thread_direct(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
                                                   const double* __restrict__ val, int32_t s_end, const Op& op,
-                                                  double (&red)[Op::kRed > 0 ? Op::kRed : 1]) {
+                                                  double (&red)[Op::kRed > 0 ? Op::kRed : 1], int blk) {
   constexpr int R = Op::kRhs;
   constexpr bool MX = Op::kMax;
-  const int s = blockIdx.x * kBlock + threadIdx.x;
+  const int s = blk * kBlock + threadIdx.x;
   int b = 0, e = 0;
   typename Op::Pre pre{};
   if (s < s_end) {
@@ -269,14 +270,13 @@ __device__ __forceinline__ void seg_thread_direct(const int32_t* __restrict__ pt
   }
 }
 
-// kPrefix: the modal-prefix variant (the plain one carries no direct path,
-// which would cost the all-uniform transport primal 8 registers and a
-// quarter of its occupancy: 10.3 -> 12.3 us).
+// One CTA's worth (block `blk`: segments [blk * kBlock, +kBlock)) of the
+// uniform kernel; the kernel runs it for blockIdx.x, the persistent block
+// kernel (persist.cuh) for the blocks it is dealt.
 template <class Op, int L, bool kPrefix>
-__global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_t* __restrict__ idx,
-                                                                    const double* __restrict__ val, int32_t s_end,
-                                                                    const Op op, double* __restrict__ red_out,
-                                                                    const int32_t* __restrict__ ptr, int32_t s_u) {
+__device__ __forceinline__ void uniform_item(int blk, const int32_t* __restrict__ idx, const double* __restrict__ val,
+                                             int32_t s_end, const Op& op, double* __restrict__ red_out,
+                                             const int32_t* __restrict__ ptr, int32_t s_u) {
   if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
@@ -285,13 +285,13 @@ __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
   if constexpr (kPrefix) {
-    if (static_cast<int>(blockIdx.x) * kBlock >= s_u) {  // CTA-uniform: past the modal prefix
-      seg_thread_direct(ptr, idx, val, s_end, op, red);
-      block_reduce_out<Op>(red, red_out);
+    if (blk * kBlock >= s_u) {  // CTA-uniform: past the modal prefix
+      seg_thread_direct(ptr, idx, val, s_end, op, red, blk);
+      block_reduce_out<Op>(red, red_out, blk);
       return;
     }
   }
-  const int s = blockIdx.x * kBlock + threadIdx.x;
+  const int s = blk * kBlock + threadIdx.x;
   typename Op::Pre pre{};
   int32_t j[L];
   double v[L];
@@ -313,7 +313,18 @@ __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_
       for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[u][r]);  // storage order
     op.finish(s, acc, pre, red);
   }
-  block_reduce_out<Op>(red, red_out);
+  block_reduce_out<Op>(red, red_out, blk);
+}
+
+// kPrefix: the modal-prefix variant (the plain one carries no direct path,
+// which would cost the all-uniform transport primal 8 registers and a
+// quarter of its occupancy: 10.3 -> 12.3 us).
+template <class Op, int L, bool kPrefix>
+__global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_t* __restrict__ idx,
+                                                                    const double* __restrict__ val, int32_t s_end,
+                                                                    const Op op, double* __restrict__ red_out,
+                                                                    const int32_t* __restrict__ ptr, int32_t s_u) {
+  uniform_item<Op, L, kPrefix>(static_cast<int>(blockIdx.x), idx, val, s_end, op, red_out, ptr, s_u);
 }
 
 template <class T, class = void>
@@ -921,11 +932,38 @@ constexpr int kCtaStageMax = 50 * 1024;
 // per-thread order (k = b + t, b + t + T, ...) and the same trees as
 // seg_cta_kernel<Op, 4>, hence bit-identical results. Used when every
 // 4-segment group fits kCtaStageMax (Layout::l_stage).
-template <class Op>
-__global__ void __launch_bounds__(kBlock, kCtaMinBlocks)
-    seg_cta4_staged_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-                           const double* __restrict__ val, int32_t s_begin, int32_t s_end, const Op op,
-                           double* __restrict__ red_out) {
+// One 4-segment group (block `blk`) of the staged kernel, with its shared
+// memory passed in: the kernel runs it for blockIdx.x; the persistent block
+// kernel (persist.cuh) for each group it is dealt, reusing the stage buffer
+// and barrier (`reuse`: wait until every thread is done with the previous
+// group's stage before the bulk copy overwrites it).
+// Thread 0 of the group's CTA: initialise the barrier and start the bulk
+// copies of group `blk`'s contiguous (val, idx) range into `stage`.
+__device__ __forceinline__ void cta4_issue(int blk, const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                           const double* __restrict__ val, int32_t s_begin, int32_t s_end,
+                                           unsigned char* stage, uint64_t* bar) {
+  const int g0 = s_begin + blk * 4;
+  const int g1 = min(g0 + 4, s_end);
+  const int32_t lo = ptr[g0], hi = ptr[g1];
+  uint32_t bv = 0, bi = 0;
+  const int64_t av = widen16<double>(lo, hi, &bv);
+  const int64_t ai = widen16<int32_t>(lo, hi, &bi);
+  mbar_init(bar, 1);
+  mbar_expect_tx(bar, hi > lo ? bv + bi : 0);
+  if (hi > lo) {
+    bulk_g2s(stage, val + av, bv, bar);
+    bulk_g2s(stage + bv, idx + ai, bi, bar);
+  }
+}
+
+// kIssued: the caller already ran cta4_issue for this group (the persistent
+// block kernel starts a CTA's first group before the grid barrier: the
+// matrix does not depend on the step it waits for).
+template <class Op, bool kReuse = false, bool kIssued = false>
+__device__ __forceinline__ void cta4_item(int blk, const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                          const double* __restrict__ val, int32_t s_begin, int32_t s_end, const Op& op,
+                                          double* __restrict__ red_out, unsigned char* stage, uint64_t* bar,
+                                          double (*sh)[4][Op::kRhs]) {
   if (skip_launch(op)) return;
   constexpr int RPC = 4;
   constexpr int R = Op::kRhs;
@@ -934,15 +972,12 @@ __global__ void __launch_bounds__(kBlock, kCtaMinBlocks)
   constexpr int T = kBlock / RPC;
   constexpr int NW = kBlock / 32;
   constexpr int U = kStrideUnroll;
-  extern __shared__ __align__(16) unsigned char stage[];
-  __shared__ uint64_t bar;
-  __shared__ double sh[NW][RPC][R];
   double red[NR];
 #pragma unroll
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane % RPC, t = warp * (32 / RPC) + lane / RPC;
-  const int g0 = s_begin + blockIdx.x * RPC;
+  const int g0 = s_begin + blk * RPC;
   const int g1 = min(g0 + RPC, s_end);
   const int32_t lo = ptr[g0], hi = ptr[g1];
   uint32_t bv = 0, bi = 0;
@@ -950,14 +985,11 @@ __global__ void __launch_bounds__(kBlock, kCtaMinBlocks)
   const int64_t ai = widen16<int32_t>(lo, hi, &bi);
   double* sval = reinterpret_cast<double*>(stage);
   int32_t* sidx = reinterpret_cast<int32_t*>(stage + bv);
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, hi > lo ? bv + bi : 0);
-    if (hi > lo) {
-      bulk_g2s(sval, val + av, bv, &bar);
-      bulk_g2s(sidx, idx + ai, bi, &bar);
-    }
+  if constexpr (kReuse && !kIssued) {
+    __syncthreads();  // the previous group's readers are done with the stage
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
+  if (!kIssued && threadIdx.x == 0) cta4_issue(blk, ptr, idx, val, s_begin, s_end, stage, bar);
   const int s = g0 + sub;
   const bool own = s < s_end;
   typename Op::Pre pre{};
@@ -969,7 +1001,7 @@ __global__ void __launch_bounds__(kBlock, kCtaMinBlocks)
   }
   __syncthreads();  // barrier initialised
   pdl_wait_trigger();
-  mbar_wait(&bar, 0);
+  mbar_wait(bar, 0);
   double acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = 0.0;
@@ -1013,7 +1045,18 @@ __global__ void __launch_bounds__(kBlock, kCtaMinBlocks)
     }
     op.finish(s, acc, pre, red);
   }
-  block_reduce_out<Op, NW>(red, red_out);
+  block_reduce_out<Op, NW>(red, red_out, blk);
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kBlock, kCtaMinBlocks)
+    seg_cta4_staged_kernel(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                           const double* __restrict__ val, int32_t s_begin, int32_t s_end, const Op op,
+                           double* __restrict__ red_out) {
+  extern __shared__ __align__(16) unsigned char stage[];
+  __shared__ uint64_t bar;
+  __shared__ double sh[kBlock / 32][4][Op::kRhs];
+  cta4_item<Op>(static_cast<int>(blockIdx.x), ptr, idx, val, s_begin, s_end, op, red_out, stage, &bar, sh);
 }
 
 // Class S of a pass, as one kernel or -- gather-window split, step Ops --

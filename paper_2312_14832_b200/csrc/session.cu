@@ -268,6 +268,8 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
     DeviceNorms();
     UniformBounds();
     for (Shard& h : shards_) BuildSplit(h.csr, h.csr_st);
+    persist_ = PersistOk();
+    if (persist_) gbar_.alloc(1, &arena_);
     phase("norms+bounds+split");
     const double iter_bytes = (24.0 * nnz_ + 68.0 * (m_ + n_)) / world_;
     l2_resident_ = iter_bytes < 100e6;
@@ -1261,17 +1263,74 @@ void Session::SumPacks(int n, const Scalars* guard) {
   comm_->AllReduceSum(red_out_.p, n, st_);
 }
 
+// Persistent block kernel eligibility (persist.cuh; opt-in PDHG_PERSIST=1,
+// measured slower): one shard, one device, the K-CSC entirely one
+// uniform-length class S, the K-CSR entirely one class L of 4-row
+// TMA-staged groups (transportation / assignment shapes), no class-S
+// variants that change the pass structure.
+bool Session::PersistOk() const {
+  const char* e = std::getenv("PDHG_PERSIST");
+  if (!(e && e[0] == '1') || world_ != 1 || shards_.size() != 1 || !comm_->local()) return false;
+  const Layout& c = shards_[0].csc;
+  const Layout& r = shards_[0].csr;
+  const bool csc_ok = c.nseg > 0 && c.s1 == c.nseg && c.s_len > 0 && c.split_w == 0;
+  const bool csr_ok = r.nseg > 0 && r.s1 == 0 && r.s2 == 0 && r.s3 == r.nseg && r.l_rpc == 4 && r.l_stage > 0;
+  return csc_ok && csr_ok;
+}
+
+template <int kBnd>
+void Session::LaunchBlockT(int parity, int count) {
+  Shard& h = shards_[0];
+  BlockArgs<OpPrimal<false, kBnd>, OpDual<false>> a{};
+  a.p_idx = h.csc.idx;
+  a.p_val = h.csc.val;
+  a.p_ptr = h.csc.ptr;
+  a.p_send = h.csc.s1;
+  a.p_su = h.csc.s_u;
+  a.p_nb = h.csc.nb_s();
+  a.d_ptr = h.csr.ptr;
+  a.d_idx = h.csr.idx;
+  a.d_val = h.csr.val;
+  a.d_s2 = h.csr.s2;
+  a.d_s3 = h.csr.s3;
+  a.d_nb = h.csr.nb_l();
+  for (int q = 0; q < 2; ++q) {
+    const int x0 = q, x1 = 1 - q;
+    a.opp[q] = OpPrimal<false, kBnd>{y_[x0].p, x_[x0].p + h.coff, x_[x1].p + h.coff, xbar_.p + h.coff,
+                                     c_s_.p + h.coff, l_s_.p + h.coff, u_s_.p + h.coff, scal_.p, 0};
+    a.opd[q] = OpDual<false>{x_[x1].p, y_[x0].p + h.roff, y_[x1].p + h.roff, ybar_.p + h.roff, kx_[x0].p + h.roff,
+                             kx_[x1].p + h.roff, q_s_.p + h.roff, h.rk, scal_.p, 0};
+  }
+  a.parity = parity;
+  a.count = count;
+  a.gbar = gbar_.p;
+  PDHG_CUDA(cudaMemsetAsync(gbar_.p, 0, sizeof(unsigned), st_));
+  launch_block(a, h.csc.s_len, h.csc.s_u < h.csc.s1, h.csr.l_stage, st_);
+}
+
+void Session::LaunchBlock(int parity, int count) {
+  switch (bnd_) {
+    case 0: return LaunchBlockT<0>(parity, count);
+    case 1: return LaunchBlockT<1>(parity, count);
+    case 2: return LaunchBlockT<2>(parity, count);
+    default: return LaunchBlockT<3>(parity, count);
+  }
+}
+
 // `count` PDHG iterations starting from buffer `parity`. Blocks are replayed
 // from captured CUDA graphs (one per parity/length/adapt combination).
 void Session::RunSteps(int parity, int count, bool adapt) {
   Graph* g = nullptr;
   for (Graph& gg : graphs_)
     if (gg.steps == count && gg.parity == parity && gg.adapt == adapt) g = &gg;
+  const bool block = persist_ && !adapt;
   if (!g && count >= 4 && comm_->graphs()) {
     cudaGraph_t graph;
     const int64_t before = launches_;
     PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-    for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
+    if (block) LaunchBlock(parity, count);
+    else
+      for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
     PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
     launches_ = before;
     Graph ng;
@@ -1286,9 +1345,11 @@ void Session::RunSteps(int parity, int count, bool adapt) {
   if (g) {
     const int64_t per = launches_csc() + launches_csr() +
                         (adapt ? static_cast<int64_t>(shards_.size()) + 1 + (shards_.size() > 1) : 0);
-    launches_ += static_cast<int64_t>(count) * per;
+    launches_ += block ? 1 : static_cast<int64_t>(count) * per;
     trace_graph("steps", count);
     PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
+  } else if (block) {
+    LaunchBlock(parity, count);
   } else {
     for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
   }
@@ -1313,7 +1374,9 @@ void Session::RunChecked(int parity, int count) {
     cudaGraph_t graph;
     const int64_t before = launches_;
     PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-    for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, false);
+    if (persist_) LaunchBlock(parity, count);
+    else
+      for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, false);
     k_inner_add<<<1, 1, 0, st_>>>(scal_.p, count);
     LaunchCheck(x_[pa].p, y_[pa].p, xbar_.p, ybar_.p, kx_[pa].p, nullptr, check_branches);
     PDHG_CUDA(cudaMemcpyAsync(host_red_, red_out_.p, sizeof(CheckOut), cudaMemcpyDeviceToHost, st_));
@@ -1328,8 +1391,8 @@ void Session::RunChecked(int parity, int count) {
     graphs_.push_back(ng);
     g = &graphs_.back();
   }
-  launches_ += static_cast<int64_t>(count) * (launches_csc() + launches_csr()) + 1 + launches_csr() + launches_csc() +
-               static_cast<int64_t>(shards_.size()) + (shards_.size() > 1);
+  launches_ += (persist_ ? 1 : static_cast<int64_t>(count) * (launches_csc() + launches_csr())) + 1 + launches_csr() +
+               launches_csc() + static_cast<int64_t>(shards_.size()) + (shards_.size() > 1);
   PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
   check_launch("pdhg block + check");
 }
@@ -2596,6 +2659,7 @@ void Session::Stats(pdhg_session_stats* s) const {
   s->csr_uniform_len = all_uniform(true);
   s->csc_uniform_len = all_uniform(false);
   s->csr_split = shards_.size() == 1 ? shards_[0].csr.split_w : 0;
+  s->block_kernel = persist_ ? 1 : 0;
 }
 
 void Session::Blocks(int64_t* row_begin, int64_t* col_begin) const {

@@ -20,6 +20,7 @@
 #include "comm.cuh"
 #include "darray.cuh"
 #include "engine.cuh"
+#include "persist.cuh"
 
 namespace pdhg {
 
@@ -118,6 +119,11 @@ class Session {
   void RunSteps(int parity, int count, bool adapt);
   void RunBlock(int parity, int count, bool adapt, bool check, int slot);
   void RunChecked(int parity, int count);
+  // Persistent block kernel (persist.cuh): `count` iterations in one launch.
+  bool PersistOk() const;
+  void LaunchBlock(int parity, int count);
+  template <int kBnd>
+  void LaunchBlockT(int parity, int count);
   void RunDeviceLoop(int parity, int count);
   void LaunchCheck(const double* x, const double* y, const double* xb, const double* yb, const double* kx,
                    const Scalars* guard = nullptr, bool branches = false);
@@ -204,6 +210,8 @@ class Session {
   DArray<double> q_s_, q_o_, rs_;                          // mp_
   double c_norm_s_ = 0, q_norm_s_ = 0, c_norm_o_ = 0, q_norm_o_ = 0;
   int bnd_ = 0;               // uniform-bound bits (UniformBounds)
+  bool persist_ = false;      // step blocks as one persistent launch (PersistOk, PDHG_PERSIST)
+  DArray<unsigned> gbar_;     // its grid-barrier counter
   int modal_col_len_ = 0;     // columns: modal class-S length placed first (Layout::s_u), or 0
   bool bnd_all_ = false;      // original bounds equal the common scaled ones too
   double lb_ = 0.0, ub_ = 0.0;

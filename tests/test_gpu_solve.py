@@ -441,3 +441,24 @@ def test_class_s_window_split_bit_identical(name, monkeypatch):
     assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
+
+
+@pytest.mark.parametrize("shape", [(520, 700), (800, 600), (1000, 1000)])
+def test_persistent_block_kernel_bit_identical(shape, monkeypatch):
+    """The persistent block kernel (persist.cuh: a block of iterations in one
+    cooperative launch, grid barriers between the passes) runs the two step
+    kernels' bodies on the same work items: whole trajectories -- iterations,
+    restarts, x, y -- are bitwise identical to the two-kernel path
+    (PDHG_PERSIST=0), at ε 1e-6 with checks and restarts inside."""
+    p = GenTransport(shape[0], shape[1], 5)  # rows of 520..1000: one class L of staged 4-row groups
+    prm = SolverParams(eps=1e-6, iter_limit=4000)
+    runs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PDHG_PERSIST", flag)
+        with rpdlp.Session(p, prm) as s:
+            assert s.stats().block_kernel == (1 if flag == "1" else 0)
+            runs.append(s.solve(prm))
+    a, b = runs
+    assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)

@@ -2,14 +2,14 @@
 per setting (env read at session creation), warm in-loop iteration time and
 the per-kernel times.
 
-    python tools/exp/pol_probe.py VAR "v1,v2,..." case [case ...]
-    python tools/exp/pol_probe.py - "A=1+B=2,A=3+B=4" case ...   (combined settings, applied cumulatively)
+    python tools/ab_kernels.py VAR "v1,v2,..." case [case ...]
+    python tools/ab_kernels.py - "A=1+B=2,A=3+B=4" case ...   (combined settings, applied cumulatively)
 """
 import os
 import sys
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2312_14832_b200 import rpdlp  # noqa: E402
 from bench import algorithmic_bytes  # noqa: E402
 

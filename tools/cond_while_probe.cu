@@ -1,6 +1,6 @@
 // Feasibility probe: a conditional WHILE graph node whose body is captured
 // from a stream (kernels + a PDL launch), the loop condition set on the
-// device. nvcc -gencode arch=compute_100a,code=sm_100a cond_while.cu
+// device. nvcc -gencode arch=compute_100a,code=sm_100a tools/cond_while_probe.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 

@@ -302,16 +302,17 @@ def pinned_copy(problem):
     return q
 
 
-def load_traffic(config: str, kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu summary of the
-    current build (profiles/ncu_summary.json, written by tools/ncu_summary.py
-    from an `ncu --set full` capture), or None."""
+def load_traffic(config: str, kernel: str, key: str = "dram_bytes_per_launch"):
+    """DRAM bytes per launch of `kernel` (or another `key` of the entry) from
+    the committed ncu summary of the current build (profiles/ncu_summary.json,
+    written from `ncu` captures of tools/gpu_evidence.sh), or None."""
     f = ROOT / "profiles" / "ncu_summary.json"
     if not f.exists():
         return None
     try:
         d = json.loads(f.read_text())
-        return d.get(config, {}).get(kernel, {}).get("dram_bytes_per_launch")
+        e = d.get(config, {}).get(kernel, {})
+        return e.get(key) if key in e else e.get("value")
     except (ValueError, AttributeError):
         return None
 
@@ -471,6 +472,17 @@ def run_ours(args, world, rank, local, dist):
                                "loop_gbs": rf["iteration_cold"]["bytes"] * tot_iters / loop_s / 1e9,
                                "note": "algorithmic bytes per iteration x loop it/s: the timed solves' average"},
                 **rf}
+    # In the loop the per-iteration working set mostly stays in L2: DRAM bytes
+    # per iteration (ncu, graph-level, write-backs included) and the
+    # iteration's algorithmic bytes against the measured L2 stream rate.
+    dram_it = load_traffic(args.config, "iteration_in_loop", "dram_bytes_per_iteration")
+    l2_gbs = load_traffic(args.config, "l2_stream_gbs")
+    if dram_it and l2_gbs and "iteration_in_loop" in roofline:
+        il = roofline["iteration_in_loop"]
+        il["dram_bytes_per_iteration"] = dram_it
+        il["dram_gbs"] = dram_it / (il["ms"] * 1e-3) / 1e9
+        il["l2_stream_peak_gbs"] = l2_gbs
+        il["l2_frac"] = il["gbs"] / l2_gbs
     sess.close()
 
     # End to end through the public C-ABI, pinned host buffers.

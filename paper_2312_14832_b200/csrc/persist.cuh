@@ -32,7 +32,9 @@
 // the standalone uniform kernel runs 8 at 32), the dual pass 5.8 us (8.2 us
 // standalone: its stream is issued before the barrier). Beating the two
 // kernels needs a sub-microsecond hierarchical barrier and a TMA-streamed
-// primal phase.
+// primal phase. Tried and no better (r02v): cooperative_groups' grid sync or
+// a release-add / relaxed-poll barrier (19.2 us), two primal blocks per CTA
+// in flight (21.5-22.2 us).
 #pragma once
 
 #include "engine.cuh"

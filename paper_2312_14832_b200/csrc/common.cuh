@@ -103,7 +103,16 @@ struct Scalars {
   int32_t halt;       // pipelined loop: skip queued blocks until the host clears it
   double adapt_iter;  // iterations_ at the start of the block (adaptive step)
   double lb, ub;      // the common scaled bound when every column shares it
+  double step_p;      // eta / omega: the primal step (solver.cpp:285-290), set with eta / omega
+  double step_d;      // eta * omega: the dual step (solver.cpp:292-298)
 };
+
+// The step sizes the step kernels read, derived once per change of eta or
+// omega instead of once per thread (IEEE division on host and device alike).
+__host__ __device__ inline void set_steps(Scalars& s) {
+  s.step_p = s.eta / s.omega;
+  s.step_d = s.eta * s.omega;
+}
 
 // Clamp with the reference's NaN behaviour: std::min(std::max(v, lo), hi)
 // (solver.cpp:33-35) returns NaN for NaN input; fmin/fmax would mask it.

@@ -277,7 +277,6 @@ template <class Op, int L, bool kPrefix>
 __device__ __forceinline__ void uniform_item(int blk, const int32_t* __restrict__ idx, const double* __restrict__ val,
                                              int32_t s_end, const Op& op, double* __restrict__ red_out,
                                              const int32_t* __restrict__ ptr, int32_t s_u) {
-  if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   constexpr bool MX = Op::kMax;
@@ -286,6 +285,7 @@ __device__ __forceinline__ void uniform_item(int blk, const int32_t* __restrict_
   for (int i = 0; i < NR; ++i) red[i] = 0.0;
   if constexpr (kPrefix) {
     if (blk * kBlock >= s_u) {  // CTA-uniform: past the modal prefix
+      if (skip_launch(op)) return;
       seg_thread_direct(ptr, idx, val, s_end, op, red, blk);
       block_reduce_out<Op>(red, red_out, blk);
       return;
@@ -296,9 +296,12 @@ __device__ __forceinline__ void uniform_item(int blk, const int32_t* __restrict_
   int32_t j[L];
   double v[L];
   if (s < s_end) {
-    pre = op.prefetch(s);
     load_uniform<L>(idx, val, static_cast<int64_t>(s) * L, j, v);
+    pre = op.prefetch(s);
   }
+  // The halt flag (pipelined loop) is tested once the loads are in flight,
+  // not before: it is one more dependent round trip ahead of every load.
+  if (skip_launch(op)) return;
   pdl_wait_trigger();
   if (s < s_end) {
     double p[L][R];
@@ -457,7 +460,6 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
                                                                       int32_t s_end, const Op op,
                                                                       double* __restrict__ red_out,
                                                                       const uint8_t* __restrict__ rm) {
-  if (skip_launch(op)) return;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
   __shared__ double sprod[kWarps][R][C];
@@ -482,6 +484,7 @@ __global__ void __launch_bounds__(kBlock, 4) seg_thread_staged_kernel(const int3
     if constexpr (HasInit<Op>::value) acc[0] = op.init(s);  // split high pass: the low pass's partial
   }
   if (kRM && s0 < s_end) seg_order = rm[s0 >> 5];  // warp-uniform
+  if (skip_launch(op)) return;  // halt flag (pipelined loop), once the loads are in flight
   pdl_wait_trigger();
   if (s0 < s_end) {  // warp-uniform
     const int wb = __shfl_sync(0xffffffffu, b, 0);
@@ -964,7 +967,7 @@ __device__ __forceinline__ void cta4_item(int blk, const int32_t* __restrict__ p
                                           const double* __restrict__ val, int32_t s_begin, int32_t s_end, const Op& op,
                                           double* __restrict__ red_out, unsigned char* stage, uint64_t* bar,
                                           double (*sh)[4][Op::kRhs]) {
-  if (skip_launch(op)) return;
+  const bool halted = skip_launch(op);  // tested after the offsets are loaded
   constexpr int RPC = 4;
   constexpr int R = Op::kRhs;
   constexpr int NR = Op::kRed > 0 ? Op::kRed : 1;
@@ -980,6 +983,10 @@ __device__ __forceinline__ void cta4_item(int blk, const int32_t* __restrict__ p
   const int g0 = s_begin + blk * RPC;
   const int g1 = min(g0 + RPC, s_end);
   const int32_t lo = ptr[g0], hi = ptr[g1];
+  if (halted) {  // before any bulk copy is issued: none may outlive the CTA
+    if constexpr (kIssued) mbar_wait(bar, 0);
+    return;
+  }
   uint32_t bv = 0, bi = 0;
   const int64_t av = widen16<double>(lo, hi, &bv);
   const int64_t ai = widen16<int32_t>(lo, hi, &bi);

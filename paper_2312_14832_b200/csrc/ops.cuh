@@ -170,7 +170,7 @@ struct OpPrimal {
   __device__ Pre staged(int32_t, const double* st, int ld) const {
     Pre p;
     p.w = sc->inner_base + static_cast<double>(j_in_block);
-    p.step = sc->eta / sc->omega;
+    p.step = sc->step_p;
     p.x = st[0];
     p.c = st[ld];
     p.l = kL ? st[kIL * ld] : sc->lb;
@@ -179,14 +179,19 @@ struct OpPrimal {
     return p;
   }
   __device__ Pre prefetch(int32_t s) const {
+    // The per-segment loads go out first (the average speculatively: it is
+    // only used when w > 0), the solver scalars after them.
     Pre p;
-    p.w = sc->inner_base + static_cast<double>(j_in_block);
-    p.step = sc->eta / sc->omega;
     p.x = x[s];
     p.c = c[s];
-    p.l = kL ? l[s] : sc->lb;
-    p.u = kU ? u[s] : sc->ub;
-    p.xbar = (p.w == 0.0) ? 0.0 : xbar[s];  // Reset() zeroes the average
+    if constexpr (kL) p.l = l[s];
+    if constexpr (kU) p.u = u[s];
+    const double xb = xbar[s];
+    p.w = sc->inner_base + static_cast<double>(j_in_block);
+    p.step = sc->step_p;
+    if constexpr (!kL) p.l = sc->lb;
+    if constexpr (!kU) p.u = sc->ub;
+    p.xbar = (p.w == 0.0) ? 0.0 : xb;  // Reset() zeroes the average
     return p;
   }
   __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double* red) const {
@@ -234,7 +239,7 @@ struct OpDual {
   __device__ Pre staged(int32_t, const double* st, int ld) const {
     Pre p;
     p.w = sc->inner_base + static_cast<double>(j_in_block);
-    p.step = sc->eta * sc->omega;
+    p.step = sc->step_d;
     p.kx = st[0];
     p.y = st[ld];
     p.q = st[2 * ld];
@@ -242,13 +247,14 @@ struct OpDual {
     return p;
   }
   __device__ Pre prefetch(int32_t s) const {
-    Pre p;
-    p.w = sc->inner_base + static_cast<double>(j_in_block);
-    p.step = sc->eta * sc->omega;
+    Pre p;  // per-segment loads first (the average speculatively), scalars after
     p.kx = kx[s];
     p.y = y[s];
     p.q = q[s];
-    p.ybar = (p.w == 0.0) ? 0.0 : ybar[s];
+    const double yb = ybar[s];
+    p.w = sc->inner_base + static_cast<double>(j_in_block);
+    p.step = sc->step_d;
+    p.ybar = (p.w == 0.0) ? 0.0 : yb;
     return p;
   }
   __device__ void finish(int32_t s, const double (&a)[1], const Pre& p, double* red) const {

@@ -1629,6 +1629,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     inner = 0;
   };
   auto push_scalars = [&] {
+    set_steps(sc);
     PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   };
 
@@ -2214,7 +2215,8 @@ double Session::OpNorm(int iters, uint64_t seed) {
   ToInternal(v, pad_c_, u, n_, np_);
   Scalars sc{};
   sc.pw_norm = vnorm;
-  PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
+  set_steps(sc);
+    PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   trace_graph("power", many);
   for (int it = 0; it < many; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph_, st_));
   for (int it = 0; it < rest; ++it) PDHG_CUDA(cudaGraphLaunch(power_graph1_, st_));
@@ -2336,7 +2338,8 @@ void Session::TimeKernels(int iters, double* ms_primal, double* ms_dual, double*
   sc.inner_base = 1.0;
   sc.lb = lb_;
   sc.ub = ub_;
-  PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
+  set_steps(sc);
+    PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   k_clamp0<<<ew_grid(np_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, np_);
   if (mp_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, mp_ * sizeof(double), st_));
   for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, fork_);
@@ -2406,7 +2409,8 @@ void Session::TimeKernelsCold(int iters, double* ms_primal, double* ms_dual, dou
   sc.inner_base = 1.0;
   sc.lb = lb_;
   sc.ub = ub_;
-  PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
+  set_steps(sc);
+    PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   k_clamp0<<<ew_grid(np_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, np_);
   if (mp_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, mp_ * sizeof(double), st_));
   for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, fork_);
@@ -2481,7 +2485,8 @@ void Session::RunBlock(int iters, bool profiler_range) {
   sc.inner_base = 1.0;
   sc.lb = lb_;
   sc.ub = ub_;
-  PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
+  set_steps(sc);
+    PDHG_CUDA(cudaMemcpyAsync(scal_.p, &sc, sizeof(Scalars), cudaMemcpyHostToDevice, st_));
   k_clamp0<<<ew_grid(np_), kEw, 0, st_>>>(l_s_.p, u_s_.p, x_[0].p, np_);
   if (mp_) PDHG_CUDA(cudaMemsetAsync(y_[0].p, 0, mp_ * sizeof(double), st_));
   for (Shard& h : shards_) run_pass(h.csr, OpSpmv{x_[0].p, kx_[0].p + h.roff}, RedSlots{}, fork_);

@@ -615,6 +615,7 @@ __global__ void k_adapt_apply(const double* sum, Scalars* sc, int j) {
   const double a1 = lim * (1.0 - pow(k, -0.3));
   const double a2 = sc->eta * (1.0 + pow(k, -0.6));
   sc->eta = (a2 < a1) ? a2 : a1;  // std::min(a1, a2)
+  set_steps(*sc);
 }
 
 }  // namespace pdhg

@@ -156,7 +156,10 @@ struct OpPrimal {
   const double* u;
   const Scalars* sc;
   int j_in_block;
-  __device__ bool skip() const { return sc->halt != 0; }  // pipelined loop: block discarded
+  // Pipelined loop only: &sc->halt, so a block queued behind a halting check
+  // is discarded. Null elsewhere -- no load of the flag ahead of the pass.
+  const int32_t* halt = nullptr;
+  __device__ bool skip() const { return halt && *halt != 0; }
   __device__ void map(int32_t i, double v, double (&p)[1]) const { p[0] = v * y[i]; }
   static constexpr int kOcc = 5;
   static constexpr int kOps = 3 + kL + kU;
@@ -228,7 +231,8 @@ struct OpDual {
   RowKind rk;  // equality rows (permuted order)
   const Scalars* sc;
   int j_in_block;
-  __device__ bool skip() const { return sc->halt != 0; }
+  const int32_t* halt = nullptr;  // as OpPrimal::halt
+  __device__ bool skip() const { return halt && *halt != 0; }
   __device__ void map(int32_t j, double v, double (&p)[1]) const { p[0] = v * xn[j]; }
   static constexpr int kOcc = 5;
   static constexpr int kOps = 4;

@@ -1206,10 +1206,10 @@ void Session::ToHost(const double* dev, const double* scale, const DArray<int32_
 template <bool kAdapt, int kBnd>
 void Session::PrimalPass(Shard& h, int a, int b, int j) {
   const int64_t o = h.coff;
-  run_pass(h.csc,
-           OpPrimal<kAdapt, kBnd>{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
-                                  scal_.p, j},
-           RedSlots{kAdapt ? h.red[1].p : nullptr}, fork_);
+  OpPrimal<kAdapt, kBnd> op{y_[a].p, x_[a].p + o, x_[b].p + o, xbar_.p + o, c_s_.p + o, l_s_.p + o, u_s_.p + o,
+                            scal_.p, j};
+  op.halt = halt_ptr_;
+  run_pass(h.csc, op, RedSlots{kAdapt ? h.red[1].p : nullptr}, fork_);
 }
 
 void Session::LaunchPrimal(Shard& h, int a, int b, int j, bool adapt) {
@@ -1232,16 +1232,17 @@ void Session::LaunchStep(int parity, int j, bool adapt) {
   GatherX(x_[b].p);
   for (Shard& h : shards_) {
     const int64_t o = h.roff;
-    if (adapt)
-      run_pass(h.csr,
-               OpDual<true>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
-                            h.rk, scal_.p, j},
-               RedSlots{h.red[0].p}, fork_);
-    else
-      run_pass(h.csr,
-               OpDual<false>{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
-                             h.rk, scal_.p, j},
-               RedSlots{}, fork_);
+    if (adapt) {
+      OpDual<true> op{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
+                      h.rk, scal_.p, j};
+      op.halt = halt_ptr_;
+      run_pass(h.csr, op, RedSlots{h.red[0].p}, fork_);
+    } else {
+      OpDual<false> op{x_[b].p, y_[a].p + o, y_[b].p + o, ybar_.p + o, kx_[a].p + o, kx_[b].p + o, q_s_.p + o,
+                       h.rk, scal_.p, j};
+      op.halt = halt_ptr_;
+      run_pass(h.csr, op, RedSlots{}, fork_);
+    }
   }
   GatherY(y_[b].p);
   if (adapt) {
@@ -1463,7 +1464,9 @@ void Session::RunBlock(int parity, int count, bool adapt, bool check, int slot) 
     if (gg.steps == count && gg.parity == key_par && gg.adapt == adapt) g = &gg;
   const int pa = (parity + count) & 1;
   auto body = [&] {
+    halt_ptr_ = &scal_.p->halt;  // queued blocks must stop after a halting check
     for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
+    halt_ptr_ = nullptr;
     k_advance<<<1, 1, 0, st_>>>(scal_.p, dstate_.p, count);
     if (check) {
       LaunchCheck(x_[pa].p, y_[pa].p, xbar_.p, ybar_.p, kx_[pa].p, scal_.p);

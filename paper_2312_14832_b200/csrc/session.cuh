@@ -211,6 +211,7 @@ class Session {
   double c_norm_s_ = 0, q_norm_s_ = 0, c_norm_o_ = 0, q_norm_o_ = 0;
   int bnd_ = 0;               // uniform-bound bits (UniformBounds)
   bool persist_ = false;      // step blocks as one persistent launch (PersistOk, PDHG_PERSIST)
+  const int32_t* halt_ptr_ = nullptr;  // step Ops' halt flag while the pipelined loop queues blocks
   DArray<unsigned> gbar_;     // its grid-barrier counter
   int modal_col_len_ = 0;     // columns: modal class-S length placed first (Layout::s_u), or 0
   bool bnd_all_ = false;      // original bounds equal the common scaled ones too

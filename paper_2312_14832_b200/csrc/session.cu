@@ -1361,7 +1361,7 @@ void Session::RunSteps(int parity, int count, bool adapt) {
 // block's steps, the inner_base advance, the check passes and the D2H of the
 // reduced pack into pinned host memory, so a check costs one graph launch and
 // one stream synchronisation instead of eager launches and a separate copy.
-void Session::RunChecked(int parity, int count) {
+void Session::RunChecked(int parity, int count, bool adapt) {
   static const bool check_branches = [] {  // PDHG_CHECK_BRANCHES=0: serial check passes (A/B)
     const char* e = std::getenv("PDHG_CHECK_BRANCHES");
     return !(e && e[0] == '0');
@@ -1369,31 +1369,35 @@ void Session::RunChecked(int parity, int count) {
   const int key = parity + 8;  // graphs_ key space: plain blocks use 0 / 1
   Graph* g = nullptr;
   for (Graph& gg : graphs_)
-    if (gg.steps == count && gg.parity == key && !gg.adapt) g = &gg;
+    if (gg.steps == count && gg.parity == key && gg.adapt == adapt) g = &gg;
   const int pa = (parity + count) & 1;
   if (!g) {
     cudaGraph_t graph;
     const int64_t before = launches_;
     PDHG_CUDA(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-    if (persist_) LaunchBlock(parity, count);
+    if (persist_ && !adapt) LaunchBlock(parity, count);
     else
-      for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, false);
+      for (int j = 0; j < count; ++j) LaunchStep((parity + j) & 1, j, adapt);
     k_inner_add<<<1, 1, 0, st_>>>(scal_.p, count);
     LaunchCheck(x_[pa].p, y_[pa].p, xbar_.p, ybar_.p, kx_[pa].p, nullptr, check_branches);
     PDHG_CUDA(cudaMemcpyAsync(host_red_, red_out_.p, sizeof(CheckOut), cudaMemcpyDeviceToHost, st_));
+    if (adapt)  // the block's adapted step size, for EvalInfo and later pushes (slot kPack - 2)
+      PDHG_CUDA(cudaMemcpyAsync(host_red_ + kPack - 2, &scal_.p->eta, sizeof(double), cudaMemcpyDeviceToHost, st_));
     PDHG_CUDA(cudaStreamEndCapture(st_, &graph));
     launches_ = before;
     Graph ng;
     ng.steps = count;
     ng.parity = key;
-    ng.adapt = false;
+    ng.adapt = adapt;
     PDHG_CUDA(cudaGraphInstantiate(&ng.exec, graph, 0));
     cudaGraphDestroy(graph);
     graphs_.push_back(ng);
     g = &graphs_.back();
   }
-  launches_ += (persist_ ? 1 : static_cast<int64_t>(count) * (launches_csc() + launches_csr())) + 1 + launches_csr() +
-               launches_csc() + static_cast<int64_t>(shards_.size()) + (shards_.size() > 1);
+  const int64_t per = launches_csc() + launches_csr() +
+                      (adapt ? static_cast<int64_t>(shards_.size()) + 1 + (shards_.size() > 1) : 0);
+  launches_ += (persist_ && !adapt ? 1 : static_cast<int64_t>(count) * per) + 1 + launches_csr() + launches_csc() +
+               static_cast<int64_t>(shards_.size()) + (shards_.size() > 1);
   PDHG_CUDA(cudaGraphLaunch(g->exec, st_));
   check_launch("pdhg block + check");
 }
@@ -1958,19 +1962,16 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
         capped = true;
       }
     }
-    // A block ending at a check runs as one graph with the check (RunChecked);
-    // adaptive steps and NCCL sessions keep the eager check.
-    const bool fused = fused_check && !adapt && !nccl() && count == to_check && count >= 4;
-    if (fused) {
-      RunChecked(par, static_cast<int>(count));
-    } else {
-      if (adapt) {
-        sc.adapt_iter = static_cast<double>(iters);
-        PDHG_CUDA(
-            cudaMemcpyAsync(&scal_.p->adapt_iter, &sc.adapt_iter, sizeof(double), cudaMemcpyHostToDevice, st_));
-      }
-      RunSteps(par, static_cast<int>(count), adapt);
+    // A block ending at a check runs as one graph with the check (RunChecked;
+    // with adaptive steps the graph also copies the adapted step size out);
+    // NCCL sessions keep the eager check.
+    const bool fused = fused_check && !nccl() && count == to_check && count >= 4;
+    if (adapt) {
+      sc.adapt_iter = static_cast<double>(iters);
+      PDHG_CUDA(cudaMemcpyAsync(&scal_.p->adapt_iter, &sc.adapt_iter, sizeof(double), cudaMemcpyHostToDevice, st_));
     }
+    if (fused) RunChecked(par, static_cast<int>(count), adapt);
+    else RunSteps(par, static_cast<int>(count), adapt);
     par = static_cast<int>((par + count) & 1);
     iters += count;
     inner += count;
@@ -1986,6 +1987,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     if (fused) {
       Sync();
       std::memcpy(&ck, host_red_, sizeof(CheckOut));
+      if (adapt) sc.eta = host_red_[kPack - 2];
     } else {
       LaunchCheck(x_[par].p, y_[par].p, xbar_.p, ybar_.p, kx_[par].p);
     }

@@ -118,7 +118,7 @@ class Session {
   void DrawStart(uint64_t seed);
   void RunSteps(int parity, int count, bool adapt);
   void RunBlock(int parity, int count, bool adapt, bool check, int slot);
-  void RunChecked(int parity, int count);
+  void RunChecked(int parity, int count, bool adapt = false);
   // Persistent block kernel (persist.cuh): `count` iterations in one launch.
   bool PersistOk() const;
   void LaunchBlock(int parity, int count);

@@ -462,3 +462,25 @@ def test_persistent_block_kernel_bit_identical(shape, monkeypatch):
     assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
+
+
+@pytest.mark.parametrize("name", ["config1", "transport"])
+def test_adaptive_fused_check_matches_eager(name, monkeypatch):
+    """Adaptive steps now run their check-ending blocks as one graph with the
+    check (RunChecked copies the adapted step size out with the check pack):
+    trajectories are bitwise those of the eager check (PDHG_FUSED_CHECK=0),
+    observer trace included (step size at every check)."""
+    from problems import config1
+    p = config1(3) if name == "config1" else GenTransport(60, 80, 2)
+    prm = SolverParams(eps=1e-6, iter_limit=6000, adaptive_step=True)
+    runs, traces = [], []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PDHG_FUSED_CHECK", flag)
+        tr = []
+        runs.append(rpdlp.Solve(p, prm, lambda info: tr.append((info.iteration, info.eta, info.omega))))
+        traces.append(tr)
+    a, b = runs
+    assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
+    assert traces[0] == traces[1]

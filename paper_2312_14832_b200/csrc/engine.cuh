@@ -330,6 +330,12 @@ __global__ void __launch_bounds__(kBlock) seg_thread_uniform_kernel(const int32_
   uniform_item<Op, L, kPrefix>(static_cast<int>(blockIdx.x), idx, val, s_end, op, red_out, ptr, s_u);
 }
 
+// Ops whose map() splits into gather(index) and prod(value, gathered, out).
+template <class T, class = void>
+struct HasGather : std::false_type {};
+template <class T>
+struct HasGather<T, std::void_t<decltype(std::declval<T>().gather(0))>> : std::true_type {};
+
 template <class T, class = void>
 struct HasInit : std::false_type {};
 template <class T>
@@ -1012,6 +1018,34 @@ __device__ __forceinline__ void cta4_item(int blk, const int32_t* __restrict__ p
   double acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = 0.0;
+  if constexpr (HasGather<Op>::value) {
+    // Gathers first (Op::gather / Op::prod): all of a thread's entries up to
+    // 2U in flight at once -- one gather latency per group for rows of up to
+    // 2U * T entries (transport's 1000) instead of one per U-batch -- then the
+    // products in the same order. The zeros of masked slots are added exactly
+    // where the U-batched loop adds them (up to the thread's entry count
+    // rounded up to U), so the sums stay bitwise those of seg_cta_kernel.
+    constexpr int G = 2 * U;
+    const int n = e > b + t ? (e - (b + t) + T - 1) / T : 0;
+    const int nz = (n + U - 1) / U * U;  // slots the U-batched loop combines
+    int base = 0;
+    for (int k = b + t; k < e; k += T * G) {
+      double g[G];
+#pragma unroll
+      for (int u = 0; u < G; ++u) g[u] = (k + T * u < e) ? op.gather(sidx[k + T * u - ai]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        if (k + T * u < e) {
+          double p[R];
+          op.prod(sval[k + T * u - av], g[u], p);
+          acc[0] = combine<MX>(acc[0], p[0]);
+        } else if (base + u < nz) {
+          acc[0] = combine<MX>(acc[0], 0.0);
+        }
+      }
+      base += G;
+    }
+  } else {  // (braced: with `else for` + `#pragma unroll`, nvcc 12.9 dropped all code after the loop)
   for (int k = b + t; k < e; k += T * U) {
     int32_t j[U];
     double v[U], p[U][R];
@@ -1034,6 +1068,7 @@ __device__ __forceinline__ void cta4_item(int blk, const int32_t* __restrict__ p
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[r] = combine<MX>(acc[r], p[u][r]);
+  }
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {

@@ -234,6 +234,8 @@ struct OpDual {
   const int32_t* halt = nullptr;  // as OpPrimal::halt
   __device__ bool skip() const { return halt && *halt != 0; }
   __device__ void map(int32_t j, double v, double (&p)[1]) const { p[0] = v * xn[j]; }
+  __device__ double gather(int32_t j) const { return xn[j]; }
+  __device__ void prod(double v, double g, double (&p)[1]) const { p[0] = v * g; }
   static constexpr int kOcc = 5;
   static constexpr int kOps = 4;
   __device__ const double* operand(int k) const {

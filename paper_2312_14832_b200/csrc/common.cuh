@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -11,6 +12,17 @@
 #include <string>
 
 namespace pdhg {
+
+// NVTX range for the duration of a scope (session setup, scaling, the power
+// iteration, the loop, every check, finish): names show up in Nsight
+// Systems / Compute timelines (`ncu --nvtx --nvtx-include "pdhg.loop/"`).
+// Without an attached tool each push / pop is a no-op call.
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+  NvtxScope(const NvtxScope&) = delete;
+  NvtxScope& operator=(const NvtxScope&) = delete;
+};
 
 // Error carrying a C-ABI code (include/pdhg.h).
 struct Error : std::runtime_error {

@@ -13,6 +13,8 @@
 //
 // Internally rows and columns live in length-class order (engine.cuh); the
 // permutation is applied once at upload and undone at the boundary.
+#include <optional>
+
 #include "session.cuh"
 
 #include <cub/cub.cuh>
@@ -202,6 +204,7 @@ Session::Session(const pdhg_lp& lp, const pdhg_params& prm, int device, const Sh
   m_ = m1_ + m2_;
   offset_ = lp.objective_offset;
   try {
+    NvtxScope nv("pdhg.session");
     const double t0 = now_s();
     {
       DArray<int32_t> ptr0, idx0;
@@ -995,6 +998,7 @@ void Session::PartitionLong(Layout& L, Store& S) {
 // shard owns whole rows (CSR) and whole columns (CSC), and the per-sweep
 // factors are all-gathered before the values are rescaled.
 void Session::ComputeScaling(const pdhg_params& prm) {
+  NvtxScope nv("pdhg.scaling");
   rs_.alloc(mp_, &arena_);
   cs_.alloc(np_, &arena_);
   c_s_.alloc(np_, &arena_);
@@ -1564,6 +1568,7 @@ void Session::ReadCheck(CheckOut* out) {
 
 // ================================================================ solve loop
 void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_result* out) {
+  NvtxScope nv("pdhg.solve");
   PDHG_CUDA(cudaSetDevice(device_));
   AllocScope scope(st_);
   if (!ev_[0]) {
@@ -1576,7 +1581,10 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   auto secs = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
 
   // eta = 0.9 / ||K|| (solver.cpp:233-234), omega0 = ||c_s|| / ||q_s|| (:235-238).
+  std::optional<NvtxScope> nv_phase;
+  nv_phase.emplace("pdhg.opnorm");
   const double op = OpNorm(100, prm.seed);
+  nv_phase.reset();
   const double t_opnorm = secs();
   double t_checks = 0.0;
   int64_t nchecks = 0;
@@ -1852,6 +1860,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   const bool device_loop = device_loop_on && fused_check && !cb && prm.log_every <= 0 && !adapt && !nccl() &&
                            prm.check_every >= 4 && prm.check_every % 2 == 0;
   const double t_loop0 = secs();
+  nv_phase.emplace("pdhg.loop");
   while (!finished) {
     if (iters >= prm.iter_limit) {
       status = PDHG_ITER_LIMIT;
@@ -1982,6 +1991,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
     if (iters % prm.check_every != 0) continue;
 
     // ---- Check (solver.cpp:390-428).
+    NvtxScope nv_check("pdhg.check");
     const double tc0 = secs();
     ++nchecks;
     if (fused) {
@@ -2097,6 +2107,7 @@ void Session::Solve(const pdhg_params& prm, pdhg_eval_cb cb, void* user, pdhg_re
   }
 
   // Finish (solver.cpp:473-481): unscale best, lambda on the original problem.
+  nv_phase.emplace("pdhg.finish");
   const double t_loop = secs();
   if (gx_.use) GatherXFull(xbest_.p);  // ghost exchange left only the read entries valid
   if (gy_.use) GatherYFull(ybest_.p);

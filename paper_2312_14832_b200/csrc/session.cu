@@ -2219,8 +2219,16 @@ double Session::OpNorm(int iters, uint64_t seed) {
   // Start vector (solver.cpp:88-97): drawn on a host thread while the
   // session was being built (upload, CSC, scaling) for the seed the session
   // was created with; another seed is drawn here.
+  const char* tenv = std::getenv("PDHG_TRACE");
+  const bool fine = tenv && tenv[0] == '2';
+  const double tj0 = fine ? now_s() : 0.0;
+  if (fine) Sync();
+  const double tj1 = fine ? now_s() : 0.0;
   if (start_.joinable()) start_.join();
   if (start_seed_ != seed || !start_host_) DrawStart(seed);
+  if (fine)
+    std::fprintf(stderr, "[pdhg]   opnorm graphs captured %.4fs, start-vector wait %.4fs\n", tj1 - tj0,
+                 now_s() - tj1);
   double* v = start_host_;  // pinned: ToInternal copies it straight to the device
   double vnorm = start_norm_;
   if (vnorm == 0.0) {

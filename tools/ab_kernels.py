@@ -4,6 +4,11 @@ the per-kernel times.
 
     python tools/ab_kernels.py VAR "v1,v2,..." case [case ...]
     python tools/ab_kernels.py - "A=1+B=2,A=3+B=4" case ...   (combined settings, applied cumulatively)
+
+Only switches the session reads when it is created take effect between
+settings; process-wide ones (read once into a static: PDHG_PDL,
+PDHG_FUSED_CHECK, PDHG_CHECK_BRANCHES, ...) need one process per setting
+(tools/profile_step.py under `VAR=value`, or tools/ab_solve.py).
 """
 import os
 import sys

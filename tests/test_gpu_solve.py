@@ -484,3 +484,26 @@ def test_adaptive_fused_check_matches_eager(name, monkeypatch):
     np.testing.assert_array_equal(a.x, b.x)
     np.testing.assert_array_equal(a.y, b.y)
     assert traces[0] == traces[1]
+
+
+@pytest.mark.parametrize("name", ["pagerank", "transport"])
+def test_tile_sweep_order_bit_identical(name, monkeypatch):
+    """The tile engine's gather-sweep execution order (CMat::order, on by
+    default; PDHG_TILE_SWEEP=0 restores segment order) only changes which CTA
+    runs which tile: per-tile outputs are indexed by the tile and cross-tile
+    partials combine in tile order, so whole trajectories are bitwise
+    identical. Every segment over 64 nonzeros is routed to the tile engine
+    here (PDHG_WARP_MAX = PDHG_CTA_MAX = 64), so many long rows and columns
+    interleave in sweep order."""
+    p = GenPagerank(40000, 0.85, 6, 3) if name == "pagerank" else GenTransport(120, 700, 2)
+    prm = SolverParams(eps=1e-6, iter_limit=3000)
+    monkeypatch.setenv("PDHG_WARP_MAX", "64")
+    monkeypatch.setenv("PDHG_CTA_MAX", "64")
+    runs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PDHG_TILE_SWEEP", flag)
+        runs.append(rpdlp.Solve(p, prm))
+    a, b = runs
+    assert (a.iterations, a.restarts, int(a.status)) == (b.iterations, b.restarts, int(b.status))
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.y, b.y)
